@@ -1,0 +1,159 @@
+/*
+ * gpmatern.h -- C ABI of the B200-native exact fast Matern kernel MVM
+ * (arXiv 2508.01864, "weighted empirical CDF" decomposition) and the GP
+ * posterior-mean pipeline built on it.
+ *
+ * Citations: "P:n" = line n of the paper text, with the section /
+ * equation it falls in.  Readings of ambiguous passages are numbered R1..Rn in
+ * DESIGN.md.
+ *
+ * Conventions for every entry point
+ *   - Array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless
+ *     the parameter says "(host)".  All doubles are IEEE float64.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is enqueued on it; calls that return host values synchronise it.
+ *   - Ownership: the caller owns every pointer it passes and may free it after the
+ *     call returns (gp_setup copies what it needs).  A plan owns its device memory
+ *     until gp_destroy.  A plan is not safe for concurrent use from two streams.
+ *   - Errors: a gp_status is returned, never an exception; gp_last_error() gives a
+ *     thread-local message for the last non-OK status.  There is no CPU fallback:
+ *     without a CUDA device every compute call returns GP_ERR_CUDA.
+ */
+#ifndef GPMATERN_H
+#define GPMATERN_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GP_API __attribute__((visibility("default")))
+#else
+#define GP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GP_OK = 0,
+    GP_ERR_INVALID_ARG = 1,   /* null pointer, n < 1, d not in {1,2,3}, outputscale/lengthscale/sigma2/rtol <= 0 */
+    GP_ERR_UNSUPPORTED = 2,   /* (nu, form, d) outside the supported set (message lists it) */
+    GP_ERR_NONFINITE = 3,     /* NaN/Inf coordinate; message names the first bad row */
+    GP_ERR_RANGE = 4,         /* reserved: the literal exp(+t) weights of P:600 are never formed (R5) */
+    GP_ERR_NOT_CONVERGED = 5, /* CG hit max_iter; last iterate left in alpha, info filled */
+    GP_ERR_BREAKDOWN = 6,     /* CG found p^T A p <= 0 (A not SPD, e.g. L1 nu>=3/2, d>=2, R4) */
+    GP_ERR_CUDA = 7,          /* CUDA runtime error (message has cudaGetErrorString) */
+    GP_ERR_OOM = 8            /* device allocation failed */
+} gp_status;
+
+enum { GP_FORM_L1 = 0, GP_FORM_PRODUCT = 1 };                 /* P:414-422 [eq product_kernel, L1_kernel] */
+enum { GP_MEAN_NONE = 0, GP_MEAN_AFFINE = 1, GP_MEAN_BASIS = 2 }; /* P:73-82 [eq BetaLin, BetaFunc] */
+
+/* Scaled Matern kernel, P:294 [eq scaled_kernel], P:1253 [eq scaled_matern]:
+ *   L1:      K(x,x') = s^2 k_nu( sum_k |x_k - x'_k| / l_k )        (§2.3)
+ *   product: K(x,x') = s^2 prod_k k_nu( |x_k - x'_k| / l_k )
+ * with k_nu the half-integer closed forms of P:1273-1275.  Supported:
+ *   two_nu in {1,3,5}; d in {1,2,3}; form L1 for every d; form PRODUCT for d <= 2
+ *   (for d == 1 or two_nu == 1 the two forms coincide, and form is ignored).
+ * Per-dimension lengthscales are reading R2 (the paper uses one l). */
+typedef struct {
+    int two_nu;            /* 1, 3, 5 (nu = two_nu / 2) */
+    int form;              /* GP_FORM_* */
+    double outputscale;    /* s > 0, K(x,x) = s^2 */
+    double lengthscale[3]; /* l_k > 0 for k < d */
+} gp_kernel;
+
+typedef struct {
+    int iters;             /* CG iterations performed (max over right-hand sides) */
+    double relres_max;     /* max over columns of the TRUE ||b - A x|| / ||b|| at exit */
+    int failed_column;     /* column that broke down / did not converge, else -1 */
+    int restarts;          /* residual-replacement restarts taken */
+} gp_cg_info;
+
+typedef struct gp_plan_s *gp_plan;    /* opaque: the stored sort / D&C structure of x */
+typedef struct gp_cross_s *gp_cross;  /* opaque: structure of the union x U z for K_zx */
+
+/* gp_setup -- build the stored structure of P:191 [§1], P:338 [§2.1], P:539 [§2.2.3]:
+ * scale coordinates t_k = sqrt(2 nu) x_k / l_k, radix-sort each dimension, and for
+ * d >= 2 the divide-and-conquer level orders (Bentley).
+ *   x   : n x d row-major (device).  n >= 1.
+ *   k   : kernel (host).
+ *   out : receives the plan (host).
+ * Errors: INVALID_ARG, UNSUPPORTED, NONFINITE (first bad row), OOM, CUDA.
+ * Synchronises `stream` once (finiteness check). */
+GP_API gp_status gp_setup(const double *x, int64_t n, int d, const gp_kernel *k, void *stream,
+                   gp_plan *out);
+
+/* gp_kmvm -- out = K v (no nugget; the diagonal s^2 is included), P:241-247 [eq Ky],
+ * computed exactly by the ECDF decomposition, P:314-325 [eq fast_exact_decomposition_1d],
+ * P:459-509 [Props 1-2].
+ *   v   : n x nrhs, column-major with leading dimension n (device).
+ *   out : n x nrhs, same layout (device); must not alias v.
+ * Asynchronous on `stream`; no host synchronisation. */
+GP_API gp_status gp_kmvm(gp_plan p, const double *v, int nrhs, double *out, void *stream);
+
+/* gp_kmvm_host -- gp_kmvm with HOST buffers (pinned or pageable): copies v to the
+ * device, applies, copies out back and synchronises `stream`.  Used for the
+ * end-to-end measurement.  v, out: n x nrhs column-major (host). */
+GP_API gp_status gp_kmvm_host(gp_plan p, const double *v, int nrhs, double *out, void *stream);
+
+/* gp_kzx_setup -- structure for the rectangular product K_zx v (P:92 [k_z],
+ * P:256 [eq kde]): the same machinery on the union x U z with data points as
+ * sources and queries as targets (reading R7).  z: m x d row-major (device), m >= 1. */
+GP_API gp_status gp_kzx_setup(gp_plan p, const double *z, int64_t m, void *stream, gp_cross *out);
+
+/* gp_kzx -- out = K_zx v: out_q = sum_i v_i K(x_i, z_q).
+ *   v   : n x nrhs column-major (device), out: m x nrhs column-major (device). */
+GP_API gp_status gp_kzx(gp_cross c, const double *v, int nrhs, double *out, void *stream);
+GP_API void gp_kzx_destroy(gp_cross c);
+
+/* gp_cg_solve -- conjugate gradients (P:155-174 [§1]; P:980-1034 [App A, Alg 2] with
+ * no preconditioner, zero initial guess) on A = K + sigma2 I for the right-hand sides
+ * [y, H] (multi-RHS), then the GLS fixed effects of P:808-812:
+ *   beta = (H^T A^-1 H)^-1 H^T A^-1 y,   alpha = A^-1 y - (A^-1 H) beta,
+ * so that the posterior mean is mu(z) = h(z)^T beta + K_zx alpha (P:86 [eq gp_mean]).
+ *   sigma2    : nugget sigma^2 > 0.
+ *   y         : n (device), user order.
+ *   mean_kind : GP_MEAN_NONE (beta empty, alpha = A^-1 y), GP_MEAN_AFFINE (H = [1, x]
+ *               from the raw coordinates, P:73 [eq BetaLin]), GP_MEAN_BASIS
+ *               (H = user basis, n x L column-major device, P:79 [eq BetaFunc]).
+ *   rtol      : per-column relative residual target ||b - A x||_2 / ||b||_2 (R8).
+ *   max_iter  : iteration cap.
+ *   alpha     : n (device) output.
+ *   beta      : (host) output of length 1+d (AFFINE) or L (BASIS); may be NULL.
+ *   info      : (host) may be NULL.
+ * Errors: BREAKDOWN (p^T A p <= 0: column + iteration in the message),
+ * NOT_CONVERGED (alpha holds the last iterate).  Synchronises `stream`. */
+GP_API gp_status gp_cg_solve(gp_plan p, double sigma2, const double *y, int mean_kind,
+                      const double *H, int L, double rtol, int max_iter, double *alpha,
+                      double *beta, gp_cg_info *info, void *stream);
+
+/* gp_predict -- posterior mean mu(z_q) = h(z_q)^T beta + sum_i K(z_q, x_i) alpha_i
+ * (P:86 [eq gp_mean], P:149 [eq gp_mean_2]).
+ *   z      : m x d row-major (device); alpha: n (device, user order);
+ *   beta   : (host) 1+d coefficients for the affine mean h(z) = [1, z], or NULL for
+ *            out = K_zx alpha exactly;
+ *   Hz     : for a basis mean, the m x L column-major basis at z (device) and
+ *            beta of length L; pass NULL and L = 0 for the affine mean.
+ *   out    : m (device).  Builds and frees a union structure internally. */
+GP_API gp_status gp_predict(gp_plan p, const double *z, int64_t m, const double *alpha,
+                     const double *beta, const double *Hz, int L, double *out, void *stream);
+
+/* gp_plan_query -- introspection for tests and the bench (host value in *value):
+ *   0 n, 1 d, 2 levels L, 3 bytes of device structure, 4 kernel launches per
+ *   single-RHS gp_kmvm, 5 algorithmic HBM bytes per single-RHS gp_kmvm,
+ *   6 d=1 apply path in use (1 = single-launch cooperative, 2 = multi-sub-tile). */
+GP_API gp_status gp_plan_query(gp_plan p, int what, int64_t *value);
+
+/* gp_plan_set_option -- testing knob: option 0 forces the d=1 apply path
+ * (0 auto, 1 cooperative single sub-tile if it fits, 2 multi-sub-tile). */
+GP_API gp_status gp_plan_set_option(gp_plan p, int option, int64_t value);
+
+GP_API void gp_destroy(gp_plan p);
+GP_API const char *gp_last_error(void);
+/* Library version string, e.g. "gpmatern 0.1 sm_100a". */
+GP_API const char *gp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPMATERN_H */

@@ -1,0 +1,265 @@
+"""paper_2508_01864_b200 -- B200-native exact fast Matern kernel MVM (arXiv 2508.01864).
+
+Thin ctypes binding over ``libgpmatern.so`` (include/gpmatern.h).  This module only
+marshals arguments: device memory and streams come from PyTorch, every step of the
+method runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+library or a CUDA device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+__all__ = [
+    "load_library", "Kernel", "Plan", "Cross", "GPError", "setup", "kmvm", "cg_solve",
+    "predict", "FORM_L1", "FORM_PRODUCT", "MEAN_NONE", "MEAN_AFFINE", "MEAN_BASIS",
+    "LIB_PATH",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgpmatern.so")
+FORM_L1, FORM_PRODUCT = 0, 1
+MEAN_NONE, MEAN_AFFINE, MEAN_BASIS = 0, 1, 2
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "NONFINITE", 4: "RANGE",
+          5: "NOT_CONVERGED", 6: "BREAKDOWN", 7: "CUDA", 8: "OOM"}
+
+_lib = None
+
+
+class GPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"gpmatern {STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class _Kernel(ctypes.Structure):
+    _fields_ = [("two_nu", ctypes.c_int), ("form", ctypes.c_int),
+                ("outputscale", ctypes.c_double), ("lengthscale", ctypes.c_double * 3)]
+
+
+class _CGInfo(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("relres_max", ctypes.c_double),
+                ("failed_column", ctypes.c_int), ("restarts", ctypes.c_int)]
+
+
+def load_library(path: str | None = None):
+    """Load libgpmatern.so (built in-tree by build.py).  Raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `python -m paper_2508_01864_b200.build` "
+                                f"(no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    vp, i64, ci, cd = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    sig = {
+        "gp_setup": [vp, i64, ci, ctypes.POINTER(_Kernel), vp, ctypes.POINTER(vp)],
+        "gp_kmvm": [vp, vp, ci, vp, vp],
+        "gp_kmvm_host": [vp, vp, ci, vp, vp],
+        "gp_kzx_setup": [vp, vp, i64, vp, ctypes.POINTER(vp)],
+        "gp_kzx": [vp, vp, ci, vp, vp],
+        "gp_cg_solve": [vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, ctypes.POINTER(_CGInfo), vp],
+        "gp_predict": [vp, vp, i64, vp, vp, vp, ci, vp, vp],
+        "gp_plan_query": [vp, ci, ctypes.POINTER(i64)],
+        "gp_plan_set_option": [vp, ci, i64],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.gp_destroy.argtypes = [vp]; lib.gp_destroy.restype = None
+    lib.gp_kzx_destroy.argtypes = [vp]; lib.gp_kzx_destroy.restype = None
+    lib.gp_last_error.argtypes = []; lib.gp_last_error.restype = ctypes.c_char_p
+    lib.gp_version.argtypes = []; lib.gp_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise GPError(st, _lib.gp_last_error().decode())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t, name, shape=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise TypeError(f"{name} must be a CUDA float64 tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass(frozen=True)
+class Kernel:
+    """Matern kernel nu = two_nu/2 with outputscale s and per-dimension lengthscales."""
+    two_nu: int = 3
+    lengthscale: tuple = (1.0,)
+    outputscale: float = 1.0
+    form: int = FORM_L1
+
+    def c(self) -> _Kernel:
+        ell = list(self.lengthscale) + [1.0] * (3 - len(self.lengthscale))
+        return _Kernel(self.two_nu, self.form, float(self.outputscale),
+                       (ctypes.c_double * 3)(*[float(e) for e in ell[:3]]))
+
+
+class Plan:
+    """Stored structure of x (gp_setup); owns device memory until closed."""
+
+    def __init__(self, x, kernel: Kernel, stream=None):
+        lib = load_library()
+        if x.dim() == 1:
+            x = x.reshape(-1, 1)
+        n, d = x.shape
+        self.n, self.d, self.kernel = int(n), int(d), kernel
+        self._x = x
+        h = ctypes.c_void_p()
+        k = kernel.c()
+        _check(lib.gp_setup(_dev(x, "x"), n, d, ctypes.byref(k), _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    def query(self, what: int) -> int:
+        v = ctypes.c_int64()
+        _check(_lib.gp_plan_query(self._h, what, ctypes.byref(v)))
+        return v.value
+
+    @property
+    def levels(self): return self.query(2)
+    @property
+    def struct_bytes(self): return self.query(3)
+    @property
+    def launches_per_apply(self): return self.query(4)
+    @property
+    def model_bytes(self): return self.query(5)
+    @property
+    def d1_path(self): return self.query(6)
+
+    def set_option(self, option: int, value: int):
+        _check(_lib.gp_plan_set_option(self._h, option, value))
+
+    def kmvm(self, v, out=None, stream=None):
+        """out = K v for v of shape (n,) or (nrhs, n) (each row one right-hand side)."""
+        import torch
+        nrhs = 1 if v.dim() == 1 else v.shape[0]
+        if v.shape[-1] != self.n:
+            raise ValueError("v has the wrong length")
+        if out is None:
+            out = torch.empty_like(v)
+        _check(_lib.gp_kmvm(self._h, _dev(v, "v"), nrhs, _dev(out, "out", v.shape), _stream(stream)))
+        return out
+
+    def kmvm_host(self, v_host, out_host, stream=None):
+        """End-to-end K v on host (numpy / pinned torch CPU) buffers."""
+        import numpy as np
+        nrhs = 1 if v_host.ndim == 1 else v_host.shape[0]
+        vp = ctypes.c_void_p(v_host.ctypes.data if isinstance(v_host, np.ndarray) else v_host.data_ptr())
+        op = ctypes.c_void_p(out_host.ctypes.data if isinstance(out_host, np.ndarray) else out_host.data_ptr())
+        _check(_lib.gp_kmvm_host(self._h, vp, nrhs, op, _stream(stream)))
+        return out_host
+
+    def cross(self, z, stream=None) -> "Cross":
+        return Cross(self, z, stream)
+
+    def cg_solve(self, y, sigma2: float, mean: int = MEAN_AFFINE, H=None, rtol: float = 1e-8,
+                 max_iter: int = 20000, stream=None):
+        """alpha, beta, info of (K + sigma^2 I) CG with GLS fixed effects (gp_cg_solve)."""
+        import torch
+        alpha = torch.empty(self.n, dtype=torch.float64, device=y.device)
+        nb = 1 + self.d if mean == MEAN_AFFINE else (H.shape[0] if mean == MEAN_BASIS else 0)
+        beta = (ctypes.c_double * max(nb, 1))()
+        info = _CGInfo()
+        Hp = _dev(H, "H") if mean == MEAN_BASIS else ctypes.c_void_p(0)
+        L = H.shape[0] if mean == MEAN_BASIS else 0
+        st = _lib.gp_cg_solve(self._h, float(sigma2), _dev(y, "y", (self.n,)), mean, Hp, L,
+                              float(rtol), int(max_iter), _dev(alpha, "alpha"), beta,
+                              ctypes.byref(info), _stream(stream))
+        res = {"iters": info.iters, "relres_max": info.relres_max,
+               "failed_column": info.failed_column, "restarts": info.restarts}
+        if st != 0:
+            err = GPError(st, _lib.gp_last_error().decode())
+            err.info = res
+            err.alpha = alpha
+            raise err
+        return alpha, [beta[i] for i in range(nb)], res
+
+    def predict(self, z, alpha, beta=None, Hz=None, stream=None):
+        import torch
+        m = z.shape[0]
+        out = torch.empty(m, dtype=torch.float64, device=z.device)
+        bp = None
+        if beta is not None:
+            bp = (ctypes.c_double * len(beta))(*beta)
+        L = Hz.shape[0] if Hz is not None else 0
+        _check(_lib.gp_predict(self._h, _dev(z, "z"), m, _dev(alpha, "alpha", (self.n,)), bp,
+                               _dev(Hz, "Hz") if Hz is not None else None, L,
+                               _dev(out, "out"), _stream(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.gp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Cross:
+    """Structure of x U z for repeated K_zx v (gp_kzx_setup / gp_kzx)."""
+
+    def __init__(self, plan: Plan, z, stream=None):
+        if z.dim() == 1:
+            z = z.reshape(-1, 1)
+        self.plan, self.m = plan, int(z.shape[0])
+        h = ctypes.c_void_p()
+        _check(_lib.gp_kzx_setup(plan._h, _dev(z, "z"), self.m, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    def kzx(self, v, out=None, stream=None):
+        import torch
+        nrhs = 1 if v.dim() == 1 else v.shape[0]
+        shape = (self.m,) if v.dim() == 1 else (nrhs, self.m)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float64, device=v.device)
+        _check(_lib.gp_kzx(self._h, _dev(v, "v"), nrhs, _dev(out, "out", shape), _stream(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.gp_kzx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def setup(x, kernel: Kernel, stream=None) -> Plan:
+    return Plan(x, kernel, stream)
+
+
+def kmvm(plan: Plan, v, out=None, stream=None):
+    return plan.kmvm(v, out, stream)
+
+
+def cg_solve(plan: Plan, y, sigma2, **kw):
+    return plan.cg_solve(y, sigma2, **kw)
+
+
+def predict(plan: Plan, z, alpha, beta=None, Hz=None, stream=None):
+    return plan.predict(z, alpha, beta, Hz, stream)

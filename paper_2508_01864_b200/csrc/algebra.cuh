@@ -1,0 +1,145 @@
+// algebra.cuh -- the overflow-free moment algebra behind the ECDF decomposition.
+//
+// The paper writes K.v as weighted ECDFs of v with global weights
+// y_i (delta.x_i)^p exp(sqrt(2nu)/l delta.x_i)   (P:598-602 [eq matern_weights]),
+// which overflow for |t| > 709 and cancel catastrophically.  We carry the SAME sums
+// referenced at the current scan position instead (reading R5):
+//
+//   moment state   M_q = sum_{i in S} u_i s_i^q e^{-s_i},  q = 0..P,  s_i >= 0 the
+//                  distance of source i from the current position;
+//   advance by D   M'_q = e^{-D} sum_{m<=q} C(q,m) D^{q-m} M_m        (all terms >= 0)
+//   inject source  M_q += u alpha^q e^{-alpha}   (alpha = offset from a split reference)
+//   read target    e^{-beta} sum_q a_q sum_{m<=q} C(q,m) beta^{q-m} M_m
+//
+// with the profile k(s) = sum_q a_q s^q e^{-s} of nu = P + 1/2 in scaled coordinates
+// (P:1282 [eq matern_explicit]: a = [1], [1,1], [1,1,1/3]).  Advances compose,
+// S(a)S(b) = S(a+b), so (span, moments) is an associative scan monoid; this is the
+// "fast sum updating" of P:326-337 [§2.1] evaluated in a numerically safe basis.
+//
+// Product form: the state is M[m][q] = sum u alpha^m e^{-alpha} s^q e^{-s};
+// the scan advance acts on q, the split offset on m.
+#pragma once
+#include <cstdint>
+
+namespace gpm {
+
+template <int P> struct Prof;
+template <> struct Prof<0> { __host__ __device__ static constexpr double a(int) { return 1.0; } };
+template <> struct Prof<1> { __host__ __device__ static constexpr double a(int) { return 1.0; } };
+template <> struct Prof<2> {
+  __host__ __device__ static constexpr double a(int q) { return q == 2 ? (1.0 / 3.0) : 1.0; }
+};
+
+__host__ __device__ constexpr double binom(int q, int m) {
+  // q <= 2 in this library
+  return (m == 0 || m == q) ? 1.0 : (q == 2 && m == 1 ? 2.0 : 1.0);
+}
+
+// Advance a (P+1)-moment vector by D (E = e^{-D}).  In place, high q first.
+template <int P>
+__device__ __forceinline__ void advance(double* M, double D, double E) {
+  if constexpr (P == 2) {
+    const double D2 = D * D;
+    M[2] = E * fma(D2, M[0], fma(2.0 * D, M[1], M[2]));
+    M[1] = E * fma(D, M[0], M[1]);
+    M[0] = E * M[0];
+  } else if constexpr (P == 1) {
+    M[1] = E * fma(D, M[0], M[1]);
+    M[0] = E * M[0];
+  } else {
+    M[0] = E * M[0];
+  }
+}
+
+// out = S(D) A + B  (elementwise on P+1 moments)
+template <int P>
+__device__ __forceinline__ void advance_add(double* A, double D, double E, const double* B) {
+  advance<P>(A, D, E);
+#pragma unroll
+  for (int q = 0; q <= P; ++q) A[q] += B[q];
+}
+
+// sum_q a_q sum_{m<=q} C(q,m) beta^{q-m} R_m   (without the e^{-beta} factor)
+template <int P>
+__device__ __forceinline__ double read_poly(const double* R, double beta) {
+  if constexpr (P == 2) {
+    // a0 R0 + a1 (R1 + b R0) + a2 (R2 + 2 b R1 + b^2 R0)
+    const double b = beta;
+    return R[0] + (R[1] + b * R[0]) + (1.0 / 3.0) * fma(b * b, R[0], fma(2.0 * b, R[1], R[2]));
+  } else if constexpr (P == 1) {
+    return R[0] + fma(beta, R[0], R[1]);
+  } else {
+    return R[0];
+  }
+}
+
+// sum_q a_q R_q  (beta = 0)
+template <int P>
+__device__ __forceinline__ double read0(const double* R) {
+  if constexpr (P == 2) return R[0] + R[1] + (1.0 / 3.0) * R[2];
+  else if constexpr (P == 1) return R[0] + R[1];
+  else return R[0];
+}
+
+// ---------------------------------------------------------------------------
+// Multi-channel algebra for the d >= 2 level passes.
+//   NCH channels (2 for d = 2: side of the x1 split; 4 for d = 3: sides of the x1 and
+//   inner x2 splits).  A source on channel c feeds targets on channel NCH-1-c.
+//   NM moments per channel: P+1 (L1) or (P+1)^2 (product, d = 2).
+template <int P_, int NCH_, bool PROD_>
+struct Alg {
+  static constexpr int P = P_;
+  static constexpr int NCH = NCH_;
+  static constexpr bool PROD = PROD_;
+  static constexpr int NQ = P + 1;
+  static constexpr int NM = PROD ? NQ * NQ : NQ;
+  static constexpr int NS = NCH * NM;
+
+  __device__ __forceinline__ static void advance_all(double* M, double D, double E) {
+#pragma unroll
+    for (int r = 0; r < NS / NQ; ++r) advance<P>(M + r * NQ, D, E);
+  }
+
+  // M[c] += injection of u at split offset alpha (ea = e^{-alpha})
+  __device__ __forceinline__ static void inject(double* M, int c, double u, double alpha,
+                                                double ea) {
+    const double w = u * ea;
+#pragma unroll
+    for (int cc = 0; cc < NCH; ++cc) {
+      if (cc == c) {
+        if constexpr (!PROD) {
+          double pw = w;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) { M[cc * NM + q] += pw; pw *= alpha; }
+        } else {
+          double pw = w;
+#pragma unroll
+          for (int m = 0; m < NQ; ++m) { M[cc * NM + m * NQ + 0] += pw; pw *= alpha; }
+        }
+      }
+    }
+  }
+
+  // value contributed to a target on channel rc at split offset beta (eb = e^{-beta})
+  __device__ __forceinline__ static double read(const double* M, int rc, double beta,
+                                                double eb) {
+    double v = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < NCH; ++cc) {
+      if (cc == rc) {
+        if constexpr (!PROD) {
+          v = read_poly<P>(M + cc * NM, beta);
+        } else {
+          // k(alpha+beta) k(s): e^{-beta} sum_a a_a sum_{m<=a} C(a,m) beta^{a-m} (sum_q a_q M[m][q])
+          double G[NQ];
+#pragma unroll
+          for (int m = 0; m < NQ; ++m) G[m] = read0<P>(M + cc * NM + m * NQ);
+          v = read_poly<P>(G, beta);
+        }
+      }
+    }
+    return eb * v;
+  }
+};
+
+}  // namespace gpm

@@ -1,0 +1,218 @@
+// api.cu -- the C ABI of include/gpmatern.h.  Argument validation, error strings and
+// plan lifetime; every compute step is a kernel in setup.cu / apply*.cu / solve.cu.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+
+namespace gpm {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+gp_status fail(gp_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+static gp_status check_kernel(const gp_kernel* k, int d) {
+  if (!k) return fail(GP_ERR_INVALID_ARG, "kernel is NULL");
+  if (d < 1 || d > 3) return fail(GP_ERR_INVALID_ARG, "d must be 1, 2 or 3");
+  if (!(k->outputscale > 0) || !std::isfinite(k->outputscale))
+    return fail(GP_ERR_INVALID_ARG, "outputscale must be > 0");
+  for (int j = 0; j < d; ++j)
+    if (!(k->lengthscale[j] > 0) || !std::isfinite(k->lengthscale[j]))
+      return fail(GP_ERR_INVALID_ARG, "lengthscale[" + std::to_string(j) + "] must be > 0");
+  if (k->two_nu != 1 && k->two_nu != 3 && k->two_nu != 5)
+    return fail(GP_ERR_UNSUPPORTED,
+                "two_nu=" + std::to_string(k->two_nu) +
+                    " unsupported; supported: two_nu in {1,3,5} x {L1 (d<=3), PRODUCT (d<=2)}");
+  if (k->form != GP_FORM_L1 && k->form != GP_FORM_PRODUCT)
+    return fail(GP_ERR_INVALID_ARG, "form must be GP_FORM_L1 or GP_FORM_PRODUCT");
+  if (k->form == GP_FORM_PRODUCT && d == 3 && k->two_nu != 1)
+    return fail(GP_ERR_UNSUPPORTED,
+                "PRODUCT form for d=3 and nu>1/2 is not implemented; supported: two_nu in "
+                "{1,3,5} x {L1 (d<=3), PRODUCT (d<=2)}");
+  return GP_OK;
+}
+
+static gp_status check_device() {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    (void)cudaGetLastError();
+    return fail(GP_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e) +
+                                 " (there is no CPU fallback)");
+  }
+  return GP_OK;
+}
+
+}  // namespace gpm
+
+using namespace gpm;
+
+extern "C" {
+
+const char* gp_last_error(void) { return g_err.c_str(); }
+const char* gp_version(void) { return "gpmatern 0.1 sm_100a"; }
+
+gp_status gp_setup(const double* x, int64_t n, int d, const gp_kernel* k, void* stream,
+                   gp_plan* out) {
+  if (!out) return fail(GP_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!x) return fail(GP_ERR_INVALID_ARG, "x is NULL");
+  if (n < 1) return fail(GP_ERR_INVALID_ARG, "n must be >= 1");
+  if (n > (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n > 2^30 not supported");
+  GPM_TRY(check_kernel(k, d));
+  GPM_TRY(check_device());
+  gp_plan p = new (std::nothrow) gp_plan_s();
+  if (!p) return fail(GP_ERR_OOM, "host allocation failed");
+  gp_status st = plan_build(p->pl, x, n, d, *k, static_cast<cudaStream_t>(stream));
+  if (st != GP_OK) {
+    plan_free(p->pl);
+    delete p;
+    return st;
+  }
+  *out = p;
+  return GP_OK;
+}
+
+gp_status gp_kmvm(gp_plan p, const double* v, int nrhs, double* out, void* stream) {
+  if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  if (v == out) return fail(GP_ERR_INVALID_ARG, "out must not alias v");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int c = 0; c < nrhs; ++c)
+    GPM_TRY(apply_user(p->pl, v + (size_t)c * p->pl.n, out + (size_t)c * p->pl.n, s));
+  return GP_OK;
+}
+
+gp_status gp_kmvm_host(gp_plan p, const double* v, int nrhs, double* out, void* stream) {
+  if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  Plan& pl = p->pl;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(double) * pl.n * nrhs;
+  if (pl.stage_in.bytes < bytes) GPM_TRY(pl.stage_in.alloc(bytes));
+  if (pl.stage_out.bytes < bytes) GPM_TRY(pl.stage_out.alloc(bytes));
+  GPM_CUDA(cudaMemcpyAsync(pl.stage_in.ptr, v, bytes, cudaMemcpyHostToDevice, s));
+  GPM_TRY(gp_kmvm(p, pl.stage_in.as<double>(), nrhs, pl.stage_out.as<double>(), stream));
+  GPM_CUDA(cudaMemcpyAsync(out, pl.stage_out.ptr, bytes, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return GP_OK;
+}
+
+gp_status gp_kzx_setup(gp_plan p, const double* z, int64_t m, void* stream, gp_cross* out) {
+  if (!out) return fail(GP_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!p || !z) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (m < 1) return fail(GP_ERR_INVALID_ARG, "m must be >= 1");
+  Plan& pl = p->pl;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nu = pl.n + m;
+  if (nu > (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n + m > 2^30 not supported");
+  DevBuf xu;
+  GPM_TRY(xu.alloc(sizeof(double) * nu * pl.d));
+  GPM_CUDA(cudaMemcpyAsync(xu.ptr, pl.x_raw.ptr, sizeof(double) * pl.n * pl.d,
+                           cudaMemcpyDeviceToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(xu.as<double>() + pl.n * pl.d, z, sizeof(double) * m * pl.d,
+                           cudaMemcpyDeviceToDevice, s));
+  gp_cross c = new (std::nothrow) gp_cross_s();
+  if (!c) return fail(GP_ERR_OOM, "host allocation failed");
+  gp_status st = plan_build(c->pl, xu.as<double>(), nu, pl.d, pl.kern, s);
+  xu.release();
+  if (st != GP_OK) {
+    plan_free(c->pl);
+    delete c;
+    return st == GP_ERR_NONFINITE ? fail(st, std::string("query points: ") + gp_last_error())
+                                  : st;
+  }
+  c->pl.n_src = pl.n;     // sources: the data points
+  c->pl.tgt_off = pl.n;   // targets: the queries
+  c->n = pl.n;
+  c->m = m;
+  *out = c;
+  return GP_OK;
+}
+
+gp_status gp_kzx(gp_cross c, const double* v, int nrhs, double* out, void* stream) {
+  if (!c || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int j = 0; j < nrhs; ++j)
+    GPM_TRY(apply_user(c->pl, v + (size_t)j * c->n, out + (size_t)j * c->m, s));
+  return GP_OK;
+}
+
+void gp_kzx_destroy(gp_cross c) {
+  if (!c) return;
+  plan_free(c->pl);
+  delete c;
+}
+
+gp_status gp_cg_solve(gp_plan p, double sigma2, const double* y, int mean_kind,
+                      const double* H, int L, double rtol, int max_iter, double* alpha,
+                      double* beta, gp_cg_info* info, void* stream) {
+  if (!p || !y || !alpha) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
+  if (!(rtol > 0)) return fail(GP_ERR_INVALID_ARG, "rtol must be > 0");
+  if (max_iter < 1) return fail(GP_ERR_INVALID_ARG, "max_iter must be >= 1");
+  if (mean_kind != GP_MEAN_NONE && mean_kind != GP_MEAN_AFFINE && mean_kind != GP_MEAN_BASIS)
+    return fail(GP_ERR_INVALID_ARG, "unknown mean_kind");
+  if (mean_kind == GP_MEAN_BASIS && (!H || L < 1 || L > 16))
+    return fail(GP_ERR_INVALID_ARG, "BASIS mean needs H and 1 <= L <= 16");
+  return cg_solve(p->pl, sigma2, y, mean_kind, H, L, rtol, max_iter, alpha, beta, info,
+                  static_cast<cudaStream_t>(stream));
+}
+
+gp_status gp_predict(gp_plan p, const double* z, int64_t m, const double* alpha,
+                     const double* beta, const double* Hz, int L, double* out, void* stream) {
+  if (!p || !z || !alpha || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (Hz && (L < 1 || !beta)) return fail(GP_ERR_INVALID_ARG, "basis mean needs beta and L >= 1");
+  gp_cross c = nullptr;
+  GPM_TRY(gp_kzx_setup(p, z, m, stream, &c));
+  gp_status st = gp_kzx(c, alpha, 1, out, stream);
+  if (st == GP_OK && beta)
+    st = launch_affine_epilogue(z, m, p->pl.d, beta, Hz, L, out,
+                                static_cast<cudaStream_t>(stream));
+  if (st == GP_OK) {
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) st = fail(GP_ERR_CUDA, cudaGetErrorString(e));
+  }
+  gp_kzx_destroy(c);
+  return st;
+}
+
+gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
+  if (!p || !value) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  const Plan& pl = p->pl;
+  switch (what) {
+    case 0: *value = pl.n; break;
+    case 1: *value = pl.d; break;
+    case 2: *value = pl.L; break;
+    case 3: *value = pl.struct_bytes; break;
+    case 4: *value = pl.launches_per_apply; break;
+    case 5: *value = apply_model_bytes(pl); break;
+    case 6: *value = pl.d == 1 ? pl.d1_path : 0; break;
+    default: return fail(GP_ERR_INVALID_ARG, "unknown query");
+  }
+  return GP_OK;
+}
+
+gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
+  if (!p) return fail(GP_ERR_INVALID_ARG, "NULL plan");
+  if (option != 0 || value < 0 || value > 2) return fail(GP_ERR_INVALID_ARG, "bad option");
+  if (p->pl.d != 1) return GP_OK;
+  p->pl.d1_force = (int)value;
+  return apply_prepare(p->pl);
+}
+
+void gp_destroy(gp_plan p) {
+  if (!p) return;
+  plan_free(p->pl);
+  delete p;
+}
+
+}  // extern "C"

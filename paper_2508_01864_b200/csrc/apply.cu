@@ -1,0 +1,98 @@
+// apply.cu -- orchestration of one K.v (or K_zx.v) apply on a stored plan:
+//   d = 1 : one cooperative launch (apply_d1.cu) with the gather / scatter fused in;
+//   d >= 2: gather u[r] = v[perm[r]] -> level passes (apply_level.cu) into acc ->
+//           epilogue out[perm[r]] = s^2 (u[r] + acc[r])  (self term + scale, a7).
+#include <algorithm>
+
+#include "internal.h"
+
+namespace gpm {
+
+gp_status d1_prepare(Plan& pl);
+gp_status d1_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s);
+gp_status level_passes(Plan& pl, const double* u_rank, cudaStream_t s, int* launches);
+int64_t level_tiles(int64_t n);
+
+namespace {
+
+__global__ void k_gather(const int* __restrict__ perm, const double* __restrict__ v, int64_t n,
+                         int64_t n_src, double* __restrict__ u) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int i = __ldg(perm + r);
+    u[r] = i < n_src ? __ldg(v + i) : 0.0;
+  }
+}
+
+// out[perm[r] - tgt_off] = os2 (u[r] + acc[r]) for targets; perm == nullptr: rank order
+__global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ u,
+                           const double* __restrict__ acc, int64_t n, int64_t tgt_off,
+                           double os2, double* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double val = os2 * (u[r] + acc[r]);
+    if (perm) {
+      const int i = __ldg(perm + r);
+      if (i >= tgt_off) out[i - tgt_off] = val;
+    } else {
+      out[r] = val;
+    }
+  }
+}
+
+inline int egrid(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+}
+
+}  // namespace
+
+gp_status apply_prepare(Plan& pl) {
+  const int64_t n = pl.n;
+  if (pl.d == 1) {
+    GPM_TRY(d1_prepare(pl));
+    pl.launches_per_apply = 1;
+  } else {
+    GPM_TRY(pl.u.alloc(sizeof(double) * n));
+    GPM_TRY(pl.acc.alloc(sizeof(double) * n));
+    GPM_TRY(pl.aggs.alloc(sizeof(LvAgg) * 2 * (size_t)level_tiles(n)));
+  }
+  GPM_TRY(pl.w.alloc(sizeof(double) * n));
+  return GP_OK;
+}
+
+static gp_status apply_levels(Plan& pl, const double* u_rank, double* out, bool user_order,
+                              cudaStream_t s) {
+  int launches = 0;
+  GPM_CUDA(cudaMemsetAsync(pl.acc.ptr, 0, sizeof(double) * pl.n, s));
+  GPM_TRY(level_passes(pl, u_rank, s, &launches));
+  k_epilogue<<<egrid(pl.n), 256, 0, s>>>(user_order ? pl.perm.as<int>() : nullptr, u_rank,
+                                         pl.acc.as<double>(), pl.n,
+                                         user_order ? pl.tgt_off : 0, pl.os2, out);
+  GPM_CUDA(cudaGetLastError());
+  pl.launches_per_apply = launches + 2 + (user_order ? 1 : 0);  // + memset-free count below
+  return GP_OK;
+}
+
+gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, cudaStream_t s) {
+  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, false, s);
+  return apply_levels(pl, u_rank, out_rank, false, s);
+}
+
+gp_status apply_user(Plan& pl, const double* v, double* out, cudaStream_t s) {
+  if (pl.d == 1) return d1_launch(pl, v, out, true, s);
+  k_gather<<<egrid(pl.n), 256, 0, s>>>(pl.perm.as<int>(), v, pl.n, pl.n_src, pl.u.as<double>());
+  GPM_CUDA(cudaGetLastError());
+  return apply_levels(pl, pl.u.as<double>(), out, true, s);
+}
+
+// Algorithmic HBM bytes of one single-RHS user-order apply:
+// the stored structure is read once and v / out are touched once.
+int64_t apply_model_bytes(const Plan& pl) {
+  const int64_t n = pl.n;
+  const int64_t L = pl.L;
+  if (pl.d == 1) return n * (8 + 4 + 8 + 8);
+  if (pl.d == 2) return n * (8 + 4 + 8 + 16 + 4 * L);
+  return n * (8 + 4 + 8 + 24 + 4 * L + 2 * L * (L + 1));
+}
+
+}  // namespace gpm

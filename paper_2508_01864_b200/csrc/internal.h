@@ -1,0 +1,112 @@
+// internal.h -- plan layout in HBM and internal entry points of libgpmatern.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/gpmatern.h"
+
+namespace gpm {
+
+// Error plumbing ------------------------------------------------------------
+void set_error(const std::string& msg);
+gp_status fail(gp_status st, const std::string& msg);
+#define GPM_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return ::gpm::fail(GP_ERR_CUDA, std::string(#call " failed: ") + cudaGetErrorString(_e) + \
+                                          " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+#define GPM_TRY(expr)                 \
+  do {                                \
+    gp_status _s = (expr);            \
+    if (_s != GP_OK) return _s;       \
+  } while (0)
+
+// Device buffer owned by a plan.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  gp_status alloc(size_t b);
+  void release();
+  template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+// d = 1 tile-aggregate record (both scan directions), P <= 2.
+struct D1Agg {
+  double D, E;      // span and e^{-span}
+  double F[3];      // forward moments of the segment's sources, referenced at its last point
+  double B[3];      // backward moments, referenced one point before its first point
+};
+
+// Level-pass tile aggregate (one direction), up to 4 channels x 4 moments.
+struct LvAgg {
+  double D, E;
+  double M[18];
+  int flag;
+  int pad;
+};
+
+// The stored structure of P:191 [§1], P:338 [§2.1], P:539 [§2.2.3], in HBM.
+//   "rank" = x1-rank: position of a point in the stable (t1, index) order.
+struct Plan {
+  int64_t n = 0;
+  int d = 0, two_nu = 1, P = 0, form = 0;
+  gp_kernel kern{};                 // kernel as given to gp_setup
+  double os2 = 1.0;                 // outputscale^2
+  double ell[3] = {1, 1, 1};
+  double scale[3] = {1, 1, 1};      // sqrt(2 nu) / l_k
+  int L = 0;                        // levels: ceil(log2 n)
+  int64_t n_src = 0;                // sources are user indices < n_src (== n except unions)
+  int64_t tgt_off = 0;              // targets are user indices >= tgt_off (0 except unions)
+
+  DevBuf x_raw;                     // n x d row-major copy of the input (for unions / H)
+  DevBuf perm;                      // int32 [n]: perm[r] = user index of rank r
+  DevBuf t;                         // double [d][n]: t_k in rank order (SoA)
+  DevBuf ord2;                      // int32 [L][n]: d>=2, level l order (ranks), t2-sorted per node
+  DevBuf ord3;                      // int32 [L(L+1)/2][n]: d=3, positions into ord2[l1], t3-sorted
+  // scratch (apply)
+  DevBuf u;                         // double [n]: input in rank order
+  DevBuf acc;                       // double [n]: level-pass accumulator (rank order)
+  DevBuf w;                         // double [n]: rank-order output scratch
+  DevBuf aggs;                      // tile aggregates
+  DevBuf bar;                       // grid barrier words (d = 1 cooperative kernel)
+  DevBuf stage_in, stage_out;       // gp_kmvm_host staging
+  // d = 1 launch geometry
+  int d1_grid = 0, d1_path = 1, d1_force = 0;
+  int64_t d1_chunk = 0;
+  int64_t struct_bytes = 0;
+  int launches_per_apply = 0;
+};
+
+// setup.cu
+gp_status plan_build(Plan& pl, const double* x_dev, int64_t n, int d, const gp_kernel& k,
+                     cudaStream_t s);
+void plan_free(Plan& pl);
+
+// apply.cu
+// Rank-space apply: out_rank = K u_rank (no nugget).  u_rank, out_rank: n doubles.
+gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, cudaStream_t s);
+// User-order apply with gather/scatter: out = K v restricted to targets (unions).
+gp_status apply_user(Plan& pl, const double* v, double* out, cudaStream_t s);
+gp_status apply_prepare(Plan& pl);   // launch geometry + scratch
+int64_t apply_model_bytes(const Plan& pl);
+
+// solve.cu
+gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,
+                   int Lb, double rtol, int max_iter, double* alpha, double* beta,
+                   gp_cg_info* info, cudaStream_t s);
+gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
+                                 const double* Hz, int Lb, double* out, cudaStream_t s);
+
+}  // namespace gpm
+
+struct gp_plan_s {
+  gpm::Plan pl;
+};
+struct gp_cross_s {
+  gpm::Plan pl;        // structure of the union x U z
+  int64_t n = 0, m = 0;
+};

@@ -1,0 +1,456 @@
+// solve.cu -- a9/a10: multi-RHS conjugate gradients on A = K + sigma^2 I and the GLS
+// fixed-effects correction.
+//   CG: P:155-174 [§1] ("the core computational step in each conjugate-gradient
+//   iteration is the multiplication of K with a vector"), P:980-1034 [App A, Alg 2]
+//   with s_P = identity (no preconditioner, reading R8) and a zero initial guess.
+//   Per column j: alpha_j = r_j^T r_j / p_j^T A p_j, x += alpha p, r -= alpha A p,
+//   beta_j = r'^T r' / r^T r, p = r' + beta p  (Alg 2 loop body).
+//   Stop per column at ||r_j|| <= rtol ||b_j|| (reading R8: per-column relative 2-norm,
+//   not Alg 2's aggregated ||R||^2 < tol); the TRUE residual b - A x is re-evaluated at
+//   exit and CG restarts from it if recursion drift left it above rtol.
+//   Breakdown p^T A p <= 0 (A not SPD, reading R4) is reported, never hidden.
+//   GLS: beta = (H^T A^-1 H)^-1 H^T A^-1 y; alpha = A^-1 y - (A^-1 H) beta.
+// All vectors live in x1-rank order so no permutation is applied inside the loop;
+// every reduction is a fixed-order two-stage tree (deterministic, no atomics).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace gpm {
+
+namespace {
+
+constexpr int CG_BLOCK = 256;
+constexpr int CG_GRID = 296;   // 2 x 148 SMs; reduction partials per column
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+  }
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// q_c += sigma2 p_c ; partial[c][block] = sum p_c . q_c     (grid.y = column)
+__global__ void k_pq(const double* __restrict__ P, double* __restrict__ Q, int64_t n,
+                     double sigma2, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  const double* p = P + (size_t)c * n;
+  double* q = Q + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double pv = p[i];
+    const double qv = fma(sigma2, pv, q[i]);
+    q[i] = qv;
+    acc = fma(pv, qv, acc);
+  }
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+
+// alpha_c = rr_c / pq_c (status 0 only); breakdown detection
+__global__ void k_alpha(const double* __restrict__ part, int nb, const double* __restrict__ rr,
+                        double* __restrict__ alpha, int* __restrict__ status,
+                        int* __restrict__ bd_iter, int iter) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(size_t)c * nb + b];
+  const double pq = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    if (status[c] == 0) {
+      if (!(pq > 0.0) || !isfinite(pq)) {
+        status[c] = 2;
+        bd_iter[c] = iter;
+      } else {
+        a = rr[c] / pq;
+      }
+    }
+    alpha[c] = a;
+  }
+}
+
+// x += alpha p ; r -= alpha q ; partial rr
+__global__ void k_update(double* __restrict__ X, double* __restrict__ R,
+                         const double* __restrict__ P, const double* __restrict__ Q,
+                         const double* __restrict__ alpha, int64_t n, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  const double a = alpha[c];
+  double* x = X + (size_t)c * n;
+  double* r = R + (size_t)c * n;
+  const double* p = P + (size_t)c * n;
+  const double* q = Q + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    const double rv = fma(-a, q[i], r[i]);
+    r[i] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+
+// beta_c = rr_new / rr ; convergence test against tol2_c = (rtol ||b_c||)^2
+__global__ void k_beta(const double* __restrict__ part, int nb, double* __restrict__ rr,
+                       const double* __restrict__ tol2, double* __restrict__ beta,
+                       int* __restrict__ status) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(size_t)c * nb + b];
+  const double rn = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    double bt = 0.0;
+    if (status[c] == 0) {
+      bt = rn / rr[c];
+      rr[c] = rn;
+      if (rn <= tol2[c]) status[c] = 1;
+    }
+    beta[c] = bt;
+  }
+}
+
+// p = r + beta p   (active columns)
+__global__ void k_pupd(double* __restrict__ P, const double* __restrict__ R,
+                       const double* __restrict__ beta, const int* __restrict__ status,
+                       int64_t n) {
+  const int c = blockIdx.y;
+  if (status[c] != 0) return;
+  const double b = beta[c];
+  double* p = P + (size_t)c * n;
+  const double* r = R + (size_t)c * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], r[i]);
+}
+
+// partial sums of squares of columns (grid.y = column)
+__global__ void k_sumsq(const double* __restrict__ V, int64_t n, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  const double* v = V + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc = fma(v[i], v[i], acc);
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+
+__global__ void k_finish_sum(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(size_t)c * nb + b];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) out[c] = t;
+}
+
+// R = B - (Q + sigma2 X)   (Q = K X)
+__global__ void k_resid(const double* __restrict__ B, const double* __restrict__ Q,
+                        const double* __restrict__ X, double sigma2, int64_t nk,
+                        double* __restrict__ R) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk;
+       i += (int64_t)gridDim.x * blockDim.x)
+    R[i] = B[i] - fma(sigma2, X[i], Q[i]);
+}
+
+// B columns in rank order: col 0 = y[perm], cols 1.. = H (affine from x_raw, or basis)
+__global__ void k_build_rhs(const int* __restrict__ perm, const double* __restrict__ y,
+                            const double* __restrict__ xraw, int d, const double* __restrict__ H,
+                            int nh, int mean_kind, int64_t n, double* __restrict__ B) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int i = perm[r];
+    B[r] = y[i];
+    if (mean_kind == GP_MEAN_AFFINE) {
+      B[n + r] = 1.0;
+      for (int k = 0; k < d; ++k) B[(size_t)(2 + k) * n + r] = xraw[(size_t)i * d + k];
+    } else if (mean_kind == GP_MEAN_BASIS) {
+      for (int c = 0; c < nh; ++c) B[(size_t)(1 + c) * n + r] = H[(size_t)c * n + i];
+    }
+  }
+}
+
+// GLS partials: G[a][b] = sum_r H_a X_{1+b}, g[a] = sum_r H_a X_0   (grid.y = a*(nh+1)+b)
+__global__ void k_gls_part(const double* __restrict__ B, const double* __restrict__ X, int nh,
+                           int64_t n, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int ab = blockIdx.y;
+  const int a = ab / (nh + 1), b = ab % (nh + 1);
+  const double* h = B + (size_t)(1 + a) * n;
+  const double* x = X + (size_t)(b == nh ? 0 : 1 + b) * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc = fma(h[i], x[i], acc);
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)ab * gridDim.x + blockIdx.x] = t;
+}
+
+// alpha[perm[r]] = X0[r] - sum_a X_{1+a}[r] beta_a
+__global__ void k_alpha_out(const int* __restrict__ perm, const double* __restrict__ X, int nh,
+                            double b0, double b1, double b2, double b3, const double* __restrict__ bdev,
+                            int64_t n, double* __restrict__ alpha) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double v = X[r];
+    for (int a = 0; a < nh; ++a) {
+      const double ba = a == 0 ? b0 : a == 1 ? b1 : a == 2 ? b2 : a == 3 ? b3 : bdev[a];
+      v -= X[(size_t)(1 + a) * n + r] * ba;
+    }
+    alpha[perm[r]] = v;
+  }
+}
+
+// out[q] += h(z_q)^T beta  (affine: h = [1, z]; basis: Hz m x L col-major)
+__global__ void k_mean_epi(const double* __restrict__ z, int64_t m, int d,
+                           const double* __restrict__ Hz, int Lb, const double* __restrict__ bdev,
+                           double* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (Hz) {
+      for (int a = 0; a < Lb; ++a) v += Hz[(size_t)a * m + q] * bdev[a];
+    } else {
+      v = bdev[0];
+      for (int k = 0; k < d; ++k) v += z[(size_t)q * d + k] * bdev[1 + k];
+    }
+    out[q] += v;
+  }
+}
+
+inline int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
+
+// small dense SPD solve (Gaussian elimination with partial pivoting), host
+bool small_solve(std::vector<double> G, std::vector<double> g, int k, std::vector<double>& x) {
+  for (int c = 0; c < k; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < k; ++r)
+      if (std::fabs(G[r * k + c]) > std::fabs(G[piv * k + c])) piv = r;
+    if (G[piv * k + c] == 0.0) return false;
+    if (piv != c) {
+      for (int j = 0; j < k; ++j) std::swap(G[c * k + j], G[piv * k + j]);
+      std::swap(g[c], g[piv]);
+    }
+    for (int r = c + 1; r < k; ++r) {
+      const double f = G[r * k + c] / G[c * k + c];
+      for (int j = c; j < k; ++j) G[r * k + j] -= f * G[c * k + j];
+      g[r] -= f * g[c];
+    }
+  }
+  x.assign(k, 0.0);
+  for (int c = k - 1; c >= 0; --c) {
+    double s = g[c];
+    for (int j = c + 1; j < k; ++j) s -= G[c * k + j] * x[j];
+    x[c] = s / G[c * k + c];
+  }
+  return true;
+}
+
+}  // namespace
+
+gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
+                                 const double* Hz, int Lb, double* out, cudaStream_t s) {
+  const int nb = Hz ? Lb : 1 + d;
+  DevBuf bd;
+  GPM_TRY(bd.alloc(sizeof(double) * nb));
+  GPM_CUDA(cudaMemcpyAsync(bd.ptr, beta_host, sizeof(double) * nb, cudaMemcpyHostToDevice, s));
+  k_mean_epi<<<g1(m), 256, 0, s>>>(z, m, d, Hz, Lb, bd.as<double>(), out);
+  GPM_CUDA(cudaGetLastError());
+  GPM_CUDA(cudaStreamSynchronize(s));
+  bd.release();
+  return GP_OK;
+}
+
+gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,
+                   int Lb, double rtol, int max_iter, double* alpha, double* beta,
+                   gp_cg_info* info, cudaStream_t s) {
+  const int64_t n = pl.n;
+  const int nh = mean_kind == GP_MEAN_AFFINE ? 1 + pl.d : mean_kind == GP_MEAN_BASIS ? Lb : 0;
+  const int k = 1 + nh;
+  const size_t nk = (size_t)n * k;
+  DevBuf bB, bX, bR, bP, bQ, bpart, bsc;
+  struct Guard {
+    DevBuf* b[7];
+    ~Guard() { for (auto* x : b) x->release(); }
+  } guard{{&bB, &bX, &bR, &bP, &bQ, &bpart, &bsc}};
+  GPM_TRY(bB.alloc(8 * nk));
+  GPM_TRY(bX.alloc(8 * nk));
+  GPM_TRY(bR.alloc(8 * nk));
+  GPM_TRY(bP.alloc(8 * nk));
+  GPM_TRY(bQ.alloc(8 * nk));
+  const int npart = std::max(k, (nh + 1) * nh);
+  GPM_TRY(bpart.alloc(8 * (size_t)CG_GRID * npart));
+  // device scalars: rr[k] tol2[k] alpha[k] beta[k] bnorm2[k] | status[k] bd_iter[k]
+  GPM_TRY(bsc.alloc(8 * 5 * k + 4 * 2 * k + 64));
+  double* B = bB.as<double>();
+  double* X = bX.as<double>();
+  double* R = bR.as<double>();
+  double* Pm = bP.as<double>();
+  double* Q = bQ.as<double>();
+  double* part = bpart.as<double>();
+  double* rr = bsc.as<double>();
+  double* tol2 = rr + k;
+  double* al = tol2 + k;
+  double* be = al + k;
+  double* bn2 = be + k;
+  int* status = reinterpret_cast<int*>(bn2 + k);
+  int* bd_iter = status + k;
+
+  k_build_rhs<<<g1(n), 256, 0, s>>>(pl.perm.as<int>(), y, pl.x_raw.as<double>(), pl.d, H, nh,
+                                     mean_kind, n, B);
+  GPM_CUDA(cudaMemsetAsync(X, 0, 8 * nk, s));
+  GPM_CUDA(cudaMemcpyAsync(R, B, 8 * nk, cudaMemcpyDeviceToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(Pm, B, 8 * nk, cudaMemcpyDeviceToDevice, s));
+  k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(B, n, part);
+  k_finish_sum<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, bn2);
+  GPM_CUDA(cudaGetLastError());
+  std::vector<double> hb2(k), hrr(k), htol2(k);
+  std::vector<int> hst(k), hbd(k);
+  GPM_CUDA(cudaMemcpyAsync(hb2.data(), bn2, 8 * k, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < k; ++c) {
+    htol2[c] = rtol * rtol * hb2[c];
+    hst[c] = hb2[c] == 0.0 ? 1 : 0;   // zero right-hand side: x = 0 is exact
+  }
+  GPM_CUDA(cudaMemcpyAsync(tol2, htol2.data(), 8 * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(rr, hb2.data(), 8 * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(status, hst.data(), 4 * k, cudaMemcpyHostToDevice, s));
+
+  const int check_every = 8;
+  int it = 0, restarts = 0;
+  gp_status result = GP_OK;
+  std::vector<double> relres(k, 0.0);
+  while (true) {
+    std::vector<char> active(k, 0);
+    for (int c = 0; c < k; ++c) active[c] = hst[c] == 0;
+    bool any = false;
+    for (int c = 0; c < k; ++c) any |= active[c] != 0;
+    while (any && it < max_iter) {
+      for (int step = 0; step < check_every && it < max_iter; ++step, ++it) {
+        for (int c = 0; c < k; ++c)
+          if (active[c]) GPM_TRY(apply_rank(pl, Pm + (size_t)c * n, Q + (size_t)c * n, s));
+        k_pq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, Q, n, sigma2, part);
+        k_alpha<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, al, status, bd_iter, it);
+        k_update<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(X, R, Pm, Q, al, n, part);
+        k_beta<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, tol2, be, status);
+        k_pupd<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, R, be, status, n);
+      }
+      GPM_CUDA(cudaGetLastError());
+      GPM_CUDA(cudaMemcpyAsync(hst.data(), status, 4 * k, cudaMemcpyDeviceToHost, s));
+      GPM_CUDA(cudaStreamSynchronize(s));
+      any = false;
+      for (int c = 0; c < k; ++c) {
+        active[c] = hst[c] == 0;
+        any |= active[c] != 0;
+      }
+      for (int c = 0; c < k; ++c)
+        if (hst[c] == 2) any = false;   // stop on breakdown
+    }
+    // true residual R = B - (K X + sigma2 X)
+    for (int c = 0; c < k; ++c)
+      GPM_TRY(apply_rank(pl, X + (size_t)c * n, Q + (size_t)c * n, s));
+    k_resid<<<g1((int64_t)nk), 256, 0, s>>>(B, Q, X, sigma2, (int64_t)nk, R);
+    k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(R, n, part);
+    k_finish_sum<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr);
+    GPM_CUDA(cudaGetLastError());
+    GPM_CUDA(cudaMemcpyAsync(hrr.data(), rr, 8 * k, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaMemcpyAsync(hbd.data(), bd_iter, 4 * k, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    bool need_restart = false, broke = false;
+    int bad_col = -1;
+    for (int c = 0; c < k; ++c) {
+      relres[c] = hb2[c] > 0 ? std::sqrt(hrr[c] / hb2[c]) : 0.0;
+      if (hst[c] == 2) { broke = true; if (bad_col < 0) bad_col = c; }
+      else if (relres[c] > rtol) { need_restart = true; if (bad_col < 0) bad_col = c; }
+    }
+    if (broke) {
+      result = fail(GP_ERR_BREAKDOWN, "CG breakdown (p^T A p <= 0) in column " +
+                                          std::to_string(bad_col) + " at iteration " +
+                                          std::to_string(hbd[bad_col]) +
+                                          ": K + sigma^2 I is not positive definite");
+      break;
+    }
+    if (!need_restart) break;
+    if (it >= max_iter || restarts >= 5) {
+      result = fail(GP_ERR_NOT_CONVERGED, "CG did not reach rtol in " + std::to_string(it) +
+                                              " iterations (column " + std::to_string(bad_col) +
+                                              ", relres " + std::to_string(relres[bad_col]) + ")");
+      break;
+    }
+    // residual replacement: restart from the true residual
+    ++restarts;
+    for (int c = 0; c < k; ++c) hst[c] = relres[c] > rtol ? 0 : 1;
+    GPM_CUDA(cudaMemcpyAsync(Pm, R, 8 * nk, cudaMemcpyDeviceToDevice, s));
+    GPM_CUDA(cudaMemcpyAsync(status, hst.data(), 4 * k, cudaMemcpyHostToDevice, s));
+  }
+  if (info) {
+    info->iters = it;
+    info->restarts = restarts;
+    info->relres_max = 0.0;
+    info->failed_column = -1;
+    for (int c = 0; c < k; ++c) info->relres_max = std::max(info->relres_max, relres[c]);
+    if (result != GP_OK) {
+      for (int c = 0; c < k; ++c)
+        if (hst[c] == 2 || relres[c] > rtol) { info->failed_column = c; break; }
+    }
+  }
+  if (result == GP_ERR_BREAKDOWN) return result;
+
+  // GLS (a10) and alpha in user order
+  std::vector<double> hbeta(std::max(nh, 1), 0.0);
+  if (nh > 0) {
+    const int nab = nh * (nh + 1);
+    k_gls_part<<<dim3(CG_GRID, nab), CG_BLOCK, 0, s>>>(B, X, nh, n, part);
+    DevBuf bg;
+    GPM_TRY(bg.alloc(8 * nab));
+    k_finish_sum<<<nab, CG_BLOCK, 0, s>>>(part, CG_GRID, bg.as<double>());
+    std::vector<double> hg(nab);
+    GPM_CUDA(cudaMemcpyAsync(hg.data(), bg.ptr, 8 * nab, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    bg.release();
+    std::vector<double> G(nh * nh), g(nh);
+    for (int a = 0; a < nh; ++a) {
+      for (int b = 0; b < nh; ++b) G[a * nh + b] = hg[a * (nh + 1) + b];
+      g[a] = hg[a * (nh + 1) + nh];
+    }
+    // symmetrise (H^T A^-1 H is symmetric in exact arithmetic)
+    for (int a = 0; a < nh; ++a)
+      for (int b = a + 1; b < nh; ++b) {
+        const double m = 0.5 * (G[a * nh + b] + G[b * nh + a]);
+        G[a * nh + b] = G[b * nh + a] = m;
+      }
+    std::vector<double> sol;
+    if (!small_solve(G, g, nh, sol))
+      return fail(GP_ERR_INVALID_ARG, "GLS system H^T A^-1 H is singular (rank-deficient H)");
+    hbeta = sol;
+    if (beta) for (int a = 0; a < nh; ++a) beta[a] = sol[a];
+  }
+  DevBuf bbd;
+  GPM_TRY(bbd.alloc(8 * std::max(nh, 1)));
+  GPM_CUDA(cudaMemcpyAsync(bbd.ptr, hbeta.data(), 8 * std::max(nh, 1), cudaMemcpyHostToDevice, s));
+  auto bv = [&](int a) { return a < nh ? hbeta[a] : 0.0; };
+  k_alpha_out<<<g1(n), 256, 0, s>>>(pl.perm.as<int>(), X, nh, bv(0), bv(1), bv(2), bv(3),
+                                     bbd.as<double>(), n, alpha);
+  GPM_CUDA(cudaGetLastError());
+  GPM_CUDA(cudaStreamSynchronize(s));
+  bbd.release();
+  return result;
+}
+
+}  // namespace gpm

@@ -1,0 +1,81 @@
+"""Full-size BASELINE.json configs on the GPU, checked on seeded row samples by the
+oracle (the protocol of SURVEY.md §8(c) c1 / c2 #14-15)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_helpers import check_rows, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config2_d1_1e6(gpm):
+    c = W.CONFIGS[2]
+    x = W.config_points(c)
+    rows = W.sample_rows(x, 2048)
+    for two_nu in c.two_nu:
+        plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, c.ell))
+        assert plan.d1_path == 1     # the single-launch path bench.py times
+        for r, nrows in [(0, 2048), (99, 128)]:
+            v = W.config_vector(c, r)
+            out = plan.kmvm(to_dev(v)).cpu().numpy()
+            rr = rows if nrows == 2048 else rows[:: len(rows) // nrows][:nrows]
+            check_rows(out, x, v, two_nu, "l1", c.ell, 1.0, rows=rr, what=f"config2 nu={two_nu}/2 r={r}")
+        plan.close()
+
+
+def test_config3_d2_ties_kzx(gpm):
+    c = W.CONFIGS[3]
+    x = W.config_points(c); z = W.config_queries(c); v = W.config_vector(c, 0)
+    rows = W.sample_rows(x, 2048)
+    for form, name in [(0, "l1"), (1, "product")]:
+        plan = gpm.Plan(to_dev(x), gpm.Kernel(3, c.ell, form=form))
+        out = plan.kmvm(to_dev(v)).cpu().numpy()
+        check_rows(out, x, v, 3, name, c.ell, 1.0, rows=rows, what=f"config3 K.v {name}")
+        if form == 0:
+            cr = plan.cross(to_dev(z))
+            kz = cr.kzx(to_dev(v)).cpu().numpy()
+            check_rows(kz, x, v, 3, name, c.ell, 1.0, z=z, what="config3 K_zx (all 20000 rows)")
+            cr.close()
+        plan.close()
+
+
+def test_config4_d3_gmm(gpm):
+    c = W.CONFIGS[4]
+    x = W.config_points(c)
+    rows = W.sample_rows(x, 2048)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, c.ell))
+    for r, nrows in [(0, 2048), (49, 128)]:
+        v = W.config_vector(c, r)
+        out = plan.kmvm(to_dev(v)).cpu().numpy()
+        rr = rows if nrows == 2048 else rows[:: len(rows) // nrows][:nrows]
+        check_rows(out, x, v, 5, "l1", c.ell, 1.0, rows=rr, what=f"config4 r={r}")
+
+
+def test_config5_gp_inference(gpm):
+    c = W.CONFIGS[5]
+    x = W.config_points(c); y = W.config_response(c, x); z = W.config_queries(c)
+    s2 = c.noise_sigma ** 2
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, c.ell, form=gpm.FORM_PRODUCT))
+    alpha, beta, info = plan.cg_solve(to_dev(y), s2, mean=gpm.MEAN_AFFINE, rtol=1e-8,
+                                      max_iter=40000)
+    assert info["relres_max"] <= 1e-8
+    a = alpha.cpu().numpy()
+    H = np.hstack([np.ones((x.shape[0], 1)), x])
+    # (K + s2 I) alpha = y - H beta on 2048 sampled rows, via the oracle's own rows
+    rows = W.sample_rows(x, 2048)
+    Ka = oracle.kmvm_rows(x, a, 3, "product", c.ell, 1.0, rows=rows)
+    rvec = (y - H @ np.array(beta))[rows] - Ka - s2 * a[rows]
+    est = np.sqrt(x.shape[0] / rows.size * np.sum(rvec ** 2))
+    # the GLS residual is a combination of 4 column residuals each <= 1e-8 ||b_j||
+    bound = 1e-8 * (np.linalg.norm(y) + sum(abs(b) * np.linalg.norm(H[:, j]) for j, b in enumerate(beta)))
+    assert est <= 3 * bound, (est, bound)
+    # posterior mean at all 10^4 queries vs the oracle given the GPU's alpha and beta
+    mu = plan.predict(to_dev(z), alpha, beta).cpu().numpy()
+    ref, ab = oracle.kzx_rows(x, a, z, 3, "product", c.ell, 1.0, return_abs=True)
+    ref = ref + np.hstack([np.ones((z.shape[0], 1)), z]) @ np.array(beta)
+    assert np.max(np.abs(mu - ref)) <= 1e-9 * ab.max() * np.abs(a).max()
+    # plausibility (not parity): the fit tracks the generating function
+    f = 1 + 0.5 * z[:, 0] - 0.3 * z[:, 1] + np.sin(6 * z[:, 0]) * np.cos(4 * z[:, 1])
+    assert np.sqrt(np.mean((mu - f) ** 2)) < 0.05
