@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""bench.py -- the BASELINE.json metric on B200: kernel MVMs/s (and HBM GB/s as a fraction
+of the measured roofline) of the exact fast Matern K.v at N = 1e6, d = 1 (configs[1]),
+plus d = 2 / d = 3 applies (configs[2], configs[3]) and the config-5 CG solve time as
+extra fields.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--cg]
+
+One "step" = one K.v apply of config 2 (d = 1, N = 1e6, nu = 5/2, l = 0.05, x ~ N(0,1))
+with a fresh v, through the C ABI (gp_kmvm), the structure set up once (as configs[1]
+says).  Inputs are larger than L2: the steps cycle through 100 distinct v / out buffers
+(1.6 GB).  value = applies of all ranks / max-over-ranks device time.  Multi-GPU runs
+are independent replicas (each rank its own plan and inputs; no data-path collective:
+DESIGN.md "Multi-GPU"), so scaling is weak.
+
+--impl reference times the CPU oracle (oracle/, dense O(N^2), all host cores) on the
+same workload, each step a bounded sample of rows, extrapolated to whole MVMs.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def ncu_traffic(key):
+    try:
+        with open(TRAFFIC_PATH) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(val: float, ws: int) -> float:
+    if ws == 1:
+        return val
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([val], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(val: float, ws: int) -> float:
+    if ws == 1:
+        return val
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([val], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class Applier:
+    """Pre-marshalled gp_kmvm calls (no per-call Python tensor work in the timed loop)."""
+
+    def __init__(self, g, plan, V, OUT, stream):
+        self.f = g.load_library().gp_kmvm
+        self.h = plan._h
+        self.vp = [ctypes.c_void_p(V[i].data_ptr()) for i in range(V.shape[0])]
+        self.op = [ctypes.c_void_p(OUT[i].data_ptr()) for i in range(OUT.shape[0])]
+        self.s = ctypes.c_void_p(stream.cuda_stream)
+        self.nv = V.shape[0]
+
+    def __call__(self, k):
+        st = self.f(self.h, self.vp[k % self.nv], 1, self.op[k % self.nv], self.s)
+        if st:
+            raise RuntimeError("gp_kmvm failed")
+
+
+def time_applies(applier, steps, warmup, stream, ws):
+    """Returns (seconds for `steps` applies, max over ranks, per-launch mean seconds)."""
+    import torch
+    for k in range(warmup):
+        applier(k)
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(steps):
+        applier(warmup + k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    sec = e0.elapsed_time(e1) / 1e3
+    return max_over_ranks(sec, ws), sec
+
+
+def per_launch(applier, steps, stream):
+    """Mean device duration of one apply (events bracketing each launch)."""
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for k, (a, b) in enumerate(evs):
+        a.record(stream)
+        applier(k)
+        b.record(stream)
+    torch.cuda.synchronize()
+    d = [a.elapsed_time(b) / 1e3 for a, b in evs]
+    return statistics.mean(d), statistics.median(d), min(d)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2508_01864_b200 as g
+    g.load_library()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    cfg = W.CONFIGS[2]
+    n = cfg.n
+    x = torch.from_numpy(W.config_points(cfg)).to(dev)
+    nv = 100
+    # 100 distinct v (and out) buffers: 1.6 GB > 126 MB L2
+    V = torch.empty((nv, n), dtype=torch.float64, device=dev)
+    for r in range(nv):
+        V[r] = torch.from_numpy(W.config_vector(cfg, r + 100 * rank))
+    OUT = torch.empty_like(V)
+    hbm, peak_kind = peaks()
+    result = {}
+
+    def measure(two_nu, steps, warmup, sampler=None):
+        plan = g.Plan(x, g.Kernel(two_nu, cfg.ell), stream)
+        ap = Applier(g, plan, V, OUT, stream)
+        if sampler:
+            with sampler:
+                sec_max, sec = time_applies(ap, steps, warmup, stream, ws)
+        else:
+            sec_max, sec = time_applies(ap, steps, warmup, stream, ws)
+        mean_l, med_l, min_l = per_launch(ap, min(steps, 200), stream)
+        return plan, ap, sec_max, sec, mean_l, med_l, min_l
+
+    sampler = ClockSampler(local)
+    two_nu = 5
+    plan, ap, sec_max, sec, mean_l, med_l, min_l = measure(two_nu, args.steps, args.warmup, sampler)
+    total = sum_over_ranks(args.steps, ws)
+    value = total / sec_max
+    model_bytes = plan.model_bytes
+    launches = plan.launches_per_apply
+    achieved = model_bytes / mean_l / 1e9
+    clocks = sampler.summary()
+
+    # e2e: host buffers through gp_kmvm_host, copies inside the timed region
+    e2e_steps = min(args.steps, 30)
+    vh = torch.empty((nv, n), dtype=torch.float64).pin_memory()
+    vh.copy_(V.cpu())
+    oh = torch.empty_like(vh).pin_memory()
+    lib = g.load_library()
+    s = ctypes.c_void_p(stream.cuda_stream)
+    for k in range(2):
+        lib.gp_kmvm_host(plan._h, ctypes.c_void_p(vh[k].data_ptr()), 1,
+                         ctypes.c_void_p(oh[k].data_ptr()), s)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(e2e_steps):
+        st = lib.gp_kmvm_host(plan._h, ctypes.c_void_p(vh[k % nv].data_ptr()), 1,
+                              ctypes.c_void_p(oh[k % nv].data_ptr()), s)
+        assert st == 0
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e2e_sec = max_over_ranks(e0.elapsed_time(e1) / 1e3, ws)
+    e2e_value = sum_over_ranks(e2e_steps, ws) / e2e_sec
+
+    line = {
+        "metric": "kernel MVMs/sec (K.v, exact Matern ECDF decomposition) at N=1e6, d=1",
+        "value": value,
+        "unit": "MVM/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": sec_max / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE.json configs[1] recipe: x ~ N(0,1) seed 0, v ~ N(0,1))",
+        "config": {
+            "workload": "config2_d1_n1e6_nu52",
+            "n": n, "d": 1, "nu": "5/2", "lengthscale": cfg.ell[0], "form": "L1(=product, d=1)",
+            "setup": "once (sort + stored structure), outside the timed region",
+            "l2": "inputs larger than L2: 100 distinct v and out buffers (1.6 GB) cycled",
+            "launch": "gp_kmvm through ctypes, one cooperative launch per apply",
+            "parallelism": f"replicas x{ws}",
+        },
+        "gpu_launches": int(args.steps * launches),
+        "clocks": clocks,
+        "roofline": {
+            "bound": "hbm", "kernel": "k_d1_coop<2>",
+            "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": achieved / hbm,
+            "traffic": ncu_traffic("d1_nu52_n1e6"),
+            "algorithmic_bytes_per_launch": model_bytes,
+            "launch_ms_mean": mean_l * 1e3, "launch_ms_median": med_l * 1e3,
+        },
+        "e2e": {"value": e2e_value, "unit": "MVM/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "steps": e2e_steps,
+                "api": "gp_kmvm_host (pinned host v/out, copies + apply + sync per step)"},
+    }
+    plan.close()
+
+    extras = {}
+    if not args.no_extras:
+        # nu = 3/2 on the same config
+        p3, ap3, smax3, _, m3, _, _ = measure(3, min(args.steps, 500), 3)
+        extras["config2_d1_nu32"] = {"mvm_per_s": sum_over_ranks(min(args.steps, 500), ws) / smax3,
+                                     "launch_ms_mean": m3 * 1e3,
+                                     "hbm_gbs": p3.model_bytes / m3 / 1e9,
+                                     "frac_hbm": p3.model_bytes / m3 / 1e9 / hbm}
+        p3.close()
+        extras.update(extra_configs(g, dev, stream, ws, rank, hbm, args))
+    if extras:
+        line["extra"] = extras
+
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, two_nu, args.cpu_rows)
+    return line
+
+
+def extra_configs(g, dev, stream, ws, rank, hbm, args):
+    """d = 2 (config 3) and d = 3 (config 4) K.v; d=1,2,3 at N = 2^20 (the metric's
+    'N=1e6, d=1..3'); config-5 CG solve time with --cg."""
+    import torch
+    out = {}
+
+    def apply_stats(x_np, kern, reps, vecs=4):
+        x = torch.from_numpy(x_np).to(dev)
+        t0 = time.perf_counter()
+        plan = g.Plan(x, kern, stream)
+        torch.cuda.synchronize()
+        setup_s = time.perf_counter() - t0
+        n = x_np.shape[0]
+        V = torch.randn((vecs, n), dtype=torch.float64, device=dev)
+        O = torch.empty_like(V)
+        ap = Applier(g, plan, V, O, stream)
+        sec_max, _ = time_applies(ap, reps, 2, stream, ws)
+        mean_l, _, _ = per_launch(ap, min(reps, 20), stream)
+        res = {"n": n, "setup_s": setup_s, "apply_ms": sec_max / reps * 1e3,
+               "mvm_per_s": sum_over_ranks(reps, ws) / sec_max,
+               "launches_per_apply": plan.launches_per_apply,
+               "model_bytes": plan.model_bytes,
+               "model_gbs": plan.model_bytes / mean_l / 1e9,
+               "frac_hbm": plan.model_bytes / mean_l / 1e9 / hbm,
+               "struct_mb": plan.struct_bytes / 1e6}
+        plan.close()
+        return res
+
+    c3 = W.CONFIGS[3]
+    out["config3_d2_n2e5_nu32_l1"] = apply_stats(W.config_points(c3), g.Kernel(3, c3.ell), 20)
+    c4 = W.CONFIGS[4]
+    out["config4_d3_n5e5_nu52_l1"] = apply_stats(W.config_points(c4), g.Kernel(5, c4.ell), 5)
+    for d, reps in [(2, 10), (3, 3)]:
+        xn = W.uniform_points(1 << 20, d, 1000 + d)
+        out[f"sweep_d{d}_n2^20_nu32_l1"] = apply_stats(xn, g.Kernel(3, (0.1,) * d), reps)
+    if args.cg:
+        c5 = W.CONFIGS[5]
+        x = W.config_points(c5); y = W.config_response(c5, x)
+        plan = g.Plan(torch.from_numpy(x).to(dev), g.Kernel(3, c5.ell, form=g.FORM_PRODUCT), stream)
+        yt = torch.from_numpy(y).to(dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        alpha, beta, info = plan.cg_solve(yt, c5.noise_sigma ** 2, mean=g.MEAN_AFFINE, rtol=1e-8,
+                                          max_iter=40000)
+        torch.cuda.synchronize()
+        cg_s = time.perf_counter() - t0
+        out["config5_cg"] = {"cg_solve_s": cg_s, "iters": info["iters"],
+                             "relres_max": info["relres_max"], "rhs": 4, "beta": beta,
+                             "ms_per_iter": cg_s / max(info["iters"], 1) * 1e3}
+        plan.close()
+    return out
+
+
+def cpu_baseline(cfg, two_nu, rows_n):
+    import oracle
+    x = W.config_points(cfg)
+    v = W.config_vector(cfg, 0)
+    rows = W.sample_rows(x, rows_n)
+    nt = os.cpu_count() or 1
+    oracle.kmvm_rows(x[:1000], v[:1000], two_nu, "l1", cfg.ell, rows=np.arange(10))  # load/warm
+    t0 = time.perf_counter()
+    oracle.kmvm_rows(x, v, two_nu, "l1", cfg.ell, rows=rows, nthreads=nt)
+    dt = time.perf_counter() - t0
+    full = dt * cfg.n / rows.size
+    return {"value": 1.0 / full, "unit": "MVM/s", "cores": nt, "kind": "oracle",
+            "sample": f"{rows.size} of {cfg.n} rows of one K.v (dense O(N) per row), "
+                      f"{dt:.2f} s; full-MVM time extrapolated x{cfg.n / rows.size:.0f}",
+            "seconds_per_mvm_extrapolated": full}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args, ws, rank):
+    import oracle
+    if rank != 0:
+        return None
+    cfg = W.CONFIGS[2]
+    x = W.config_points(cfg)
+    nt = os.cpu_count() or 1
+    # bound the whole run to a few minutes: rows per step from a short calibration
+    oracle.kmvm_rows(x[:1000], np.ones(1000), 5, "l1", cfg.ell, rows=np.arange(10))
+    t0 = time.perf_counter()
+    oracle.kmvm_rows(x, W.config_vector(cfg, 0), 5, "l1", cfg.ell, rows=np.arange(64), nthreads=nt)
+    per_row = (time.perf_counter() - t0) / 64
+    budget = 120.0 / max(args.steps + args.warmup, 1)
+    rows_per_step = int(max(16, min(1024, budget / per_row)))
+    rng = np.random.default_rng(7)
+    for k in range(args.warmup):
+        oracle.kmvm_rows(x, W.config_vector(cfg, k), 5, "l1", cfg.ell,
+                         rows=rng.choice(cfg.n, rows_per_step, replace=False), nthreads=nt)
+    tot = 0.0
+    for k in range(args.steps):
+        rows = np.sort(rng.choice(cfg.n, rows_per_step, replace=False))
+        v = W.config_vector(cfg, k)
+        t0 = time.perf_counter()
+        oracle.kmvm_rows(x, v, 5, "l1", cfg.ell, rows=rows, nthreads=nt)
+        tot += time.perf_counter() - t0
+    sec_per_mvm = tot / args.steps * cfg.n / rows_per_step
+    value = 1.0 / sec_per_mvm
+    sample = (f"{rows_per_step} random rows per step of the {cfg.n}-row K.v, "
+              f"MVM time extrapolated x{cfg.n / rows_per_step:.0f}")
+    return {
+        "impl": "reference",
+        "metric": "kernel MVMs/sec (K.v, exact Matern ECDF decomposition) at N=1e6, d=1",
+        "value": value, "unit": "MVM/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec_per_mvm * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json configs[1] recipe)",
+        "config": {"workload": "config2_d1_n1e6_nu52", "n": cfg.n, "d": 1, "nu": "5/2",
+                   "lengthscale": cfg.ell[0], "impl": "dense CPU oracle (oracle/), OpenMP"},
+        "cpu_baseline": {"value": value, "unit": "MVM/s", "cores": nt, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "MVM/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cg", action="store_true", help="also time the config-5 CG solve")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=4096)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        line = run_reference(args, ws, rank)
+    else:
+        line = run_ours(args, ws, rank, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
