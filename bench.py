@@ -159,8 +159,9 @@ def sum_over_ranks(val: float, ws: int) -> float:
 class Applier:
     """Pre-marshalled gp_kmvm calls (no per-call Python tensor work in the timed loop)."""
 
-    def __init__(self, g, plan, V, OUT, stream):
-        self.f = g.load_library().gp_kmvm
+    def __init__(self, g, plan, V, OUT, stream, rank_order=False):
+        lib = g.load_library()
+        self.f = lib.gp_kmvm_rank if rank_order else lib.gp_kmvm
         self.h = plan._h
         self.vp = [ctypes.c_void_p(V[i].data_ptr()) for i in range(V.shape[0])]
         self.op = [ctypes.c_void_p(OUT[i].data_ptr()) for i in range(OUT.shape[0])]
@@ -317,6 +318,21 @@ def run_ours(args, ws, rank, local):
                                      "hbm_gbs": p3.model_bytes / m3 / 1e9,
                                      "frac_hbm": p3.model_bytes / m3 / 1e9 / hbm}
         p3.close()
+        # the same apply in the plan's stored order (the operator inside CG: no gather/scatter)
+        p5 = g.Plan(x, g.Kernel(5, cfg.ell), stream)
+        VR = torch.stack([p5.to_rank(V[i]) for i in range(nv)])
+        OR = torch.empty_like(VR)
+        apr = Applier(g, p5, VR, OR, stream, rank_order=True)
+        sr = min(args.steps, 1000)
+        smax_r, _ = time_applies(apr, sr, 5, stream, ws)
+        mr, _, _ = per_launch(apr, 200, stream)
+        rb = n * 24   # t + v + out, all coalesced
+        extras["config2_d1_nu52_rank_order"] = {
+            "api": "gp_kmvm_rank", "mvm_per_s": sum_over_ranks(sr, ws) / smax_r,
+            "launch_ms_mean": mr * 1e3, "model_bytes": rb, "hbm_gbs": rb / mr / 1e9,
+            "frac_hbm": rb / mr / 1e9 / hbm}
+        del VR, OR
+        p5.close()
         extras.update(extra_configs(g, dev, stream, ws, rank, hbm, args))
     if extras:
         line["extra"] = extras

@@ -96,6 +96,19 @@ GP_API gp_status gp_kmvm(gp_plan p, const double *v, int nrhs, double *out, void
  * end-to-end measurement.  v, out: n x nrhs column-major (host). */
 GP_API gp_status gp_kmvm_host(gp_plan p, const double *v, int nrhs, double *out, void *stream);
 
+/* gp_kmvm_rank -- out = K v with v and out in the plan's STORED order (x1-rank order:
+ * element r belongs to the point of rank r).  This is the operator used inside CG
+ * (P:155-174 [§1]): with the data presorted, an MVM needs no permutation at all
+ * (P:336-338 [§2.1] "when the data comes pre-sorted ... O(N)").  Layout as gp_kmvm. */
+GP_API gp_status gp_kmvm_rank(gp_plan p, const double *v_rank, int nrhs, double *out_rank,
+                              void *stream);
+
+/* gp_permute -- move n x nrhs column-major vectors between user order and the plan's
+ * stored order: to_rank != 0: dst[r] = src[perm[r]]; to_rank == 0: dst[perm[r]] = src[r].
+ * src and dst must not alias. */
+GP_API gp_status gp_permute(gp_plan p, const double *src, int nrhs, double *dst, int to_rank,
+                            void *stream);
+
 /* gp_kzx_setup -- structure for the rectangular product K_zx v (P:92 [k_z],
  * P:256 [eq kde]): the same machinery on the union x U z with data points as
  * sources and queries as targets (reading R7).  z: m x d row-major (device), m >= 1. */
@@ -141,11 +154,14 @@ GP_API gp_status gp_predict(gp_plan p, const double *z, int64_t m, const double 
 /* gp_plan_query -- introspection for tests and the bench (host value in *value):
  *   0 n, 1 d, 2 levels L, 3 bytes of device structure, 4 kernel launches per
  *   single-RHS gp_kmvm, 5 algorithmic HBM bytes per single-RHS gp_kmvm,
- *   6 d=1 apply path in use (1 = single-launch cooperative, 2 = multi-sub-tile). */
+ *   6 d=1 apply path in use (1 = single-launch cooperative, 2 = multi-sub-tile),
+ *   7 d=1 thread-block shape of path 1 (see gp_plan_set_option). */
 GP_API gp_status gp_plan_query(gp_plan p, int what, int64_t *value);
 
-/* gp_plan_set_option -- testing knob: option 0 forces the d=1 apply path
- * (0 auto, 1 cooperative single sub-tile if it fits, 2 multi-sub-tile). */
+/* gp_plan_set_option -- tuning / testing knobs (d = 1 only; ignored otherwise):
+ *   option 0: force the d=1 apply path (0 auto, 1 single-sub-tile if it fits, 2 multi-sub-tile);
+ *   option 1: thread-block shape of path 1: 0 = 512x15, 1 = 640x11, 2 = 768x9, 3 = 1024x7
+ *             (threads x points per thread). */
 GP_API gp_status gp_plan_set_option(gp_plan p, int option, int64_t value);
 
 GP_API void gp_destroy(gp_plan p);

@@ -58,6 +58,8 @@ def load_library(path: str | None = None):
         "gp_setup": [vp, i64, ci, ctypes.POINTER(_Kernel), vp, ctypes.POINTER(vp)],
         "gp_kmvm": [vp, vp, ci, vp, vp],
         "gp_kmvm_host": [vp, vp, ci, vp, vp],
+        "gp_kmvm_rank": [vp, vp, ci, vp, vp],
+        "gp_permute": [vp, vp, ci, vp, ci, vp],
         "gp_kzx_setup": [vp, vp, i64, vp, ctypes.POINTER(vp)],
         "gp_kzx": [vp, vp, ci, vp, vp],
         "gp_cg_solve": [vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, ctypes.POINTER(_CGInfo), vp],
@@ -156,6 +158,31 @@ class Plan:
         if out is None:
             out = torch.empty_like(v)
         _check(_lib.gp_kmvm(self._h, _dev(v, "v"), nrhs, _dev(out, "out", v.shape), _stream(stream)))
+        return out
+
+    def kmvm_rank(self, v_rank, out=None, stream=None):
+        """out = K v with vectors in the plan's stored (x1-rank) order (CG operator)."""
+        import torch
+        nrhs = 1 if v_rank.dim() == 1 else v_rank.shape[0]
+        if out is None:
+            out = torch.empty_like(v_rank)
+        _check(_lib.gp_kmvm_rank(self._h, _dev(v_rank, "v"), nrhs, _dev(out, "out", v_rank.shape),
+                                 _stream(stream)))
+        return out
+
+    def to_rank(self, v, stream=None):
+        import torch
+        out = torch.empty_like(v)
+        nrhs = 1 if v.dim() == 1 else v.shape[0]
+        _check(_lib.gp_permute(self._h, _dev(v, "v"), nrhs, _dev(out, "out", v.shape), 1, _stream(stream)))
+        return out
+
+    def from_rank(self, v_rank, stream=None):
+        import torch
+        out = torch.empty_like(v_rank)
+        nrhs = 1 if v_rank.dim() == 1 else v_rank.shape[0]
+        _check(_lib.gp_permute(self._h, _dev(v_rank, "v"), nrhs, _dev(out, "out", v_rank.shape), 0,
+                               _stream(stream)))
         return out
 
     def kmvm_host(self, v_host, out_host, stream=None):

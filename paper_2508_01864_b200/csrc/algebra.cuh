@@ -39,9 +39,10 @@ __host__ __device__ constexpr double binom(int q, int m) {
 template <int P>
 __device__ __forceinline__ void advance(double* M, double D, double E) {
   if constexpr (P == 2) {
-    const double D2 = D * D;
-    M[2] = E * fma(D2, M[0], fma(2.0 * D, M[1], M[2]));
-    M[1] = E * fma(D, M[0], M[1]);
+    // M2 + 2D M1 + D^2 M0 = M2 + D (M1 + (M1 + D M0)):  6 FP64 ops
+    const double a = fma(D, M[0], M[1]);
+    M[2] = E * fma(D, M[1] + a, M[2]);
+    M[1] = E * a;
     M[0] = E * M[0];
   } else if constexpr (P == 1) {
     M[1] = E * fma(D, M[0], M[1]);
@@ -76,7 +77,7 @@ __device__ __forceinline__ double read_poly(const double* R, double beta) {
 // sum_q a_q R_q  (beta = 0)
 template <int P>
 __device__ __forceinline__ double read0(const double* R) {
-  if constexpr (P == 2) return R[0] + R[1] + (1.0 / 3.0) * R[2];
+  if constexpr (P == 2) return fma(1.0 / 3.0, R[2], R[0] + R[1]);
   else if constexpr (P == 1) return R[0] + R[1];
   else return R[0];
 }

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "internal.h"
 
@@ -86,6 +88,28 @@ gp_status gp_kmvm(gp_plan p, const double* v, int nrhs, double* out, void* strea
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int c = 0; c < nrhs; ++c)
     GPM_TRY(apply_user(p->pl, v + (size_t)c * p->pl.n, out + (size_t)c * p->pl.n, s));
+  return GP_OK;
+}
+
+gp_status gp_kmvm_rank(gp_plan p, const double* v, int nrhs, double* out, void* stream) {
+  if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  if (v == out) return fail(GP_ERR_INVALID_ARG, "out must not alias v");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int c = 0; c < nrhs; ++c)
+    GPM_TRY(apply_rank(p->pl, v + (size_t)c * p->pl.n, out + (size_t)c * p->pl.n, s));
+  return GP_OK;
+}
+
+gp_status gp_permute(gp_plan p, const double* src, int nrhs, double* dst, int to_rank,
+                     void* stream) {
+  if (!p || !src || !dst) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  if (src == dst) return fail(GP_ERR_INVALID_ARG, "dst must not alias src");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int c = 0; c < nrhs; ++c)
+    GPM_TRY(permute_vec(p->pl, src + (size_t)c * p->pl.n, dst + (size_t)c * p->pl.n,
+                        to_rank != 0, s));
   return GP_OK;
 }
 
@@ -196,6 +220,21 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
     case 4: *value = pl.launches_per_apply; break;
     case 5: *value = apply_model_bytes(pl); break;
     case 6: *value = pl.d == 1 ? pl.d1_path : 0; break;
+    case 7: *value = pl.d == 1 ? pl.d1_shape : -1; break;
+    case 8: case 9: case 10: case 11: case 12: case 13: case 14: {
+      // debug (GPM_D1_TIMING): mean over CTAs of stamp[what-7] - stamp[0], ns, last launch
+      if (!pl.dbg.bytes) return fail(GP_ERR_INVALID_ARG, "GPM_D1_TIMING not enabled");
+      std::vector<unsigned long long> h(pl.dbg.bytes / 8);
+      if (cudaMemcpy(h.data(), pl.dbg.ptr, pl.dbg.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(GP_ERR_CUDA, "dbg copy failed");
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < pl.d1_grid; ++b) t0 = std::min(t0, h[b * 8]);
+      double acc = 0;
+      const int slot = what == 13 ? 6 : what - 7;
+      for (int b = 0; b < pl.d1_grid; ++b) acc += (double)(h[b * 8 + slot] - t0);
+      *value = (int64_t)(acc / pl.d1_grid);
+      break;
+    }
     default: return fail(GP_ERR_INVALID_ARG, "unknown query");
   }
   return GP_OK;
@@ -203,9 +242,16 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
 
 gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
   if (!p) return fail(GP_ERR_INVALID_ARG, "NULL plan");
-  if (option != 0 || value < 0 || value > 2) return fail(GP_ERR_INVALID_ARG, "bad option");
+  if (option == 0) {
+    if (value < 0 || value > 2) return fail(GP_ERR_INVALID_ARG, "bad value for option 0");
+    p->pl.d1_force = (int)value;
+  } else if (option == 1) {
+    if (value < 0 || value > 3) return fail(GP_ERR_INVALID_ARG, "bad value for option 1");
+    p->pl.d1_shape = (int)value;
+  } else {
+    return fail(GP_ERR_INVALID_ARG, "unknown option");
+  }
   if (p->pl.d != 1) return GP_OK;
-  p->pl.d1_force = (int)value;
   return apply_prepare(p->pl);
 }
 

@@ -40,6 +40,13 @@ __global__ void k_epilogue(const int* __restrict__ perm, const double* __restric
   }
 }
 
+__global__ void k_scatter_user(const int* __restrict__ perm, const double* __restrict__ src,
+                               int64_t n, double* __restrict__ dst) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    dst[__ldg(perm + r)] = src[r];
+}
+
 inline int egrid(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
 }
@@ -70,6 +77,15 @@ static gp_status apply_levels(Plan& pl, const double* u_rank, double* out, bool 
                                          user_order ? pl.tgt_off : 0, pl.os2, out);
   GPM_CUDA(cudaGetLastError());
   pl.launches_per_apply = launches + 2 + (user_order ? 1 : 0);  // + memset-free count below
+  return GP_OK;
+}
+
+gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cudaStream_t s) {
+  if (to_rank)
+    k_gather<<<egrid(pl.n), 256, 0, s>>>(pl.perm.as<int>(), src, pl.n, pl.n, dst);
+  else
+    k_scatter_user<<<egrid(pl.n), 256, 0, s>>>(pl.perm.as<int>(), src, pl.n, dst);
+  GPM_CUDA(cudaGetLastError());
   return GP_OK;
 }
 

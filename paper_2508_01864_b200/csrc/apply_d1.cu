@@ -476,6 +476,10 @@ static cudaError_t d1_set_attr() {
                               (int)sizeof(D1Smem));
 }
 
+gp_status df_shape_info(int shape, int* capacity, int* max_grid);
+gp_status df_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s);
+int df_default_shape();
+
 gp_status d1_prepare(Plan& pl) {
   static int attr_done = 0;
   if (!attr_done) {
@@ -489,12 +493,34 @@ gp_status d1_prepare(Plan& pl) {
   GPM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   GPM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return fail(GP_ERR_UNSUPPORTED, "device does not support cooperative launch");
+  // fast path: one shared-memory chunk per CTA (apply_d1_fast.cu)
+  int fast_grid = 0, cap = 0;
+  if (pl.d1_shape < 0) pl.d1_shape = df_default_shape();
+  GPM_TRY(df_shape_info(pl.d1_shape, &cap, &fast_grid));
+  if (pl.d1_force != 2 && fast_grid > 0) {
+    int64_t g = std::min<int64_t>(fast_grid, std::max<int64_t>(1, (pl.n + 1023) / 1024));
+    int64_t chunk = ((pl.n + g - 1) / g + 3) & ~int64_t(3);   // multiple of 4 (TMA alignment)
+    g = (pl.n + chunk - 1) / chunk;
+    if (chunk <= cap && g <= fast_grid) {
+      pl.d1_grid = (int)g;
+      pl.d1_chunk = chunk;
+      pl.d1_path = 1;
+      GPM_TRY(pl.aggs.alloc(96 * (size_t)g));   // D1Pub records (apply_d1_fast.cu)
+      GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
+      GPM_TRY(pl.bar.alloc(64));
+      GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));
+      if (getenv("GPM_D1_TIMING")) {
+        GPM_TRY(pl.dbg.alloc(sizeof(unsigned long long) * 8 * (size_t)g));
+        GPM_CUDA(cudaMemset(pl.dbg.ptr, 0, pl.dbg.bytes));
+      }
+      return GP_OK;
+    }
+  }
   int occ = 0;
   GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_d1_coop<2>, D1_BLOCK,
                                                          sizeof(D1Smem)));
   if (occ < 1) return fail(GP_ERR_CUDA, "d=1 kernel cannot be resident (shared memory)");
   const int64_t maxg = (int64_t)nsm * occ;
-  // small problems: fewer CTAs (>= 1024 points each) to keep the barrier cheap
   int64_t g = std::min<int64_t>(maxg, std::max<int64_t>(1, (pl.n + 1023) / 1024));
   int64_t chunk = (pl.n + g - 1) / g;
   if (pl.d1_force == 2 && chunk <= D1_SUB) {
@@ -509,7 +535,7 @@ gp_status d1_prepare(Plan& pl) {
                                         std::to_string(pl.n) + ")");
   pl.d1_grid = (int)g;
   pl.d1_chunk = chunk;
-  pl.d1_path = nsub == 1 ? 1 : 2;
+  pl.d1_path = 2;
   GPM_TRY(pl.aggs.alloc(sizeof(D1Agg) * (size_t)g * (1 + D1_MAXSUB)));
   GPM_TRY(pl.bar.alloc(64));
   GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));
@@ -517,6 +543,7 @@ gp_status d1_prepare(Plan& pl) {
 }
 
 gp_status d1_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s) {
+  if (pl.d1_path == 1) return df_launch(pl, v, out, user_order, s);
   D1Args a;
   a.ts = pl.t.as<double>();
   a.perm = user_order ? pl.perm.as<int>() : nullptr;

@@ -74,8 +74,9 @@ struct Plan {
   DevBuf aggs;                      // tile aggregates
   DevBuf bar;                       // grid barrier words (d = 1 cooperative kernel)
   DevBuf stage_in, stage_out;       // gp_kmvm_host staging
+  DevBuf dbg;                       // d=1 phase timestamps (env GPM_D1_TIMING)
   // d = 1 launch geometry
-  int d1_grid = 0, d1_path = 1, d1_force = 0;
+  int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;
   int64_t d1_chunk = 0;
   int64_t struct_bytes = 0;
   int launches_per_apply = 0;
@@ -92,6 +93,7 @@ gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, cudaStrea
 // User-order apply with gather/scatter: out = K v restricted to targets (unions).
 gp_status apply_user(Plan& pl, const double* v, double* out, cudaStream_t s);
 gp_status apply_prepare(Plan& pl);   // launch geometry + scratch
+gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cudaStream_t s);
 int64_t apply_model_bytes(const Plan& pl);
 
 // solve.cu

@@ -100,7 +100,7 @@ void DevBuf::release() {
 
 void plan_free(Plan& pl) {
   for (DevBuf* b : {&pl.x_raw, &pl.perm, &pl.t, &pl.ord2, &pl.ord3, &pl.u, &pl.acc, &pl.w,
-                    &pl.aggs, &pl.bar, &pl.stage_in, &pl.stage_out})
+                    &pl.aggs, &pl.bar, &pl.stage_in, &pl.stage_out, &pl.dbg})
     b->release();
 }
 
@@ -133,8 +133,8 @@ gp_status plan_build(Plan& pl, const double* x, int64_t n, int d, const gp_kerne
 
   GPM_TRY(pl.x_raw.alloc(sizeof(double) * n * d));
   GPM_CUDA(cudaMemcpyAsync(pl.x_raw.ptr, x, sizeof(double) * n * d, cudaMemcpyDeviceToDevice, s));
-  GPM_TRY(pl.perm.alloc(sizeof(int) * n));
-  GPM_TRY(pl.t.alloc(sizeof(double) * n * d));
+  GPM_TRY(pl.perm.alloc(sizeof(int) * (n + 16)));   // padded: TMA bulk copies round up
+  GPM_TRY(pl.t.alloc(sizeof(double) * (n * d + 16)));
 
   // scratch for sorting
   DevBuf keys, keys2, vals, bad, tmp, seq, seq3, inv, qseq;

@@ -144,6 +144,20 @@ def test_d1_determinism_bitwise(gpm):
         assert torch.equal(plan.kmvm(v), ref)
 
 
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_rank_order_operator(gpm, d):
+    """gp_kmvm_rank on permuted vectors equals gp_kmvm; gp_permute round-trips bitwise."""
+    import torch
+    n = 9000 if d < 3 else 3000
+    x = _points("uniform", n, d, 40 + d)
+    v = to_dev(np.random.default_rng(d).standard_normal(n))
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, (0.1, 0.2, 0.3)[:d]))
+    vr = plan.to_rank(v)
+    assert torch.equal(plan.from_rank(vr), v)
+    out_r = plan.kmvm_rank(vr)
+    assert torch.equal(plan.from_rank(out_r), plan.kmvm(v))
+
+
 def test_host_buffers_e2e(gpm):
     n = 5000
     x = _points("uniform", n, 2, 8)

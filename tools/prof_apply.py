@@ -17,6 +17,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--nu2", type=int, default=5)
 ap.add_argument("--applies", type=int, default=5)
 ap.add_argument("--form", type=int, default=0)
+ap.add_argument("--rank", action="store_true")
 args = ap.parse_args()
 c = W.CONFIGS[args.config]
 x = torch.from_numpy(W.config_points(c)).cuda()
@@ -24,6 +25,9 @@ plan = g.Plan(x, g.Kernel(args.nu2, c.ell, form=args.form))
 V = [torch.from_numpy(W.config_vector(c, r)).cuda() for r in range(min(args.applies, 8))]
 out = torch.empty_like(V[0])
 for k in range(args.applies):
-    plan.kmvm(V[k % len(V)], out)
+    if args.rank:
+        plan.kmvm_rank(V[k % len(V)], out)
+    else:
+        plan.kmvm(V[k % len(V)], out)
 torch.cuda.synchronize()
 print("ok", plan.launches_per_apply, plan.model_bytes)
