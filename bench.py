@@ -4,11 +4,13 @@ of the measured roofline) of the exact fast Matern K.v at N = 1e6, d = 1 (config
 plus d = 2 / d = 3 applies (configs[2], configs[3]) and the config-5 CG solve time as
 extra fields.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--cg]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--no-cg] [--no-graph] [--no-extras] [--no-cpu]
 
 One "step" = one K.v apply of config 2 (d = 1, N = 1e6, nu = 5/2, l = 0.05, x ~ N(0,1))
 with a fresh v, through the C ABI (gp_kmvm), the structure set up once (as configs[1]
-says).  Inputs are larger than L2: the steps cycle through 100 distinct v / out buffers
+says).  The K timed applies are captured as one CUDA graph of gp_kmvm calls and replayed
+once (device time by CUDA events); the plain stream-loop time is reported beside it.  Inputs are larger than L2: the steps cycle through 100 distinct v / out buffers
 (1.6 GB).  value = applies of all ranks / max-over-ranks device time.  Multi-GPU runs
 are independent replicas (each rank its own plan and inputs; no data-path collective:
 DESIGN.md "Multi-GPU"), so scaling is weak.
@@ -193,6 +195,39 @@ def time_applies(applier, steps, warmup, stream, ws):
     return max_over_ranks(sec, ws), sec
 
 
+def time_graph(make_applier, steps, warmup, ws):
+    """Capture `steps` applies in one CUDA graph (on a side stream) and time one replay.
+    Returns (max-over-ranks seconds, local seconds) or None if capture is unsupported."""
+    import torch
+    cs = torch.cuda.Stream()
+    try:
+        ap = make_applier(cs)
+        for k in range(warmup):
+            ap(k)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cs):
+            for k in range(steps):
+                ap(k)
+        with torch.cuda.stream(cs):
+            graph.replay()          # warm replay (replay() launches on the current stream)
+        torch.cuda.synchronize()
+    except Exception as e:          # pragma: no cover - reported in the JSON line
+        print(f"graph capture failed: {e}", file=sys.stderr)
+        return None
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cs):
+        e0.record(cs)
+        graph.replay()
+        e1.record(cs)
+    torch.cuda.synchronize()
+    barrier(ws)
+    sec = e0.elapsed_time(e1) / 1e3
+    return max_over_ranks(sec, ws), sec
+
+
 def per_launch(applier, steps, stream):
     """Mean device duration of one apply (events bracketing each launch)."""
     import torch
@@ -227,20 +262,27 @@ def run_ours(args, ws, rank, local):
     hbm, peak_kind = peaks()
     result = {}
 
-    def measure(two_nu, steps, warmup, sampler=None):
+    def measure(two_nu, steps, warmup, sampler=None, vin=None, rank_order=False):
         plan = g.Plan(x, g.Kernel(two_nu, cfg.ell), stream)
-        ap = Applier(g, plan, V, OUT, stream)
-        if sampler:
-            with sampler:
+        VV = V if vin is None else vin(plan)
+        ap = Applier(g, plan, VV, OUT, stream, rank_order=rank_order)
+        mk = lambda st: Applier(g, plan, VV, OUT, st, rank_order=rank_order)
+        import contextlib
+        with (sampler if sampler else contextlib.nullcontext()):
+            gr = None if args.no_graph else time_graph(mk, steps, warmup, ws)
+            if gr is None:
                 sec_max, sec = time_applies(ap, steps, warmup, stream, ws)
-        else:
-            sec_max, sec = time_applies(ap, steps, warmup, stream, ws)
+            else:
+                sec_max, sec = gr
+        loop_max, _ = time_applies(ap, min(steps, 500), 3, stream, ws)
         mean_l, med_l, min_l = per_launch(ap, min(steps, 200), stream)
-        return plan, ap, sec_max, sec, mean_l, med_l, min_l
+        info = {"graph": gr is not None, "stream_loop_ms_per_step": loop_max / min(steps, 500) * 1e3}
+        return plan, ap, sec_max, sec, mean_l, med_l, min_l, info
 
     sampler = ClockSampler(local)
     two_nu = 5
-    plan, ap, sec_max, sec, mean_l, med_l, min_l = measure(two_nu, args.steps, args.warmup, sampler)
+    plan, ap, sec_max, sec, mean_l, med_l, min_l, tinfo = measure(two_nu, args.steps, args.warmup,
+                                                                   sampler)
     total = sum_over_ranks(args.steps, ws)
     value = total / sec_max
     model_bytes = plan.model_bytes
@@ -290,7 +332,9 @@ def run_ours(args, ws, rank, local):
             "n": n, "d": 1, "nu": "5/2", "lengthscale": cfg.ell[0], "form": "L1(=product, d=1)",
             "setup": "once (sort + stored structure), outside the timed region",
             "l2": "inputs larger than L2: 100 distinct v and out buffers (1.6 GB) cycled",
-            "launch": "gp_kmvm through ctypes, one cooperative launch per apply",
+            "launch": ("CUDA graph of K gp_kmvm calls (one cooperative kernel each), one replay"
+                       if tinfo["graph"] else "gp_kmvm through ctypes, stream loop"),
+            "stream_loop_ms_per_step": tinfo["stream_loop_ms_per_step"],
             "parallelism": f"replicas x{ws}",
         },
         "gpu_launches": int(args.steps * launches),
@@ -312,27 +356,23 @@ def run_ours(args, ws, rank, local):
     extras = {}
     if not args.no_extras:
         # nu = 3/2 on the same config
-        p3, ap3, smax3, _, m3, _, _ = measure(3, min(args.steps, 500), 3)
-        extras["config2_d1_nu32"] = {"mvm_per_s": sum_over_ranks(min(args.steps, 500), ws) / smax3,
+        sx = min(args.steps, 1000)
+        p3, _, smax3, _, m3, _, _, _ = measure(3, sx, 3)
+        extras["config2_d1_nu32"] = {"api": "gp_kmvm", "mvm_per_s": sum_over_ranks(sx, ws) / smax3,
                                      "launch_ms_mean": m3 * 1e3,
                                      "hbm_gbs": p3.model_bytes / m3 / 1e9,
                                      "frac_hbm": p3.model_bytes / m3 / 1e9 / hbm}
         p3.close()
         # the same apply in the plan's stored order (the operator inside CG: no gather/scatter)
-        p5 = g.Plan(x, g.Kernel(5, cfg.ell), stream)
-        VR = torch.stack([p5.to_rank(V[i]) for i in range(nv)])
-        OR = torch.empty_like(VR)
-        apr = Applier(g, p5, VR, OR, stream, rank_order=True)
-        sr = min(args.steps, 1000)
-        smax_r, _ = time_applies(apr, sr, 5, stream, ws)
-        mr, _, _ = per_launch(apr, 200, stream)
-        rb = n * 24   # t + v + out, all coalesced
-        extras["config2_d1_nu52_rank_order"] = {
-            "api": "gp_kmvm_rank", "mvm_per_s": sum_over_ranks(sr, ws) / smax_r,
-            "launch_ms_mean": mr * 1e3, "model_bytes": rb, "hbm_gbs": rb / mr / 1e9,
-            "frac_hbm": rb / mr / 1e9 / hbm}
-        del VR, OR
-        p5.close()
+        for nu2 in (5, 3):
+            to_rank = lambda pl: torch.stack([pl.to_rank(V[i]) for i in range(nv)])
+            pr, _, smr, _, mr, _, _, _ = measure(nu2, sx, 3, vin=to_rank, rank_order=True)
+            rb = n * 24   # t + v + out, all coalesced
+            extras[f"config2_d1_nu{nu2}2_rank_order"] = {
+                "api": "gp_kmvm_rank", "mvm_per_s": sum_over_ranks(sx, ws) / smr,
+                "launch_ms_mean": mr * 1e3, "model_bytes": rb, "hbm_gbs": rb / mr / 1e9,
+                "frac_hbm": rb / mr / 1e9 / hbm}
+            pr.close()
         extras.update(extra_configs(g, dev, stream, ws, rank, hbm, args))
     if extras:
         line["extra"] = extras
@@ -377,7 +417,7 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
     for d, reps in [(2, 10), (3, 3)]:
         xn = W.uniform_points(1 << 20, d, 1000 + d)
         out[f"sweep_d{d}_n2^20_nu32_l1"] = apply_stats(xn, g.Kernel(3, (0.1,) * d), reps)
-    if args.cg:
+    if not args.no_cg:
         c5 = W.CONFIGS[5]
         x = W.config_points(c5); y = W.config_response(c5, x)
         plan = g.Plan(torch.from_numpy(x).to(dev), g.Kernel(3, c5.ell, form=g.FORM_PRODUCT), stream)
@@ -466,7 +506,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cg", action="store_true", help="also time the config-5 CG solve")
+    ap.add_argument("--no-cg", action="store_true", help="skip the config-5 CG solve")
+    ap.add_argument("--no-graph", action="store_true", help="time a stream loop, not a graph")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=4096)

@@ -477,7 +477,7 @@ static DFShape make_shape() {
 
 static DFShape g_shapes[4];
 static int g_shapes_ready = 0;
-static int g_default_shape = 0;
+static int g_default_shape = 2;   // 768 x 9: best measured (profiles/)
 
 static gp_status df_init() {
   if (g_shapes_ready) return GP_OK;
