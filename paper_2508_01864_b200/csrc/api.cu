@@ -85,20 +85,14 @@ gp_status gp_kmvm(gp_plan p, const double* v, int nrhs, double* out, void* strea
   if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
   if (v == out) return fail(GP_ERR_INVALID_ARG, "out must not alias v");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int c = 0; c < nrhs; ++c)
-    GPM_TRY(apply_user(p->pl, v + (size_t)c * p->pl.n, out + (size_t)c * p->pl.n, s));
-  return GP_OK;
+  return apply_user(p->pl, v, out, nrhs, static_cast<cudaStream_t>(stream));
 }
 
 gp_status gp_kmvm_rank(gp_plan p, const double* v, int nrhs, double* out, void* stream) {
   if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
   if (v == out) return fail(GP_ERR_INVALID_ARG, "out must not alias v");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int c = 0; c < nrhs; ++c)
-    GPM_TRY(apply_rank(p->pl, v + (size_t)c * p->pl.n, out + (size_t)c * p->pl.n, s));
-  return GP_OK;
+  return apply_rank(p->pl, v, out, nrhs, static_cast<cudaStream_t>(stream));
 }
 
 gp_status gp_permute(gp_plan p, const double* src, int nrhs, double* dst, int to_rank,
@@ -164,10 +158,7 @@ gp_status gp_kzx_setup(gp_plan p, const double* z, int64_t m, void* stream, gp_c
 gp_status gp_kzx(gp_cross c, const double* v, int nrhs, double* out, void* stream) {
   if (!c || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int j = 0; j < nrhs; ++j)
-    GPM_TRY(apply_user(c->pl, v + (size_t)j * c->n, out + (size_t)j * c->m, s));
-  return GP_OK;
+  return apply_user(c->pl, v, out, nrhs, static_cast<cudaStream_t>(stream));
 }
 
 void gp_kzx_destroy(gp_cross c) {
@@ -221,6 +212,19 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
     case 5: *value = apply_model_bytes(pl); break;
     case 6: *value = pl.d == 1 ? pl.d1_path : 0; break;
     case 7: *value = pl.d == 1 ? pl.d1_shape : -1; break;
+    case 20: case 21: case 22: case 23: case 24: case 25: {
+      // debug (GPM_D1_TIMING): MAX over CTAs of stamp[what-19] - min stamp[0], ns
+      if (!pl.dbg.bytes) return fail(GP_ERR_INVALID_ARG, "GPM_D1_TIMING not enabled");
+      std::vector<unsigned long long> h(pl.dbg.bytes / 8);
+      if (cudaMemcpy(h.data(), pl.dbg.ptr, pl.dbg.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(GP_ERR_CUDA, "dbg copy failed");
+      unsigned long long t0 = ~0ull, mx = 0;
+      for (int b = 0; b < pl.d1_grid; ++b) t0 = std::min(t0, h[b * 8]);
+      const int slot = what == 25 ? 6 : what - 19;
+      for (int b = 0; b < pl.d1_grid; ++b) mx = std::max(mx, h[b * 8 + slot] - t0);
+      *value = (int64_t)mx;
+      break;
+    }
     case 8: case 9: case 10: case 11: case 12: case 13: case 14: {
       // debug (GPM_D1_TIMING): mean over CTAs of stamp[what-7] - stamp[0], ns, last launch
       if (!pl.dbg.bytes) return fail(GP_ERR_INVALID_ARG, "GPM_D1_TIMING not enabled");

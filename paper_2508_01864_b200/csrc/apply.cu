@@ -3,6 +3,8 @@
 //   d >= 2: gather u[r] = v[perm[r]] -> level passes (apply_level.cu) into acc ->
 //           epilogue out[perm[r]] = s^2 (u[r] + acc[r])  (self term + scale, a7).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -10,7 +12,9 @@ namespace gpm {
 
 gp_status d1_prepare(Plan& pl);
 gp_status d1_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s);
-gp_status level_passes(Plan& pl, const double* u_rank, cudaStream_t s, int* launches);
+gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches);
+gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
+size_t level_pt_bytes();
 int64_t level_tiles(int64_t n);
 
 namespace {
@@ -24,13 +28,17 @@ __global__ void k_gather(const int* __restrict__ perm, const double* __restrict_
   }
 }
 
-// out[perm[r] - tgt_off] = os2 (u[r] + acc[r]) for targets; perm == nullptr: rank order
-__global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ u,
+// out[perm[r] - tgt_off] = os2 (u[r] + acc[r]) for targets; perm == nullptr: rank order.
+// u is read from the packed point records (stride 4 doubles, u at offset 3).
+__global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ pts,
                            const double* __restrict__ acc, int64_t n, int64_t tgt_off,
-                           double os2, double* __restrict__ out) {
+                           double os2, double* __restrict__ out, int64_t ostride) {
+  pts += blockIdx.y * 4 * n;
+  acc += blockIdx.y * n;
+  out += blockIdx.y * ostride;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const double val = os2 * (u[r] + acc[r]);
+    const double val = os2 * (pts[4 * r + 3] + acc[r]);
     if (perm) {
       const int i = __ldg(perm + r);
       if (i >= tgt_off) out[i - tgt_off] = val;
@@ -53,30 +61,51 @@ inline int egrid(int64_t n) {
 
 }  // namespace
 
+static gp_status level_buffers(Plan& pl, int nrhs);
+
 gp_status apply_prepare(Plan& pl) {
   const int64_t n = pl.n;
   if (pl.d == 1) {
     GPM_TRY(d1_prepare(pl));
     pl.launches_per_apply = 1;
   } else {
-    GPM_TRY(pl.u.alloc(sizeof(double) * n));
-    GPM_TRY(pl.acc.alloc(sizeof(double) * n));
-    GPM_TRY(pl.aggs.alloc(sizeof(LvAgg) * 2 * (size_t)level_tiles(n)));
+    GPM_TRY(level_buffers(pl, 1));
+    if (const char* e = getenv("GPM_NEAR_LB")) {   // tuning knob: "lb2,lb3,lb3m"
+      int a = pl.near_lb2, b = pl.near_lb3, c = pl.near_lb3m;
+      if (sscanf(e, "%d,%d,%d", &a, &b, &c) >= 1) { pl.near_lb2 = a; pl.near_lb3 = b; pl.near_lb3m = c; }
+    }
   }
   GPM_TRY(pl.w.alloc(sizeof(double) * n));
   return GP_OK;
 }
 
-static gp_status apply_levels(Plan& pl, const double* u_rank, double* out, bool user_order,
+static constexpr int LV_MAXB = 8;   // right-hand sides per level-pass batch
+
+static gp_status level_buffers(Plan& pl, int nrhs) {
+  const size_t need = (size_t)nrhs * pl.n;
+  if (pl.acc.bytes < sizeof(double) * need) GPM_TRY(pl.acc.alloc(sizeof(double) * need));
+  if (pl.pts.bytes < level_pt_bytes() * need) GPM_TRY(pl.pts.alloc(level_pt_bytes() * need));
+  const size_t ag = sizeof(LvAgg) * 2 * (size_t)level_tiles(pl.n) * nrhs;
+  if (pl.aggs.bytes < ag) GPM_TRY(pl.aggs.alloc(ag));
+  return GP_OK;
+}
+
+static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
                               cudaStream_t s) {
-  int launches = 0;
-  GPM_CUDA(cudaMemsetAsync(pl.acc.ptr, 0, sizeof(double) * pl.n, s));
-  GPM_TRY(level_passes(pl, u_rank, s, &launches));
-  k_epilogue<<<egrid(pl.n), 256, 0, s>>>(user_order ? pl.perm.as<int>() : nullptr, u_rank,
-                                         pl.acc.as<double>(), pl.n,
-                                         user_order ? pl.tgt_off : 0, pl.os2, out);
-  GPM_CUDA(cudaGetLastError());
-  pl.launches_per_apply = launches + 2 + (user_order ? 1 : 0);  // + memset-free count below
+  const int64_t vstride = user_order ? pl.n_src : pl.n;
+  const int64_t ostride = user_order ? pl.n - pl.tgt_off : pl.n;
+  for (int c0 = 0; c0 < nrhs; c0 += LV_MAXB) {
+    const int nb = std::min(LV_MAXB, nrhs - c0);
+    GPM_TRY(level_buffers(pl, nb));
+    int launches = 0;
+    GPM_TRY(level_pack(pl, v + c0 * vstride, nb, user_order, s));   // packed points (+ gather)
+    GPM_TRY(level_passes(pl, nb, s, &launches));   // first level launch initialises acc
+    k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
+        user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(), pl.n,
+        user_order ? pl.tgt_off : 0, pl.os2, out + c0 * ostride, ostride);
+    GPM_CUDA(cudaGetLastError());
+    pl.launches_per_apply = launches + 2;   // + pack + epilogue (per batch of columns)
+  }
   return GP_OK;
 }
 
@@ -89,16 +118,23 @@ gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cu
   return GP_OK;
 }
 
-gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, cudaStream_t s) {
-  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, false, s);
-  return apply_levels(pl, u_rank, out_rank, false, s);
+gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s) {
+  if (pl.d == 1) {
+    for (int c = 0; c < nrhs; ++c)
+      GPM_TRY(d1_launch(pl, u_rank + (size_t)c * pl.n, out_rank + (size_t)c * pl.n, false, s));
+    return GP_OK;
+  }
+  return apply_levels(pl, u_rank, out_rank, nrhs, false, s);
 }
 
-gp_status apply_user(Plan& pl, const double* v, double* out, cudaStream_t s) {
-  if (pl.d == 1) return d1_launch(pl, v, out, true, s);
-  k_gather<<<egrid(pl.n), 256, 0, s>>>(pl.perm.as<int>(), v, pl.n, pl.n_src, pl.u.as<double>());
-  GPM_CUDA(cudaGetLastError());
-  return apply_levels(pl, pl.u.as<double>(), out, true, s);
+gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s) {
+  if (pl.d == 1) {
+    const int64_t m = pl.n - pl.tgt_off;
+    for (int c = 0; c < nrhs; ++c)
+      GPM_TRY(d1_launch(pl, v + (size_t)c * pl.n_src, out + (size_t)c * m, true, s));
+    return GP_OK;
+  }
+  return apply_levels(pl, v, out, nrhs, true, s);
 }
 
 // Algorithmic HBM bytes of one single-RHS user-order apply:

@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   __shared__ double s_tot[2][5];
   __shared__ double s_part[2][8][5];
   __shared__ double s_carry[2][3];
-  __shared__ unsigned long long s_epoch;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * a.chunk;

@@ -14,52 +14,47 @@
 // of eq L1_decomposition / product_decomposition without forming the overflowing
 // weights of eq matern_weights (R5).
 //
-// Kernel layout: tile = 2048 positions per 256-thread CTA; element data
-// staged in shared memory (padded, conflict-free); per-thread sequential recurrences,
-// warp-shuffle block scans with segment flags; segments longer than a tile get carries
-// from a tile-aggregate kernel (a reduce-then-scan across the tiles of one segment).
+// B200 layout: a pass engine works on one 1024-position tile staged in
+// shared memory (256 threads x 4 consecutive positions, flag-segmented warp-shuffle
+// scans, rolled loops: every launch walks the code once).  Launch structure per apply:
+//   d = 2: ONE fused launch for all levels l <= 10 (point data loaded once per tile,
+//          outputs accumulated in shared memory), then per level l > 10 an aggregate
+//          launch + an apply launch with carries across the tiles of a node;
+//   d = 3: ONE fused launch for all (l1 <= 10, l2 <= l1); per l1 > 10 one launch for
+//          all l2 <= 10 (the tile's points gathered once); aggregate + apply launches
+//          for (l1 > 10, l2 > 10).
 #include <algorithm>
 
 #include "algebra.cuh"
+#include "fexp.cuh"
 #include "internal.h"
 
 namespace gpm {
 
-__device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
-
 constexpr int LV_BLOCK = 256;
-constexpr int LV_ITEMS = 8;
-constexpr int LV_LOGTILE = 11;
+constexpr int LV_ITEMS = 4;
+constexpr int LV_LOGTILE = 10;
 constexpr int LV_TILE = 1 << LV_LOGTILE;  // == LV_BLOCK * LV_ITEMS
 constexpr int LV_WARPS = LV_BLOCK / 32;
-__host__ __device__ constexpr int lvpad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int lvpad(int i) { return i + (i >> 3); }  // <= 2-way conflicts
 constexpr int LV_PADN = LV_TILE + LV_TILE / 8;
 
-struct PassDesc {
-  const int* ord;      // this pass's order (positions [0, n_act))
-  const int* ord2l1;   // d = 3: ord2[l1] (position -> rank); d = 2: unused
-  const double* t1;
-  const double* t2;
-  const double* t3;
-  const double* u;     // rank-order input
-  double* acc;         // rank-order accumulator
-  LvAgg* aggs;         // [2 * tiles]
-  int64_t n, n_act;
-  int mode;            // 2 or 3
-  int lseg;            // log2 of the segment (node) size of this pass
-  int l1;              // d = 3: outer level
-  int ntiles;
-};
-
-struct LvSmem {
+// Per-pass element arrays (scan order, padded index).
+struct LvElems {
   double d[LV_PADN];   // last coordinate y, then the gap Delta to the previous position
   double e[LV_PADN];   // e^{-Delta}
   double u[LV_PADN];   // source weight
-  double a[LV_PADN];   // alpha = distance to the split reference(s)
+  double a[LV_PADN];   // alpha
   double ea[LV_PADN];  // e^{-alpha}
-  int r[LV_TILE];      // rank of the point (output slot)
+  double o[LV_PADN];   // pass output (read values)
+  int rl[LV_TILE];     // output slot (tile-local point index, or global rank)
   signed char ch[LV_TILE];
+};
+
+// Point arrays of the fused kernels (tile-local point index).
+struct LvPoints {
+  double u[LV_TILE], t1[LV_TILE], t2[LV_TILE], t3[LV_TILE], acc[LV_TILE];
+  int o2[LV_TILE];     // d = 3: ord2[l1] tile (local ranks) / global ranks (mid kernel)
 };
 
 template <int NS>
@@ -139,184 +134,90 @@ __device__ __forceinline__ LSt<NS> agg_get(const LvAgg* g) {
   return s;
 }
 
+template <class A>
+struct LvScratch {
+  LSt<A::NS> w[LV_WARPS], wx[LV_WARPS], tot;
+  double carry[2][A::NS];
+  double tab[64];
+};
+
 // Block-wide exclusive scan in one direction (FWD: threads < me; else threads > me),
-// plus the tile total.  Uses shared warp totals; ends with a barrier.
+// plus the tile total.  Ends with a barrier.
 template <class A, bool FWD>
 __device__ __forceinline__ void lv_block_scan(const LSt<A::NS>& mine, LSt<A::NS>& excl,
-                                              LSt<A::NS>& tot, LSt<A::NS>* s_w,
-                                              LSt<A::NS>* s_wx, LSt<A::NS>* s_tot) {
+                                              LSt<A::NS>& tot, LvScratch<A>& sc) {
   using S = LSt<A::NS>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   S x = mine;
-#pragma unroll
+#pragma unroll 1
   for (int off = 1; off < 32; off <<= 1) {
-    if (FWD) {
-      S l = lshfl<A::NS>(x, off, true);
-      if (lane >= off) x = lcf<A>(l, x);
-    } else {
-      S r = lshfl<A::NS>(x, off, false);
-      if (lane + off < 32) x = lcb<A>(x, r);
-    }
+    S y = lshfl<A::NS>(x, off, FWD);
+    if (FWD && lane >= off) x = lcf<A>(y, x);
+    if (!FWD && lane + off < 32) x = lcb<A>(x, y);
   }
-  if (FWD && lane == 31) s_w[warp] = x;
-  if (!FWD && lane == 0) s_w[warp] = x;
+  if (FWD && lane == 31) sc.w[warp] = x;
+  if (!FWD && lane == 0) sc.w[warp] = x;
   S ex = lshfl<A::NS>(x, 1, FWD);
   if ((FWD && lane == 0) || (!FWD && lane == 31)) ex = lid<A>();
   __syncthreads();
   if (warp == 0) {
-    S y = lane < LV_WARPS ? s_w[lane] : lid<A>();
-#pragma unroll
+    S y = lane < LV_WARPS ? sc.w[lane] : lid<A>();
+#pragma unroll 1
     for (int off = 1; off < LV_WARPS; off <<= 1) {
-      if (FWD) {
-        S l = lshfl<A::NS>(y, off, true);
-        if (lane >= off) y = lcf<A>(l, y);
-      } else {
-        S r = lshfl<A::NS>(y, off, false);
-        if (lane + off < 32) y = lcb<A>(y, r);
-      }
+      S z = lshfl<A::NS>(y, off, FWD);
+      if (FWD && lane >= off) y = lcf<A>(z, y);
+      if (!FWD && lane + off < 32) y = lcb<A>(y, z);
     }
     S ye = lshfl<A::NS>(y, 1, FWD);
     if ((FWD && lane == 0) || (!FWD && lane >= LV_WARPS - 1)) ye = lid<A>();
-    if (lane < LV_WARPS) s_wx[lane] = ye;
-    if (FWD && lane == LV_WARPS - 1) *s_tot = y;
-    if (!FWD && lane == 0) *s_tot = y;
+    if (lane < LV_WARPS) sc.wx[lane] = ye;
+    if (FWD && lane == LV_WARPS - 1) sc.tot = y;
+    if (!FWD && lane == 0) sc.tot = y;
   }
   __syncthreads();
-  excl = FWD ? lcf<A>(s_wx[warp], ex) : lcb<A>(ex, s_wx[warp]);
-  tot = *s_tot;
+  excl = FWD ? lcf<A>(sc.wx[warp], ex) : lcb<A>(ex, sc.wx[warp]);
+  tot = sc.tot;
   __syncthreads();
 }
 
-// Element of a pass at position pos: scan coordinate y, weight u, split offset alpha,
-// channel, rank.
-struct Elem {
-  double y, u, a;
-  int r, ch;
-};
-
-__device__ __forceinline__ Elem lv_elem(const PassDesc& pd, int64_t pos) {
-  Elem el;
-  if (pd.mode == 2) {
-    const int l = pd.lseg;
-    const int r = __ldg(pd.ord + pos);
-    const int64_t mid = ((pos >> l) << l) + (int64_t(1) << (l - 1));
-    const double m = __ldg(pd.t1 + mid);
-    el.a = fabs(__ldg(pd.t1 + r) - m);
-    el.ch = (r >> (l - 1)) & 1;
-    el.y = __ldg(pd.t2 + r);
-    el.u = __ldg(pd.u + r);
-    el.r = r;
-  } else {
-    const int l1 = pd.l1, l2 = pd.lseg;
-    const int q = __ldg(pd.ord + pos);
-    const int r = __ldg(pd.ord2l1 + q);
-    const int64_t mid1 = ((int64_t)(q >> l1) << l1) + (int64_t(1) << (l1 - 1));
-    const int64_t mid2 = ((pos >> l2) << l2) + (int64_t(1) << (l2 - 1));
-    const double m1 = __ldg(pd.t1 + mid1);
-    const double m2 = __ldg(pd.t2 + __ldg(pd.ord2l1 + mid2));
-    el.a = fabs(__ldg(pd.t1 + r) - m1) + fabs(__ldg(pd.t2 + r) - m2);
-    el.ch = 2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1);
-    el.y = __ldg(pd.t3 + r);
-    el.u = __ldg(pd.u + r);
-    el.r = r;
-  }
-  return el;
-}
-
-__device__ __forceinline__ double lv_y(const PassDesc& pd, int64_t pos) {
-  if (pd.mode == 2) return __ldg(pd.t2 + __ldg(pd.ord + pos));
-  return __ldg(pd.t3 + __ldg(pd.ord2l1 + __ldg(pd.ord + pos)));
-}
-
-// KMODE 0: apply (segments fit in a tile), 1: tile aggregates only, 2: apply with carries
-template <class A, int KMODE>
-__global__ void __launch_bounds__(LV_BLOCK) k_level(PassDesc pd) {
+// ---------------------------------------------------------------------------
+// The pass engine.  E.d holds y (scan coordinate) for positions [0, cnt) of a tile whose
+// first global position is T0; segments are aligned blocks of (smask + 1) positions;
+// nend = one past the last active position (a segment end).  mode: 0 apply (segments fit
+// the tile), 1 aggregates only (write tile totals to aggs[2*tile + {0,1}]), 2 apply with
+// the carries folded into sc.carry.  y_before = y of position T0 - 1 (mode 1/2 only).
+template <class A>
+__device__ __forceinline__ void lv_engine(LvElems& E, LvScratch<A>& sc, int cnt, int64_t T0,
+                                          int64_t smask, int64_t nend, int mode,
+                                          double y_before, LvAgg* aggs) {
   using S = LSt<A::NS>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  LvSmem& sm = *reinterpret_cast<LvSmem*>(smem_raw);
-  __shared__ S s_w[LV_WARPS], s_wx[LV_WARPS], s_tot;
-  __shared__ double s_carry[2][A::NS];
-
   const int tid = threadIdx.x;
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
-  const int cnt = (int)lmin(LV_TILE, pd.n_act - T0);
-  const int64_t smask = (int64_t(1) << pd.lseg) - 1;
-
-  // ---- tile carries (from the aggregate kernel), warp 0 forward / warp 1 backward
-  if (KMODE == 2) {
-    const int lane = tid & 31, warp = tid >> 5;
-    if (warp < 2) {
-      const int tps = 1 << (pd.lseg - LV_LOGTILE);
-      const int t = blockIdx.x;
-      const int first = t & ~(tps - 1);
-      const int last = min(first + tps, pd.ntiles) - 1;
-      const int lo = warp == 0 ? first : t + 1;
-      const int hi = warp == 0 ? t : last + 1;
-      const int cntc = max(0, hi - lo);
-      const int per = (cntc + 31) / 32;
-      S X = lid<A>();
-      for (int k = 0; k < per; ++k) {
-        const int j = lo + lane * per + k;
-        if (j < hi) {
-          S g = agg_get<A::NS>(pd.aggs + 2 * j + warp);
-          X = warp == 0 ? lcf<A>(X, g) : lcb<A>(X, g);
-        }
-      }
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        S Y = lshfl<A::NS>(X, off, false);
-        if (lane + off < 32) X = warp == 0 ? lcf<A>(X, Y) : lcb<A>(X, Y);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < A::NS; ++i) s_carry[warp][i] = X.M[i];
-      }
-    }
-  }
-
-  // ---- phase 0: element data into shared memory (coalesced over positions)
-  for (int i = tid; i < cnt; i += LV_BLOCK) {
-    const Elem el = lv_elem(pd, T0 + i);
-    const int pi = lvpad(i);
-    sm.d[pi] = el.y;
-    sm.u[pi] = el.u;
-    sm.a[pi] = el.a;
-    sm.ea[pi] = exp(-el.a);
-    sm.r[i] = el.r;
-    sm.ch[i] = (signed char)el.ch;
-  }
-  __syncthreads();
   const int i0 = tid * LV_ITEMS;
+  auto is_start = [&](int i) { return ((T0 + i) & smask) == 0; };
+  auto is_end = [&](int i) { return (((T0 + i + 1) & smask) == 0) || (T0 + i + 1 == nend); };
+
+  // gaps and e^{-gap}
   double yprev = 0.0;
-  if (i0 < cnt) {
-    const int64_t pos0 = T0 + i0;
-    if ((pos0 & smask) == 0) yprev = sm.d[lvpad(i0)];
-    else if (i0 > 0) yprev = sm.d[lvpad(i0 - 1)];
-    else yprev = lv_y(pd, pos0 - 1);
-  }
+  if (i0 < cnt) yprev = i0 > 0 ? E.d[lvpad(i0 - 1)] : y_before;
   __syncthreads();
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < LV_ITEMS; ++k) {
     const int i = i0 + k;
     if (i < cnt) {
       const int pi = lvpad(i);
-      const double y = sm.d[pi];
-      const double dl = (((T0 + i) & smask) == 0) ? 0.0 : y - yprev;
+      const double y = E.d[pi];
+      const double dl = is_start(i) ? 0.0 : y - yprev;
       yprev = y;
-      sm.d[pi] = dl;
-      sm.e[pi] = exp(-dl);
+      E.d[pi] = dl;
+      E.e[pi] = fexp_neg(dl, sc.tab);
     }
   }
-  __syncthreads();
 
-  auto is_start = [&](int i) { return ((T0 + i) & smask) == 0; };
-  auto is_end = [&](int i) { return (((T0 + i + 1) & smask) == 0) || (T0 + i == pd.n_act - 1); };
-
-  // ---- forward direction
+  // ---- forward
   S Fx, Ft;
   {
     S X = lid<A>();
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < LV_ITEMS; ++k) {
       const int i = i0 + k;
       if (i < cnt) {
@@ -325,53 +226,49 @@ __global__ void __launch_bounds__(LV_BLOCK) k_level(PassDesc pd) {
           X = lid<A>();
           X.f = 1;
         } else {
-          A::advance_all(X.M, sm.d[pi], sm.e[pi]);
-          X.D += sm.d[pi];
-          X.E *= sm.e[pi];
+          A::advance_all(X.M, E.d[pi], E.e[pi]);
+          X.D += E.d[pi];
+          X.E *= E.e[pi];
         }
-        A::inject(X.M, sm.ch[i], sm.u[pi], sm.a[pi], sm.ea[pi]);
+        A::inject(X.M, E.ch[i], E.u[pi], E.a[pi], E.ea[pi]);
       }
     }
-    lv_block_scan<A, true>(X, Fx, Ft, s_w, s_wx, &s_tot);
+    lv_block_scan<A, true>(X, Fx, Ft, sc);
   }
-  if (KMODE == 1) {
-    if (tid == 0) agg_put<A::NS>(pd.aggs + 2 * blockIdx.x, Ft);
-  }
-  double rf[LV_ITEMS];
-  if (KMODE != 1) {
+  if (mode == 1 && tid == 0) agg_put<A::NS>(aggs + 2 * blockIdx.x, Ft);
+  if (mode != 1) {
     S C = lid<A>();
-    if (KMODE == 2) {
+    if (mode == 2) {
 #pragma unroll
-      for (int i = 0; i < A::NS; ++i) C.M[i] = s_carry[0][i];
+      for (int i = 0; i < A::NS; ++i) C.M[i] = sc.carry[0][i];
     }
     const S Cin = lcf<A>(C, Fx);
     double M[A::NS];
 #pragma unroll
     for (int i = 0; i < A::NS; ++i) M[i] = Cin.M[i];
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < LV_ITEMS; ++k) {
       const int i = i0 + k;
-      rf[k] = 0.0;
       if (i < cnt) {
         const int pi = lvpad(i);
         if (is_start(i)) {
 #pragma unroll
           for (int j = 0; j < A::NS; ++j) M[j] = 0.0;
         } else {
-          A::advance_all(M, sm.d[pi], sm.e[pi]);
+          A::advance_all(M, E.d[pi], E.e[pi]);
         }
-        const int c = sm.ch[i];
-        rf[k] = A::read(M, A::NCH - 1 - c, sm.a[pi], sm.ea[pi]);
-        A::inject(M, c, sm.u[pi], sm.a[pi], sm.ea[pi]);
+        const int c = E.ch[i];
+        E.o[pi] = A::read(M, A::NCH - 1 - c, E.a[pi], E.ea[pi]);
+        A::inject(M, c, E.u[pi], E.a[pi], E.ea[pi]);
       }
     }
   }
 
-  // ---- backward direction
+  // ---- backward
   S Bx, Bt;
   {
     S X = lid<A>();
-#pragma unroll
+#pragma unroll 1
     for (int k = LV_ITEMS - 1; k >= 0; --k) {
       const int i = i0 + k;
       if (i < cnt) {
@@ -380,29 +277,29 @@ __global__ void __launch_bounds__(LV_BLOCK) k_level(PassDesc pd) {
           X = lid<A>();
           X.f = 1;
         }
-        A::inject(X.M, sm.ch[i], sm.u[pi], sm.a[pi], sm.ea[pi]);
-        A::advance_all(X.M, sm.d[pi], sm.e[pi]);
-        X.D += sm.d[pi];
-        X.E *= sm.e[pi];
+        A::inject(X.M, E.ch[i], E.u[pi], E.a[pi], E.ea[pi]);
+        A::advance_all(X.M, E.d[pi], E.e[pi]);
+        X.D += E.d[pi];
+        X.E *= E.e[pi];
       }
     }
-    lv_block_scan<A, false>(X, Bx, Bt, s_w, s_wx, &s_tot);
+    lv_block_scan<A, false>(X, Bx, Bt, sc);
   }
-  if (KMODE == 1) {
-    if (tid == 0) agg_put<A::NS>(pd.aggs + 2 * blockIdx.x + 1, Bt);
+  if (mode == 1) {
+    if (tid == 0) agg_put<A::NS>(aggs + 2 * blockIdx.x + 1, Bt);
     return;
   }
   {
     S C = lid<A>();
-    if (KMODE == 2) {
+    if (mode == 2) {
 #pragma unroll
-      for (int i = 0; i < A::NS; ++i) C.M[i] = s_carry[1][i];
+      for (int i = 0; i < A::NS; ++i) C.M[i] = sc.carry[1][i];
     }
     const S Cin = lcb<A>(Bx, C);
     double M[A::NS];
 #pragma unroll
     for (int i = 0; i < A::NS; ++i) M[i] = Cin.M[i];
-#pragma unroll
+#pragma unroll 1
     for (int k = LV_ITEMS - 1; k >= 0; --k) {
       const int i = i0 + k;
       if (i < cnt) {
@@ -411,114 +308,538 @@ __global__ void __launch_bounds__(LV_BLOCK) k_level(PassDesc pd) {
 #pragma unroll
           for (int j = 0; j < A::NS; ++j) M[j] = 0.0;
         }
-        const int c = sm.ch[i];
-        const double val = rf[k] + A::read(M, A::NCH - 1 - c, sm.a[pi], sm.ea[pi]);
-        A::inject(M, c, sm.u[pi], sm.a[pi], sm.ea[pi]);
-        A::advance_all(M, sm.d[pi], sm.e[pi]);
-        const int r = sm.r[i];
-        pd.acc[r] += val;
+        const int c = E.ch[i];
+        E.o[pi] += A::read(M, A::NCH - 1 - c, E.a[pi], E.ea[pi]);
+        A::inject(M, c, E.u[pi], E.a[pi], E.ea[pi]);
+        A::advance_all(M, E.d[pi], E.e[pi]);
       }
     }
+  }
+  __syncthreads();
+}
+
+// tile carries from the aggregate launch: warp 0 forward, warp 1 backward
+template <class A>
+__device__ __forceinline__ void lv_carries(LvScratch<A>& sc, const LvAgg* aggs, int lseg,
+                                           int ntiles) {
+  using S = LSt<A::NS>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < 2) {
+    const int tps = 1 << (lseg - LV_LOGTILE);
+    const int t = blockIdx.x;
+    const int first = t & ~(tps - 1);
+    const int last = min(first + tps, ntiles) - 1;
+    const int lo = warp == 0 ? first : t + 1;
+    const int hi = warp == 0 ? t : last + 1;
+    const int per = (max(0, hi - lo) + 31) / 32;
+    S X = lid<A>();
+#pragma unroll 1
+    for (int k = 0; k < per; ++k) {
+      const int j = lo + lane * per + k;
+      if (j < hi) {
+        S g = agg_get<A::NS>(aggs + 2 * j + warp);
+        X = warp == 0 ? lcf<A>(X, g) : lcb<A>(X, g);
+      }
+    }
+#pragma unroll 1
+    for (int off = 1; off < 32; off <<= 1) {
+      S Y = lshfl<A::NS>(X, off, false);
+      if (lane + off < 32) X = warp == 0 ? lcf<A>(X, Y) : lcb<A>(X, Y);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < A::NS; ++i) sc.carry[warp][i] = X.M[i];
+    }
+  }
+}
+
+// Packed per-point record (rank order), rebuilt per apply by k_pack (apply.cu): one random
+// access touches one 32-byte sector instead of four.
+struct __align__(32) Pt4 {
+  double t1, t2, t3, u;
+};
+
+struct LvArgs {
+  const Pt4* pts;      // [n] packed points (rank order)
+  int lb, lb2;         // near-field block log2 sizes: low (x1 ranks) / mid (ord2[l1] positions)
+  const int* ord2;     // [L][n]
+  const int* ord3;     // [L(L+1)/2][n]
+  const double* t1;
+  const double* t2;
+  const double* t3;
+  const double* u;     // rank-order input
+  double* acc;         // rank-order accumulator
+  LvAgg* aggs;
+  int64_t n;
+  int L;
+  // single-pass kernels
+  const int* ord;      // this pass's order
+  const int* ord2l1;   // d = 3: ord2[l1]
+  int lseg, l1, ntiles;
+  int64_t n_act;
+  int mode;            // 2 or 3 (dimension)
+  int64_t agg_stride;  // LvAgg records per right-hand side
+};
+
+// right-hand side handled by this CTA (blockIdx.y): offset the per-column buffers
+__device__ __forceinline__ void lv_col(LvArgs& g) {
+  const int64_t c = blockIdx.y;
+  g.pts += c * g.n;
+  g.acc += c * g.n;
+  g.aggs += c * g.agg_stride;
+}
+
+__device__ __forceinline__ int ord3_index(int l1, int l2) { return (l1 - 1) * l1 / 2 + (l2 - 1); }
+
+// Kernel value from per-dimension distances d_k = |t_ik - t_jk| (scaled coordinates):
+// L1: k(d1+d2(+d3)); product (d = 2): k(d1) k(d2); k(s) = sum_q a_q s^q e^{-s}.
+template <class A, int D>
+__device__ __forceinline__ double kval(double d1, double d2, double d3, const double* tab) {
+  constexpr int P = A::P;
+  if constexpr (!A::PROD) {
+    const double s = D == 3 ? (d1 + d2) + d3 : d1 + d2;
+    const double e = fexp_neg(s, tab);
+    if constexpr (P == 0) return e;
+    else if constexpr (P == 1) return e * (1.0 + s);
+    else return e * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0);
+  } else {
+    const double e = fexp_neg(d1 + d2, tab);
+    if constexpr (P == 0) return e;
+    else if constexpr (P == 1) return e * ((1.0 + d1) * (1.0 + d2));
+    else return e * (fma(d1, fma(d1, 1.0 / 3.0, 1.0), 1.0) * fma(d2, fma(d2, 1.0 / 3.0, 1.0), 1.0));
+  }
+}
+
+// Near field by direct summation: every pair i != j of the same aligned block of 2^lb
+// tile-local points (x1-rank blocks in the low kernels: exactly the pairs split at levels
+// <= lb; position blocks of ord2[l1] in the d=3 mid kernel, restricted to opposite x1
+// sides: exactly the pairs split at (l1, l2 <= lb)).  Pt.acc[i] += sum_j K(i,j) u_j.
+template <class A, int D>
+__device__ __forceinline__ void near_field(LvPoints& Pt, int cnt, int lb, int l1side,
+                                           const double* tab) {
+  const int i0 = threadIdx.x * LV_ITEMS;
+  if (i0 >= cnt) return;
+  double ti1[LV_ITEMS], ti2[LV_ITEMS], ti3[LV_ITEMS], acc[LV_ITEMS];
+  int hi[LV_ITEMS];
+#pragma unroll
+  for (int k = 0; k < LV_ITEMS; ++k) {
+    const int i = min(i0 + k, cnt - 1);
+    ti1[k] = Pt.t1[i];
+    ti2[k] = Pt.t2[i];
+    ti3[k] = D == 3 ? Pt.t3[i] : 0.0;
+    hi[k] = l1side ? (Pt.o2[i] >> (l1side - 1)) & 1 : 0;
+    acc[k] = 0.0;
+  }
+  const int bs = (i0 >> lb) << lb;
+  const int be = min(bs + (1 << lb), cnt);
+#pragma unroll 1
+  for (int j = bs; j < be; ++j) {
+    const double tj1 = Pt.t1[j], tj2 = Pt.t2[j], uj = Pt.u[j];
+    const double tj3 = D == 3 ? Pt.t3[j] : 0.0;
+    const int hj = l1side ? (Pt.o2[j] >> (l1side - 1)) & 1 : 0;
+#pragma unroll
+    for (int k = 0; k < LV_ITEMS; ++k) {
+      const bool ok = (i0 + k != j) && (!l1side || hj != hi[k]);
+      const double v = kval<A, D>(fabs(ti1[k] - tj1), fabs(ti2[k] - tj2), fabs(ti3[k] - tj3), tab);
+      acc[k] = ok ? fma(v, uj, acc[k]) : acc[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < LV_ITEMS; ++k)
+    if (i0 + k < cnt) Pt.acc[i0 + k] += acc[k];
+}
+
+// ---- fused low levels, d = 2: every level l <= min(10, L) of one 1024-rank tile
+template <class A>
+__global__ void __launch_bounds__(LV_BLOCK, 2) k_low2(LvArgs g) {
+  lv_col(g);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
+  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
+  __shared__ LvScratch<A> sc;
+  const int tid = threadIdx.x;
+  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
+  fexp_table_init(sc.tab);
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) {
+    const Pt4 p = g.pts[T0 + i];
+    Pt.u[i] = p.u;
+    Pt.t1[i] = p.t1;
+    Pt.t2[i] = p.t2;
+    Pt.acc[i] = 0.0;
+  }
+  __syncthreads();
+  const int lmax = min(LV_LOGTILE, g.L);
+  const int lb = min(g.lb, lmax);
+  if (lb > 0) near_field<A, 2>(Pt, cnt, lb, 0, sc.tab);
+  __syncthreads();
+#pragma unroll 1
+  for (int l = lb + 1; l <= lmax; ++l) {
+    const int* ord = g.ord2 + (size_t)(l - 1) * g.n + T0;
+#pragma unroll 1
+    for (int i = tid; i < cnt; i += LV_BLOCK) {
+      const int r = __ldg(ord + i) - (int)T0;
+      const int mid = ((i >> l) << l) + (1 << (l - 1));
+      const bool act = T0 + mid < g.n;
+      const int pi = lvpad(i);
+      const double al = act ? fabs(Pt.t1[r] - Pt.t1[mid]) : 0.0;
+      E.d[pi] = Pt.t2[r];
+      E.u[pi] = Pt.u[r];
+      E.a[pi] = al;
+      E.ea[pi] = fexp_neg(al, sc.tab);
+      E.ch[i] = act ? (signed char)((r >> (l - 1)) & 1) : (signed char)-1;
+      E.rl[i] = r;
+    }
+    __syncthreads();
+    lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l) - 1, g.n, 0, 0.0, nullptr);
+#pragma unroll 1
+    for (int i = tid; i < cnt; i += LV_BLOCK) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+    __syncthreads();
+  }
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[T0 + i] = Pt.acc[i];
+}
+
+// ---- fused low levels, d = 3: every (l1 <= min(10, L), l2 <= l1) of one tile
+template <class A>
+__global__ void __launch_bounds__(LV_BLOCK, 2) k_low3(LvArgs g) {
+  lv_col(g);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
+  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
+  __shared__ LvScratch<A> sc;
+  const int tid = threadIdx.x;
+  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
+  fexp_table_init(sc.tab);
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) {
+    const Pt4 p = g.pts[T0 + i];
+    Pt.u[i] = p.u;
+    Pt.t1[i] = p.t1;
+    Pt.t2[i] = p.t2;
+    Pt.t3[i] = p.t3;
+    Pt.acc[i] = 0.0;
+  }
+  __syncthreads();
+  const int lmax = min(LV_LOGTILE, g.L);
+  const int lb = min(g.lb, lmax);
+  if (lb > 0) near_field<A, 3>(Pt, cnt, lb, 0, sc.tab);
+#pragma unroll 1
+  for (int l1 = lb + 1; l1 <= lmax; ++l1) {
+    __syncthreads();
+#pragma unroll 1
+    for (int i = tid; i < cnt; i += LV_BLOCK)
+      Pt.o2[i] = __ldg(g.ord2 + (size_t)(l1 - 1) * g.n + T0 + i) - (int)T0;
+    __syncthreads();
+#pragma unroll 1
+    for (int l2 = 1; l2 <= l1; ++l2) {
+      const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
+#pragma unroll 1
+      for (int i = tid; i < cnt; i += LV_BLOCK) {
+        const int q = __ldg(ord + i) - (int)T0;   // position in ord2[l1] (tile-local)
+        const int r = Pt.o2[q];                   // rank (tile-local)
+        const int mid1 = ((q >> l1) << l1) + (1 << (l1 - 1));
+        const int mid2 = ((i >> l2) << l2) + (1 << (l2 - 1));
+        const bool act = (T0 + mid1 < g.n) && (T0 + mid2 < g.n);
+        const int pi = lvpad(i);
+        const double al =
+            act ? fabs(Pt.t1[r] - Pt.t1[mid1]) + fabs(Pt.t2[r] - Pt.t2[Pt.o2[mid2]]) : 0.0;
+        E.d[pi] = Pt.t3[r];
+        E.u[pi] = Pt.u[r];
+        E.a[pi] = al;
+        E.ea[pi] = fexp_neg(al, sc.tab);
+        E.ch[i] = act ? (signed char)(2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1))
+                      : (signed char)-1;
+        E.rl[i] = r;
+      }
+      __syncthreads();
+      lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l2) - 1, g.n, 0, 0.0, nullptr);
+#pragma unroll 1
+      for (int i = tid; i < cnt; i += LV_BLOCK) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[T0 + i] = Pt.acc[i];
+}
+
+// ---- d = 3, one outer level l1 > 10, all inner levels l2 <= 10 (tile = 1024 positions of
+// ord2[l1], i.e. one slice of one outer node; its points are gathered once)
+template <class A>
+__global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
+  lv_col(g);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
+  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
+  __shared__ LvScratch<A> sc;
+  const int tid = threadIdx.x;
+  const int l1 = g.l1;
+  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
+  const int64_t mid1 = ((T0 >> l1) << l1) + (int64_t(1) << (l1 - 1));
+  if (mid1 >= g.n) return;   // outer node without cross pairs (uniform per CTA)
+  fexp_table_init(sc.tab);
+  const double m1 = __ldg(g.t1 + mid1);
+  const int* o2g = g.ord2 + (size_t)(l1 - 1) * g.n + T0;
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) {
+    const int r = __ldg(o2g + i);
+    const Pt4 p = g.pts[r];
+    Pt.o2[i] = r;
+    Pt.u[i] = p.u;
+    Pt.t1[i] = p.t1;
+    Pt.t2[i] = p.t2;
+    Pt.t3[i] = p.t3;
+    Pt.acc[i] = 0.0;
+  }
+  __syncthreads();
+  const int lb2 = min(g.lb2, LV_LOGTILE);
+  if (lb2 > 0) near_field<A, 3>(Pt, cnt, lb2, l1, sc.tab);
+  __syncthreads();
+#pragma unroll 1
+  for (int l2 = lb2 + 1; l2 <= LV_LOGTILE; ++l2) {
+    const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
+#pragma unroll 1
+    for (int i = tid; i < cnt; i += LV_BLOCK) {
+      const int q = __ldg(ord + i) - (int)T0;    // tile-local position = point index
+      const int mid2 = ((i >> l2) << l2) + (1 << (l2 - 1));
+      const bool act = T0 + mid2 < g.n;
+      const int pi = lvpad(i);
+      const double al = act ? fabs(Pt.t1[q] - m1) + fabs(Pt.t2[q] - Pt.t2[mid2]) : 0.0;
+      E.d[pi] = Pt.t3[q];
+      E.u[pi] = Pt.u[q];
+      E.a[pi] = al;
+      E.ea[pi] = fexp_neg(al, sc.tab);
+      E.ch[i] = act ? (signed char)(2 * ((Pt.o2[q] >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1))
+                    : (signed char)-1;
+      E.rl[i] = q;
+    }
+    __syncthreads();
+    lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l2) - 1, g.n, 0, 0.0, nullptr);
+#pragma unroll 1
+    for (int i = tid; i < cnt; i += LV_BLOCK) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+    __syncthreads();
+  }
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[Pt.o2[i]] += Pt.acc[i];
+}
+
+// ---- one pass whose segments span several tiles (mode 1: aggregates, 2: apply)
+struct Elem {
+  double y, u, a;
+  int r, ch;
+};
+
+__device__ __forceinline__ Elem lv_elem(const LvArgs& g, int64_t pos) {
+  Elem el;
+  if (g.mode == 2) {
+    const int l = g.lseg;
+    const int r = __ldg(g.ord + pos);
+    const int64_t mid = ((pos >> l) << l) + (int64_t(1) << (l - 1));
+    const Pt4 p = g.pts[r];
+    el.a = fabs(p.t1 - __ldg(g.t1 + mid));
+    el.ch = (r >> (l - 1)) & 1;
+    el.y = p.t2;
+    el.u = p.u;
+    el.r = r;
+  } else {
+    const int l1 = g.l1, l2 = g.lseg;
+    const int q = __ldg(g.ord + pos);
+    const int r = __ldg(g.ord2l1 + q);
+    const int64_t mid1 = ((int64_t)(q >> l1) << l1) + (int64_t(1) << (l1 - 1));
+    const int64_t mid2 = ((pos >> l2) << l2) + (int64_t(1) << (l2 - 1));
+    const Pt4 p = g.pts[r];
+    el.a = fabs(p.t1 - __ldg(g.t1 + mid1)) + fabs(p.t2 - __ldg(g.t2 + __ldg(g.ord2l1 + mid2)));
+    el.ch = 2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1);
+    el.y = p.t3;
+    el.u = p.u;
+    el.r = r;
+  }
+  return el;
+}
+
+__device__ __forceinline__ double lv_y(const LvArgs& g, int64_t pos) {
+  if (g.mode == 2) return g.pts[__ldg(g.ord + pos)].t2;
+  return g.pts[__ldg(g.ord2l1 + __ldg(g.ord + pos))].t3;
+}
+
+template <class A, int KMODE>
+__global__ void __launch_bounds__(LV_BLOCK, 2) k_pass(LvArgs g) {
+  lv_col(g);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
+  __shared__ LvScratch<A> sc;
+  __shared__ double s_yb;
+  const int tid = threadIdx.x;
+  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int cnt = (int)min((int64_t)LV_TILE, g.n_act - T0);
+  fexp_table_init(sc.tab);
+  if (KMODE == 2) lv_carries<A>(sc, g.aggs, g.lseg, g.ntiles);
+  const int64_t smask = (int64_t(1) << g.lseg) - 1;
+  if (tid == 0) s_yb = (T0 & smask) != 0 ? lv_y(g, T0 - 1) : 0.0;
+  __syncthreads();
+#pragma unroll 1
+  for (int i = tid; i < cnt; i += LV_BLOCK) {
+    const Elem el = lv_elem(g, T0 + i);
+    const int pi = lvpad(i);
+    E.d[pi] = el.y;
+    E.u[pi] = el.u;
+    E.a[pi] = el.a;
+    E.ea[pi] = fexp_neg(el.a, sc.tab);
+    E.ch[i] = (signed char)el.ch;
+    E.rl[i] = el.r;
+  }
+  __syncthreads();
+  lv_engine<A>(E, sc, cnt, T0, smask, g.n_act, KMODE, s_yb, g.aggs);
+  if (KMODE == 2) {
+#pragma unroll 1
+    for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[E.rl[i]] += E.o[lvpad(i)];
   }
 }
 
 // ---------------------------------------------------------------------------
-// Host side: pass list and launches.
+// Host side.
+static size_t lv_smem_fused() { return sizeof(LvElems) + sizeof(LvPoints); }
+static size_t lv_smem_pass() { return sizeof(LvElems); }
 
 template <class A>
-static cudaError_t lv_set_attr() {
+static cudaError_t lv_set_attrs() {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_level<A, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(LvSmem))))
+  const int fused = (int)lv_smem_fused(), pass = (int)lv_smem_pass();
+  if ((e = cudaFuncSetAttribute(k_low2<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
     return e;
-  if ((e = cudaFuncSetAttribute(k_level<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(LvSmem))))
+  if ((e = cudaFuncSetAttribute(k_low3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
     return e;
-  return cudaFuncSetAttribute(k_level<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(LvSmem));
+  if ((e = cudaFuncSetAttribute(k_mid3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
+    return e;
+  if ((e = cudaFuncSetAttribute(k_pass<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
+    return e;
+  return cudaFuncSetAttribute(k_pass<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass);
 }
 
 template <class A>
-static gp_status lv_launch_pass(PassDesc pd, cudaStream_t s, int* launches) {
+static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   static bool attr = false;
   if (!attr) {
-    GPM_CUDA(lv_set_attr<A>());
+    GPM_CUDA(lv_set_attrs<A>());
     attr = true;
   }
-  const int tiles = (int)((pd.n_act + LV_TILE - 1) / LV_TILE);
-  pd.ntiles = tiles;
-  if (pd.lseg <= LV_LOGTILE) {
-    k_level<A, 0><<<tiles, LV_BLOCK, sizeof(LvSmem), s>>>(pd);
-    *launches += 1;
-  } else {
-    k_level<A, 1><<<tiles, LV_BLOCK, sizeof(LvSmem), s>>>(pd);
-    k_level<A, 2><<<tiles, LV_BLOCK, sizeof(LvSmem), s>>>(pd);
-    *launches += 2;
-  }
-  GPM_CUDA(cudaGetLastError());
-  return GP_OK;
-}
-
-template <class A>
-static gp_status lv_all_passes(Plan& pl, const double* u_rank, cudaStream_t s, int* launches) {
   const int64_t n = pl.n;
   const int L = pl.L;
-  PassDesc pd;
-  pd.t1 = pl.t.as<double>();
-  pd.t2 = pl.t.as<double>() + n;
-  pd.t3 = pl.d == 3 ? pl.t.as<double>() + 2 * n : nullptr;
-  pd.u = u_rank;
-  pd.acc = pl.acc.as<double>();
-  pd.aggs = pl.aggs.as<LvAgg>();
-  pd.n = n;
-  pd.mode = pl.d;
-  for (int l1 = 1; l1 <= L; ++l1) {
-    // outer node activity: the last node has cross pairs only if its mid < n
+  LvArgs g{};
+  g.ord2 = pl.ord2.as<int>();
+  g.ord3 = pl.ord3.as<int>();
+  g.t1 = pl.t.as<double>();
+  g.t2 = pl.t.as<double>() + n;
+  g.t3 = pl.d == 3 ? pl.t.as<double>() + 2 * n : nullptr;
+  g.u = nullptr;
+  g.pts = reinterpret_cast<const Pt4*>(pl.pts.ptr);
+  g.lb = pl.d == 2 ? pl.near_lb2 : pl.near_lb3;
+  g.lb2 = pl.near_lb3m;
+  g.acc = pl.acc.as<double>();
+  g.aggs = pl.aggs.as<LvAgg>();
+  g.n = n;
+  g.L = L;
+  g.mode = pl.d;
+  const int tiles = (int)((n + LV_TILE - 1) / LV_TILE);
+  g.agg_stride = 2 * (int64_t)tiles;
+  const dim3 gt(tiles, nrhs);
+  // fused low levels (writes acc for every point: no memset needed)
+  if (pl.d == 2)
+    k_low2<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
+  else
+    k_low3<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
+  *launches += 1;
+  GPM_CUDA(cudaGetLastError());
+  auto pass = [&](const int* ord, const int* ord2l1, int lseg, int l1, int64_t nact) -> gp_status {
+    if (nact <= 0) return GP_OK;
+    g.ord = ord;
+    g.ord2l1 = ord2l1;
+    g.lseg = lseg;
+    g.l1 = l1;
+    g.n_act = nact;
+    g.ntiles = (int)((nact + LV_TILE - 1) / LV_TILE);
+    k_pass<A, 1><<<dim3(g.ntiles, nrhs), LV_BLOCK, lv_smem_pass(), s>>>(g);
+    k_pass<A, 2><<<dim3(g.ntiles, nrhs), LV_BLOCK, lv_smem_pass(), s>>>(g);
+    *launches += 2;
+    GPM_CUDA(cudaGetLastError());
+    return GP_OK;
+  };
+  for (int l1 = LV_LOGTILE + 1; l1 <= L; ++l1) {
     const int64_t b_last = (n - 1) >> l1;
     const int64_t mid1 = (b_last << l1) + (int64_t(1) << (l1 - 1));
     const int64_t nact1 = mid1 >= n ? (b_last << l1) : n;
     if (pl.d == 2) {
-      if (nact1 <= 0) continue;
-      pd.ord = pl.ord2.as<int>() + (size_t)(l1 - 1) * n;
-      pd.ord2l1 = nullptr;
-      pd.lseg = l1;
-      pd.l1 = l1;
-      pd.n_act = nact1;
-      GPM_TRY(lv_launch_pass<A>(pd, s, launches));
+      GPM_TRY(pass(pl.ord2.as<int>() + (size_t)(l1 - 1) * n, nullptr, l1, l1, nact1));
     } else {
-      for (int l2 = 1; l2 <= l1; ++l2) {
+      g.l1 = l1;
+      k_mid3<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
+      *launches += 1;
+      GPM_CUDA(cudaGetLastError());
+      for (int l2 = LV_LOGTILE + 1; l2 <= l1; ++l2) {
         const int64_t c_last = (n - 1) >> l2;
         const int64_t mid2 = (c_last << l2) + (int64_t(1) << (l2 - 1));
         int64_t nact = nact1;
         if (mid2 >= n) nact = std::min(nact, c_last << l2);
-        if (nact <= 0) continue;
-        pd.ord = pl.ord3.as<int>() + ((size_t)(l1 - 1) * l1 / 2 + (l2 - 1)) * n;
-        pd.ord2l1 = pl.ord2.as<int>() + (size_t)(l1 - 1) * n;
-        pd.lseg = l2;
-        pd.l1 = l1;
-        pd.n_act = nact;
-        GPM_TRY(lv_launch_pass<A>(pd, s, launches));
+        GPM_TRY(pass(pl.ord3.as<int>() + ((size_t)(l1 - 1) * l1 / 2 + (l2 - 1)) * n,
+                     pl.ord2.as<int>() + (size_t)(l1 - 1) * n, l2, l1, nact));
       }
     }
   }
   return GP_OK;
 }
 
-gp_status level_passes(Plan& pl, const double* u_rank, cudaStream_t s, int* launches) {
+// pack the rank-order point records (t1, t2, t3, u) used by every level kernel
+__global__ void k_pack(const double* __restrict__ t, int64_t n, int d,
+                       const int* __restrict__ perm, const double* __restrict__ v, int64_t n_src,
+                       int64_t vstride, Pt4* __restrict__ pts) {
+  v += blockIdx.y * vstride;
+  pts += blockIdx.y * n;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    Pt4 p;
+    p.t1 = t[r];
+    p.t2 = t[n + r];
+    p.t3 = d == 3 ? t[2 * n + r] : 0.0;
+    if (perm) {
+      const int i = __ldg(perm + r);
+      p.u = i < n_src ? __ldg(v + i) : 0.0;
+    } else {
+      p.u = v[r];
+    }
+    pts[r] = p;
+  }
+}
+
+gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((pl.n + 255) / 256, 148 * 8));
+  const int64_t vstride = user_order ? pl.n_src : pl.n;
+  k_pack<<<dim3(grid, nrhs), 256, 0, s>>>(pl.t.as<double>(), pl.n, pl.d,
+                                          user_order ? pl.perm.as<int>() : nullptr, v,
+                                          user_order ? pl.n_src : pl.n, vstride,
+                                          reinterpret_cast<Pt4*>(pl.pts.ptr));
+  GPM_CUDA(cudaGetLastError());
+  return GP_OK;
+}
+size_t level_pt_bytes() { return sizeof(Pt4); }
+
+gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
   if (pl.d == 2) {
     if (!prod) {
-      if (pl.P == 0) return lv_all_passes<Alg<0, 2, false>>(pl, u_rank, s, launches);
-      if (pl.P == 1) return lv_all_passes<Alg<1, 2, false>>(pl, u_rank, s, launches);
-      return lv_all_passes<Alg<2, 2, false>>(pl, u_rank, s, launches);
+      if (pl.P == 0) return lv_run<Alg<0, 2, false>>(pl, nrhs, s, launches);
+      if (pl.P == 1) return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
+      return lv_run<Alg<2, 2, false>>(pl, nrhs, s, launches);
     }
-    if (pl.P == 0) return lv_all_passes<Alg<0, 2, true>>(pl, u_rank, s, launches);
-    if (pl.P == 1) return lv_all_passes<Alg<1, 2, true>>(pl, u_rank, s, launches);
-    return lv_all_passes<Alg<2, 2, true>>(pl, u_rank, s, launches);
+    if (pl.P == 0) return lv_run<Alg<0, 2, true>>(pl, nrhs, s, launches);
+    if (pl.P == 1) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
+    return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
   }
-  if (pl.P == 0) return lv_all_passes<Alg<0, 4, false>>(pl, u_rank, s, launches);
-  if (pl.P == 1) return lv_all_passes<Alg<1, 4, false>>(pl, u_rank, s, launches);
-  return lv_all_passes<Alg<2, 4, false>>(pl, u_rank, s, launches);
+  if (pl.P == 0) return lv_run<Alg<0, 4, false>>(pl, nrhs, s, launches);
+  if (pl.P == 1) return lv_run<Alg<1, 4, false>>(pl, nrhs, s, launches);
+  return lv_run<Alg<2, 4, false>>(pl, nrhs, s, launches);
 }
 
 int64_t level_tiles(int64_t n) { return (n + LV_TILE - 1) / LV_TILE; }

@@ -75,6 +75,8 @@ struct Plan {
   DevBuf bar;                       // grid barrier words (d = 1 cooperative kernel)
   DevBuf stage_in, stage_out;       // gp_kmvm_host staging
   DevBuf dbg;                       // d=1 phase timestamps (env GPM_D1_TIMING)
+  DevBuf pts;                       // d>=2: packed (t1, t2, t3, u) per rank, rebuilt per apply
+  int near_lb2 = 7, near_lb3 = 9, near_lb3m = 8;   // near-field block log2 sizes
   // d = 1 launch geometry
   int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;
   int64_t d1_chunk = 0;
@@ -89,9 +91,10 @@ void plan_free(Plan& pl);
 
 // apply.cu
 // Rank-space apply: out_rank = K u_rank (no nugget).  u_rank, out_rank: n doubles.
-gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, cudaStream_t s);
+gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s);
 // User-order apply with gather/scatter: out = K v restricted to targets (unions).
-gp_status apply_user(Plan& pl, const double* v, double* out, cudaStream_t s);
+// Columns: v stride n_src, out stride n - tgt_off.
+gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s);
 gp_status apply_prepare(Plan& pl);   // launch geometry + scratch
 gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cudaStream_t s);
 int64_t apply_model_bytes(const Plan& pl);

@@ -264,6 +264,21 @@ bool small_solve(std::vector<double> G, std::vector<double> g, int k, std::vecto
 
 }  // namespace
 
+// Q[:, c] = K P[:, c] for the active columns: maximal runs of consecutive active columns
+// go through one multi-RHS apply.
+static gp_status apply_active(Plan& pl, const double* P, double* Q, const std::vector<char>& act,
+                              int k, cudaStream_t s) {
+  const size_t n = (size_t)pl.n;
+  for (int c = 0; c < k;) {
+    if (!act[c]) { ++c; continue; }
+    int e = c;
+    while (e < k && act[e]) ++e;
+    GPM_TRY(apply_rank(pl, P + c * n, Q + c * n, e - c, s));
+    c = e;
+  }
+  return GP_OK;
+}
+
 gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
                                  const double* Hz, int Lb, double* out, cudaStream_t s) {
   const int nb = Hz ? Lb : 1 + d;
@@ -343,8 +358,7 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
     for (int c = 0; c < k; ++c) any |= active[c] != 0;
     while (any && it < max_iter) {
       for (int step = 0; step < check_every && it < max_iter; ++step, ++it) {
-        for (int c = 0; c < k; ++c)
-          if (active[c]) GPM_TRY(apply_rank(pl, Pm + (size_t)c * n, Q + (size_t)c * n, s));
+        GPM_TRY(apply_active(pl, Pm, Q, active, k, s));
         k_pq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, Q, n, sigma2, part);
         k_alpha<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, al, status, bd_iter, it);
         k_update<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(X, R, Pm, Q, al, n, part);
@@ -363,8 +377,7 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
         if (hst[c] == 2) any = false;   // stop on breakdown
     }
     // true residual R = B - (K X + sigma2 X)
-    for (int c = 0; c < k; ++c)
-      GPM_TRY(apply_rank(pl, X + (size_t)c * n, Q + (size_t)c * n, s));
+    GPM_TRY(apply_rank(pl, X, Q, k, s));
     k_resid<<<g1((int64_t)nk), 256, 0, s>>>(B, Q, X, sigma2, (int64_t)nk, R);
     k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(R, n, part);
     k_finish_sum<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr);

@@ -10,7 +10,7 @@ c = W.CONFIGS[2]
 names = ["tma+load", "pass1", "scan", "grid.sync", "carries", "pass2+store"]
 for n in (10000, 1000000):
     x = torch.from_numpy(W.config_points(c)[:n]).cuda()
-    for shape in (0, 1, 2, 3):
+    for shape in (2,):
         plan = g.Plan(x, g.Kernel(int(os.environ.get("NU2", "5")), c.ell))
         plan.set_option(1, shape)
         v = torch.randn(n, dtype=torch.float64, device="cuda")
@@ -22,4 +22,6 @@ for n in (10000, 1000000):
             st = [plan.query(8 + k) for k in range(6)]
             parts = [f"{nm}={(st[i] - (st[i-1] if i else 0)) / 1e3:.2f}" for i, nm in enumerate(names)]
             parts.append(f"total={st[-1]/1e3:.2f}")
+            mx = [plan.query(20 + k) for k in range(6)]
+            parts.append("| max: " + " ".join(f"{nm}={m/1e3:.2f}" for nm, m in zip(names, mx)))
             print(f"n={n} shape={shape} rank={rank} " + " ".join(parts), flush=True)
