@@ -223,3 +223,42 @@ def test_cg_breakdown_on_indefinite_l1(gpm):
     with pytest.raises(gpm.GPError) as e:
         plan.cg_solve(to_dev(y), 0.01, mean=gpm.MEAN_AFFINE, rtol=1e-8)
     assert e.value.name == "BREAKDOWN"
+
+
+# ------------------------------------------------------------------ d >= 2 launch structure
+
+@pytest.mark.parametrize("lb", ["0,0,0", "3,4,2", "5,7,6", "10,10,10"])
+@pytest.mark.parametrize("d,two_nu,form", [(2, 3, 0), (2, 5, 1), (3, 5, 0), (3, 1, 0)])
+def test_near_field_block_sizes(gpm, monkeypatch, lb, d, two_nu, form):
+    """Every split of the D&C levels between exact near-field block sums, the fused
+    scan kernels, the d=3 mid kernel and the carried multi-tile passes gives the same
+    K.v (N = 6000 > 4 tiles: levels up to 13, l1 > 10 and l2 > 10 all exercised)."""
+    monkeypatch.setenv("GPM_NEAR_LB", lb)
+    n = 6000
+    x = _points("ties", n, d, 300 + d)
+    v = np.random.default_rng(5).standard_normal(n)
+    ell = (0.1, 0.2, 0.3)[:d]
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.0, form=form))
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    rows = np.arange(0, n, 3)
+    check_rows(out, x, v, two_nu, FORM[form], ell, 1.0, rows=rows, what=f"near lb={lb} d={d}")
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_multi_rhs_batches(gpm, d):
+    """nrhs = 11 (> one batch of 8 columns) equals column-by-column applies bitwise."""
+    import torch
+    n = 3000
+    x = _points("uniform", n, d, 70 + d)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.2, 0.3)[:d]))
+    V = to_dev(np.random.default_rng(d).standard_normal((11, n)))
+    KV = plan.kmvm(V)
+    for c in (0, 7, 8, 10):
+        assert torch.equal(KV[c], plan.kmvm(V[c].contiguous()))
+    z = to_dev(_points("uniform", 500, d, 80 + d))
+    cr = plan.cross(z)
+    KZ = cr.kzx(V)
+    for c in (0, 9):
+        assert torch.equal(KZ[c], cr.kzx(V[c].contiguous()))
+    ref = oracle.kzx_rows(x, V[9].cpu().numpy(), z.cpu().numpy(), 3, "l1", (0.1, 0.2, 0.3)[:d])
+    assert np.max(np.abs(KZ[9].cpu().numpy() - ref)) < 1e-9 * np.abs(ref).max() * 50
