@@ -373,6 +373,33 @@ def run_ours(args, ws, rank, local):
                 "launch_ms_mean": mr * 1e3, "model_bytes": rb, "hbm_gbs": rb / mr / 1e9,
                 "frac_hbm": rb / mr / 1e9 / hbm}
             pr.close()
+        # f1: batched multi-RHS applies (one gp_kmvm call with nb fresh vectors)
+        for nb, rank_order in ((16, False), (16, True)):
+            pb = g.Plan(x, g.Kernel(5, cfg.ell), stream)
+            VB = V[:nb] if not rank_order else torch.stack([pb.to_rank(V[i]) for i in range(nb)])
+            OB = torch.empty_like(VB)
+            lib = g.load_library()
+            f = lib.gp_kmvm_rank if rank_order else lib.gp_kmvm
+            vp, op, sp = ctypes.c_void_p(VB.data_ptr()), ctypes.c_void_p(OB.data_ptr()), ctypes.c_void_p(stream.cuda_stream)
+            reps = 20
+            for _ in range(3):
+                f(pb._h, vp, nb, op, sp)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                f(pb._h, vp, nb, op, sp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sec = max_over_ranks(e0.elapsed_time(e1) / 1e3, ws)
+            key = f"config2_d1_nu52_batched{nb}_{'rank' if rank_order else 'user'}_order"
+            bpm = n * (24 if rank_order else 28)
+            per = sec / (reps * nb)
+            extras[key] = {"api": "gp_kmvm_rank" if rank_order else "gp_kmvm", "nrhs_per_call": nb,
+                           "mvm_per_s": sum_over_ranks(reps * nb, ws) / sec,
+                           "us_per_mvm": per * 1e6, "hbm_gbs": bpm / per / 1e9,
+                           "frac_hbm": bpm / per / 1e9 / hbm}
+            pb.close()
         extras.update(extra_configs(g, dev, stream, ws, rank, hbm, args))
     if extras:
         line["extra"] = extras

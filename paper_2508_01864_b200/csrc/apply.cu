@@ -11,7 +11,8 @@
 namespace gpm {
 
 gp_status d1_prepare(Plan& pl);
-gp_status d1_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s);
+gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
+                    cudaStream_t s);
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches);
 gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
 size_t level_pt_bytes();
@@ -119,21 +120,12 @@ gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cu
 }
 
 gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s) {
-  if (pl.d == 1) {
-    for (int c = 0; c < nrhs; ++c)
-      GPM_TRY(d1_launch(pl, u_rank + (size_t)c * pl.n, out_rank + (size_t)c * pl.n, false, s));
-    return GP_OK;
-  }
+  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, nrhs, false, s);
   return apply_levels(pl, u_rank, out_rank, nrhs, false, s);
 }
 
 gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s) {
-  if (pl.d == 1) {
-    const int64_t m = pl.n - pl.tgt_off;
-    for (int c = 0; c < nrhs; ++c)
-      GPM_TRY(d1_launch(pl, v + (size_t)c * pl.n_src, out + (size_t)c * m, true, s));
-    return GP_OK;
-  }
+  if (pl.d == 1) return d1_launch(pl, v, out, nrhs, true, s);
   return apply_levels(pl, v, out, nrhs, true, s);
 }
 

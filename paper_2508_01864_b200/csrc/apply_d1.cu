@@ -477,7 +477,8 @@ static cudaError_t d1_set_attr() {
 }
 
 gp_status df_shape_info(int shape, int* capacity, int* max_grid);
-gp_status df_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s);
+gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
+                    cudaStream_t s);
 int df_default_shape();
 
 gp_status d1_prepare(Plan& pl) {
@@ -505,7 +506,7 @@ gp_status d1_prepare(Plan& pl) {
       pl.d1_grid = (int)g;
       pl.d1_chunk = chunk;
       pl.d1_path = 1;
-      GPM_TRY(pl.aggs.alloc(96 * (size_t)g));   // D1Pub records (apply_d1_fast.cu)
+      GPM_TRY(pl.aggs.alloc(96 * 2 * (size_t)g));   // D1Pub records x 2 (apply_d1_fast.cu)
       GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
       GPM_TRY(pl.bar.alloc(64));
       GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));
@@ -542,8 +543,14 @@ gp_status d1_prepare(Plan& pl) {
   return GP_OK;
 }
 
-gp_status d1_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s) {
-  if (pl.d1_path == 1) return df_launch(pl, v, out, user_order, s);
+gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
+                    cudaStream_t s) {
+  if (pl.d1_path == 1) return df_launch(pl, v, out, nrhs, user_order, s);
+  const int64_t vs = user_order ? pl.n_src : pl.n, os = user_order ? pl.n - pl.tgt_off : pl.n;
+  for (int c = 0; c + 1 < nrhs; ++c)
+    GPM_TRY(d1_launch(pl, v + c * vs, out + c * os, 1, user_order, s));
+  v += (nrhs - 1) * vs;
+  out += (nrhs - 1) * os;
   D1Args a;
   a.ts = pl.t.as<double>();
   a.perm = user_order ? pl.perm.as<int>() : nullptr;

@@ -32,8 +32,10 @@ struct DFArgs {
   double* out;        // output: user order (targets only) or rank order
   int64_t n, n_src, tgt_off, chunk;
   int user_order;
+  int nrhs;               // columns processed in this launch (multi-RHS, §8(f) f1)
+  int64_t vstride, ostride;
   double os2;
-  D1Agg* chunk_aggs;      // D1Pub[grid] (see below)
+  D1Agg* chunk_aggs;      // D1Pub[2][grid] (see below; double-buffered per column)
   unsigned* bar;          // [0]: finished-CTA counter, [2..3]: 64-bit launch epoch
   unsigned long long* dbg;   // optional per-CTA phase timestamps (GPM_D1_TIMING)
 };
@@ -246,6 +248,22 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   }
   DF_STAMP(1);
 
+#pragma unroll 1
+  for (int col = 0; col < a.nrhs; ++col) {
+  const double* vcol = a.v + col * a.vstride;
+  double* ocol = a.out + col * a.ostride;
+  D1Pub* pubc = pub + (col & 1) * gridDim.x;   // slots alternate: a CTA runs <= 1 sync ahead
+  if (col > 0) {
+    __syncthreads();   // s_u of the previous column fully consumed
+    if (!a.user_order) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int j = k * BLOCK + tid;
+        s_u[j] = j < cnt ? __ldg(vcol + c0 + j) : 0.0;
+      }
+      __syncthreads();
+    }
+  }
   // ---- gathers (user order) first: all ITEMS loads in flight ...
   double uu[ITEMS];
   if (a.user_order) {
@@ -253,11 +271,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     for (int k = 0; k < ITEMS; ++k) {
       const int j = j0 + k;
       const int pi = j < cnt ? s_pi[j] : INT_MAX;
-      uu[k] = pi < a.n_src ? __ldg(a.v + pi) : 0.0;
+      uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
     }
   }
-  // ... while the gaps and e^{-gap} are computed (independent of v)
-  {
+  // ... while the gaps and e^{-gap} are computed (independent of v; first column only)
+  if (col == 0) {
     double tp = tprev;
 #pragma unroll 1
     for (int k = 0; k < ITEMS; ++k) {
@@ -336,7 +354,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   __syncthreads();
   // ---- publish the chunk aggregate, grid-wide sync (cooperative launch)
   if (tid == 0) {
-    D1Pub* me = pub + blockIdx.x;
+    D1Pub* me = pubc + blockIdx.x;
     me->v[0] = s_tot[0][0];
     me->v[1] = s_tot[0][1];
 #pragma unroll
@@ -362,7 +380,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
       const bool take = fw ? (jj < b) : (jj > b && jj < G);
       SF<P> X = sf_id<P>();
       if (take) {
-        const D1Pub* o = pub + jj;
+        const D1Pub* o = pubc + jj;
         X.D = __ldcg(&o->v[0]);
         X.E = __ldcg(&o->v[1]);
 #pragma unroll
@@ -427,7 +445,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     if (a.user_order) {
       if (j < cnt) {
         const int pi = s_pi[j];
-        if (pi >= a.tgt_off) a.out[pi - a.tgt_off] = val;
+        if (pi >= a.tgt_off) ocol[pi - a.tgt_off] = val;
       }
     } else {
       s_u[j] = val;   // staged for a coalesced write-back
@@ -438,9 +456,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
       const int j = k * BLOCK + tid;
-      if (j < cnt) a.out[c0 + j] = s_u[j];
+      if (j < cnt) ocol[c0 + j] = s_u[j];
     }
   }
+  }   // column loop
   if (a.dbg) {
     __syncthreads();
     DF_STAMP(6);
@@ -508,7 +527,8 @@ gp_status df_shape_info(int shape, int* capacity, int* max_grid) {
   return GP_OK;
 }
 
-gp_status df_launch(Plan& pl, const double* v, double* out, bool user_order, cudaStream_t s) {
+gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
+                    cudaStream_t s) {
   const DFShape& sh = g_shapes[pl.d1_shape];
   DFArgs a;
   a.ts = pl.t.as<double>();
@@ -520,6 +540,9 @@ gp_status df_launch(Plan& pl, const double* v, double* out, bool user_order, cud
   a.tgt_off = user_order ? pl.tgt_off : 0;
   a.chunk = pl.d1_chunk;
   a.user_order = user_order ? 1 : 0;
+  a.nrhs = nrhs;
+  a.vstride = user_order ? pl.n_src : pl.n;
+  a.ostride = user_order ? pl.n - pl.tgt_off : pl.n;
   a.os2 = pl.os2;
   a.chunk_aggs = pl.aggs.as<D1Agg>();
   a.bar = pl.bar.as<unsigned>();
