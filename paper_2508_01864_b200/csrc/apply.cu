@@ -16,6 +16,8 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches);
 gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
 size_t level_pt_bytes();
+int level_nparts(const Plan& pl);
+gp_status level_setup(Plan& pl, cudaStream_t s);
 int64_t level_tiles(int64_t n);
 
 namespace {
@@ -32,14 +34,18 @@ __global__ void k_gather(const int* __restrict__ perm, const double* __restrict_
 // out[perm[r] - tgt_off] = os2 (u[r] + acc[r]) for targets; perm == nullptr: rank order.
 // u is read from the packed point records (stride 4 doubles, u at offset 3).
 __global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ pts,
-                           const double* __restrict__ acc, int64_t n, int64_t tgt_off,
-                           double os2, double* __restrict__ out, int64_t ostride) {
+                           const double* __restrict__ acc, const double* __restrict__ part,
+                           int nparts, int64_t n, int64_t tgt_off, double os2,
+                           double* __restrict__ out, int64_t ostride) {
   pts += blockIdx.y * 4 * n;
   acc += blockIdx.y * n;
+  part += blockIdx.y * nparts * n;
   out += blockIdx.y * ostride;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const double val = os2 * (pts[4 * r + 3] + acc[r]);
+    double a = acc[r];
+    for (int p = 0; p < nparts; ++p) a += part[(int64_t)p * n + r];   // fixed order
+    const double val = os2 * (pts[4 * r + 3] + a);
     if (perm) {
       const int i = __ldg(perm + r);
       if (i >= tgt_off) out[i - tgt_off] = val;
@@ -71,6 +77,12 @@ gp_status apply_prepare(Plan& pl) {
     pl.launches_per_apply = 1;
   } else {
     GPM_TRY(level_buffers(pl, 1));
+    // stage the carried passes' structure (lv_elem reads t through the packed records)
+    if (!pl.hpbuf.bytes) {
+      GPM_TRY(level_pack(pl, pl.t.as<double>(), 1, false, nullptr));   // u := t1 (unused)
+      GPM_TRY(level_setup(pl, nullptr));
+      GPM_CUDA(cudaDeviceSynchronize());
+    }
     if (const char* e = getenv("GPM_NEAR_LB")) {   // tuning knob: "lb2,lb3,lb3m"
       int a = pl.near_lb2, b = pl.near_lb3, c = pl.near_lb3m;
       if (sscanf(e, "%d,%d,%d", &a, &b, &c) >= 1) { pl.near_lb2 = a; pl.near_lb3 = b; pl.near_lb3m = c; }
@@ -86,8 +98,11 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
   const size_t need = (size_t)nrhs * pl.n;
   if (pl.acc.bytes < sizeof(double) * need) GPM_TRY(pl.acc.alloc(sizeof(double) * need));
   if (pl.pts.bytes < level_pt_bytes() * need) GPM_TRY(pl.pts.alloc(level_pt_bytes() * need));
-  const size_t ag = sizeof(LvAgg) * 2 * (size_t)level_tiles(pl.n) * nrhs;
+  const size_t ag = sizeof(LvAgg) * 2 * (size_t)level_tiles(pl.n) * nrhs *
+                   std::max(1, pl.hp_npass);
   if (pl.aggs.bytes < ag) GPM_TRY(pl.aggs.alloc(ag));
+  const size_t pb = sizeof(double) * (size_t)std::max(1, level_nparts(pl)) * pl.n * nrhs;
+  if (pl.part.bytes < pb) GPM_TRY(pl.part.alloc(pb));
   return GP_OK;
 }
 
@@ -102,8 +117,9 @@ static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, 
     GPM_TRY(level_pack(pl, v + c0 * vstride, nb, user_order, s));   // packed points (+ gather)
     GPM_TRY(level_passes(pl, nb, s, &launches));   // first level launch initialises acc
     k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
-        user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(), pl.n,
-        user_order ? pl.tgt_off : 0, pl.os2, out + c0 * ostride, ostride);
+        user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
+        pl.part.as<double>(), level_nparts(pl), pl.n, user_order ? pl.tgt_off : 0, pl.os2,
+        out + c0 * ostride, ostride);
     GPM_CUDA(cudaGetLastError());
     pl.launches_per_apply = launches + 2;   // + pack + epilogue (per batch of columns)
   }

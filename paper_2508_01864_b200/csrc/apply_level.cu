@@ -24,6 +24,7 @@
 //          all l2 <= 10 (the tile's points gathered once); aggregate + apply launches
 //          for (l1 > 10, l2 > 10).
 #include <algorithm>
+#include <vector>
 
 #include "algebra.cuh"
 #include "fexp.cuh"
@@ -189,19 +190,19 @@ __device__ __forceinline__ void lv_block_scan(const LSt<A::NS>& mine, LSt<A::NS>
 template <class A>
 __device__ __forceinline__ void lv_engine(LvElems& E, LvScratch<A>& sc, int cnt, int64_t T0,
                                           int64_t smask, int64_t nend, int mode,
-                                          double y_before, LvAgg* aggs) {
+                                          double y_before, LvAgg* aggs, bool preconv = false) {
   using S = LSt<A::NS>;
   const int tid = threadIdx.x;
   const int i0 = tid * LV_ITEMS;
   auto is_start = [&](int i) { return ((T0 + i) & smask) == 0; };
   auto is_end = [&](int i) { return (((T0 + i + 1) & smask) == 0) || (T0 + i + 1 == nend); };
 
-  // gaps and e^{-gap}
+  // gaps and e^{-gap} (unless staged by the setup, preconv)
   double yprev = 0.0;
-  if (i0 < cnt) yprev = i0 > 0 ? E.d[lvpad(i0 - 1)] : y_before;
-  __syncthreads();
+  if (!preconv && i0 < cnt) yprev = i0 > 0 ? E.d[lvpad(i0 - 1)] : y_before;
+  if (!preconv) __syncthreads();
 #pragma unroll 1
-  for (int k = 0; k < LV_ITEMS; ++k) {
+  for (int k = 0; k < LV_ITEMS && !preconv; ++k) {
     const int i = i0 + k;
     if (i < cnt) {
       const int pi = lvpad(i);
@@ -318,43 +319,59 @@ __device__ __forceinline__ void lv_engine(LvElems& E, LvScratch<A>& sc, int cnt,
   __syncthreads();
 }
 
-// tile carries from the aggregate launch: warp 0 forward, warp 1 backward
+// tile carries from the aggregate launch: warps 0-3 fold the forward aggregates of the
+// tiles before this one in its segment, warps 4-7 the backward ones after it; each lane
+// loads at most LV_CPL aggregates (all in flight), partials combined in order in smem.
+constexpr int LV_CPL = 2;
 template <class A>
-__device__ __forceinline__ void lv_carries(LvScratch<A>& sc, const LvAgg* aggs, int lseg,
-                                           int ntiles) {
+__device__ __forceinline__ void lv_carries(LvScratch<A>& sc, LSt<A::NS>* part, const LvAgg* aggs,
+                                           int lseg, int ntiles) {
   using S = LSt<A::NS>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp < 2) {
-    const int tps = 1 << (lseg - LV_LOGTILE);
-    const int t = blockIdx.x;
-    const int first = t & ~(tps - 1);
-    const int last = min(first + tps, ntiles) - 1;
-    const int lo = warp == 0 ? first : t + 1;
-    const int hi = warp == 0 ? t : last + 1;
-    const int per = (max(0, hi - lo) + 31) / 32;
-    S X = lid<A>();
+  const int tps = 1 << (lseg - LV_LOGTILE);
+  const int t = blockIdx.x;
+  const int first = t & ~(tps - 1);
+  const int last = min(first + tps, ntiles) - 1;
+  const bool fw = warp < 4;
+  const int w4 = warp & 3;
+  const int lo = fw ? first : t + 1;
+  const int hi = fw ? t : last + 1;
+  const int cntc = max(0, hi - lo);
+  const int span = (cntc + 3) / 4;                 // tiles per warp
+  const int per = (span + 31) / 32;                // tiles per lane (any segment length)
+  const int wlo = lo + w4 * span;
+  const int whi = min(hi, wlo + span);
+  S X = lid<A>();
 #pragma unroll 1
-    for (int k = 0; k < per; ++k) {
-      const int j = lo + lane * per + k;
-      if (j < hi) {
-        S g = agg_get<A::NS>(aggs + 2 * j + warp);
-        X = warp == 0 ? lcf<A>(X, g) : lcb<A>(X, g);
-      }
-    }
-#pragma unroll 1
-    for (int off = 1; off < 32; off <<= 1) {
-      S Y = lshfl<A::NS>(X, off, false);
-      if (lane + off < 32) X = warp == 0 ? lcf<A>(X, Y) : lcb<A>(X, Y);
-    }
-    if (lane == 0) {
+  for (int k0 = 0; k0 < per; k0 += LV_CPL) {       // LV_CPL loads in flight per step
+    S y[LV_CPL];
 #pragma unroll
-      for (int i = 0; i < A::NS; ++i) sc.carry[warp][i] = X.M[i];
+    for (int k = 0; k < LV_CPL; ++k) {
+      const int j = wlo + lane * per + k0 + k;
+      y[k] = (k0 + k < per && j < whi) ? agg_get<A::NS>(aggs + 2 * j + (fw ? 0 : 1)) : lid<A>();
     }
+#pragma unroll
+    for (int k = 0; k < LV_CPL; ++k) X = fw ? lcf<A>(X, y[k]) : lcb<A>(X, y[k]);
+  }
+#pragma unroll 1
+  for (int off = 1; off < 32; off <<= 1) {
+    S Y = lshfl<A::NS>(X, off, false);
+    if (lane + off < 32) X = fw ? lcf<A>(X, Y) : lcb<A>(X, Y);
+  }
+  if (lane == 0) part[warp] = X;
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const bool f = threadIdx.x == 0;
+    S Z = lid<A>();
+#pragma unroll 1
+    for (int w = 0; w < 4; ++w) Z = f ? lcf<A>(Z, part[w]) : lcb<A>(Z, part[4 + w]);
+#pragma unroll
+    for (int i = 0; i < A::NS; ++i) sc.carry[threadIdx.x][i] = Z.M[i];
   }
 }
 
-// Packed per-point record (rank order), rebuilt per apply by k_pack (apply.cu): one random
-// access touches one 32-byte sector instead of four.
+// Packed per-point record (rank order), rebuilt per apply by k_pack: one random access
+// touches one 32-byte sector instead of four.
 struct __align__(32) Pt4 {
   double t1, t2, t3, u;
 };
@@ -379,6 +396,9 @@ struct LvArgs {
   int64_t n_act;
   int mode;            // 2 or 3 (dimension)
   int64_t agg_stride;  // LvAgg records per right-hand side
+  double* part;        // [nparts][n] per-pass contributions (rank order), summed in order
+  int npass;           // carried passes (their part slots come first, then d=3 mid levels)
+  int64_t part_stride; // doubles per right-hand side in part
 };
 
 // right-hand side handled by this CTA (blockIdx.y): offset the per-column buffers
@@ -387,6 +407,7 @@ __device__ __forceinline__ void lv_col(LvArgs& g) {
   g.pts += c * g.n;
   g.acc += c * g.n;
   g.aggs += c * g.agg_stride;
+  g.part += c * g.part_stride;
 }
 
 __device__ __forceinline__ int ord3_index(int l1, int l2) { return (l1 - 1) * l1 / 2 + (l2 - 1); }
@@ -461,8 +482,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low2(LvArgs g) {
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
     const Pt4 p = g.pts[T0 + i];
     Pt.u[i] = p.u;
     Pt.t1[i] = p.t1;
@@ -477,8 +498,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low2(LvArgs g) {
 #pragma unroll 1
   for (int l = lb + 1; l <= lmax; ++l) {
     const int* ord = g.ord2 + (size_t)(l - 1) * g.n + T0;
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
       const int r = __ldg(ord + i) - (int)T0;
       const int mid = ((i >> l) << l) + (1 << (l - 1));
       const bool act = T0 + mid < g.n;
@@ -493,12 +514,12 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low2(LvArgs g) {
     }
     __syncthreads();
     lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l) - 1, g.n, 0, 0.0, nullptr);
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += LV_BLOCK) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
     __syncthreads();
   }
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[T0 + i] = Pt.acc[i];
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
 }
 
 // ---- fused low levels, d = 3: every (l1 <= min(10, L), l2 <= l1) of one tile
@@ -513,8 +534,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low3(LvArgs g) {
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
     const Pt4 p = g.pts[T0 + i];
     Pt.u[i] = p.u;
     Pt.t1[i] = p.t1;
@@ -529,15 +550,15 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low3(LvArgs g) {
 #pragma unroll 1
   for (int l1 = lb + 1; l1 <= lmax; ++l1) {
     __syncthreads();
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += LV_BLOCK)
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt)
       Pt.o2[i] = __ldg(g.ord2 + (size_t)(l1 - 1) * g.n + T0 + i) - (int)T0;
     __syncthreads();
 #pragma unroll 1
     for (int l2 = 1; l2 <= l1; ++l2) {
       const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
-#pragma unroll 1
-      for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+      for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
         const int q = __ldg(ord + i) - (int)T0;   // position in ord2[l1] (tile-local)
         const int r = Pt.o2[q];                   // rank (tile-local)
         const int mid1 = ((q >> l1) << l1) + (1 << (l1 - 1));
@@ -556,13 +577,13 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low3(LvArgs g) {
       }
       __syncthreads();
       lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l2) - 1, g.n, 0, 0.0, nullptr);
-#pragma unroll 1
-      for (int i = tid; i < cnt; i += LV_BLOCK) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+#pragma unroll
+      for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
     }
   }
   __syncthreads();
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[T0 + i] = Pt.acc[i];
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
 }
 
 // ---- d = 3, one outer level l1 > 10, all inner levels l2 <= 10 (tile = 1024 positions of
@@ -575,16 +596,21 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
   LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
   __shared__ LvScratch<A> sc;
   const int tid = threadIdx.x;
-  const int l1 = g.l1;
+  const int l1 = g.l1 + (int)blockIdx.z;   // one launch covers every outer level l1 > 10
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   const int64_t mid1 = ((T0 >> l1) << l1) + (int64_t(1) << (l1 - 1));
-  if (mid1 >= g.n) return;   // outer node without cross pairs (uniform per CTA)
+  double* slot = g.part + (int64_t)(g.npass + blockIdx.z) * g.n;
+  if (mid1 >= g.n) {   // outer node without cross pairs (uniform per CTA): zero contribution
+    const int* o2z = g.ord2 + (size_t)(l1 - 1) * g.n + T0;
+    for (int i = tid; i < cnt; i += LV_BLOCK) slot[__ldg(o2z + i)] = 0.0;
+    return;
+  }
   fexp_table_init(sc.tab);
   const double m1 = __ldg(g.t1 + mid1);
   const int* o2g = g.ord2 + (size_t)(l1 - 1) * g.n + T0;
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
     const int r = __ldg(o2g + i);
     const Pt4 p = g.pts[r];
     Pt.o2[i] = r;
@@ -601,8 +627,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
 #pragma unroll 1
   for (int l2 = lb2 + 1; l2 <= LV_LOGTILE; ++l2) {
     const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
       const int q = __ldg(ord + i) - (int)T0;    // tile-local position = point index
       const int mid2 = ((i >> l2) << l2) + (1 << (l2 - 1));
       const bool act = T0 + mid2 < g.n;
@@ -618,12 +644,12 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
     }
     __syncthreads();
     lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l2) - 1, g.n, 0, 0.0, nullptr);
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += LV_BLOCK) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
     __syncthreads();
   }
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[Pt.o2[i]] += Pt.acc[i];
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) slot[Pt.o2[i]] = Pt.acc[i];   // own slot: summed in order by the epilogue
 }
 
 // ---- one pass whose segments span several tiles (mode 1: aggregates, 2: apply)
@@ -665,6 +691,107 @@ __device__ __forceinline__ double lv_y(const LvArgs& g, int64_t pos) {
   return g.pts[__ldg(g.ord2l1 + __ldg(g.ord + pos))].t3;
 }
 
+// Structure of one carried (multi-tile) pass, precomputed at setup (it does not depend on
+// v): per position the gap to the previous position of its node, e^{-gap}, the split
+// offset alpha, e^{-alpha}, the rank and the channel.  37 B per position, read coalesced.
+struct HpView {
+  const double* d;
+  const double* e;
+  const double* a;
+  const double* ea;
+  const int* r;
+  const signed char* ch;
+};
+__host__ __device__ inline size_t hp_bytes(int64_t nact) {
+  return ((size_t)nact * 37 + 255) & ~size_t(255);
+}
+__host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nact) {
+  HpView v;
+  v.d = reinterpret_cast<const double*>(base);
+  v.e = v.d + nact;
+  v.a = v.e + nact;
+  v.ea = v.a + nact;
+  v.r = reinterpret_cast<const int*>(v.ea + nact);
+  v.ch = reinterpret_cast<const signed char*>(v.r + nact);
+  return v;
+}
+
+__global__ void k_hp_prep(LvArgs g, unsigned char* base) {
+  __shared__ double tab[64];
+  fexp_table_init(tab);
+  __syncthreads();
+  HpView v = hp_view(base, g.n_act);
+  double* d = const_cast<double*>(v.d);
+  double* e = const_cast<double*>(v.e);
+  double* a = const_cast<double*>(v.a);
+  double* ea = const_cast<double*>(v.ea);
+  int* r = const_cast<int*>(v.r);
+  signed char* ch = const_cast<signed char*>(v.ch);
+  const int64_t smask = (int64_t(1) << g.lseg) - 1;
+  for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < g.n_act;
+       pos += (int64_t)gridDim.x * blockDim.x) {
+    const Elem el = lv_elem(g, pos);
+    const double dl = (pos & smask) == 0 ? 0.0 : el.y - lv_y(g, pos - 1);
+    d[pos] = dl;
+    e[pos] = fexp_neg(dl, tab);
+    a[pos] = el.a;
+    ea[pos] = fexp_neg(el.a, tab);
+    r[pos] = el.r;
+    ch[pos] = (signed char)el.ch;
+  }
+}
+
+// one carried pass of a batched launch (blockIdx.z selects the pass)
+struct HpDesc {
+  int64_t off;      // byte offset of the staged structure in hpbuf
+  int64_t nact;     // active positions
+  int lseg, ntiles;
+};
+
+template <class A, int KMODE>
+__global__ void __launch_bounds__(LV_BLOCK, 2) k_pass_hp(LvArgs g, const unsigned char* hpbase,
+                                                         const HpDesc* descs, int max_tiles) {
+  lv_col(g);
+  const HpDesc hd = descs[blockIdx.z];
+  if ((int)blockIdx.x >= hd.ntiles) return;     // uniform per CTA
+  const unsigned char* base = hpbase + hd.off;
+  g.lseg = hd.lseg;
+  g.n_act = hd.nact;
+  g.ntiles = hd.ntiles;
+  g.aggs += (int64_t)blockIdx.z * 2 * max_tiles;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
+  __shared__ LvScratch<A> sc;
+  __shared__ LSt<A::NS> s_part[LV_WARPS];
+  const int tid = threadIdx.x;
+  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int cnt = (int)min((int64_t)LV_TILE, g.n_act - T0);
+  fexp_table_init(sc.tab);
+  if (KMODE == 2) lv_carries<A>(sc, s_part, g.aggs, g.lseg, g.ntiles);
+  const HpView v = hp_view(base, g.n_act);
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
+    const int64_t pos = T0 + i;
+    const int pi = lvpad(i);
+    const int r = __ldg(v.r + pos);
+    E.rl[i] = r;
+    E.u[pi] = g.pts[r].u;
+    E.d[pi] = __ldg(v.d + pos);
+    E.e[pi] = __ldg(v.e + pos);
+    E.a[pi] = __ldg(v.a + pos);
+    E.ea[pi] = __ldg(v.ea + pos);
+    E.ch[i] = v.ch[pos];
+  }
+  __syncthreads();
+  const int64_t smask = (int64_t(1) << g.lseg) - 1;
+  lv_engine<A>(E, sc, cnt, T0, smask, g.n_act, KMODE, 0.0, g.aggs, true);
+  if (KMODE == 2) {   // own slot per pass: deterministic sum in the epilogue
+    double* slot = g.part + (int64_t)blockIdx.z * g.n;
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) slot[E.rl[i]] = E.o[lvpad(i)];
+  }
+}
+
 template <class A, int KMODE>
 __global__ void __launch_bounds__(LV_BLOCK, 2) k_pass(LvArgs g) {
   lv_col(g);
@@ -676,12 +803,13 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_pass(LvArgs g) {
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n_act - T0);
   fexp_table_init(sc.tab);
-  if (KMODE == 2) lv_carries<A>(sc, g.aggs, g.lseg, g.ntiles);
+  __shared__ LSt<A::NS> s_part[LV_WARPS];
+  if (KMODE == 2) lv_carries<A>(sc, s_part, g.aggs, g.lseg, g.ntiles);
   const int64_t smask = (int64_t(1) << g.lseg) - 1;
   if (tid == 0) s_yb = (T0 & smask) != 0 ? lv_y(g, T0 - 1) : 0.0;
   __syncthreads();
-#pragma unroll 1
-  for (int i = tid; i < cnt; i += LV_BLOCK) {
+#pragma unroll
+  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
     const Elem el = lv_elem(g, T0 + i);
     const int pi = lvpad(i);
     E.d[pi] = el.y;
@@ -694,8 +822,8 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_pass(LvArgs g) {
   __syncthreads();
   lv_engine<A>(E, sc, cnt, T0, smask, g.n_act, KMODE, s_yb, g.aggs);
   if (KMODE == 2) {
-#pragma unroll 1
-    for (int i = tid; i < cnt; i += LV_BLOCK) g.acc[E.rl[i]] += E.o[lvpad(i)];
+#pragma unroll
+    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) atomicAdd(g.acc + E.rl[i], E.o[lvpad(i)]);   // RED: each rank once per pass -> deterministic
   }
 }
 
@@ -716,8 +844,103 @@ static cudaError_t lv_set_attrs() {
     return e;
   if ((e = cudaFuncSetAttribute(k_pass<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
     return e;
+  if ((e = cudaFuncSetAttribute(k_pass_hp<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
+    return e;
+  if ((e = cudaFuncSetAttribute(k_pass_hp<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
+    return e;
   return cudaFuncSetAttribute(k_pass<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass);
 }
+
+// The carried passes of a plan, in apply order: (ord, ord2l1, lseg, l1, n_act).
+struct HPass {
+  const int* ord;
+  const int* ord2l1;
+  int lseg, l1;
+  int64_t nact;
+};
+static std::vector<HPass> high_passes(const Plan& pl) {
+  std::vector<HPass> v;
+  const int64_t n = pl.n;
+  for (int l1 = LV_LOGTILE + 1; l1 <= pl.L; ++l1) {
+    const int64_t b_last = (n - 1) >> l1;
+    const int64_t mid1 = (b_last << l1) + (int64_t(1) << (l1 - 1));
+    const int64_t nact1 = mid1 >= n ? (b_last << l1) : n;
+    if (pl.d == 2) {
+      if (nact1 > 0) v.push_back({pl.ord2.as<int>() + (size_t)(l1 - 1) * n, nullptr, l1, l1, nact1});
+    } else {
+      for (int l2 = LV_LOGTILE + 1; l2 <= l1; ++l2) {
+        const int64_t c_last = (n - 1) >> l2;
+        const int64_t mid2 = (c_last << l2) + (int64_t(1) << (l2 - 1));
+        int64_t nact = nact1;
+        if (mid2 >= n) nact = std::min(nact, c_last << l2);
+        if (nact > 0)
+          v.push_back({pl.ord3.as<int>() + ((size_t)(l1 - 1) * l1 / 2 + (l2 - 1)) * n,
+                       pl.ord2.as<int>() + (size_t)(l1 - 1) * n, l2, l1, nact});
+      }
+    }
+  }
+  return v;
+}
+
+static LvArgs lv_base_args(const Plan& pl) {
+  LvArgs g{};
+  const int64_t n = pl.n;
+  g.ord2 = pl.ord2.as<int>();
+  g.ord3 = pl.ord3.as<int>();
+  g.t1 = pl.t.as<double>();
+  g.t2 = pl.t.as<double>() + n;
+  g.t3 = pl.d == 3 ? pl.t.as<double>() + 2 * n : nullptr;
+  g.n = n;
+  g.L = pl.L;
+  g.mode = pl.d;
+  return g;
+}
+
+// setup: stage the structure of every carried pass (lv_elem reads t through pts, which
+// the caller packs first)
+gp_status level_setup(Plan& pl, cudaStream_t s) {
+  if (pl.d < 2) return GP_OK;
+  const std::vector<HPass> hp = high_passes(pl);
+  size_t total = 0;
+  for (const HPass& h : hp) total += hp_bytes(h.nact);
+  if (total == 0) return GP_OK;
+  GPM_TRY(pl.hpbuf.alloc(total));
+  {
+    std::vector<HpDesc> dv;
+    size_t o = 0;
+    int mt = 0;
+    for (const HPass& h : hp) {
+      const int nt = (int)((h.nact + LV_TILE - 1) / LV_TILE);
+      dv.push_back({(int64_t)o, h.nact, h.lseg, nt});
+      o += hp_bytes(h.nact);
+      mt = std::max(mt, nt);
+    }
+    pl.hp_tail.clear();
+    for (const HPass& h : hp) pl.hp_tail.push_back(h.nact < pl.n ? 1 : 0);
+    GPM_TRY(pl.hpdesc.alloc(sizeof(HpDesc) * dv.size()));
+    GPM_CUDA(cudaMemcpy(pl.hpdesc.ptr, dv.data(), sizeof(HpDesc) * dv.size(), cudaMemcpyHostToDevice));
+    pl.hp_npass = (int)dv.size();
+    pl.hp_maxtiles = mt;
+  }
+  LvArgs g = lv_base_args(pl);
+  g.pts = reinterpret_cast<const Pt4*>(pl.pts.ptr);
+  size_t off = 0;
+  for (const HPass& h : hp) {
+    g.ord = h.ord;
+    g.ord2l1 = h.ord2l1;
+    g.lseg = h.lseg;
+    g.l1 = h.l1;
+    g.n_act = h.nact;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h.nact + 255) / 256, 148 * 8));
+    k_hp_prep<<<grid, 256, 0, s>>>(g, pl.hpbuf.as<unsigned char>() + off);
+    GPM_CUDA(cudaGetLastError());
+    off += hp_bytes(h.nact);
+  }
+  pl.struct_bytes += (int64_t)total;
+  return GP_OK;
+}
+
+int level_nparts(const Plan& pl);
 
 template <class A>
 static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
@@ -744,7 +967,10 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   g.L = L;
   g.mode = pl.d;
   const int tiles = (int)((n + LV_TILE - 1) / LV_TILE);
-  g.agg_stride = 2 * (int64_t)tiles;
+  g.agg_stride = 2 * (int64_t)tiles * std::max(1, pl.hp_npass);
+  g.part = pl.part.as<double>();
+  g.npass = pl.hp_npass;
+  g.part_stride = (int64_t)level_nparts(pl) * n;
   const dim3 gt(tiles, nrhs);
   // fused low levels (writes acc for every point: no memset needed)
   if (pl.d == 2)
@@ -753,42 +979,34 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     k_low3<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
   *launches += 1;
   GPM_CUDA(cudaGetLastError());
-  auto pass = [&](const int* ord, const int* ord2l1, int lseg, int l1, int64_t nact) -> gp_status {
-    if (nact <= 0) return GP_OK;
-    g.ord = ord;
-    g.ord2l1 = ord2l1;
-    g.lseg = lseg;
-    g.l1 = l1;
-    g.n_act = nact;
-    g.ntiles = (int)((nact + LV_TILE - 1) / LV_TILE);
-    k_pass<A, 1><<<dim3(g.ntiles, nrhs), LV_BLOCK, lv_smem_pass(), s>>>(g);
-    k_pass<A, 2><<<dim3(g.ntiles, nrhs), LV_BLOCK, lv_smem_pass(), s>>>(g);
+  if (pl.d == 3 && L > LV_LOGTILE) {   // d = 3: every outer level l1 > 10 (inner l2 <= 10)
+    g.l1 = LV_LOGTILE + 1;
+    k_mid3<A><<<dim3(tiles, nrhs, L - LV_LOGTILE), LV_BLOCK, lv_smem_fused(), s>>>(g);
+    *launches += 1;
+    GPM_CUDA(cudaGetLastError());
+  }
+  // every carried pass in one aggregate launch + one apply launch (staged structure)
+  if (pl.hp_npass > 0) {
+    for (int p = 0; p < pl.hp_npass; ++p)   // ranks past n_act get no write: zero the slot
+      if (pl.hp_tail[p])
+        for (int c = 0; c < nrhs; ++c)
+          GPM_CUDA(cudaMemsetAsync(g.part + c * g.part_stride + (int64_t)p * n, 0,
+                                   sizeof(double) * n, s));
+    const dim3 gh(pl.hp_maxtiles, nrhs, pl.hp_npass);
+    const HpDesc* dd = pl.hpdesc.as<HpDesc>();
+    k_pass_hp<A, 1><<<gh, LV_BLOCK, lv_smem_pass(), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
+                                                         pl.hp_maxtiles);
+    k_pass_hp<A, 2><<<gh, LV_BLOCK, lv_smem_pass(), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
+                                                         pl.hp_maxtiles);
     *launches += 2;
     GPM_CUDA(cudaGetLastError());
-    return GP_OK;
-  };
-  for (int l1 = LV_LOGTILE + 1; l1 <= L; ++l1) {
-    const int64_t b_last = (n - 1) >> l1;
-    const int64_t mid1 = (b_last << l1) + (int64_t(1) << (l1 - 1));
-    const int64_t nact1 = mid1 >= n ? (b_last << l1) : n;
-    if (pl.d == 2) {
-      GPM_TRY(pass(pl.ord2.as<int>() + (size_t)(l1 - 1) * n, nullptr, l1, l1, nact1));
-    } else {
-      g.l1 = l1;
-      k_mid3<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
-      *launches += 1;
-      GPM_CUDA(cudaGetLastError());
-      for (int l2 = LV_LOGTILE + 1; l2 <= l1; ++l2) {
-        const int64_t c_last = (n - 1) >> l2;
-        const int64_t mid2 = (c_last << l2) + (int64_t(1) << (l2 - 1));
-        int64_t nact = nact1;
-        if (mid2 >= n) nact = std::min(nact, c_last << l2);
-        GPM_TRY(pass(pl.ord3.as<int>() + ((size_t)(l1 - 1) * l1 / 2 + (l2 - 1)) * n,
-                     pl.ord2.as<int>() + (size_t)(l1 - 1) * n, l2, l1, nact));
-      }
-    }
   }
   return GP_OK;
+}
+
+// per-pass contribution slots: carried passes, then (d = 3) one per outer level l1 > 10
+int level_nparts(const Plan& pl) {
+  return pl.hp_npass + (pl.d == 3 ? std::max(0, pl.L - LV_LOGTILE) : 0);
 }
 
 // pack the rank-order point records (t1, t2, t3, u) used by every level kernel

@@ -76,6 +76,11 @@ struct Plan {
   DevBuf stage_in, stage_out;       // gp_kmvm_host staging
   DevBuf dbg;                       // d=1 phase timestamps (env GPM_D1_TIMING)
   DevBuf pts;                       // d>=2: packed (t1, t2, t3, u) per rank, rebuilt per apply
+  DevBuf hpbuf;                     // d>=2: staged structure of the carried passes (setup)
+  DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)
+  int hp_npass = 0, hp_maxtiles = 0;
+  std::vector<char> hp_tail;        // carried pass has an inactive tail (slot must be zeroed)
+  DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
   int near_lb2 = 7, near_lb3 = 9, near_lb3m = 8;   // near-field block log2 sizes
   // d = 1 launch geometry
   int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;

@@ -262,3 +262,16 @@ def test_multi_rhs_batches(gpm, d):
         assert torch.equal(KZ[c], cr.kzx(V[c].contiguous()))
     ref = oracle.kzx_rows(x, V[9].cpu().numpy(), z.cpu().numpy(), 3, "l1", (0.1, 0.2, 0.3)[:d])
     assert np.max(np.abs(KZ[9].cpu().numpy() - ref)) < 1e-9 * np.abs(ref).max() * 50
+
+
+@pytest.mark.parametrize("d,ell", [(2, (0.6, 0.9)), (3, (0.7, 0.8, 0.9))])
+def test_large_n_segments_over_256_tiles(gpm, d, ell):
+    """N > 2^18: the top D&C node spans > 256 tiles (carry folds over many tile
+    aggregates); long lengthscales make those far pairs matter."""
+    n = 300_000
+    x = _points("uniform", n, d, 900 + d)
+    v = np.random.default_rng(11).standard_normal(n)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, ell, 1.0))
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    rows = W.sample_rows(x, 256)
+    check_rows(out, x, v, 3, "l1", ell, 1.0, rows=rows, what=f"large-n d={d}")
