@@ -81,7 +81,7 @@ struct Plan {
   int hp_npass = 0, hp_maxtiles = 0;
   std::vector<char> hp_tail;        // carried pass has an inactive tail (slot must be zeroed)
   DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
-  int near_lb2 = 7, near_lb3 = 9, near_lb3m = 8;   // near-field block log2 sizes
+  int near_lb2 = 5, near_lb3 = 8, near_lb3m = 7;   // near-field block log2 sizes (tuned)
   // d = 1 launch geometry
   int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;
   int64_t d1_chunk = 0;
