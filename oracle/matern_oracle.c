@@ -51,6 +51,31 @@ static double profile(int two_nu, double r)
     }
 }
 
+/* k'_nu(r), the first derivative of the profile (PAPER.md L1320-1322 [eq dmatern12_dl,
+ * dmatern32_dl, dmatern52_dl]). */
+static double dprofile(int two_nu, double r)
+{
+    switch (two_nu) {
+    case 1: return -exp(-r);
+    case 3: return -(3.0 * r) * exp(-sqrt(3.0) * r);
+    case 5: return -((5.0 / 3.0) * r + (5.0 * sqrt(5.0) / 3.0) * r * r) * exp(-sqrt(5.0) * r);
+    default: return NAN;
+    }
+}
+
+/* Lengthscale derivative of Ktilde(a, b), L1 form only (form != 0 returns NAN): with every
+ * l_k = c l_k0, d Ktilde / d log c at c = 1 is
+ *   l dK/dl = -s^2 r k'_nu(r),   r = sum_k |a_k - b_k| / l_k
+ * (PAPER.md L1314 [eq dkernel_dl] multiplied by l; one l: divide by l for dK/dl). */
+double oracle_dkernel_value(int two_nu, int form, int d, const double *ell, double outputscale,
+                            const double *a, const double *b)
+{
+    if (form != 0) return NAN;
+    double r = 0.0;
+    for (int k = 0; k < d; ++k) r += fabs(a[k] - b[k]) / ell[k];
+    return -outputscale * outputscale * r * dprofile(two_nu, r);
+}
+
 /* Ktilde(a, b) for one pair of d-dimensional points (form 0 = L1, 1 = product). */
 double oracle_kernel_value(int two_nu, int form, int d, const double *ell, double outputscale,
                            const double *a, const double *b)
@@ -73,10 +98,10 @@ double oracle_kernel_value(int two_nu, int form, int d, const double *ell, doubl
  * rows == NULL means rows[k] = k, nrows targets.
  * src: n x d row-major, tgt: (any) x d row-major.  nthreads <= 0: OpenMP default.
  */
-void oracle_cross_mvm(int two_nu, int form, int d, const double *ell, double outputscale,
-                      const double *src, const double *v, int64_t n,
-                      const double *tgt, const int64_t *rows, int64_t nrows,
-                      double *out, double *absrow, int nthreads)
+static void cross_rows(int kind, int two_nu, int form, int d, const double *ell,
+                       double outputscale, const double *src, const double *v, int64_t n,
+                       const double *tgt, const int64_t *rows, int64_t nrows,
+                       double *out, double *absrow, int nthreads)
 {
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -89,14 +114,34 @@ void oracle_cross_mvm(int two_nu, int form, int d, const double *ell, double out
         const double *z = tgt + (size_t)j * d;
         long double acc = 0.0L, aacc = 0.0L;
         for (int64_t i = 0; i < n; ++i) {
-            const double kv = oracle_kernel_value(two_nu, form, d, ell, outputscale,
-                                                  src + (size_t)i * d, z);
+            const double kv = kind == 0
+                ? oracle_kernel_value(two_nu, form, d, ell, outputscale, src + (size_t)i * d, z)
+                : oracle_dkernel_value(two_nu, form, d, ell, outputscale, src + (size_t)i * d, z);
             acc += (long double)v[i] * (long double)kv;
             aacc += (long double)fabs(kv);
         }
         out[k] = (double)acc;
         if (absrow) absrow[k] = (double)aacc;
     }
+}
+
+void oracle_cross_mvm(int two_nu, int form, int d, const double *ell, double outputscale,
+                      const double *src, const double *v, int64_t n,
+                      const double *tgt, const int64_t *rows, int64_t nrows,
+                      double *out, double *absrow, int nthreads)
+{
+    cross_rows(0, two_nu, form, d, ell, outputscale, src, v, n, tgt, rows, nrows, out, absrow,
+               nthreads);
+}
+
+/* As oracle_cross_mvm with the lengthscale derivative l dKtilde/dl (L1 form). */
+void oracle_cross_dmvm(int two_nu, int form, int d, const double *ell, double outputscale,
+                       const double *src, const double *v, int64_t n,
+                       const double *tgt, const int64_t *rows, int64_t nrows,
+                       double *out, double *absrow, int nthreads)
+{
+    cross_rows(1, two_nu, form, d, ell, outputscale, src, v, n, tgt, rows, nrows, out, absrow,
+               nthreads);
 }
 
 /* Dense block Kout[i*n + j] = Ktilde(a_i, b_j), a: m x d, b: n x d (small sizes only). */

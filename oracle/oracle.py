@@ -14,7 +14,7 @@ import time
 import numpy as np
 
 __all__ = [
-    "build_oracle", "kernel_value", "kmvm_rows", "kzx_rows", "dense_kernel",
+    "build_oracle", "kernel_value", "dkernel_value", "kmvm_rows", "dkmvm_rows", "dkzx_rows", "kzx_rows", "dense_kernel",
     "ols", "gp_dense", "max_threads", "FORMS",
 ]
 
@@ -48,6 +48,10 @@ def _load():
         lib.oracle_cross_mvm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp,
                                          ctypes.c_double, dp, dp, ctypes.c_int64, dp, lp,
                                          ctypes.c_int64, dp, dp, ctypes.c_int]
+        lib.oracle_dkernel_value.restype = ctypes.c_double
+        lib.oracle_dkernel_value.argtypes = lib.oracle_kernel_value.argtypes
+        lib.oracle_cross_dmvm.restype = None
+        lib.oracle_cross_dmvm.argtypes = lib.oracle_cross_mvm.argtypes
         lib.oracle_dense.restype = None
         lib.oracle_dense.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp,
                                      ctypes.c_double, dp, ctypes.c_int64, dp, ctypes.c_int64,
@@ -79,8 +83,30 @@ def kernel_value(two_nu: int, form: str, ell, outputscale: float, a, b) -> float
                                              outputscale, _dp(a), _dp(b)))
 
 
+def dkernel_value(two_nu: int, form: str, ell, outputscale: float, a, b) -> float:
+    """l dKtilde/dl = -s^2 r k'_nu(r) (L1 form, every l_k scaled together)
+    [eq dkernel_dl] times l, with the L1320-1322 derivative profiles."""
+    a = _f64(np.atleast_1d(a)); b = _f64(np.atleast_1d(b)); ell = _f64(np.atleast_1d(ell))
+    return float(_load().oracle_dkernel_value(two_nu, FORMS[form], a.size, _dp(ell),
+                                              outputscale, _dp(a), _dp(b)))
+
+
+def dkzx_rows(x, v, z, two_nu: int, form: str, ell, outputscale: float = 1.0, rows=None,
+              nthreads: int = 0, return_abs: bool = False):
+    """(l dK_zx/dl v)_q = sum_i v_i l dKtilde(x_i, z_q)/dl for q in rows (L1 form)."""
+    return kzx_rows(x, v, z, two_nu, form, ell, outputscale, rows, nthreads, return_abs,
+                    _kind=1)
+
+
+def dkmvm_rows(x, v, two_nu: int, form: str, ell, outputscale: float = 1.0, rows=None,
+               nthreads: int = 0, return_abs: bool = False):
+    """(l dK/dl v)_j, the lengthscale-gradient MVM (PAPER.md L1301-1314 [§ Derivative of
+    Matern covariance functions]) used by gradient-based hyperparameter fitting."""
+    return dkzx_rows(x, v, x, two_nu, form, ell, outputscale, rows, nthreads, return_abs)
+
+
 def kzx_rows(x, v, z, two_nu: int, form: str, ell, outputscale: float = 1.0, rows=None,
-             nthreads: int = 0, return_abs: bool = False):
+             nthreads: int = 0, return_abs: bool = False, _kind: int = 0):
     """(K_zx v)_q = sum_i v_i Ktilde(x_i, z_q) for q in rows (all if None).
 
     PAPER.md L92 [k_z], L256 [eq kde].  x: N x d sources, z: M x d targets.
@@ -94,9 +120,9 @@ def kzx_rows(x, v, z, two_nu: int, form: str, ell, outputscale: float = 1.0, row
         rows = np.ascontiguousarray(rows, dtype=np.int64); nrows = rows.size
         rp = rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
     out = np.empty(nrows); ab = np.empty(nrows)
-    _load().oracle_cross_mvm(two_nu, FORMS[form], d, _dp(ell), float(outputscale), _dp(x),
-                             _dp(v), x.shape[0], _dp(z), rp, nrows, _dp(out), _dp(ab),
-                             int(nthreads))
+    fn = _load().oracle_cross_dmvm if _kind else _load().oracle_cross_mvm
+    fn(two_nu, FORMS[form], d, _dp(ell), float(outputscale), _dp(x), _dp(v), x.shape[0],
+       _dp(z), rp, nrows, _dp(out), _dp(ab), int(nthreads))
     return (out, ab) if return_abs else out
 
 

@@ -300,3 +300,86 @@ def test_workloads_recipes():
     rows = W.sample_rows(x4, 256)
     assert rows.size == 256 and np.all(np.diff(rows) > 0)
     assert int(np.argmax(x4[:, 2])) in set(rows.tolist())
+
+
+# ---------------------------------------------------------------- lengthscale gradient (f2)
+
+def explicit_dcoeffs(p):
+    """Coefficients c_i of u^i in -k'_{p+1/2}(u) e^{sqrt(2p+1) u}
+    [eq dmatern_explicit_dl], returned as c_i / (2p+1)^{i/2} in s = sqrt(2p+1) u units
+    (exact rationals; the sqrt(2p+1) factors cancel to (2p+1)^{(i+1)/2 - i/2} = sqrt(2p+1)
+    overall, which is dropped: -k'(u) = sqrt(2p+1) sum_i c_i s^i e^{-s})."""
+    return [Fraction(0)] + [Fraction(i * math.comb(p, i) * math.factorial(2 * p - i) * 2 ** i,
+                                     (2 * p - i) * math.factorial(2 * p))
+                            for i in range(1, p + 1)]
+
+
+def test_dmatern_explicit_matches_paper_table_and_derivative():
+    """eq dmatern_explicit_dl (L1327) reproduces the displayed k'_{3/2..9/2} (L1321-1324)
+    and equals the exact derivative of eq matern_explicit (L1282).  For p = 0 the general
+    formula is an empty sum while eq dmatern12_dl (L1320) prints -e^{-u}: DESIGN.md reading
+    R11 takes the displayed formula."""
+    # -k'(s) in s units from differentiating sum_i a_i s^i e^{-s}: sum_i (a_i - (i+1) a_{i+1}) s^i
+    for p in range(1, 5):
+        a = explicit_coeffs(p) + [Fraction(0)]
+        deriv = [a[i] - (i + 1) * a[i + 1] for i in range(p + 1)]
+        assert explicit_dcoeffs(p) == deriv, p
+    # displayed table, e.g. k'_{5/2}(u) = -(5/3 u + 5 sqrt5/3 u^2) e^{-sqrt5 u}:
+    # in s = sqrt5 u: -k' = sqrt5 (1/3 s + 1/3 s^2) e^{-s}
+    assert explicit_dcoeffs(1) == [0, 1]
+    assert explicit_dcoeffs(2) == [0, Fraction(1, 3), Fraction(1, 3)]
+    # k'_{7/2}: 7/5 u + 7 sqrt7/5 u^2 + 49/15 u^3 -> /sqrt7 in s: 1/5 s, 1/5 s^2, 1/15 s^3
+    assert explicit_dcoeffs(3) == [0, Fraction(1, 5), Fraction(1, 5), Fraction(1, 15)]
+    assert explicit_dcoeffs(0) == [0]
+
+
+def bessel_dprofile_scaled(two_nu, r, dps=50):
+    """-r k_nu'(r) from the Bessel definition: mpmath high-precision numerical derivative."""
+    with mp.workdps(dps):
+        r = mp.mpf(r)
+        if r == 0:
+            return mp.mpf(0)
+        # the profile must run at a higher precision than diff's own (it raises it)
+        return -r * mp.diff(lambda t: bessel_profile(two_nu, t, 3 * dps), r)
+
+
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+def test_dprofile_against_bessel_derivative(two_nu):
+    for r in [0.0, 1e-3, 0.05, 0.3, 1.0, 2.5, 7.0, 30.0]:
+        ref = float(bessel_dprofile_scaled(two_nu, r))
+        got = oracle.dkernel_value(two_nu, "l1", [1.0], 1.0, [0.0], [r])
+        rel = 4.5e-16 * (6.0 + 2 * math.sqrt(two_nu) * r)
+        assert got == pytest.approx(ref, rel=rel, abs=1e-300), (two_nu, r)
+
+
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_dkmvm_bruteforce_lengthscale_derivative(two_nu, d):
+    """Tiny N: l dK/dl v (every l_k scaled together) vs the 40-digit derivative
+    d/dc [sum_i v_i s^2 k_nu(sum_k |dx_k| / (c l_k))] at c = 1 on the Bessel definition."""
+    rng = np.random.default_rng(300 + 10 * d + two_nu)
+    n = 8
+    x = rng.random((n, d))
+    x[3] = x[1]
+    v = rng.standard_normal(n)
+    ell = [0.3, 0.5, 0.2][:d]
+    sig = 1.3
+    got, ab = oracle.dkmvm_rows(x, v, two_nu, "l1", ell, sig, return_abs=True)
+    with mp.workdps(40):
+        ref = []
+        for j in range(n):
+            def f(c):
+                tot = mp.mpf(0)
+                for i in range(n):
+                    r = sum(abs(mp.mpf(x[i, k]) - mp.mpf(x[j, k])) / (c * mp.mpf(ell[k]))
+                            for k in range(d))
+                    tot += mp.mpf(v[i]) * mp.mpf(sig) ** 2 * bessel_profile(two_nu, r, 120)
+                return tot
+            ref.append(float(mp.diff(f, mp.mpf(1))))
+    tol = 1e-14 * np.max(ab) * np.max(np.abs(v))
+    assert np.max(np.abs(got - np.array(ref))) <= tol
+    # zero on the diagonal: duplicates and the self pair contribute nothing
+    e = np.zeros(n); e[1] = 1.0
+    col = oracle.dkmvm_rows(x, e, two_nu, "l1", ell, sig)
+    assert col[1] == 0.0 and col[3] == 0.0
+    assert np.isnan(oracle.dkernel_value(two_nu, "product", ell, 1.0, x[0], x[2]))
