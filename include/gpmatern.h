@@ -103,6 +103,21 @@ GP_API gp_status gp_kmvm_host(gp_plan p, const double *v, int nrhs, double *out,
 GP_API gp_status gp_kmvm_rank(gp_plan p, const double *v_rank, int nrhs, double *out_rank,
                               void *stream);
 
+/* gp_kmvm_dlengthscale -- out = (l dK/dl) v, the lengthscale-gradient MVM of the plan's
+ * kernel (PAPER.md L1301-1327 [§ Derivative of Matern covariance functions],
+ * eq dkernel_dl): with every lengthscale l_k scaled by a common factor c,
+ *   out_j = d/dc [sum_i Ktilde_c(x_i, x_j) v_i] at c = 1
+ *         = s^2 sum_i g(r_ij) v_i,   g(r) = -r k_nu'(r),  r = sum_k |x_ik - x_jk| / l_k.
+ * For one lengthscale l, dK/dl v = out / l; the outputscale gradient is dK/ds v = (2/s) K v
+ * (eq dkernel_dvarsigma) and needs no extra MVM.  Computed by the same decomposition with
+ * one more moment (g(s) = (s, s^2, (s^2 + s^3)/3) e^{-s} for nu = 1/2, 3/2, 5/2 in scaled
+ * distance s = sqrt(2 nu) r): exact like gp_kmvm, no nugget, zero diagonal.
+ * Supported: d = 1 (n <= 148 x 6912 = 1022976 points) and the L1 form for d = 2, 3;
+ * the product form returns GP_ERR_UNSUPPORTED.  v_order: 0 = user order (layout as
+ * gp_kmvm), 1 = the plan's stored order (as gp_kmvm_rank). */
+GP_API gp_status gp_kmvm_dlengthscale(gp_plan p, const double *v, int nrhs, double *out,
+                                      int v_order, void *stream);
+
 /* gp_permute -- move n x nrhs column-major vectors between user order and the plan's
  * stored order: to_rank != 0: dst[r] = src[perm[r]]; to_rank == 0: dst[perm[r]] = src[r].
  * src and dst must not alias. */
@@ -161,7 +176,8 @@ GP_API gp_status gp_plan_query(gp_plan p, int what, int64_t *value);
 /* gp_plan_set_option -- tuning / testing knobs (d = 1 only; ignored otherwise):
  *   option 0: force the d=1 apply path (0 auto, 1 single-sub-tile if it fits, 2 multi-sub-tile);
  *   option 1: thread-block shape of path 1: 0 = 512x15, 1 = 640x11, 2 = 768x9, 3 = 1024x7
- *             (threads x points per thread). */
+ *             (threads x points per thread);
+ *   option 2: programmatic dependent launch of the d=1 kernel (1 default, 0 off). */
 GP_API gp_status gp_plan_set_option(gp_plan p, int option, int64_t value);
 
 GP_API void gp_destroy(gp_plan p);

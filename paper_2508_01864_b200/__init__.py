@@ -59,6 +59,7 @@ def load_library(path: str | None = None):
         "gp_kmvm": [vp, vp, ci, vp, vp],
         "gp_kmvm_host": [vp, vp, ci, vp, vp],
         "gp_kmvm_rank": [vp, vp, ci, vp, vp],
+        "gp_kmvm_dlengthscale": [vp, vp, ci, vp, ci, vp],
         "gp_permute": [vp, vp, ci, vp, ci, vp],
         "gp_kzx_setup": [vp, vp, i64, vp, ctypes.POINTER(vp)],
         "gp_kzx": [vp, vp, ci, vp, vp],
@@ -168,6 +169,18 @@ class Plan:
             out = torch.empty_like(v_rank)
         _check(_lib.gp_kmvm_rank(self._h, _dev(v_rank, "v"), nrhs, _dev(out, "out", v_rank.shape),
                                  _stream(stream)))
+        return out
+
+    def kmvm_dlengthscale(self, v, out=None, rank_order=False, stream=None):
+        """out = (l dK/dl) v, all lengthscales scaled together (gp_kmvm_dlengthscale)."""
+        import torch
+        nrhs = 1 if v.dim() == 1 else v.shape[0]
+        if v.shape[-1] != self.n:
+            raise ValueError("v has the wrong length")
+        if out is None:
+            out = torch.empty_like(v)
+        _check(_lib.gp_kmvm_dlengthscale(self._h, _dev(v, "v"), nrhs, _dev(out, "out", v.shape),
+                                         1 if rank_order else 0, _stream(stream)))
         return out
 
     def to_rank(self, v, stream=None):

@@ -35,10 +35,18 @@ __host__ __device__ constexpr double binom(int q, int m) {
   return (m == 0 || m == q) ? 1.0 : (q == 2 && m == 1 ? 2.0 : 1.0);
 }
 
-// Advance a (P+1)-moment vector by D (E = e^{-D}).  In place, high q first.
+// Advance a (P+1)-moment vector by D (E = e^{-D}).  In place, high q first.  P <= 3.
 template <int P>
 __device__ __forceinline__ void advance(double* M, double D, double E) {
-  if constexpr (P == 2) {
+  if constexpr (P == 3) {
+    // M3 + 3D M2 + 3D^2 M1 + D^3 M0 = M3 + D (3 M2 + D (3 M1 + D M0))
+    const double a = fma(D, M[0], M[1]);
+    const double b = fma(D, fma(D, M[0], 3.0 * M[1]), 3.0 * M[2]);
+    M[3] = E * fma(D, b, M[3]);
+    M[2] = E * fma(D, M[1] + a, M[2]);
+    M[1] = E * a;
+    M[0] = E * M[0];
+  } else if constexpr (P == 2) {
     // M2 + 2D M1 + D^2 M0 = M2 + D (M1 + (M1 + D M0)):  6 FP64 ops
     const double a = fma(D, M[0], M[1]);
     M[2] = E * fma(D, M[1] + a, M[2]);
@@ -83,15 +91,65 @@ __device__ __forceinline__ double read0(const double* R) {
 }
 
 // ---------------------------------------------------------------------------
+// Read profiles.  KIND 0: the Matern profile k(s) = sum_q a_q s^q e^{-s} of nu = PM + 1/2
+// (moments q <= PM).  KIND 1: the lengthscale-gradient profile of nu = PM - 1/2,
+//   g(s) = -s k'(s) = sum_m b_m s^m e^{-s},  b_m = a_{m-1} - m a_m   (moments m <= PM),
+// so that dK/d(log l) = varsigma^2 g(s): P:1309 [eq dkernel_dl] with the closed forms
+// P:1321-1323 (nu=1/2: s e^{-s}; 3/2: s^2 e^{-s}; 5/2: (s^2 + s^3)/3 e^{-s}).
+__host__ __device__ constexpr double rcoef(int PM, int KIND, int q) {
+  return KIND == 0 ? (q == 2 && PM == 2 ? 1.0 / 3.0 : (q <= PM ? 1.0 : 0.0))
+                   : (PM == 1 ? (q == 1 ? 1.0 : 0.0)
+                      : PM == 2 ? (q == 2 ? 1.0 : 0.0)
+                                : (q >= 2 ? 1.0 / 3.0 : 0.0));
+}
+__host__ __device__ constexpr double binom3(int q, int m) {
+  return (m == 0 || m == q) ? 1.0 : (q == 2 ? 2.0 : (q == 3 ? 3.0 : 1.0));
+}
+// sum_q c_q R_q
+template <int PM, int KIND>
+__device__ __forceinline__ double readc0(const double* R) {
+  if constexpr (KIND == 0) {
+    return read0<PM>(R);
+  } else {
+    if constexpr (PM == 1) return R[1];
+    else if constexpr (PM == 2) return R[2];
+    else return (1.0 / 3.0) * (R[2] + R[3]);
+  }
+}
+// sum_q c_q sum_{m<=q} C(q,m) beta^{q-m} R_m   (without e^{-beta})
+template <int PM, int KIND>
+__device__ __forceinline__ double readc_poly(const double* R, double beta) {
+  if constexpr (KIND == 0) {
+    return read_poly<PM>(R, beta);
+  } else {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q <= PM; ++q) {
+      if (rcoef(PM, KIND, q) != 0.0) {
+        double t = 0.0, bp = 1.0;
+#pragma unroll
+        for (int m = q; m >= 0; --m) {   // sum_m C(q,m) beta^{q-m} R_m
+          t = fma(binom3(q, m) * bp, R[m], t);
+          bp *= beta;
+        }
+        acc = fma(rcoef(PM, KIND, q), t, acc);
+      }
+    }
+    return acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Multi-channel algebra for the d >= 2 level passes.
 //   NCH channels (2 for d = 2: side of the x1 split; 4 for d = 3: sides of the x1 and
 //   inner x2 splits).  A source on channel c feeds targets on channel NCH-1-c.
 //   NM moments per channel: P+1 (L1) or (P+1)^2 (product, d = 2).
-template <int P_, int NCH_, bool PROD_>
+template <int P_, int NCH_, bool PROD_, int KIND_ = 0>
 struct Alg {
-  static constexpr int P = P_;
+  static constexpr int P = P_;          // moment order (gradient: nu - 1/2 + 1)
   static constexpr int NCH = NCH_;
-  static constexpr bool PROD = PROD_;
+  static constexpr bool PROD = PROD_;   // product form (KIND 0 only)
+  static constexpr int KIND = KIND_;
   static constexpr int NQ = P + 1;
   static constexpr int NM = PROD ? NQ * NQ : NQ;
   static constexpr int NS = NCH * NM;
@@ -129,7 +187,7 @@ struct Alg {
     for (int cc = 0; cc < NCH; ++cc) {
       if (cc == rc) {
         if constexpr (!PROD) {
-          v = read_poly<P>(M + cc * NM, beta);
+          v = readc_poly<P, KIND>(M + cc * NM, beta);
         } else {
           // k(alpha+beta) k(s): e^{-beta} sum_a a_a sum_{m<=a} C(a,m) beta^{a-m} (sum_q a_q M[m][q])
           double G[NQ];

@@ -95,6 +95,17 @@ gp_status gp_kmvm_rank(gp_plan p, const double* v, int nrhs, double* out, void* 
   return apply_rank(p->pl, v, out, nrhs, static_cast<cudaStream_t>(stream));
 }
 
+gp_status gp_kmvm_dlengthscale(gp_plan p, const double* v, int nrhs, double* out, int v_order,
+                               void* stream) {
+  if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  if (v == out) return fail(GP_ERR_INVALID_ARG, "out must not alias v");
+  if (v_order != 0 && v_order != 1) return fail(GP_ERR_INVALID_ARG, "v_order must be 0 or 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return v_order == 0 ? apply_user(p->pl, v, out, nrhs, s, 1)
+                      : apply_rank(p->pl, v, out, nrhs, s, 1);
+}
+
 gp_status gp_permute(gp_plan p, const double* src, int nrhs, double* dst, int to_rank,
                      void* stream) {
   if (!p || !src || !dst) return fail(GP_ERR_INVALID_ARG, "NULL argument");
@@ -252,6 +263,8 @@ gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
   } else if (option == 1) {
     if (value < 0 || value > 3) return fail(GP_ERR_INVALID_ARG, "bad value for option 1");
     p->pl.d1_shape = (int)value;
+  } else if (option == 2) {
+    p->pl.d1_pdl = value != 0;
   } else {
     return fail(GP_ERR_INVALID_ARG, "unknown option");
   }

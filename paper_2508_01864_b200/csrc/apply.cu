@@ -12,8 +12,8 @@ namespace gpm {
 
 gp_status d1_prepare(Plan& pl);
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s);
-gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches);
+                    cudaStream_t s, int kind);
+gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind);
 gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
 size_t level_pt_bytes();
 int level_nparts(const Plan& pl);
@@ -31,11 +31,12 @@ __global__ void k_gather(const int* __restrict__ perm, const double* __restrict_
   }
 }
 
-// out[perm[r] - tgt_off] = os2 (u[r] + acc[r]) for targets; perm == nullptr: rank order.
-// u is read from the packed point records (stride 4 doubles, u at offset 3).
+// out[perm[r] - tgt_off] = os2 (self u[r] + acc[r]) for targets; perm == nullptr: rank order.
+// u is read from the packed point records (stride 4 doubles, u at offset 3); self = k(0)
+// (1 for K, 0 for the lengthscale gradient).
 __global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ pts,
                            const double* __restrict__ acc, const double* __restrict__ part,
-                           int nparts, int64_t n, int64_t tgt_off, double os2,
+                           int nparts, int64_t n, int64_t tgt_off, double os2, double self,
                            double* __restrict__ out, int64_t ostride) {
   pts += blockIdx.y * 4 * n;
   acc += blockIdx.y * n;
@@ -45,7 +46,7 @@ __global__ void k_epilogue(const int* __restrict__ perm, const double* __restric
        r += (int64_t)gridDim.x * blockDim.x) {
     double a = acc[r];
     for (int p = 0; p < nparts; ++p) a += part[(int64_t)p * n + r];   // fixed order
-    const double val = os2 * (pts[4 * r + 3] + a);
+    const double val = os2 * fma(self, pts[4 * r + 3], a);
     if (perm) {
       const int i = __ldg(perm + r);
       if (i >= tgt_off) out[i - tgt_off] = val;
@@ -107,7 +108,7 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
 }
 
 static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                              cudaStream_t s) {
+                              cudaStream_t s, int kind) {
   const int64_t vstride = user_order ? pl.n_src : pl.n;
   const int64_t ostride = user_order ? pl.n - pl.tgt_off : pl.n;
   for (int c0 = 0; c0 < nrhs; c0 += LV_MAXB) {
@@ -115,11 +116,11 @@ static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, 
     GPM_TRY(level_buffers(pl, nb));
     int launches = 0;
     GPM_TRY(level_pack(pl, v + c0 * vstride, nb, user_order, s));   // packed points (+ gather)
-    GPM_TRY(level_passes(pl, nb, s, &launches));   // first level launch initialises acc
+    GPM_TRY(level_passes(pl, nb, s, &launches, kind));   // first level launch initialises acc
     k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
         user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
         pl.part.as<double>(), level_nparts(pl), pl.n, user_order ? pl.tgt_off : 0, pl.os2,
-        out + c0 * ostride, ostride);
+        kind == 0 ? 1.0 : 0.0, out + c0 * ostride, ostride);
     GPM_CUDA(cudaGetLastError());
     pl.launches_per_apply = launches + 2;   // + pack + epilogue (per batch of columns)
   }
@@ -135,14 +136,15 @@ gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cu
   return GP_OK;
 }
 
-gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s) {
-  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, nrhs, false, s);
-  return apply_levels(pl, u_rank, out_rank, nrhs, false, s);
+gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s,
+                     int kind) {
+  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, nrhs, false, s, kind);
+  return apply_levels(pl, u_rank, out_rank, nrhs, false, s, kind);
 }
 
-gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s) {
-  if (pl.d == 1) return d1_launch(pl, v, out, nrhs, true, s);
-  return apply_levels(pl, v, out, nrhs, true, s);
+gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s, int kind) {
+  if (pl.d == 1) return d1_launch(pl, v, out, nrhs, true, s, kind);
+  return apply_levels(pl, v, out, nrhs, true, s, kind);
 }
 
 // Algorithmic HBM bytes of one single-RHS user-order apply:

@@ -478,7 +478,7 @@ static cudaError_t d1_set_attr() {
 
 gp_status df_shape_info(int shape, int* capacity, int* max_grid);
 gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s);
+                    cudaStream_t s, int kind);
 int df_default_shape();
 
 gp_status d1_prepare(Plan& pl) {
@@ -544,11 +544,13 @@ gp_status d1_prepare(Plan& pl) {
 }
 
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s) {
-  if (pl.d1_path == 1) return df_launch(pl, v, out, nrhs, user_order, s);
+                    cudaStream_t s, int kind) {
+  if (pl.d1_path == 1) return df_launch(pl, v, out, nrhs, user_order, s, kind);
+  if (kind != 0)
+    return fail(GP_ERR_UNSUPPORTED, "lengthscale-gradient MVM for d=1 needs n <= #SMs x 6912");
   const int64_t vs = user_order ? pl.n_src : pl.n, os = user_order ? pl.n - pl.tgt_off : pl.n;
   for (int c = 0; c + 1 < nrhs; ++c)
-    GPM_TRY(d1_launch(pl, v + c * vs, out + c * os, 1, user_order, s));
+    GPM_TRY(d1_launch(pl, v + c * vs, out + c * os, 1, user_order, s, 0));
   v += (nrhs - 1) * vs;
   out += (nrhs - 1) * os;
   D1Args a;

@@ -147,8 +147,8 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 
 // Published chunk aggregate: D, E, F[3], B[3] and the launch epoch (written last).
-struct __align__(16) D1Pub {
-  double v[8];
+struct __align__(16) D1Pub {   // 96 B (apply_d1.cu allocates 96 x 2 x grid)
+  double v[10];   // D, E, F[4], B[4]
   unsigned long long epoch;
   unsigned long long pad;
 };
@@ -164,8 +164,9 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 
 constexpr int DF_NPART = 4;   // TMA load pipeline depth (parts of the chunk)
 
-template <int P, int BLOCK, int ITEMS>
+template <int P, int KIND, int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
+  // P = moment order; KIND 0: K v (Matern nu = P + 1/2), KIND 1: dK/dlog(l) v (nu = P - 1/2)
   // Loops over the per-thread points are rolled where the body is large: every launch
   // walks the kernel once and instruction fetch from L2 is not free.
   constexpr int SUB = BLOCK * ITEMS;
@@ -179,10 +180,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   int* s_pi = reinterpret_cast<int*>(s_e + SUB);       // SUB + 8
   __shared__ uint64_t mbar[DF_NPART];
   __shared__ double s_tab[64];
-  __shared__ double s_wf[NW][5], s_wb[NW][5];
-  __shared__ double s_tot[2][5];
-  __shared__ double s_part[2][8][5];
-  __shared__ double s_carry[2][3];
+  __shared__ double s_wf[NW][6], s_wb[NW][6];
+  __shared__ double s_tot[2][6];
+  __shared__ double s_part[2][8][6];
+  __shared__ double s_carry[2][4];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * a.chunk;
@@ -196,8 +197,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // rank-order input through TMA when 16B-aligned (all internal vectors are)
-  const bool u_tma = !a.user_order && ((reinterpret_cast<uintptr_t>(a.v + c0) & 15) == 0);
+  // v is read only after griddepcontrol.wait (PDL: the previous kernel may produce it);
+  // t and perm are plan-owned and read-only, so their TMA copies start immediately
+  const bool u_tma = false;
   if (tid < DF_NPART && cnt > 0) {
     const int p = tid;
     const int lo = p * PSZ;
@@ -223,38 +225,33 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     const int64_t gp = c0 + min(j0, cnt) - 1;
     tprev = gp >= 0 ? __ldg(a.ts + gp) : __ldg(a.ts);
     if (j0 >= cnt) tprev = tlast;
-    if (!a.user_order) {
-      if (!u_tma) {
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-          const int j = j0 + k;
-          s_u[j] = j < cnt ? __ldg(a.v + c0 + j) : 0.0;
-        }
-      } else {
-        // odd tail of a part (not covered by the 16-byte TMA copy) and padding
-#pragma unroll 1
-        for (int k = 0; k < ITEMS; ++k) {
-          const int j = j0 + k;
-          const int lo = (j / PSZ) * PSZ;
-          const int hi = min(cnt, lo + PSZ);
-          if (j >= cnt) s_u[j] = 0.0;
-          else if (j >= lo + ((hi - lo) & ~1)) s_u[j] = __ldg(a.v + c0 + j);
-        }
-      }
-    }
     if (mypart * PSZ < cnt)
       while (!mbar_try_wait(&mbar[mypart], 0)) {
       }
   }
   DF_STAMP(1);
+  // gaps and e^{-gap}: plan data only -> overlaps the previous kernel's tail under PDL
+  {
+    double tp = tprev;
+#pragma unroll 1
+    for (int k = 0; k < ITEMS; ++k) {
+      const int j = j0 + k;
+      const double t = j < cnt ? s_t[j] : tlast;
+      const double dl = t - tp;            // neutral (0) past the chunk end
+      tp = t;
+      s_t[j] = dl;                         // t -> gap (own slot; neighbours use tprev)
+      s_e[j] = fexp_neg(dl, s_tab);
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // no-op without a PDL predecessor
 
 #pragma unroll 1
   for (int col = 0; col < a.nrhs; ++col) {
   const double* vcol = a.v + col * a.vstride;
   double* ocol = a.out + col * a.ostride;
   D1Pub* pubc = pub + (col & 1) * gridDim.x;   // slots alternate: a CTA runs <= 1 sync ahead
-  if (col > 0) {
-    __syncthreads();   // s_u of the previous column fully consumed
+  {
+    if (col > 0) __syncthreads();   // s_u of the previous column fully consumed
     if (!a.user_order) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
@@ -272,19 +269,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
       const int j = j0 + k;
       const int pi = j < cnt ? s_pi[j] : INT_MAX;
       uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
-    }
-  }
-  // ... while the gaps and e^{-gap} are computed (independent of v; first column only)
-  if (col == 0) {
-    double tp = tprev;
-#pragma unroll 1
-    for (int k = 0; k < ITEMS; ++k) {
-      const int j = j0 + k;
-      const double t = j < cnt ? s_t[j] : tlast;
-      const double dl = t - tp;            // neutral (0) past the chunk end
-      tp = t;
-      s_t[j] = dl;                         // t -> gap (own slot; neighbours use tprev)
-      s_e[j] = fexp_neg(dl, s_tab);
     }
   }
   if (a.user_order) {
@@ -309,7 +293,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
       if (P >= 1) {
         const double wd = w * Dc;
         B.M[P >= 1 ? 1 : 0] += wd;
-        if (P >= 2) B.M[P >= 2 ? 2 : 0] = fma(wd, Dc, B.M[P >= 2 ? 2 : 0]);
+        if (P >= 2) {
+          const double wdd = wd * Dc;
+          B.M[P >= 2 ? 2 : 0] += wdd;
+          if (P >= 3) B.M[P >= 3 ? 3 : 0] = fma(wdd, Dc, B.M[P >= 3 ? 3 : 0]);
+        }
       }
       advance<P>(F.M, dl, e);
       F.M[0] += u;
@@ -358,9 +346,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     me->v[0] = s_tot[0][0];
     me->v[1] = s_tot[0][1];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 4; ++q) {
       me->v[2 + q] = q <= P ? s_tot[0][2 + q] : 0.0;
-      me->v[5 + q] = q <= P ? s_tot[1][2 + q] : 0.0;
+      me->v[6 + q] = q <= P ? s_tot[1][2 + q] : 0.0;
     }
     __threadfence();
   }
@@ -384,7 +372,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
         X.D = __ldcg(&o->v[0]);
         X.E = __ldcg(&o->v[1]);
 #pragma unroll
-        for (int q = 0; q <= P; ++q) X.M[q] = __ldcg(&o->v[(fw ? 2 : 5) + q]);
+        for (int q = 0; q <= P; ++q) X.M[q] = __ldcg(&o->v[(fw ? 2 : 6) + q]);
       }
 #pragma unroll 1
       for (int off = 1; off < 32; off <<= 1) {
@@ -424,7 +412,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   for (int k = 0; k < ITEMS; ++k) {
     const int j = j0 + k;
     advance<P>(M, s_t[j], s_e[j]);       // s_t now holds the gaps
-    rf[k] = read0<P>(M);
+    rf[k] = readc0<P, KIND>(M);
     M[0] += s_u[j];
   }
   {
@@ -439,7 +427,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   for (int k = ITEMS - 1; k >= 0; --k) {
     const int j = j0 + k;
     const double uj = s_u[j];
-    const double val = a.os2 * (uj + (rf[k] + read0<P>(M)));
+    const double val = a.os2 * ((KIND == 0 ? uj : 0.0) + (rf[k] + readc0<P, KIND>(M)));
     M[0] += uj;
     advance<P>(M, s_t[j], s_e[j]);
     if (a.user_order) {
@@ -460,6 +448,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     }
   }
   }   // column loop
+  asm volatile("griddepcontrol.launch_dependents;");
   if (a.dbg) {
     __syncthreads();
     DF_STAMP(6);
@@ -477,7 +466,7 @@ static size_t df_smem() {
 
 struct DFShape {
   int block, items;
-  const void* fn[3];
+  const void* fn[6];   // [KIND * 3 + p]: KIND 0 moment order p, KIND 1 moment order p + 1
   size_t smem;
 };
 
@@ -486,9 +475,12 @@ static DFShape make_shape() {
   DFShape s;
   s.block = BLOCK;
   s.items = ITEMS;
-  s.fn[0] = (const void*)k_d1_fast<0, BLOCK, ITEMS>;
-  s.fn[1] = (const void*)k_d1_fast<1, BLOCK, ITEMS>;
-  s.fn[2] = (const void*)k_d1_fast<2, BLOCK, ITEMS>;
+  s.fn[0] = (const void*)k_d1_fast<0, 0, BLOCK, ITEMS>;
+  s.fn[1] = (const void*)k_d1_fast<1, 0, BLOCK, ITEMS>;
+  s.fn[2] = (const void*)k_d1_fast<2, 0, BLOCK, ITEMS>;
+  s.fn[3] = (const void*)k_d1_fast<1, 1, BLOCK, ITEMS>;
+  s.fn[4] = (const void*)k_d1_fast<2, 1, BLOCK, ITEMS>;
+  s.fn[5] = (const void*)k_d1_fast<3, 1, BLOCK, ITEMS>;
   s.smem = df_smem<BLOCK, ITEMS>();
   return s;
 }
@@ -504,7 +496,7 @@ static gp_status df_init() {
   g_shapes[2] = make_shape<768, 9>();
   g_shapes[3] = make_shape<1024, 7>();
   for (auto& s : g_shapes)
-    for (int p = 0; p < 3; ++p)
+    for (int p = 0; p < 6; ++p)
       GPM_CUDA(cudaFuncSetAttribute(s.fn[p], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)s.smem));
   if (const char* e = getenv("GPM_D1_SHAPE")) g_default_shape = std::max(0, std::min(3, atoi(e)));
@@ -528,7 +520,7 @@ gp_status df_shape_info(int shape, int* capacity, int* max_grid) {
 }
 
 gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s) {
+                    cudaStream_t s, int kind) {
   const DFShape& sh = g_shapes[pl.d1_shape];
   DFArgs a;
   a.ts = pl.t.as<double>();
@@ -547,9 +539,20 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   a.chunk_aggs = pl.aggs.as<D1Agg>();
   a.bar = pl.bar.as<unsigned>();
   a.dbg = pl.dbg.bytes ? pl.dbg.as<unsigned long long>() : nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.d1_grid);
+  cfg.blockDim = dim3(sh.block);
+  cfg.dynamicSmemBytes = sh.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pl.d1_pdl ? 2 : 1;
   void* args[] = {&a};
-  GPM_CUDA(cudaLaunchCooperativeKernel(sh.fn[pl.P], dim3(pl.d1_grid), dim3(sh.block), args,
-                                       sh.smem, s));
+  GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[kind * 3 + pl.P], args));
   return GP_OK;
 }
 

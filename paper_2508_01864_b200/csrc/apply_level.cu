@@ -420,9 +420,15 @@ __device__ __forceinline__ double kval(double d1, double d2, double d3, const do
   if constexpr (!A::PROD) {
     const double s = D == 3 ? (d1 + d2) + d3 : d1 + d2;
     const double e = fexp_neg(s, tab);
-    if constexpr (P == 0) return e;
-    else if constexpr (P == 1) return e * (1.0 + s);
-    else return e * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0);
+    if constexpr (A::KIND == 0) {
+      if constexpr (P == 0) return e;
+      else if constexpr (P == 1) return e * (1.0 + s);
+      else return e * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0);
+    } else {   // gradient profile g(s) = -s k'(s) (algebra.cuh rcoef)
+      if constexpr (P == 1) return e * s;
+      else if constexpr (P == 2) return e * (s * s);
+      else return e * ((1.0 / 3.0) * (s * s) * (1.0 + s));
+    }
   } else {
     const double e = fexp_neg(d1 + d2, tab);
     if constexpr (P == 0) return e;
@@ -1043,8 +1049,19 @@ gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaS
 }
 size_t level_pt_bytes() { return sizeof(Pt4); }
 
-gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
+gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
+  if (kind != 0) {   // lengthscale gradient (L1 form only): moment order p + 1
+    if (prod) return fail(GP_ERR_UNSUPPORTED, "lengthscale-gradient MVM needs the L1 form");
+    if (pl.d == 2) {
+      if (pl.P == 0) return lv_run<Alg<1, 2, false, 1>>(pl, nrhs, s, launches);
+      if (pl.P == 1) return lv_run<Alg<2, 2, false, 1>>(pl, nrhs, s, launches);
+      return lv_run<Alg<3, 2, false, 1>>(pl, nrhs, s, launches);
+    }
+    if (pl.P == 0) return lv_run<Alg<1, 4, false, 1>>(pl, nrhs, s, launches);
+    if (pl.P == 1) return lv_run<Alg<2, 4, false, 1>>(pl, nrhs, s, launches);
+    return lv_run<Alg<3, 4, false, 1>>(pl, nrhs, s, launches);
+  }
   if (pl.d == 2) {
     if (!prod) {
       if (pl.P == 0) return lv_run<Alg<0, 2, false>>(pl, nrhs, s, launches);

@@ -84,6 +84,7 @@ struct Plan {
   int near_lb2 = 5, near_lb3 = 8, near_lb3m = 7;   // near-field block log2 sizes (tuned)
   // d = 1 launch geometry
   int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;
+  int d1_pdl = 1;                   // programmatic dependent launch for back-to-back applies
   int64_t d1_chunk = 0;
   int64_t struct_bytes = 0;
   int launches_per_apply = 0;
@@ -96,10 +97,13 @@ void plan_free(Plan& pl);
 
 // apply.cu
 // Rank-space apply: out_rank = K u_rank (no nugget).  u_rank, out_rank: n doubles.
-gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s);
+// kind 0: K; kind 1: dK/dlog(l) (lengthscale gradient, L1 / d = 1 only).
+gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s,
+                     int kind = 0);
 // User-order apply with gather/scatter: out = K v restricted to targets (unions).
 // Columns: v stride n_src, out stride n - tgt_off.
-gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s);
+gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s,
+                     int kind = 0);
 gp_status apply_prepare(Plan& pl);   // launch geometry + scratch
 gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cudaStream_t s);
 int64_t apply_model_bytes(const Plan& pl);

@@ -12,10 +12,14 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
 
 
-def check_rows(got, x, v, two_nu, form, ell, os_, rows=None, z=None, tol=TOL, what=""):
-    """Compare GPU output rows with the oracle; return (maxerr, bound)."""
+def check_rows(got, x, v, two_nu, form, ell, os_, rows=None, z=None, tol=TOL, what="",
+               grad=False):
+    """Compare GPU output rows with the oracle; return (maxerr, bound).
+    grad: the lengthscale-gradient MVM (l dK/dl) v, bounded by its own ||.||_inf."""
     got = np.asarray(got)
-    if z is None:
+    if grad:
+        ref, ab = oracle.dkmvm_rows(x, v, two_nu, form, ell, os_, rows=rows, return_abs=True)
+    elif z is None:
         ref, ab = oracle.kmvm_rows(x, v, two_nu, form, ell, os_, rows=rows, return_abs=True)
     else:
         ref, ab = oracle.kzx_rows(x, v, z, two_nu, form, ell, os_, rows=rows, return_abs=True)

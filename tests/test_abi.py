@@ -31,7 +31,8 @@ def test_header_declares_the_boundary():
     names = _declared_symbols()
     for must in ["gp_setup", "gp_kmvm", "gp_kmvm_host", "gp_kzx_setup", "gp_kzx", "gp_kzx_destroy",
                  "gp_cg_solve", "gp_predict", "gp_destroy", "gp_last_error", "gp_plan_query",
-                 "gp_plan_set_option", "gp_version", "gp_kmvm_rank", "gp_permute"]:
+                 "gp_plan_set_option", "gp_version", "gp_kmvm_rank", "gp_permute",
+                 "gp_kmvm_dlengthscale"]:
         assert must in names, must
 
 

@@ -1,0 +1,112 @@
+"""GPU parity of the lengthscale-gradient MVM (gp_kmvm_dlengthscale)
+against the oracle's l dK/dl rows (oracle.dkmvm_rows).
+
+Bar: max|d| <= 1e-9 * ||l dK/dl||_inf * ||v||_inf (the same per-MVM bound as K v, with the
+gradient matrix's own row-sum norm over the checked rows).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from gpu_helpers import check_rows, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _pts(n, d, seed, ties=False):
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, d))
+    if ties:
+        x = np.floor(x * 17) / 17
+        if n > 4:
+            x[n // 2] = x[1]
+    return x
+
+
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("n", [1, 2, 7, 1000, 7681, 20000])
+@pytest.mark.parametrize("ties", [False, True])
+def test_d1_grad_all_rows(gpm, two_nu, n, ties):
+    x = _pts(n, 1, 7 * n + two_nu, ties)
+    v = np.random.default_rng(n + 3).standard_normal(n)
+    ell = (0.07,)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.3))
+    out = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "l1", ell, 1.3, grad=True,
+               what=f"grad d1 nu={two_nu}/2 n={n} ties={ties}")
+
+
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+def test_d1_grad_config2_full_size(gpm, two_nu):
+    """Config 2 size (N = 10^6, the bench workload) on sampled rows, 3 right-hand sides."""
+    import torch
+    c = W.CONFIGS[2]
+    x = W.config_points(c)
+    V = np.stack([W.config_vector(c, r) for r in range(3)])
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, c.ell))
+    out = plan.kmvm_dlengthscale(to_dev(V)).cpu().numpy()
+    rows = W.sample_rows(x, 384)
+    for r in range(3):
+        check_rows(out[r], x, V[r], two_nu, "l1", c.ell, 1.0, rows=rows, grad=True,
+                   what=f"grad config2 nu={two_nu}/2 rhs {r}")
+    # rank-order entry point and single-column calls agree bitwise with the batch
+    vr = plan.to_rank(to_dev(V[1]))
+    o_r = plan.kmvm_dlengthscale(vr, rank_order=True)
+    assert torch.equal(plan.from_rank(o_r).cpu(), torch.from_numpy(out[1]))
+
+
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("n", [1, 3, 64, 2049, 5000])
+def test_l1_grad_all_rows(gpm, d, two_nu, n):
+    x = _pts(n, d, 11 * n + d, ties=(n % 2 == 1))
+    v = np.random.default_rng(n + d).standard_normal(n)
+    ell = (0.1, 0.2, 0.15)[:d]
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 0.9, form=0))
+    out = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "l1", ell, 0.9, grad=True,
+               what=f"grad d{d} nu={two_nu}/2 n={n}")
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_l1_grad_multi_level_sampled(gpm, d):
+    """Enough points for carried (high) passes and several right-hand sides."""
+    n = 300000 if d == 2 else 120000
+    x = _pts(n, d, 99 + d)
+    V = np.random.default_rng(d).standard_normal((2, n))
+    ell = (0.05, 0.08, 0.1)[:d]
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, ell, form=0))
+    out = plan.kmvm_dlengthscale(to_dev(V)).cpu().numpy()
+    rows = W.sample_rows(x, 256)
+    for r in range(2):
+        check_rows(out[r], x, V[r], 5, "l1", ell, 1.0, rows=rows, grad=True,
+                   what=f"grad d{d} sampled rhs {r}")
+
+
+def test_grad_unsupported_and_errors(gpm):
+    x = _pts(500, 2, 1)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.1), form=1))
+    with pytest.raises(gpm.GPError) as e:
+        plan.kmvm_dlengthscale(to_dev(np.ones(500)))
+    assert e.value.name == "UNSUPPORTED"
+    x1 = _pts(60000, 1, 2)
+    p1 = gpm.Plan(to_dev(x1), gpm.Kernel(3, (0.02,)))
+    p1.set_option(0, 2)            # force the multi-sub-tile path: no gradient there
+    with pytest.raises(gpm.GPError) as e:
+        p1.kmvm_dlengthscale(to_dev(np.ones(60000)))
+    assert e.value.name == "UNSUPPORTED"
+
+
+def test_grad_matches_finite_difference_of_kmvm(gpm):
+    """Independent of the oracle: (K(l(1+h)) - K(l(1-h))) v / 2h through gp_kmvm."""
+    n = 4000
+    x = _pts(n, 2, 5)
+    v = np.random.default_rng(6).standard_normal(n)
+    ell = np.array([0.1, 0.2])
+    h = 1e-5
+    g = gpm.Plan(to_dev(x), gpm.Kernel(5, tuple(ell), form=0)).kmvm_dlengthscale(to_dev(v))
+    kp = gpm.Plan(to_dev(x), gpm.Kernel(5, tuple(ell * (1 + h)), form=0)).kmvm(to_dev(v))
+    km = gpm.Plan(to_dev(x), gpm.Kernel(5, tuple(ell * (1 - h)), form=0)).kmvm(to_dev(v))
+    fd = ((kp - km) / (2 * h)).cpu().numpy()
+    g = g.cpu().numpy()
+    assert np.max(np.abs(g - fd)) <= 1e-6 * np.max(np.abs(g))
