@@ -159,43 +159,71 @@ struct Alg {
     for (int r = 0; r < NS / NQ; ++r) advance<P>(M + r * NQ, D, E);
   }
 
-  // M[c] += injection of u at split offset alpha (ea = e^{-alpha})
+  // M[c] += injection of u at split offset alpha (ea = e^{-alpha}).  Branch-free: the
+  // channel is a per-lane value (divergent), so every channel takes a masked FMA.
   __device__ __forceinline__ static void inject(double* M, int c, double u, double alpha,
                                                 double ea) {
-    const double w = u * ea;
+    double pw[NQ];
+    pw[0] = u * ea;
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) pw[q] = pw[q - 1] * alpha;
 #pragma unroll
     for (int cc = 0; cc < NCH; ++cc) {
-      if (cc == c) {
-        if constexpr (!PROD) {
-          double pw = w;
+      const double msk = cc == c ? 1.0 : 0.0;
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) { M[cc * NM + q] += pw; pw *= alpha; }
-        } else {
-          double pw = w;
+      for (int q = 0; q < NQ; ++q) {
+        if constexpr (!PROD) M[cc * NM + q] = fma(msk, pw[q], M[cc * NM + q]);
+        else M[cc * NM + q * NQ + 0] = fma(msk, pw[q], M[cc * NM + q * NQ + 0]);
+      }
+    }
+  }
+
+  // M[c] += the injection of u at split offset alpha, shifted along the scan by a span D
+  // (E = e^{-D}): the source's moments seen from a point D further on (direct form of
+  // inject followed by advance(D), used by the reduce loops: no full-state advance).
+  __device__ __forceinline__ static void inject_at(double* M, int c, double u, double alpha,
+                                                   double ea, double D, double E) {
+    if constexpr (!PROD) {
+      inject(M, c, u * E, alpha + D, ea);
+    } else {
+      double pm[NM];
+      double pa = u * ea * E;
 #pragma unroll
-          for (int m = 0; m < NQ; ++m) { M[cc * NM + m * NQ + 0] += pw; pw *= alpha; }
-        }
+      for (int m = 0; m < NQ; ++m) {
+        double pq = pa;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) { pm[m * NQ + q] = pq; pq *= D; }
+        pa *= alpha;
+      }
+#pragma unroll
+      for (int cc = 0; cc < NCH; ++cc) {
+        const double msk = cc == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int i = 0; i < NM; ++i) M[cc * NM + i] = fma(msk, pm[i], M[cc * NM + i]);
       }
     }
   }
 
   // value contributed to a target on channel rc at split offset beta (eb = e^{-beta})
+  // Branch-free: the channel's moments are selected first, then read once.
   __device__ __forceinline__ static double read(const double* M, int rc, double beta,
                                                 double eb) {
-    double v = 0.0;
+    double Ms[NM];
 #pragma unroll
-    for (int cc = 0; cc < NCH; ++cc) {
-      if (cc == rc) {
-        if constexpr (!PROD) {
-          v = readc_poly<P, KIND>(M + cc * NM, beta);
-        } else {
-          // k(alpha+beta) k(s): e^{-beta} sum_a a_a sum_{m<=a} C(a,m) beta^{a-m} (sum_q a_q M[m][q])
-          double G[NQ];
+    for (int i = 0; i < NM; ++i) Ms[i] = M[i];
 #pragma unroll
-          for (int m = 0; m < NQ; ++m) G[m] = read0<P>(M + cc * NM + m * NQ);
-          v = read_poly<P>(G, beta);
-        }
-      }
+    for (int cc = 1; cc < NCH; ++cc)
+#pragma unroll
+      for (int i = 0; i < NM; ++i) Ms[i] = cc == rc ? M[cc * NM + i] : Ms[i];
+    double v;
+    if constexpr (!PROD) {
+      v = readc_poly<P, KIND>(Ms, beta);
+    } else {
+      // k(alpha+beta) k(s): e^{-beta} sum_a a_a sum_{m<=a} C(a,m) beta^{a-m} (sum_q a_q M[m][q])
+      double G[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) G[m] = read0<P>(Ms + m * NQ);
+      v = read_poly<P>(G, beta);
     }
     return eb * v;
   }

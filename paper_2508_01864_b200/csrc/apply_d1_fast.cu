@@ -20,6 +20,7 @@
 #include "algebra.cuh"
 #include "fexp.cuh"
 #include "internal.h"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -113,37 +114,6 @@ __device__ __forceinline__ SF<P> sf_ld(const double* p) {
 #pragma unroll
   for (int q = 0; q <= P; ++q) s.M[q] = p[2 + q];
   return s;
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* m, unsigned phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(m)), "r"(phase)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
-                                            uint64_t* m) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(m))
-      : "memory");
 }
 
 // Published chunk aggregate: D, E, F[3], B[3] and the launch epoch (written last).

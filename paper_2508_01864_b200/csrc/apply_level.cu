@@ -29,6 +29,7 @@
 #include "algebra.cuh"
 #include "fexp.cuh"
 #include "internal.h"
+#include "tma.cuh"
 
 namespace gpm {
 
@@ -697,6 +698,14 @@ __device__ __forceinline__ double lv_y(const LvArgs& g, int64_t pos) {
   return g.pts[__ldg(g.ord2l1 + __ldg(g.ord + pos))].t3;
 }
 
+constexpr int CP_BLOCK = 128;
+constexpr int CP_ITEMS = 8;
+constexpr int CP_WARPS = CP_BLOCK / 32;
+static_assert(CP_BLOCK * CP_ITEMS == LV_TILE, "tile = block x items");
+// Swizzle of the 8-item rows (no padding): thread t's item k lives at 8t + ((k + t/2) & 7),
+// so the 16 lanes of each half-warp 64-bit shared access hit 16 distinct bank pairs.
+__host__ __device__ __forceinline__ int cpz(int i) { return (i & ~7) | ((i + (i >> 4)) & 7); }
+
 // Structure of one carried (multi-tile) pass, precomputed at setup (it does not depend on
 // v): per position the gap to the previous position of its node, e^{-gap}, the split
 // offset alpha, e^{-alpha}, the rank and the channel.  37 B per position, read coalesced.
@@ -708,17 +717,23 @@ struct HpView {
   const int* r;
   const signed char* ch;
 };
+// Padded to whole tiles; within a tile, position i is stored at cpz(i) (the k_cp shared
+// layout), padding positions are identities (no gap, no source, no target).
+__host__ __device__ inline int64_t hp_padded(int64_t nact) {
+  return (nact + LV_TILE - 1) / LV_TILE * LV_TILE;
+}
 __host__ __device__ inline size_t hp_bytes(int64_t nact) {
-  return ((size_t)nact * 37 + 255) & ~size_t(255);
+  return ((size_t)hp_padded(nact) * 37 + 255) & ~size_t(255);
 }
 __host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nact) {
+  const int64_t np = hp_padded(nact);
   HpView v;
   v.d = reinterpret_cast<const double*>(base);
-  v.e = v.d + nact;
-  v.a = v.e + nact;
-  v.ea = v.a + nact;
-  v.r = reinterpret_cast<const int*>(v.ea + nact);
-  v.ch = reinterpret_cast<const signed char*>(v.r + nact);
+  v.e = v.d + np;
+  v.a = v.e + np;
+  v.ea = v.a + np;
+  v.r = reinterpret_cast<const int*>(v.ea + np);
+  v.ch = reinterpret_cast<const signed char*>(v.r + np);
   return v;
 }
 
@@ -734,127 +749,398 @@ __global__ void k_hp_prep(LvArgs g, unsigned char* base) {
   int* r = const_cast<int*>(v.r);
   signed char* ch = const_cast<signed char*>(v.ch);
   const int64_t smask = (int64_t(1) << g.lseg) - 1;
-  for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < g.n_act;
+  const int64_t np = hp_padded(g.n_act);
+  for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < np;
        pos += (int64_t)gridDim.x * blockDim.x) {
-    const Elem el = lv_elem(g, pos);
-    const double dl = (pos & smask) == 0 ? 0.0 : el.y - lv_y(g, pos - 1);
-    d[pos] = dl;
-    e[pos] = fexp_neg(dl, tab);
-    a[pos] = el.a;
-    ea[pos] = fexp_neg(el.a, tab);
-    r[pos] = el.r;
-    ch[pos] = (signed char)el.ch;
+    const int64_t w = (pos & ~int64_t(LV_TILE - 1)) | cpz((int)(pos & (LV_TILE - 1)));
+    if (pos < g.n_act) {
+      const Elem el = lv_elem(g, pos);
+      const double dl = (pos & smask) == 0 ? 0.0 : el.y - lv_y(g, pos - 1);
+      d[w] = dl;
+      e[w] = fexp_neg(dl, tab);
+      a[w] = el.a;
+      ea[w] = fexp_neg(el.a, tab);
+      r[w] = el.r;
+      ch[w] = (signed char)el.ch;
+    } else {
+      d[w] = 0.0; e[w] = 1.0; a[w] = 0.0; ea[w] = 0.0; r[w] = -1; ch[w] = 0;
+    }
   }
 }
 
-// one carried pass of a batched launch (blockIdx.z selects the pass)
+// one carried pass (flattened work items item0 .. item0 + ntiles - 1 of k_cp)
 struct HpDesc {
   int64_t off;      // byte offset of the staged structure in hpbuf
   int64_t nact;     // active positions
   int lseg, ntiles;
+  int item0, pad;
 };
 
-template <class A, int KMODE>
-__global__ void __launch_bounds__(LV_BLOCK, 2) k_pass_hp(LvArgs g, const unsigned char* hpbase,
-                                                         const HpDesc* descs, int max_tiles) {
-  lv_col(g);
-  const HpDesc hd = descs[blockIdx.z];
-  if ((int)blockIdx.x >= hd.ntiles) return;     // uniform per CTA
-  const unsigned char* base = hpbase + hd.off;
-  g.lseg = hd.lseg;
-  g.n_act = hd.nact;
-  g.ntiles = hd.ntiles;
-  g.aggs += (int64_t)blockIdx.z * 2 * max_tiles;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
-  __shared__ LvScratch<A> sc;
-  __shared__ LSt<A::NS> s_part[LV_WARPS];
-  const int tid = threadIdx.x;
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
-  const int cnt = (int)min((int64_t)LV_TILE, g.n_act - T0);
-  fexp_table_init(sc.tab);
-  if (KMODE == 2) lv_carries<A>(sc, s_part, g.aggs, g.lseg, g.ntiles);
-  const HpView v = hp_view(base, g.n_act);
+// ---------------------------------------------------------------------------
+// Carried passes (k_cp).  A carried pass's nodes span whole 1024-position tiles, so no
+// node boundary falls inside a tile: the tile scan needs no flags.  The structure of every
+// carried pass is staged at setup (k_hp_prep) tile by tile in the exact shared-memory
+// layout below, padded to whole tiles with identity positions, so one tile arrives as six
+// 1-D bulk copies.  The kernel is persistent: each CTA walks the flattened (pass, tile)
+// list with a two-stage bulk-copy pipeline (tile k + 2 loads while tile k computes), and
+// processes every right-hand side of a tile from the staged copy; the gather of the next
+// (tile, column)'s sources is in flight during the current one.  Per tile and column:
+// 128 threads x 8 consecutive positions; per-thread aggregates in the direct form
+// (Alg::inject_at), warp scans, block carry, apply loops.
+//   MODE 1: tile aggregates (forward, backward) -> aggs;
+//   MODE 2: apply, with the tile carries folded from MODE 1's aggregates of the node.
+struct CpStage {
+  double d[LV_TILE], e[LV_TILE], a[LV_TILE], ea[LV_TILE];
+  int r[LV_TILE];
+  signed char ch[LV_TILE];
+};
+struct CpSmem {
+  CpStage st[2];
+};
+constexpr unsigned CP_STAGE_BYTES = 37u * LV_TILE;
+
+template <int NS>
+struct CSt {
+  double D, E;
+  double M[NS];
+};
+template <class A>
+__device__ __forceinline__ CSt<A::NS> cs_id() {
+  CSt<A::NS> s;
+  s.D = 0.0; s.E = 1.0;
 #pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
-    const int64_t pos = T0 + i;
-    const int pi = lvpad(i);
-    const int r = __ldg(v.r + pos);
-    E.rl[i] = r;
-    E.u[pi] = g.pts[r].u;
-    E.d[pi] = __ldg(v.d + pos);
-    E.e[pi] = __ldg(v.e + pos);
-    E.a[pi] = __ldg(v.a + pos);
-    E.ea[pi] = __ldg(v.ea + pos);
-    E.ch[i] = v.ch[pos];
-  }
-  __syncthreads();
-  const int64_t smask = (int64_t(1) << g.lseg) - 1;
-  lv_engine<A>(E, sc, cnt, T0, smask, g.n_act, KMODE, 0.0, g.aggs, true);
-  if (KMODE == 2) {   // own slot per pass: deterministic sum in the epilogue
-    double* slot = g.part + (int64_t)blockIdx.z * g.n;
+  for (int i = 0; i < A::NS; ++i) s.M[i] = 0.0;
+  return s;
+}
+// forward: X then Y along the scan, moments referenced at the end of Y
+template <class A>
+__device__ __forceinline__ CSt<A::NS> cs_fw(const CSt<A::NS>& X, const CSt<A::NS>& Y) {
+  CSt<A::NS> R;
 #pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) slot[E.rl[i]] = E.o[lvpad(i)];
+  for (int i = 0; i < A::NS; ++i) R.M[i] = X.M[i];
+  A::advance_all(R.M, Y.D, Y.E);
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] += Y.M[i];
+  R.D = X.D + Y.D; R.E = X.E * Y.E;
+  return R;
+}
+// backward: X left of Y, moments referenced just before the start of X
+template <class A>
+__device__ __forceinline__ CSt<A::NS> cs_bw(const CSt<A::NS>& X, const CSt<A::NS>& Y) {
+  CSt<A::NS> R;
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] = Y.M[i];
+  A::advance_all(R.M, X.D, X.E);
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] += X.M[i];
+  R.D = X.D + Y.D; R.E = X.E * Y.E;
+  return R;
+}
+template <int NS>
+__device__ __forceinline__ CSt<NS> cs_shfl(const CSt<NS>& s, int off, bool up) {
+  CSt<NS> r;
+  if (up) {
+    r.D = __shfl_up_sync(0xffffffffu, s.D, off);
+    r.E = __shfl_up_sync(0xffffffffu, s.E, off);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_up_sync(0xffffffffu, s.M[i], off);
+  } else {
+    r.D = __shfl_down_sync(0xffffffffu, s.D, off);
+    r.E = __shfl_down_sync(0xffffffffu, s.E, off);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_down_sync(0xffffffffu, s.M[i], off);
   }
+  return r;
+}
+template <int NS>
+__device__ __forceinline__ void cs_put(LvAgg* g, const CSt<NS>& s) {
+  g->D = s.D; g->E = s.E;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) g->M[i] = s.M[i];
+}
+template <int NS>
+__device__ __forceinline__ CSt<NS> cs_get(const LvAgg* g) {
+  CSt<NS> s;
+  s.D = __ldcg(&g->D); s.E = __ldcg(&g->E);
+#pragma unroll
+  for (int i = 0; i < NS; ++i) s.M[i] = __ldcg(&g->M[i]);
+  return s;
 }
 
-template <class A, int KMODE>
-__global__ void __launch_bounds__(LV_BLOCK, 2) k_pass(LvArgs g) {
-  lv_col(g);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
-  __shared__ LvScratch<A> sc;
-  __shared__ double s_yb;
-  const int tid = threadIdx.x;
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
-  const int cnt = (int)min((int64_t)LV_TILE, g.n_act - T0);
-  fexp_table_init(sc.tab);
-  __shared__ LSt<A::NS> s_part[LV_WARPS];
-  if (KMODE == 2) lv_carries<A>(sc, s_part, g.aggs, g.lseg, g.ntiles);
-  const int64_t smask = (int64_t(1) << g.lseg) - 1;
-  if (tid == 0) s_yb = (T0 & smask) != 0 ? lv_y(g, T0 - 1) : 0.0;
-  __syncthreads();
+template <class A>
+struct CpScratch {
+  CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS], part[CP_WARPS], cf, cb;
+};
+
+// Tile carries of one column: warps 0-1 fold the forward aggregates of the node's tiles
+// before tile t, warps 2-3 the backward aggregates after it (each lane a contiguous run,
+// then an ordered warp fold).  Result in sc.cf / sc.cb.  Ends with a barrier.
+template <class A>
+__device__ __forceinline__ void cp_carries(CpScratch<A>& sc, const LvAgg* aggs, int t, int first,
+                                           int last) {
+  using S = CSt<A::NS>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool fw = warp < 2;
+  const int lo = fw ? first : t + 1;
+  const int hi = fw ? t : last + 1;
+  const int cnt = max(0, hi - lo);
+  const int span = (cnt + 1) / 2;                   // tiles per warp
+  const int per = (span + 31) / 32;                 // tiles per lane
+  const int wlo = lo + (warp & 1) * span;
+  const int whi = min(hi, wlo + span);
+  S X = cs_id<A>();
+#pragma unroll 1
+  for (int k0 = 0; k0 < per; k0 += 2) {             // two loads in flight per step
+    S y[2];
 #pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
-    const Elem el = lv_elem(g, T0 + i);
-    const int pi = lvpad(i);
-    E.d[pi] = el.y;
-    E.u[pi] = el.u;
-    E.a[pi] = el.a;
-    E.ea[pi] = fexp_neg(el.a, sc.tab);
-    E.ch[i] = (signed char)el.ch;
-    E.rl[i] = el.r;
+    for (int k = 0; k < 2; ++k) {
+      const int j = wlo + lane * per + k0 + k;
+      y[k] = (k0 + k < per && j < whi) ? cs_get<A::NS>(aggs + 2 * j + (fw ? 0 : 1)) : cs_id<A>();
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) X = fw ? cs_fw<A>(X, y[k]) : cs_bw<A>(X, y[k]);
+  }
+#pragma unroll 1
+  for (int off = 1; off < 32; off <<= 1) {
+    S Y = cs_shfl<A::NS>(X, off, false);
+    if (lane + off < 32) X = fw ? cs_fw<A>(X, Y) : cs_bw<A>(X, Y);
+  }
+  if (lane == 0) sc.part[warp] = X;
+  __syncthreads();
+  if (threadIdx.x == 0) sc.cf = cs_fw<A>(sc.part[0], sc.part[1]);
+  if (threadIdx.x == 1) sc.cb = cs_bw<A>(sc.part[2], sc.part[3]);
+  __syncthreads();
+}
+
+// flattened work item -> pass (item0 table of the passes in shared memory)
+constexpr int CP_MAXPASS = 512;
+__device__ __forceinline__ int cp_pass_of(const int* item0, int npass, int item) {
+  int lo = 0, hi = npass - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (item0[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// thread 0: bulk-copy tile `item` into stage buffer st (expects 37 KB on bar)
+__device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDesc* descs,
+                                         const int* item0, int npass, int item, CpStage& st,
+                                         uint64_t* bar) {
+  const int p = cp_pass_of(item0, npass, item);
+  const HpDesc hd = descs[p];
+  const int64_t T0 = (int64_t)(item - hd.item0) * LV_TILE;
+  const HpView v = hp_view(hpbase + hd.off, hd.nact);
+  mbar_expect_tx(bar, CP_STAGE_BYTES);
+  tma_load_1d(st.d, v.d + T0, 8 * LV_TILE, bar);
+  tma_load_1d(st.e, v.e + T0, 8 * LV_TILE, bar);
+  tma_load_1d(st.a, v.a + T0, 8 * LV_TILE, bar);
+  tma_load_1d(st.ea, v.ea + T0, 8 * LV_TILE, bar);
+  tma_load_1d(st.r, v.r + T0, 4 * LV_TILE, bar);
+  tma_load_1d(st.ch, v.ch + T0, LV_TILE, bar);
+}
+
+template <class A, int MODE>
+__global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned char* hpbase,
+                                                   const HpDesc* descs, int npass, int total,
+                                                   int max_tiles, int nrhs) {
+  using S = CSt<A::NS>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
+  __shared__ CpScratch<A> sc;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_item0[CP_MAXPASS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = tid * CP_ITEMS;
+  const int G = gridDim.x;
+  for (int q = tid; q < npass; q += CP_BLOCK) s_item0[q] = descs[q].item0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
   }
   __syncthreads();
-  lv_engine<A>(E, sc, cnt, T0, smask, g.n_act, KMODE, s_yb, g.aggs);
-  if (KMODE == 2) {
+  if (tid == 0) {
+    if (blockIdx.x < total) cp_issue(hpbase, descs, s_item0, npass, blockIdx.x, SM.st[0], &bar[0]);
+    if (blockIdx.x + G < total)
+      cp_issue(hpbase, descs, s_item0, npass, blockIdx.x + G, SM.st[1], &bar[1]);
+  }
+  // sources of the first (tile, column)
+  double un[CP_ITEMS];
+  if (blockIdx.x < total) {
+    mbar_wait(&bar[0], 0);
 #pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) atomicAdd(g.acc + E.rl[i], E.o[lvpad(i)]);   // RED: each rank once per pass -> deterministic
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      const int r = SM.st[0].r[cpz(i0 + k)];
+      un[k] = r >= 0 ? g.pts[r].u : 0.0;
+    }
+  }
+  int j = 0;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < total; item += G, ++j) {
+    const int sidx = j & 1;
+    CpStage& E = SM.st[sidx];
+    mbar_wait(&bar[sidx], (j >> 1) & 1);
+    const int p = cp_pass_of(s_item0, npass, item);
+    const HpDesc hd = descs[p];
+    const int t = item - hd.item0;
+    const int tps = 1 << (hd.lseg - LV_LOGTILE);    // tiles per node
+    const int first = t & ~(tps - 1);
+    const int last = min(first + tps, hd.ntiles) - 1;
+#pragma unroll 1
+    for (int c = 0; c < nrhs; ++c) {
+      LvAgg* aggs = g.aggs + ((int64_t)c * npass + p) * 2 * max_tiles;
+      double uc[CP_ITEMS], of[CP_ITEMS];
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k) uc[k] = un[k];
+      // prefetch the sources of the next (tile, column)
+      if (c + 1 < nrhs) {
+        const Pt4* pn = g.pts + (int64_t)(c + 1) * g.n;
+#pragma unroll
+        for (int k = 0; k < CP_ITEMS; ++k) {
+          const int r = E.r[cpz(i0 + k)];
+          un[k] = r >= 0 ? pn[r].u : 0.0;
+        }
+      } else if (item + G < total) {
+        CpStage& En = SM.st[sidx ^ 1];
+        mbar_wait(&bar[sidx ^ 1], ((j + 1) >> 1) & 1);
+#pragma unroll
+        for (int k = 0; k < CP_ITEMS; ++k) {
+          const int r = En.r[cpz(i0 + k)];
+          un[k] = r >= 0 ? g.pts[r].u : 0.0;
+        }
+      }
+      if (MODE == 2) cp_carries<A>(sc, aggs, t, first, last);   // (barriers inside)
+      // ---- forward: per-thread aggregate (direct form), warp scan, block carry, apply.
+      {
+        S X;
+        double D = 0.0, Ee = 1.0;
+#pragma unroll
+        for (int q = 0; q < A::NS; ++q) X.M[q] = 0.0;
+#pragma unroll
+        for (int k = CP_ITEMS - 1; k >= 0; --k) {    // reference at item 7
+          const int z = cpz(i0 + k);
+          A::inject_at(X.M, E.ch[z], uc[k], E.a[z], E.ea[z], D, Ee);
+          D += E.d[z];
+          Ee *= E.e[z];
+        }
+        X.D = D; X.E = Ee;
+#pragma unroll 1
+        for (int off = 1; off < 32; off <<= 1) {
+          const S Y = cs_shfl<A::NS>(X, off, true);
+          if (lane >= off) X = cs_fw<A>(Y, X);
+        }
+        if (lane == 31) sc.wf[warp] = X;
+        S ex = cs_shfl<A::NS>(X, 1, true);
+        if (lane == 0) ex = cs_id<A>();
+        __syncthreads();
+        if (MODE == 1) {
+          if (tid == 0) {
+            S T = sc.wf[0];
+#pragma unroll 1
+            for (int w = 1; w < CP_WARPS; ++w) T = cs_fw<A>(T, sc.wf[w]);
+            cs_put<A::NS>(aggs + 2 * t, T);
+          }
+        } else {
+          S C = sc.cf;
+#pragma unroll 1
+          for (int w = 0; w < warp; ++w) C = cs_fw<A>(C, sc.wf[w]);
+          C = cs_fw<A>(C, ex);
+          double M[A::NS];
+#pragma unroll
+          for (int q = 0; q < A::NS; ++q) M[q] = C.M[q];
+#pragma unroll
+          for (int k = 0; k < CP_ITEMS; ++k) {
+            const int z = cpz(i0 + k);
+            A::advance_all(M, E.d[z], E.e[z]);
+            const int ch = E.ch[z];
+            const double a = E.a[z], ea = E.ea[z];
+            of[k] = A::read(M, A::NCH - 1 - ch, a, ea);
+            A::inject(M, ch, uc[k], a, ea);
+          }
+        }
+      }
+      // ---- backward
+      {
+        S X;
+        double D = 0.0, Ee = 1.0;
+#pragma unroll
+        for (int q = 0; q < A::NS; ++q) X.M[q] = 0.0;
+#pragma unroll
+        for (int k = 0; k < CP_ITEMS; ++k) {         // reference just before item 0
+          const int z = cpz(i0 + k);
+          D += E.d[z];
+          Ee *= E.e[z];
+          A::inject_at(X.M, E.ch[z], uc[k], E.a[z], E.ea[z], D, Ee);
+        }
+        X.D = D; X.E = Ee;
+#pragma unroll 1
+        for (int off = 1; off < 32; off <<= 1) {
+          const S Y = cs_shfl<A::NS>(X, off, false);
+          if (lane + off < 32) X = cs_bw<A>(X, Y);
+        }
+        if (lane == 0) sc.wb[warp] = X;
+        S ex = cs_shfl<A::NS>(X, 1, false);
+        if (lane == 31) ex = cs_id<A>();
+        __syncthreads();
+        if (MODE == 1) {
+          if (tid == 0) {
+            S T = sc.wb[CP_WARPS - 1];
+#pragma unroll 1
+            for (int w = CP_WARPS - 2; w >= 0; --w) T = cs_bw<A>(sc.wb[w], T);
+            cs_put<A::NS>(aggs + 2 * t + 1, T);
+          }
+        } else {
+          S C = sc.cb;
+#pragma unroll 1
+          for (int w = CP_WARPS - 1; w > warp; --w) C = cs_bw<A>(sc.wb[w], C);
+          C = cs_bw<A>(ex, C);
+          double M[A::NS];
+#pragma unroll
+          for (int q = 0; q < A::NS; ++q) M[q] = C.M[q];
+          double* slot = g.part + (int64_t)c * g.part_stride + (int64_t)p * g.n;
+#pragma unroll
+          for (int k = CP_ITEMS - 1; k >= 0; --k) {
+            const int z = cpz(i0 + k);
+            const int ch = E.ch[z];
+            const double a = E.a[z], ea = E.ea[z];
+            const double val = of[k] + A::read(M, A::NCH - 1 - ch, a, ea);
+            A::inject(M, ch, uc[k], a, ea);
+            A::advance_all(M, E.d[z], E.e[z]);
+            const int r = E.r[z];
+            if (r >= 0) slot[r] = val;
+          }
+        }
+      }
+      __syncthreads();                               // scratch reuse by the next column
+    }
+    // stage sidx is free: load tile item + 2G into it
+    if (tid == 0 && item + 2 * G < total) {
+      fence_proxy_async_smem();
+      cp_issue(hpbase, descs, s_item0, npass, item + 2 * G, E, &bar[sidx]);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // Host side.
 static size_t lv_smem_fused() { return sizeof(LvElems) + sizeof(LvPoints); }
-static size_t lv_smem_pass() { return sizeof(LvElems); }
 
 template <class A>
 static cudaError_t lv_set_attrs() {
   cudaError_t e;
-  const int fused = (int)lv_smem_fused(), pass = (int)lv_smem_pass();
+  const int fused = (int)lv_smem_fused();
   if ((e = cudaFuncSetAttribute(k_low2<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
     return e;
   if ((e = cudaFuncSetAttribute(k_low3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
     return e;
   if ((e = cudaFuncSetAttribute(k_mid3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
     return e;
-  if ((e = cudaFuncSetAttribute(k_pass<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
+  if ((e = cudaFuncSetAttribute(k_cp<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(CpSmem))))
     return e;
-  if ((e = cudaFuncSetAttribute(k_pass_hp<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_pass_hp<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass)))
-    return e;
-  return cudaFuncSetAttribute(k_pass<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass);
+  return cudaFuncSetAttribute(k_cp<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(CpSmem));
 }
 
 // The carried passes of a plan, in apply order: (ord, ord2l1, lseg, l1, n_act).
@@ -915,17 +1201,21 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     std::vector<HpDesc> dv;
     size_t o = 0;
     int mt = 0;
+    int items = 0;
     for (const HPass& h : hp) {
       const int nt = (int)((h.nact + LV_TILE - 1) / LV_TILE);
-      dv.push_back({(int64_t)o, h.nact, h.lseg, nt});
+      dv.push_back({(int64_t)o, h.nact, h.lseg, nt, items, 0});
       o += hp_bytes(h.nact);
       mt = std::max(mt, nt);
+      items += nt;
     }
+    pl.hp_items = items;
     pl.hp_tail.clear();
     for (const HPass& h : hp) pl.hp_tail.push_back(h.nact < pl.n ? 1 : 0);
     GPM_TRY(pl.hpdesc.alloc(sizeof(HpDesc) * dv.size()));
     GPM_CUDA(cudaMemcpy(pl.hpdesc.ptr, dv.data(), sizeof(HpDesc) * dv.size(), cudaMemcpyHostToDevice));
     pl.hp_npass = (int)dv.size();
+    if (pl.hp_npass > CP_MAXPASS) return fail(GP_ERR_UNSUPPORTED, "too many carried passes");
     pl.hp_maxtiles = mt;
   }
   LvArgs g = lv_base_args(pl);
@@ -937,7 +1227,7 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     g.lseg = h.lseg;
     g.l1 = h.l1;
     g.n_act = h.nact;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h.nact + 255) / 256, 148 * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hp_padded(h.nact) + 255) / 256, 148 * 8));
     k_hp_prep<<<grid, 256, 0, s>>>(g, pl.hpbuf.as<unsigned char>() + off);
     GPM_CUDA(cudaGetLastError());
     off += hp_bytes(h.nact);
@@ -998,12 +1288,14 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
         for (int c = 0; c < nrhs; ++c)
           GPM_CUDA(cudaMemsetAsync(g.part + c * g.part_stride + (int64_t)p * n, 0,
                                    sizeof(double) * n, s));
-    const dim3 gh(pl.hp_maxtiles, nrhs, pl.hp_npass);
     const HpDesc* dd = pl.hpdesc.as<HpDesc>();
-    k_pass_hp<A, 1><<<gh, LV_BLOCK, lv_smem_pass(), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
-                                                         pl.hp_maxtiles);
-    k_pass_hp<A, 2><<<gh, LV_BLOCK, lv_smem_pass(), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
-                                                         pl.hp_maxtiles);
+    const int grid = std::min(pl.hp_items, 3 * 148);   // persistent: 3 CTAs per SM
+    k_cp<A, 1><<<grid, CP_BLOCK, sizeof(CpSmem), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
+                                                      pl.hp_npass, pl.hp_items, pl.hp_maxtiles,
+                                                      nrhs);
+    k_cp<A, 2><<<grid, CP_BLOCK, sizeof(CpSmem), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
+                                                      pl.hp_npass, pl.hp_items, pl.hp_maxtiles,
+                                                      nrhs);
     *launches += 2;
     GPM_CUDA(cudaGetLastError());
   }

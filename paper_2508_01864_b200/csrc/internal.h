@@ -78,7 +78,7 @@ struct Plan {
   DevBuf pts;                       // d>=2: packed (t1, t2, t3, u) per rank, rebuilt per apply
   DevBuf hpbuf;                     // d>=2: staged structure of the carried passes (setup)
   DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)
-  int hp_npass = 0, hp_maxtiles = 0;
+  int hp_npass = 0, hp_maxtiles = 0, hp_items = 0;   // carried passes, max tiles, total tiles
   std::vector<char> hp_tail;        // carried pass has an inactive tail (slot must be zeroed)
   DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
   int near_lb2 = 5, near_lb3 = 8, near_lb3m = 7;   // near-field block log2 sizes (tuned)
