@@ -14,15 +14,17 @@
 // of eq L1_decomposition / product_decomposition without forming the overflowing
 // weights of eq matern_weights (R5).
 //
-// B200 layout: a pass engine works on one 1024-position tile staged in
-// shared memory (256 threads x 4 consecutive positions, flag-segmented warp-shuffle
-// scans, rolled loops: every launch walks the code once).  Launch structure per apply:
-//   d = 2: ONE fused launch for all levels l <= 10 (point data loaded once per tile,
-//          outputs accumulated in shared memory), then per level l > 10 an aggregate
-//          launch + an apply launch with carries across the tiles of a node;
-//   d = 3: ONE fused launch for all (l1 <= 10, l2 <= l1); per l1 > 10 one launch for
-//          all l2 <= 10 (the tile's points gathered once); aggregate + apply launches
-//          for (l1 > 10, l2 > 10).
+// B200 layout: 128 threads x 8 consecutive positions of a 1024-position tile
+// per CTA; nodes are aligned power-of-two position blocks, so node boundaries fall between
+// threads and the scans need no per-position flags.  Launch structure per apply:
+//   k_pack: rank-order point records (t1, t2, t3, u);
+//   d = 2: k_low2 -- near field (pairs split at levels <= lb) + levels lb < l <= 10 of each
+//          tile (point data staged once in shared memory);
+//   d = 3: k_low3 -- the same for (l1 <= 10, all l2); k_mid3 -- every l1 > 10 with l2 <= 10
+//          (one launch, blockIdx.z = l1);
+//   carried passes (nodes longer than a tile): k_cp<1> tile aggregates + k_cp<2> apply,
+//          persistent over all passes with a bulk-copy pipeline of setup-staged tiles;
+//   k_epilogue (apply.cu): fixed-order sum of the per-pass slots, scale, scatter.
 #include <algorithm>
 #include <vector>
 
@@ -33,343 +35,14 @@
 
 namespace gpm {
 
-constexpr int LV_BLOCK = 256;
-constexpr int LV_ITEMS = 4;
 constexpr int LV_LOGTILE = 10;
-constexpr int LV_TILE = 1 << LV_LOGTILE;  // == LV_BLOCK * LV_ITEMS
-constexpr int LV_WARPS = LV_BLOCK / 32;
-__host__ __device__ constexpr int lvpad(int i) { return i + (i >> 3); }  // <= 2-way conflicts
-constexpr int LV_PADN = LV_TILE + LV_TILE / 8;
-
-// Per-pass element arrays (scan order, padded index).
-struct LvElems {
-  double d[LV_PADN];   // last coordinate y, then the gap Delta to the previous position
-  double e[LV_PADN];   // e^{-Delta}
-  double u[LV_PADN];   // source weight
-  double a[LV_PADN];   // alpha
-  double ea[LV_PADN];  // e^{-alpha}
-  double o[LV_PADN];   // pass output (read values)
-  int rl[LV_TILE];     // output slot (tile-local point index, or global rank)
-  signed char ch[LV_TILE];
-};
+constexpr int LV_TILE = 1 << LV_LOGTILE;
 
 // Point arrays of the fused kernels (tile-local point index).
 struct LvPoints {
   double u[LV_TILE], t1[LV_TILE], t2[LV_TILE], t3[LV_TILE], acc[LV_TILE];
   int o2[LV_TILE];     // d = 3: ord2[l1] tile (local ranks) / global ranks (mid kernel)
 };
-
-template <int NS>
-struct LSt {
-  double D, E;
-  double M[NS];
-  int f;
-};
-
-template <class A>
-__device__ __forceinline__ LSt<A::NS> lid() {
-  LSt<A::NS> s;
-  s.D = 0.0; s.E = 1.0; s.f = 0;
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) s.M[i] = 0.0;
-  return s;
-}
-
-// forward (X left of Y): a segment start inside Y cuts X off
-template <class A>
-__device__ __forceinline__ LSt<A::NS> lcf(const LSt<A::NS>& X, const LSt<A::NS>& Y) {
-  if (Y.f) return Y;
-  LSt<A::NS> R;
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] = X.M[i];
-  A::advance_all(R.M, Y.D, Y.E);
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] += Y.M[i];
-  R.D = X.D + Y.D; R.E = X.E * Y.E; R.f = X.f;
-  return R;
-}
-// backward (X left of Y): a segment end inside X cuts Y off
-template <class A>
-__device__ __forceinline__ LSt<A::NS> lcb(const LSt<A::NS>& X, const LSt<A::NS>& Y) {
-  if (X.f) return X;
-  LSt<A::NS> R;
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] = Y.M[i];
-  A::advance_all(R.M, X.D, X.E);
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] += X.M[i];
-  R.D = X.D + Y.D; R.E = X.E * Y.E; R.f = Y.f;
-  return R;
-}
-
-template <int NS>
-__device__ __forceinline__ LSt<NS> lshfl(const LSt<NS>& s, int off, bool up) {
-  LSt<NS> r;
-  if (up) {
-    r.D = __shfl_up_sync(0xffffffffu, s.D, off);
-    r.E = __shfl_up_sync(0xffffffffu, s.E, off);
-    r.f = __shfl_up_sync(0xffffffffu, s.f, off);
-#pragma unroll
-    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_up_sync(0xffffffffu, s.M[i], off);
-  } else {
-    r.D = __shfl_down_sync(0xffffffffu, s.D, off);
-    r.E = __shfl_down_sync(0xffffffffu, s.E, off);
-    r.f = __shfl_down_sync(0xffffffffu, s.f, off);
-#pragma unroll
-    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_down_sync(0xffffffffu, s.M[i], off);
-  }
-  return r;
-}
-
-template <int NS>
-__device__ __forceinline__ void agg_put(LvAgg* g, const LSt<NS>& s) {
-  g->D = s.D; g->E = s.E; g->flag = s.f;
-#pragma unroll
-  for (int i = 0; i < NS; ++i) g->M[i] = s.M[i];
-}
-template <int NS>
-__device__ __forceinline__ LSt<NS> agg_get(const LvAgg* g) {
-  LSt<NS> s;
-  s.D = __ldcg(&g->D); s.E = __ldcg(&g->E); s.f = __ldcg(&g->flag);
-#pragma unroll
-  for (int i = 0; i < NS; ++i) s.M[i] = __ldcg(&g->M[i]);
-  return s;
-}
-
-template <class A>
-struct LvScratch {
-  LSt<A::NS> w[LV_WARPS], wx[LV_WARPS], tot;
-  double carry[2][A::NS];
-  double tab[64];
-};
-
-// Block-wide exclusive scan in one direction (FWD: threads < me; else threads > me),
-// plus the tile total.  Ends with a barrier.
-template <class A, bool FWD>
-__device__ __forceinline__ void lv_block_scan(const LSt<A::NS>& mine, LSt<A::NS>& excl,
-                                              LSt<A::NS>& tot, LvScratch<A>& sc) {
-  using S = LSt<A::NS>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  S x = mine;
-#pragma unroll 1
-  for (int off = 1; off < 32; off <<= 1) {
-    S y = lshfl<A::NS>(x, off, FWD);
-    if (FWD && lane >= off) x = lcf<A>(y, x);
-    if (!FWD && lane + off < 32) x = lcb<A>(x, y);
-  }
-  if (FWD && lane == 31) sc.w[warp] = x;
-  if (!FWD && lane == 0) sc.w[warp] = x;
-  S ex = lshfl<A::NS>(x, 1, FWD);
-  if ((FWD && lane == 0) || (!FWD && lane == 31)) ex = lid<A>();
-  __syncthreads();
-  if (warp == 0) {
-    S y = lane < LV_WARPS ? sc.w[lane] : lid<A>();
-#pragma unroll 1
-    for (int off = 1; off < LV_WARPS; off <<= 1) {
-      S z = lshfl<A::NS>(y, off, FWD);
-      if (FWD && lane >= off) y = lcf<A>(z, y);
-      if (!FWD && lane + off < 32) y = lcb<A>(y, z);
-    }
-    S ye = lshfl<A::NS>(y, 1, FWD);
-    if ((FWD && lane == 0) || (!FWD && lane >= LV_WARPS - 1)) ye = lid<A>();
-    if (lane < LV_WARPS) sc.wx[lane] = ye;
-    if (FWD && lane == LV_WARPS - 1) sc.tot = y;
-    if (!FWD && lane == 0) sc.tot = y;
-  }
-  __syncthreads();
-  excl = FWD ? lcf<A>(sc.wx[warp], ex) : lcb<A>(ex, sc.wx[warp]);
-  tot = sc.tot;
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------------------
-// The pass engine.  E.d holds y (scan coordinate) for positions [0, cnt) of a tile whose
-// first global position is T0; segments are aligned blocks of (smask + 1) positions;
-// nend = one past the last active position (a segment end).  mode: 0 apply (segments fit
-// the tile), 1 aggregates only (write tile totals to aggs[2*tile + {0,1}]), 2 apply with
-// the carries folded into sc.carry.  y_before = y of position T0 - 1 (mode 1/2 only).
-template <class A>
-__device__ __forceinline__ void lv_engine(LvElems& E, LvScratch<A>& sc, int cnt, int64_t T0,
-                                          int64_t smask, int64_t nend, int mode,
-                                          double y_before, LvAgg* aggs, bool preconv = false) {
-  using S = LSt<A::NS>;
-  const int tid = threadIdx.x;
-  const int i0 = tid * LV_ITEMS;
-  auto is_start = [&](int i) { return ((T0 + i) & smask) == 0; };
-  auto is_end = [&](int i) { return (((T0 + i + 1) & smask) == 0) || (T0 + i + 1 == nend); };
-
-  // gaps and e^{-gap} (unless staged by the setup, preconv)
-  double yprev = 0.0;
-  if (!preconv && i0 < cnt) yprev = i0 > 0 ? E.d[lvpad(i0 - 1)] : y_before;
-  if (!preconv) __syncthreads();
-#pragma unroll 1
-  for (int k = 0; k < LV_ITEMS && !preconv; ++k) {
-    const int i = i0 + k;
-    if (i < cnt) {
-      const int pi = lvpad(i);
-      const double y = E.d[pi];
-      const double dl = is_start(i) ? 0.0 : y - yprev;
-      yprev = y;
-      E.d[pi] = dl;
-      E.e[pi] = fexp_neg(dl, sc.tab);
-    }
-  }
-
-  // ---- forward
-  S Fx, Ft;
-  {
-    S X = lid<A>();
-#pragma unroll 1
-    for (int k = 0; k < LV_ITEMS; ++k) {
-      const int i = i0 + k;
-      if (i < cnt) {
-        const int pi = lvpad(i);
-        if (is_start(i)) {
-          X = lid<A>();
-          X.f = 1;
-        } else {
-          A::advance_all(X.M, E.d[pi], E.e[pi]);
-          X.D += E.d[pi];
-          X.E *= E.e[pi];
-        }
-        A::inject(X.M, E.ch[i], E.u[pi], E.a[pi], E.ea[pi]);
-      }
-    }
-    lv_block_scan<A, true>(X, Fx, Ft, sc);
-  }
-  if (mode == 1 && tid == 0) agg_put<A::NS>(aggs + 2 * blockIdx.x, Ft);
-  if (mode != 1) {
-    S C = lid<A>();
-    if (mode == 2) {
-#pragma unroll
-      for (int i = 0; i < A::NS; ++i) C.M[i] = sc.carry[0][i];
-    }
-    const S Cin = lcf<A>(C, Fx);
-    double M[A::NS];
-#pragma unroll
-    for (int i = 0; i < A::NS; ++i) M[i] = Cin.M[i];
-#pragma unroll 1
-    for (int k = 0; k < LV_ITEMS; ++k) {
-      const int i = i0 + k;
-      if (i < cnt) {
-        const int pi = lvpad(i);
-        if (is_start(i)) {
-#pragma unroll
-          for (int j = 0; j < A::NS; ++j) M[j] = 0.0;
-        } else {
-          A::advance_all(M, E.d[pi], E.e[pi]);
-        }
-        const int c = E.ch[i];
-        E.o[pi] = A::read(M, A::NCH - 1 - c, E.a[pi], E.ea[pi]);
-        A::inject(M, c, E.u[pi], E.a[pi], E.ea[pi]);
-      }
-    }
-  }
-
-  // ---- backward
-  S Bx, Bt;
-  {
-    S X = lid<A>();
-#pragma unroll 1
-    for (int k = LV_ITEMS - 1; k >= 0; --k) {
-      const int i = i0 + k;
-      if (i < cnt) {
-        const int pi = lvpad(i);
-        if (is_end(i)) {
-          X = lid<A>();
-          X.f = 1;
-        }
-        A::inject(X.M, E.ch[i], E.u[pi], E.a[pi], E.ea[pi]);
-        A::advance_all(X.M, E.d[pi], E.e[pi]);
-        X.D += E.d[pi];
-        X.E *= E.e[pi];
-      }
-    }
-    lv_block_scan<A, false>(X, Bx, Bt, sc);
-  }
-  if (mode == 1) {
-    if (tid == 0) agg_put<A::NS>(aggs + 2 * blockIdx.x + 1, Bt);
-    return;
-  }
-  {
-    S C = lid<A>();
-    if (mode == 2) {
-#pragma unroll
-      for (int i = 0; i < A::NS; ++i) C.M[i] = sc.carry[1][i];
-    }
-    const S Cin = lcb<A>(Bx, C);
-    double M[A::NS];
-#pragma unroll
-    for (int i = 0; i < A::NS; ++i) M[i] = Cin.M[i];
-#pragma unroll 1
-    for (int k = LV_ITEMS - 1; k >= 0; --k) {
-      const int i = i0 + k;
-      if (i < cnt) {
-        const int pi = lvpad(i);
-        if (is_end(i)) {
-#pragma unroll
-          for (int j = 0; j < A::NS; ++j) M[j] = 0.0;
-        }
-        const int c = E.ch[i];
-        E.o[pi] += A::read(M, A::NCH - 1 - c, E.a[pi], E.ea[pi]);
-        A::inject(M, c, E.u[pi], E.a[pi], E.ea[pi]);
-        A::advance_all(M, E.d[pi], E.e[pi]);
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// tile carries from the aggregate launch: warps 0-3 fold the forward aggregates of the
-// tiles before this one in its segment, warps 4-7 the backward ones after it; each lane
-// loads at most LV_CPL aggregates (all in flight), partials combined in order in smem.
-constexpr int LV_CPL = 2;
-template <class A>
-__device__ __forceinline__ void lv_carries(LvScratch<A>& sc, LSt<A::NS>* part, const LvAgg* aggs,
-                                           int lseg, int ntiles) {
-  using S = LSt<A::NS>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tps = 1 << (lseg - LV_LOGTILE);
-  const int t = blockIdx.x;
-  const int first = t & ~(tps - 1);
-  const int last = min(first + tps, ntiles) - 1;
-  const bool fw = warp < 4;
-  const int w4 = warp & 3;
-  const int lo = fw ? first : t + 1;
-  const int hi = fw ? t : last + 1;
-  const int cntc = max(0, hi - lo);
-  const int span = (cntc + 3) / 4;                 // tiles per warp
-  const int per = (span + 31) / 32;                // tiles per lane (any segment length)
-  const int wlo = lo + w4 * span;
-  const int whi = min(hi, wlo + span);
-  S X = lid<A>();
-#pragma unroll 1
-  for (int k0 = 0; k0 < per; k0 += LV_CPL) {       // LV_CPL loads in flight per step
-    S y[LV_CPL];
-#pragma unroll
-    for (int k = 0; k < LV_CPL; ++k) {
-      const int j = wlo + lane * per + k0 + k;
-      y[k] = (k0 + k < per && j < whi) ? agg_get<A::NS>(aggs + 2 * j + (fw ? 0 : 1)) : lid<A>();
-    }
-#pragma unroll
-    for (int k = 0; k < LV_CPL; ++k) X = fw ? lcf<A>(X, y[k]) : lcb<A>(X, y[k]);
-  }
-#pragma unroll 1
-  for (int off = 1; off < 32; off <<= 1) {
-    S Y = lshfl<A::NS>(X, off, false);
-    if (lane + off < 32) X = fw ? lcf<A>(X, Y) : lcb<A>(X, Y);
-  }
-  if (lane == 0) part[warp] = X;
-  __syncthreads();
-  if (threadIdx.x < 2) {
-    const bool f = threadIdx.x == 0;
-    S Z = lid<A>();
-#pragma unroll 1
-    for (int w = 0; w < 4; ++w) Z = f ? lcf<A>(Z, part[w]) : lcb<A>(Z, part[4 + w]);
-#pragma unroll
-    for (int i = 0; i < A::NS; ++i) sc.carry[threadIdx.x][i] = Z.M[i];
-  }
-}
 
 // Packed per-point record (rank order), rebuilt per apply by k_pack: one random access
 // touches one 32-byte sector instead of four.
@@ -438,59 +111,284 @@ __device__ __forceinline__ double kval(double d1, double d2, double d3, const do
   }
 }
 
+constexpr int CP_BLOCK = 128;
+constexpr int CP_ITEMS = 8;
+constexpr int CP_WARPS = CP_BLOCK / 32;
+static_assert(CP_BLOCK * CP_ITEMS == LV_TILE, "tile = block x items");
+// Swizzle of the 8-item rows (no padding): thread t's item k lives at 8t + ((k + t/2) & 7),
+// so the 16 lanes of each half-warp 64-bit shared access hit 16 distinct bank pairs.
+__host__ __device__ __forceinline__ int cpz(int i) { return (i & ~7) | ((i + (i >> 4)) & 7); }
+
+template <int NS>
+struct CSt {
+  double D, E;
+  double M[NS];
+};
+template <class A>
+__device__ __forceinline__ CSt<A::NS> cs_id() {
+  CSt<A::NS> s;
+  s.D = 0.0; s.E = 1.0;
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) s.M[i] = 0.0;
+  return s;
+}
+// forward: X then Y along the scan, moments referenced at the end of Y
+template <class A>
+__device__ __forceinline__ CSt<A::NS> cs_fw(const CSt<A::NS>& X, const CSt<A::NS>& Y) {
+  CSt<A::NS> R;
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] = X.M[i];
+  A::advance_all(R.M, Y.D, Y.E);
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] += Y.M[i];
+  R.D = X.D + Y.D; R.E = X.E * Y.E;
+  return R;
+}
+// backward: X left of Y, moments referenced just before the start of X
+template <class A>
+__device__ __forceinline__ CSt<A::NS> cs_bw(const CSt<A::NS>& X, const CSt<A::NS>& Y) {
+  CSt<A::NS> R;
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] = Y.M[i];
+  A::advance_all(R.M, X.D, X.E);
+#pragma unroll
+  for (int i = 0; i < A::NS; ++i) R.M[i] += X.M[i];
+  R.D = X.D + Y.D; R.E = X.E * Y.E;
+  return R;
+}
+template <int NS>
+__device__ __forceinline__ CSt<NS> cs_shfl(const CSt<NS>& s, int off, bool up) {
+  CSt<NS> r;
+  if (up) {
+    r.D = __shfl_up_sync(0xffffffffu, s.D, off);
+    r.E = __shfl_up_sync(0xffffffffu, s.E, off);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_up_sync(0xffffffffu, s.M[i], off);
+  } else {
+    r.D = __shfl_down_sync(0xffffffffu, s.D, off);
+    r.E = __shfl_down_sync(0xffffffffu, s.E, off);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_down_sync(0xffffffffu, s.M[i], off);
+  }
+  return r;
+}
+template <int NS>
+__device__ __forceinline__ void cs_put(LvAgg* g, const CSt<NS>& s) {
+  g->D = s.D; g->E = s.E;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) g->M[i] = s.M[i];
+}
+template <int NS>
+__device__ __forceinline__ CSt<NS> cs_get(const LvAgg* g) {
+  CSt<NS> s;
+  s.D = __ldcg(&g->D); s.E = __ldcg(&g->E);
+#pragma unroll
+  for (int i = 0; i < NS; ++i) s.M[i] = __ldcg(&g->M[i]);
+  return s;
+}
+
+template <class A>
+struct CpScratch {
+  CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS], part[CP_WARPS], cf, cb;
+};
+
+// ---------------------------------------------------------------------------
+// Within-tile levels: k_low2 / k_low3 / k_mid3.  One 1024-point tile per CTA of 128
+// threads; point data staged once in shared memory (LvPoints); per level each thread
+// builds its 8 consecutive positions of the level order in registers.  Nodes are aligned
+// blocks of 2^ls positions with ls >= 3, so node boundaries fall between threads: the
+// scans need no per-position flags (masked warp scans, per-warp carries).
+
 // Near field by direct summation: every pair i != j of the same aligned block of 2^lb
-// tile-local points (x1-rank blocks in the low kernels: exactly the pairs split at levels
-// <= lb; position blocks of ord2[l1] in the d=3 mid kernel, restricted to opposite x1
-// sides: exactly the pairs split at (l1, l2 <= lb)).  Pt.acc[i] += sum_j K(i,j) u_j.
-template <class A, int D>
+// tile-local positions (x1-rank blocks in k_low2 / k_low3: exactly the pairs split at
+// levels <= lb; position blocks of ord2[l1] with opposite x1 sides (l1side > 0): exactly
+// the pairs split at (l1, l2 <= lb)).  IND: position p holds point Pt.o2[p] (k_low3's inner
+// blocks), else point p.  Pt.acc[point] += sum_j K(i,j) u_j.
+template <class A, int D, bool IND>
 __device__ __forceinline__ void near_field(LvPoints& Pt, int cnt, int lb, int l1side,
                                            const double* tab) {
-  const int i0 = threadIdx.x * LV_ITEMS;
+  const int i0 = threadIdx.x * CP_ITEMS;
   if (i0 >= cnt) return;
-  double ti1[LV_ITEMS], ti2[LV_ITEMS], ti3[LV_ITEMS], acc[LV_ITEMS];
-  int hi[LV_ITEMS];
+  double ti1[CP_ITEMS], ti2[CP_ITEMS], ti3[CP_ITEMS], acc[CP_ITEMS];
+  int hi[CP_ITEMS];
 #pragma unroll
-  for (int k = 0; k < LV_ITEMS; ++k) {
+  for (int k = 0; k < CP_ITEMS; ++k) {
     const int i = min(i0 + k, cnt - 1);
-    ti1[k] = Pt.t1[i];
-    ti2[k] = Pt.t2[i];
-    ti3[k] = D == 3 ? Pt.t3[i] : 0.0;
-    hi[k] = l1side ? (Pt.o2[i] >> (l1side - 1)) & 1 : 0;
+    const int pi = IND ? Pt.o2[i] : i;
+    ti1[k] = Pt.t1[pi];
+    ti2[k] = Pt.t2[pi];
+    ti3[k] = D == 3 ? Pt.t3[pi] : 0.0;
+    hi[k] = l1side ? ((IND ? pi : Pt.o2[i]) >> (l1side - 1)) & 1 : 0;
     acc[k] = 0.0;
   }
   const int bs = (i0 >> lb) << lb;
   const int be = min(bs + (1 << lb), cnt);
 #pragma unroll 1
   for (int j = bs; j < be; ++j) {
-    const double tj1 = Pt.t1[j], tj2 = Pt.t2[j], uj = Pt.u[j];
-    const double tj3 = D == 3 ? Pt.t3[j] : 0.0;
-    const int hj = l1side ? (Pt.o2[j] >> (l1side - 1)) & 1 : 0;
+    const int pj = IND ? Pt.o2[j] : j;
+    const double tj1 = Pt.t1[pj], tj2 = Pt.t2[pj], uj = Pt.u[pj];
+    const double tj3 = D == 3 ? Pt.t3[pj] : 0.0;
+    const int hj = l1side ? ((IND ? pj : Pt.o2[j]) >> (l1side - 1)) & 1 : 0;
 #pragma unroll
-    for (int k = 0; k < LV_ITEMS; ++k) {
+    for (int k = 0; k < CP_ITEMS; ++k) {
       const bool ok = (i0 + k != j) && (!l1side || hj != hi[k]);
       const double v = kval<A, D>(fabs(ti1[k] - tj1), fabs(ti2[k] - tj2), fabs(ti3[k] - tj3), tab);
       acc[k] = ok ? fma(v, uj, acc[k]) : acc[k];
     }
   }
 #pragma unroll
-  for (int k = 0; k < LV_ITEMS; ++k)
-    if (i0 + k < cnt) Pt.acc[i0 + k] += acc[k];
+  for (int k = 0; k < CP_ITEMS; ++k)
+    if (i0 + k < cnt) Pt.acc[IND ? Pt.o2[i0 + k] : i0 + k] += acc[k];
 }
+
+// One thread's 8 positions of a level: gap to the previous position of the node (0 at a
+// node start), e^{-gap}, split offset alpha, e^{-alpha}, source weight, channel (-1: the
+// node has no cross pairs), output point (-1: none).
+struct TItems {
+  double d[CP_ITEMS], e[CP_ITEMS], a[CP_ITEMS], ea[CP_ITEMS], u[CP_ITEMS];
+  int ch[CP_ITEMS], o[CP_ITEMS];
+};
+
+template <class A>
+struct TScratch {
+  CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS];
+  double tab[64];
+};
+
+// The level scan of one tile, nodes of 2^ls positions (ls >= 3): of[k] = the level's
+// contribution to item k (both directions).  Barriers inside; uniform call.
+template <class A>
+__device__ __forceinline__ void seg_engine(const TItems& it, int ls, double* of,
+                                           TScratch<A>& sc) {
+  using S = CSt<A::NS>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = tid * CP_ITEMS;
+  const int smask = (1 << ls) - 1;
+  const int seg = i0 >> ls;
+  // ---- forward
+  {
+    S X;
+    double D = 0.0, Ee = 1.0;
+#pragma unroll
+    for (int q = 0; q < A::NS; ++q) X.M[q] = 0.0;
+#pragma unroll
+    for (int k = CP_ITEMS - 1; k >= 0; --k) {
+      A::inject_at(X.M, it.ch[k], it.u[k], it.a[k], it.ea[k], D, Ee);
+      D += it.d[k];
+      Ee *= it.e[k];
+    }
+    X.D = D; X.E = Ee;
+#pragma unroll 1
+    for (int off = 1; off < 32; off <<= 1) {
+      const S Y = cs_shfl<A::NS>(X, off, true);
+      if (lane >= off && ((i0 - CP_ITEMS * off) >> ls) == seg) X = cs_fw<A>(Y, X);
+    }
+    if (lane == 31) sc.wf[warp] = X;
+    S C = cs_shfl<A::NS>(X, 1, true);
+    if (lane == 0 || (i0 & smask) == 0) C = cs_id<A>();
+    __syncthreads();
+    const int w0 = (i0 & ~smask) / (32 * CP_ITEMS);   // first warp of my node
+    if (w0 < warp) {
+      S W = sc.wf[w0];
+#pragma unroll 1
+      for (int w = w0 + 1; w < warp; ++w) W = cs_fw<A>(W, sc.wf[w]);
+      C = cs_fw<A>(W, C);
+    }
+    double M[A::NS];
+#pragma unroll
+    for (int q = 0; q < A::NS; ++q) M[q] = C.M[q];
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      A::advance_all(M, it.d[k], it.e[k]);
+      of[k] = A::read(M, A::NCH - 1 - it.ch[k], it.a[k], it.ea[k]);
+      A::inject(M, it.ch[k], it.u[k], it.a[k], it.ea[k]);
+    }
+  }
+  // ---- backward
+  {
+    S X;
+    double D = 0.0, Ee = 1.0;
+#pragma unroll
+    for (int q = 0; q < A::NS; ++q) X.M[q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      D += it.d[k];
+      Ee *= it.e[k];
+      A::inject_at(X.M, it.ch[k], it.u[k], it.a[k], it.ea[k], D, Ee);
+    }
+    X.D = D; X.E = Ee;
+#pragma unroll 1
+    for (int off = 1; off < 32; off <<= 1) {
+      const S Y = cs_shfl<A::NS>(X, off, false);
+      if (lane + off < 32 && ((i0 + CP_ITEMS * off) >> ls) == seg) X = cs_bw<A>(X, Y);
+    }
+    if (lane == 0) sc.wb[warp] = X;
+    S C = cs_shfl<A::NS>(X, 1, false);
+    if (lane == 31 || ((i0 + CP_ITEMS) & smask) == 0) C = cs_id<A>();
+    const int w1 = min(((i0 | smask) + 1) / (32 * CP_ITEMS), CP_WARPS) - 1;   // last warp of my node
+    __syncthreads();
+    if (w1 > warp) {
+      S W = sc.wb[w1];
+#pragma unroll 1
+      for (int w = w1 - 1; w > warp; --w) W = cs_bw<A>(sc.wb[w], W);
+      C = cs_bw<A>(C, W);
+    }
+    double M[A::NS];
+#pragma unroll
+    for (int q = 0; q < A::NS; ++q) M[q] = C.M[q];
+#pragma unroll
+    for (int k = CP_ITEMS - 1; k >= 0; --k) {
+      const double v = of[k] + A::read(M, A::NCH - 1 - it.ch[k], it.a[k], it.ea[k]);
+      of[k] = it.ch[k] >= 0 ? v : 0.0;
+      A::inject(M, it.ch[k], it.u[k], it.a[k], it.ea[k]);
+      A::advance_all(M, it.d[k], it.e[k]);
+    }
+  }
+  __syncthreads();   // scratch reuse
+}
+
+// Gaps from the scan coordinates y[k] (ypre: y of the position before the thread's first,
+// ignored at a node start); padding items (o < 0) repeat the last y (gap 0).
+__device__ __forceinline__ void titems_gaps(TItems& it, const double* y, double ypre,
+                                            bool node_start, const double* tab) {
+#pragma unroll
+  for (int k = 0; k < CP_ITEMS; ++k) {
+    const double dl = k == 0 ? (node_start ? 0.0 : y[0] - ypre) : y[k] - y[k - 1];
+    it.d[k] = dl;
+    it.e[k] = fexp_neg(dl, tab);
+    it.ea[k] = fexp_neg(it.a[k], tab);
+  }
+}
+
+// this thread's 8 entries of a tile-local order array (ranks relative to T0)
+__device__ __forceinline__ void load_ord8(const int* ord, int i0, int cnt, int base, int* r) {
+  if (i0 + CP_ITEMS <= cnt && (reinterpret_cast<uintptr_t>(ord) & 15) == 0) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(ord + i0));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(ord + i0) + 1);
+    r[0] = a.x - base; r[1] = a.y - base; r[2] = a.z - base; r[3] = a.w - base;
+    r[4] = b.x - base; r[5] = b.y - base; r[6] = b.z - base; r[7] = b.w - base;
+  } else {
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) r[k] = i0 + k < cnt ? __ldg(ord + i0 + k) - base : -1;
+  }
+}
+
+__device__ __forceinline__ int lv_clamp_lb(int lb, int lmax) { return min(max(lb, 3), lmax); }
 
 // ---- fused low levels, d = 2: every level l <= min(10, L) of one 1024-rank tile
 template <class A>
-__global__ void __launch_bounds__(LV_BLOCK, 2) k_low2(LvArgs g) {
+__global__ void __launch_bounds__(CP_BLOCK, 3) k_low2(LvArgs g) {
   lv_col(g);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
-  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
-  __shared__ LvScratch<A> sc;
+  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw);
+  __shared__ TScratch<A> sc;
   const int tid = threadIdx.x;
+  const int i0 = tid * CP_ITEMS;
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
-#pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
+#pragma unroll 4
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) {
     const Pt4 p = g.pts[T0 + i];
     Pt.u[i] = p.u;
     Pt.t1[i] = p.t1;
@@ -499,50 +397,53 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low2(LvArgs g) {
   }
   __syncthreads();
   const int lmax = min(LV_LOGTILE, g.L);
-  const int lb = min(g.lb, lmax);
-  if (lb > 0) near_field<A, 2>(Pt, cnt, lb, 0, sc.tab);
+  const int lb = min(lv_clamp_lb(g.lb, LV_LOGTILE), lmax);
+  if (lb > 0) near_field<A, 2, false>(Pt, cnt, lb, 0, sc.tab);
   __syncthreads();
 #pragma unroll 1
   for (int l = lb + 1; l <= lmax; ++l) {
     const int* ord = g.ord2 + (size_t)(l - 1) * g.n + T0;
+    TItems it;
+    double y[CP_ITEMS];
+    load_ord8(ord, i0, cnt, (int)T0, it.o);
 #pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
-      const int r = __ldg(ord + i) - (int)T0;
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      const int i = i0 + k;
+      const int r = it.o[k];
       const int mid = ((i >> l) << l) + (1 << (l - 1));
-      const bool act = T0 + mid < g.n;
-      const int pi = lvpad(i);
-      const double al = act ? fabs(Pt.t1[r] - Pt.t1[mid]) : 0.0;
-      E.d[pi] = Pt.t2[r];
-      E.u[pi] = Pt.u[r];
-      E.a[pi] = al;
-      E.ea[pi] = fexp_neg(al, sc.tab);
-      E.ch[i] = act ? (signed char)((r >> (l - 1)) & 1) : (signed char)-1;
-      E.rl[i] = r;
+      const bool act = r >= 0 && T0 + mid < g.n;
+      y[k] = r >= 0 ? Pt.t2[r] : (k > 0 ? y[k - 1] : 0.0);
+      it.u[k] = r >= 0 ? Pt.u[r] : 0.0;
+      it.a[k] = act ? fabs(Pt.t1[r] - Pt.t1[mid]) : 0.0;
+      it.ch[k] = act ? (r >> (l - 1)) & 1 : -1;
     }
-    __syncthreads();
-    lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l) - 1, g.n, 0, 0.0, nullptr);
+    const bool nstart = (i0 & ((1 << l) - 1)) == 0;
+    const double ypre = (!nstart && i0 <= cnt) ? Pt.t2[__ldg(ord + i0 - 1) - (int)T0] : 0.0;
+    titems_gaps(it, y, ypre, nstart, sc.tab);
+    double of[CP_ITEMS];
+    seg_engine<A>(it, l, of, sc);
 #pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
-    __syncthreads();
+    for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
   }
-#pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
+  __syncthreads();
+#pragma unroll 4
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
 }
 
 // ---- fused low levels, d = 3: every (l1 <= min(10, L), l2 <= l1) of one tile
 template <class A>
-__global__ void __launch_bounds__(LV_BLOCK, 2) k_low3(LvArgs g) {
+__global__ void __launch_bounds__(CP_BLOCK, 3) k_low3(LvArgs g) {
   lv_col(g);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
-  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
-  __shared__ LvScratch<A> sc;
+  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw);
+  __shared__ TScratch<A> sc;
   const int tid = threadIdx.x;
+  const int i0 = tid * CP_ITEMS;
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
-#pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
+#pragma unroll 4
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) {
     const Pt4 p = g.pts[T0 + i];
     Pt.u[i] = p.u;
     Pt.t1[i] = p.t1;
@@ -552,57 +453,64 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_low3(LvArgs g) {
   }
   __syncthreads();
   const int lmax = min(LV_LOGTILE, g.L);
-  const int lb = min(g.lb, lmax);
-  if (lb > 0) near_field<A, 3>(Pt, cnt, lb, 0, sc.tab);
+  const int lb = min(lv_clamp_lb(g.lb, LV_LOGTILE), lmax);
+  if (lb > 0) near_field<A, 3, false>(Pt, cnt, lb, 0, sc.tab);
 #pragma unroll 1
   for (int l1 = lb + 1; l1 <= lmax; ++l1) {
     __syncthreads();
-#pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt)
+#pragma unroll 4
+    for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt)
       Pt.o2[i] = __ldg(g.ord2 + (size_t)(l1 - 1) * g.n + T0 + i) - (int)T0;
     __syncthreads();
+    // inner levels l2 <= 3: opposite-x1-side pairs of the same 8-position block of ord2[l1]
+    near_field<A, 3, true>(Pt, cnt, 3, l1, sc.tab);
+    __syncthreads();
 #pragma unroll 1
-    for (int l2 = 1; l2 <= l1; ++l2) {
+    for (int l2 = 4; l2 <= l1; ++l2) {
       const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
+      TItems it;
+      double y[CP_ITEMS];
+      int qq[CP_ITEMS];
+      load_ord8(ord, i0, cnt, (int)T0, qq);
 #pragma unroll
-      for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
-        const int q = __ldg(ord + i) - (int)T0;   // position in ord2[l1] (tile-local)
-        const int r = Pt.o2[q];                   // rank (tile-local)
-        const int mid1 = ((q >> l1) << l1) + (1 << (l1 - 1));
+      for (int k = 0; k < CP_ITEMS; ++k) {
+        const int i = i0 + k;
+        const int q = qq[k];                       // position in ord2[l1] (tile-local)
+        const int r = q >= 0 ? Pt.o2[q] : -1;      // rank (tile-local)
+        const int mid1 = ((max(q, 0) >> l1) << l1) + (1 << (l1 - 1));
         const int mid2 = ((i >> l2) << l2) + (1 << (l2 - 1));
-        const bool act = (T0 + mid1 < g.n) && (T0 + mid2 < g.n);
-        const int pi = lvpad(i);
-        const double al =
-            act ? fabs(Pt.t1[r] - Pt.t1[mid1]) + fabs(Pt.t2[r] - Pt.t2[Pt.o2[mid2]]) : 0.0;
-        E.d[pi] = Pt.t3[r];
-        E.u[pi] = Pt.u[r];
-        E.a[pi] = al;
-        E.ea[pi] = fexp_neg(al, sc.tab);
-        E.ch[i] = act ? (signed char)(2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1))
-                      : (signed char)-1;
-        E.rl[i] = r;
+        const bool act = r >= 0 && (T0 + mid1 < g.n) && (T0 + mid2 < g.n);
+        it.o[k] = r;
+        y[k] = r >= 0 ? Pt.t3[r] : (k > 0 ? y[k - 1] : 0.0);
+        it.u[k] = r >= 0 ? Pt.u[r] : 0.0;
+        it.a[k] = act ? fabs(Pt.t1[r] - Pt.t1[mid1]) + fabs(Pt.t2[r] - Pt.t2[Pt.o2[mid2]]) : 0.0;
+        it.ch[k] = act ? 2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1) : -1;
       }
-      __syncthreads();
-      lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l2) - 1, g.n, 0, 0.0, nullptr);
+      const bool nstart = (i0 & ((1 << l2) - 1)) == 0;
+      const double ypre =
+          (!nstart && i0 <= cnt) ? Pt.t3[Pt.o2[__ldg(ord + i0 - 1) - (int)T0]] : 0.0;
+      titems_gaps(it, y, ypre, nstart, sc.tab);
+      double of[CP_ITEMS];
+      seg_engine<A>(it, l2, of, sc);
 #pragma unroll
-      for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
+      for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
+#pragma unroll 4
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
 }
 
 // ---- d = 3, one outer level l1 > 10, all inner levels l2 <= 10 (tile = 1024 positions of
 // ord2[l1], i.e. one slice of one outer node; its points are gathered once)
 template <class A>
-__global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
+__global__ void __launch_bounds__(CP_BLOCK, 3) k_mid3(LvArgs g) {
   lv_col(g);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LvElems& E = *reinterpret_cast<LvElems*>(smem_raw);
-  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw + sizeof(LvElems));
-  __shared__ LvScratch<A> sc;
+  LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw);
+  __shared__ TScratch<A> sc;
   const int tid = threadIdx.x;
+  const int i0 = tid * CP_ITEMS;
   const int l1 = g.l1 + (int)blockIdx.z;   // one launch covers every outer level l1 > 10
   const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
@@ -610,14 +518,14 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
   double* slot = g.part + (int64_t)(g.npass + blockIdx.z) * g.n;
   if (mid1 >= g.n) {   // outer node without cross pairs (uniform per CTA): zero contribution
     const int* o2z = g.ord2 + (size_t)(l1 - 1) * g.n + T0;
-    for (int i = tid; i < cnt; i += LV_BLOCK) slot[__ldg(o2z + i)] = 0.0;
+    for (int i = tid; i < cnt; i += CP_BLOCK) slot[__ldg(o2z + i)] = 0.0;
     return;
   }
   fexp_table_init(sc.tab);
   const double m1 = __ldg(g.t1 + mid1);
   const int* o2g = g.ord2 + (size_t)(l1 - 1) * g.n + T0;
-#pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
+#pragma unroll 4
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) {
     const int r = __ldg(o2g + i);
     const Pt4 p = g.pts[r];
     Pt.o2[i] = r;
@@ -628,35 +536,37 @@ __global__ void __launch_bounds__(LV_BLOCK, 2) k_mid3(LvArgs g) {
     Pt.acc[i] = 0.0;
   }
   __syncthreads();
-  const int lb2 = min(g.lb2, LV_LOGTILE);
-  if (lb2 > 0) near_field<A, 3>(Pt, cnt, lb2, l1, sc.tab);
+  const int lb2 = lv_clamp_lb(g.lb2, LV_LOGTILE);
+  near_field<A, 3, false>(Pt, cnt, lb2, l1, sc.tab);
   __syncthreads();
 #pragma unroll 1
   for (int l2 = lb2 + 1; l2 <= LV_LOGTILE; ++l2) {
     const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
+    TItems it;
+    double y[CP_ITEMS];
+    load_ord8(ord, i0, cnt, (int)T0, it.o);          // tile-local position = point index
 #pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) {
-      const int q = __ldg(ord + i) - (int)T0;    // tile-local position = point index
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      const int i = i0 + k;
+      const int q = it.o[k];
       const int mid2 = ((i >> l2) << l2) + (1 << (l2 - 1));
-      const bool act = T0 + mid2 < g.n;
-      const int pi = lvpad(i);
-      const double al = act ? fabs(Pt.t1[q] - m1) + fabs(Pt.t2[q] - Pt.t2[mid2]) : 0.0;
-      E.d[pi] = Pt.t3[q];
-      E.u[pi] = Pt.u[q];
-      E.a[pi] = al;
-      E.ea[pi] = fexp_neg(al, sc.tab);
-      E.ch[i] = act ? (signed char)(2 * ((Pt.o2[q] >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1))
-                    : (signed char)-1;
-      E.rl[i] = q;
+      const bool act = q >= 0 && T0 + mid2 < g.n;
+      y[k] = q >= 0 ? Pt.t3[q] : (k > 0 ? y[k - 1] : 0.0);
+      it.u[k] = q >= 0 ? Pt.u[q] : 0.0;
+      it.a[k] = act ? fabs(Pt.t1[q] - m1) + fabs(Pt.t2[q] - Pt.t2[mid2]) : 0.0;
+      it.ch[k] = act ? 2 * ((Pt.o2[q] >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1) : -1;
     }
-    __syncthreads();
-    lv_engine<A>(E, sc, cnt, T0, (int64_t(1) << l2) - 1, g.n, 0, 0.0, nullptr);
+    const bool nstart = (i0 & ((1 << l2) - 1)) == 0;
+    const double ypre = (!nstart && i0 <= cnt) ? Pt.t3[__ldg(ord + i0 - 1) - (int)T0] : 0.0;
+    titems_gaps(it, y, ypre, nstart, sc.tab);
+    double of[CP_ITEMS];
+    seg_engine<A>(it, l2, of, sc);
 #pragma unroll
-    for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) Pt.acc[E.rl[i]] += E.o[lvpad(i)];
-    __syncthreads();
+    for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
   }
-#pragma unroll
-  for (int i = tid; i < LV_TILE; i += LV_BLOCK) if (i < cnt) slot[Pt.o2[i]] = Pt.acc[i];   // own slot: summed in order by the epilogue
+  __syncthreads();
+#pragma unroll 4
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) slot[Pt.o2[i]] = Pt.acc[i];   // own slot: summed in order by the epilogue
 }
 
 // ---- one pass whose segments span several tiles (mode 1: aggregates, 2: apply)
@@ -697,14 +607,6 @@ __device__ __forceinline__ double lv_y(const LvArgs& g, int64_t pos) {
   if (g.mode == 2) return g.pts[__ldg(g.ord + pos)].t2;
   return g.pts[__ldg(g.ord2l1 + __ldg(g.ord + pos))].t3;
 }
-
-constexpr int CP_BLOCK = 128;
-constexpr int CP_ITEMS = 8;
-constexpr int CP_WARPS = CP_BLOCK / 32;
-static_assert(CP_BLOCK * CP_ITEMS == LV_TILE, "tile = block x items");
-// Swizzle of the 8-item rows (no padding): thread t's item k lives at 8t + ((k + t/2) & 7),
-// so the 16 lanes of each half-warp 64-bit shared access hit 16 distinct bank pairs.
-__host__ __device__ __forceinline__ int cpz(int i) { return (i & ~7) | ((i + (i >> 4)) & 7); }
 
 // Structure of one carried (multi-tile) pass, precomputed at setup (it does not depend on
 // v): per position the gap to the previous position of its node, e^{-gap}, the split
@@ -799,79 +701,6 @@ struct CpSmem {
 };
 constexpr unsigned CP_STAGE_BYTES = 37u * LV_TILE;
 
-template <int NS>
-struct CSt {
-  double D, E;
-  double M[NS];
-};
-template <class A>
-__device__ __forceinline__ CSt<A::NS> cs_id() {
-  CSt<A::NS> s;
-  s.D = 0.0; s.E = 1.0;
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) s.M[i] = 0.0;
-  return s;
-}
-// forward: X then Y along the scan, moments referenced at the end of Y
-template <class A>
-__device__ __forceinline__ CSt<A::NS> cs_fw(const CSt<A::NS>& X, const CSt<A::NS>& Y) {
-  CSt<A::NS> R;
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] = X.M[i];
-  A::advance_all(R.M, Y.D, Y.E);
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] += Y.M[i];
-  R.D = X.D + Y.D; R.E = X.E * Y.E;
-  return R;
-}
-// backward: X left of Y, moments referenced just before the start of X
-template <class A>
-__device__ __forceinline__ CSt<A::NS> cs_bw(const CSt<A::NS>& X, const CSt<A::NS>& Y) {
-  CSt<A::NS> R;
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] = Y.M[i];
-  A::advance_all(R.M, X.D, X.E);
-#pragma unroll
-  for (int i = 0; i < A::NS; ++i) R.M[i] += X.M[i];
-  R.D = X.D + Y.D; R.E = X.E * Y.E;
-  return R;
-}
-template <int NS>
-__device__ __forceinline__ CSt<NS> cs_shfl(const CSt<NS>& s, int off, bool up) {
-  CSt<NS> r;
-  if (up) {
-    r.D = __shfl_up_sync(0xffffffffu, s.D, off);
-    r.E = __shfl_up_sync(0xffffffffu, s.E, off);
-#pragma unroll
-    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_up_sync(0xffffffffu, s.M[i], off);
-  } else {
-    r.D = __shfl_down_sync(0xffffffffu, s.D, off);
-    r.E = __shfl_down_sync(0xffffffffu, s.E, off);
-#pragma unroll
-    for (int i = 0; i < NS; ++i) r.M[i] = __shfl_down_sync(0xffffffffu, s.M[i], off);
-  }
-  return r;
-}
-template <int NS>
-__device__ __forceinline__ void cs_put(LvAgg* g, const CSt<NS>& s) {
-  g->D = s.D; g->E = s.E;
-#pragma unroll
-  for (int i = 0; i < NS; ++i) g->M[i] = s.M[i];
-}
-template <int NS>
-__device__ __forceinline__ CSt<NS> cs_get(const LvAgg* g) {
-  CSt<NS> s;
-  s.D = __ldcg(&g->D); s.E = __ldcg(&g->E);
-#pragma unroll
-  for (int i = 0; i < NS; ++i) s.M[i] = __ldcg(&g->M[i]);
-  return s;
-}
-
-template <class A>
-struct CpScratch {
-  CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS], part[CP_WARPS], cf, cb;
-};
-
 // Tile carries of one column: warps 0-1 fold the forward aggregates of the node's tiles
 // before tile t, warps 2-3 the backward aggregates after it (each lane a contiguous run,
 // then an ordered warp fold).  Result in sc.cf / sc.cb.  Ends with a barrier.
@@ -945,7 +774,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
                                                    const HpDesc* descs, int npass, int total,
                                                    int max_tiles, int nrhs) {
   using S = CSt<A::NS>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
   __shared__ CpScratch<A> sc;
   __shared__ __align__(8) uint64_t bar[2];
@@ -1124,7 +953,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
 
 // ---------------------------------------------------------------------------
 // Host side.
-static size_t lv_smem_fused() { return sizeof(LvElems) + sizeof(LvPoints); }
+static size_t lv_smem_fused() { return sizeof(LvPoints); }
 
 template <class A>
 static cudaError_t lv_set_attrs() {
@@ -1270,14 +1099,14 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   const dim3 gt(tiles, nrhs);
   // fused low levels (writes acc for every point: no memset needed)
   if (pl.d == 2)
-    k_low2<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
+    k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
   else
-    k_low3<A><<<gt, LV_BLOCK, lv_smem_fused(), s>>>(g);
+    k_low3<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
   *launches += 1;
   GPM_CUDA(cudaGetLastError());
   if (pl.d == 3 && L > LV_LOGTILE) {   // d = 3: every outer level l1 > 10 (inner l2 <= 10)
     g.l1 = LV_LOGTILE + 1;
-    k_mid3<A><<<dim3(tiles, nrhs, L - LV_LOGTILE), LV_BLOCK, lv_smem_fused(), s>>>(g);
+    k_mid3<A><<<dim3(tiles, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), s>>>(g);
     *launches += 1;
     GPM_CUDA(cudaGetLastError());
   }
