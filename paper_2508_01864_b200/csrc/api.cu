@@ -66,7 +66,7 @@ gp_status gp_setup(const double* x, int64_t n, int d, const gp_kernel* k, void* 
   *out = nullptr;
   if (!x) return fail(GP_ERR_INVALID_ARG, "x is NULL");
   if (n < 1) return fail(GP_ERR_INVALID_ARG, "n must be >= 1");
-  if (n > (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n > 2^30 not supported");
+  if (n >= (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n >= 2^30 not supported");
   GPM_TRY(check_kernel(k, d));
   GPM_TRY(check_device());
   gp_plan p = new (std::nothrow) gp_plan_s();
@@ -141,7 +141,7 @@ gp_status gp_kzx_setup(gp_plan p, const double* z, int64_t m, void* stream, gp_c
   Plan& pl = p->pl;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t nu = pl.n + m;
-  if (nu > (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n + m > 2^30 not supported");
+  if (nu >= (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n + m >= 2^30 not supported");
   DevBuf xu;
   GPM_TRY(xu.alloc(sizeof(double) * nu * pl.d));
   GPM_CUDA(cudaMemcpyAsync(xu.ptr, pl.x_raw.ptr, sizeof(double) * pl.n * pl.d,

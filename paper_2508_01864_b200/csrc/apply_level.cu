@@ -616,16 +616,17 @@ struct HpView {
   const double* e;
   const double* a;
   const double* ea;
-  const int* r;
-  const signed char* ch;
+  const unsigned* rc;   // rank | channel << 30; CP_NONE: padding
 };
+constexpr unsigned CP_RMASK = 0x3FFFFFFFu;
+constexpr unsigned CP_NONE = 0xFFFFFFFFu;   // rank field CP_RMASK: no point (n < 2^30)
 // Padded to whole tiles; within a tile, position i is stored at cpz(i) (the k_cp shared
 // layout), padding positions are identities (no gap, no source, no target).
 __host__ __device__ inline int64_t hp_padded(int64_t nact) {
   return (nact + LV_TILE - 1) / LV_TILE * LV_TILE;
 }
 __host__ __device__ inline size_t hp_bytes(int64_t nact) {
-  return ((size_t)hp_padded(nact) * 37 + 255) & ~size_t(255);
+  return ((size_t)hp_padded(nact) * 36 + 255) & ~size_t(255);
 }
 __host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nact) {
   const int64_t np = hp_padded(nact);
@@ -634,8 +635,7 @@ __host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nac
   v.e = v.d + np;
   v.a = v.e + np;
   v.ea = v.a + np;
-  v.r = reinterpret_cast<const int*>(v.ea + np);
-  v.ch = reinterpret_cast<const signed char*>(v.r + np);
+  v.rc = reinterpret_cast<const unsigned*>(v.ea + np);
   return v;
 }
 
@@ -648,8 +648,7 @@ __global__ void k_hp_prep(LvArgs g, unsigned char* base) {
   double* e = const_cast<double*>(v.e);
   double* a = const_cast<double*>(v.a);
   double* ea = const_cast<double*>(v.ea);
-  int* r = const_cast<int*>(v.r);
-  signed char* ch = const_cast<signed char*>(v.ch);
+  unsigned* rc = const_cast<unsigned*>(v.rc);
   const int64_t smask = (int64_t(1) << g.lseg) - 1;
   const int64_t np = hp_padded(g.n_act);
   for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < np;
@@ -662,10 +661,9 @@ __global__ void k_hp_prep(LvArgs g, unsigned char* base) {
       e[w] = fexp_neg(dl, tab);
       a[w] = el.a;
       ea[w] = fexp_neg(el.a, tab);
-      r[w] = el.r;
-      ch[w] = (signed char)el.ch;
+      rc[w] = (unsigned)el.r | ((unsigned)el.ch << 30);
     } else {
-      d[w] = 0.0; e[w] = 1.0; a[w] = 0.0; ea[w] = 0.0; r[w] = -1; ch[w] = 0;
+      d[w] = 0.0; e[w] = 1.0; a[w] = 0.0; ea[w] = 0.0; rc[w] = CP_NONE;
     }
   }
 }
@@ -693,13 +691,12 @@ struct HpDesc {
 //   MODE 2: apply, with the tile carries folded from MODE 1's aggregates of the node.
 struct CpStage {
   double d[LV_TILE], e[LV_TILE], a[LV_TILE], ea[LV_TILE];
-  int r[LV_TILE];
-  signed char ch[LV_TILE];
+  unsigned rc[LV_TILE];   // rank | channel << 30
 };
 struct CpSmem {
   CpStage st[2];
 };
-constexpr unsigned CP_STAGE_BYTES = 37u * LV_TILE;
+constexpr unsigned CP_STAGE_BYTES = 36u * LV_TILE;
 
 // Tile carries of one column: warps 0-1 fold the forward aggregates of the node's tiles
 // before tile t, warps 2-3 the backward aggregates after it (each lane a contiguous run,
@@ -741,22 +738,16 @@ __device__ __forceinline__ void cp_carries(CpScratch<A>& sc, const LvAgg* aggs, 
   __syncthreads();
 }
 
-// flattened work item -> pass (item0 table of the passes in shared memory)
-constexpr int CP_MAXPASS = 512;
-__device__ __forceinline__ int cp_pass_of(const int* item0, int npass, int item) {
-  int lo = 0, hi = npass - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (item0[mid] <= item) lo = mid; else hi = mid - 1;
-  }
-  return lo;
+// flattened work item -> pass: items are visited in increasing order, so each CTA keeps a
+// running pass index
+__device__ __forceinline__ int cp_pass_at(const HpDesc* descs, int npass, int p, int item) {
+  while (p + 1 < npass && __ldg(&descs[p + 1].item0) <= item) ++p;
+  return p;
 }
 
-// thread 0: bulk-copy tile `item` into stage buffer st (expects 37 KB on bar)
-__device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDesc* descs,
-                                         const int* item0, int npass, int item, CpStage& st,
-                                         uint64_t* bar) {
-  const int p = cp_pass_of(item0, npass, item);
+// thread 0: bulk-copy tile `item` of pass p into stage buffer st (expects 36 KB on bar)
+__device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDesc* descs, int p,
+                                         int item, CpStage& st, uint64_t* bar) {
   const HpDesc hd = descs[p];
   const int64_t T0 = (int64_t)(item - hd.item0) * LV_TILE;
   const HpView v = hp_view(hpbase + hd.off, hd.nact);
@@ -765,8 +756,7 @@ __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDe
   tma_load_1d(st.e, v.e + T0, 8 * LV_TILE, bar);
   tma_load_1d(st.a, v.a + T0, 8 * LV_TILE, bar);
   tma_load_1d(st.ea, v.ea + T0, 8 * LV_TILE, bar);
-  tma_load_1d(st.r, v.r + T0, 4 * LV_TILE, bar);
-  tma_load_1d(st.ch, v.ch + T0, LV_TILE, bar);
+  tma_load_1d(st.rc, v.rc + T0, 4 * LV_TILE, bar);
 }
 
 template <class A, int MODE>
@@ -778,11 +768,10 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
   CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
   __shared__ CpScratch<A> sc;
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ int s_item0[CP_MAXPASS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = tid * CP_ITEMS;
   const int G = gridDim.x;
-  for (int q = tid; q < npass; q += CP_BLOCK) s_item0[q] = descs[q].item0;
+  int p_iss = 0;   // pass of the last issued tile (thread 0)
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -790,9 +779,14 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
   }
   __syncthreads();
   if (tid == 0) {
-    if (blockIdx.x < total) cp_issue(hpbase, descs, s_item0, npass, blockIdx.x, SM.st[0], &bar[0]);
-    if (blockIdx.x + G < total)
-      cp_issue(hpbase, descs, s_item0, npass, blockIdx.x + G, SM.st[1], &bar[1]);
+    if (blockIdx.x < total) {
+      p_iss = cp_pass_at(descs, npass, p_iss, blockIdx.x);
+      cp_issue(hpbase, descs, p_iss, blockIdx.x, SM.st[0], &bar[0]);
+    }
+    if (blockIdx.x + G < total) {
+      p_iss = cp_pass_at(descs, npass, p_iss, blockIdx.x + G);
+      cp_issue(hpbase, descs, p_iss, blockIdx.x + G, SM.st[1], &bar[1]);
+    }
   }
   // sources of the first (tile, column)
   double un[CP_ITEMS];
@@ -800,17 +794,17 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
     mbar_wait(&bar[0], 0);
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
-      const int r = SM.st[0].r[cpz(i0 + k)];
-      un[k] = r >= 0 ? g.pts[r].u : 0.0;
+      const unsigned r = SM.st[0].rc[cpz(i0 + k)] & CP_RMASK;
+      un[k] = r != CP_RMASK ? g.pts[r].u : 0.0;
     }
   }
-  int j = 0;
+  int j = 0, p = 0;
 #pragma unroll 1
   for (int item = blockIdx.x; item < total; item += G, ++j) {
     const int sidx = j & 1;
     CpStage& E = SM.st[sidx];
     mbar_wait(&bar[sidx], (j >> 1) & 1);
-    const int p = cp_pass_of(s_item0, npass, item);
+    p = cp_pass_at(descs, npass, p, item);
     const HpDesc hd = descs[p];
     const int t = item - hd.item0;
     const int tps = 1 << (hd.lseg - LV_LOGTILE);    // tiles per node
@@ -827,16 +821,16 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
         const Pt4* pn = g.pts + (int64_t)(c + 1) * g.n;
 #pragma unroll
         for (int k = 0; k < CP_ITEMS; ++k) {
-          const int r = E.r[cpz(i0 + k)];
-          un[k] = r >= 0 ? pn[r].u : 0.0;
+          const unsigned r = E.rc[cpz(i0 + k)] & CP_RMASK;
+          un[k] = r != CP_RMASK ? pn[r].u : 0.0;
         }
       } else if (item + G < total) {
         CpStage& En = SM.st[sidx ^ 1];
         mbar_wait(&bar[sidx ^ 1], ((j + 1) >> 1) & 1);
 #pragma unroll
         for (int k = 0; k < CP_ITEMS; ++k) {
-          const int r = En.r[cpz(i0 + k)];
-          un[k] = r >= 0 ? g.pts[r].u : 0.0;
+          const unsigned r = En.rc[cpz(i0 + k)] & CP_RMASK;
+          un[k] = r != CP_RMASK ? g.pts[r].u : 0.0;
         }
       }
       if (MODE == 2) cp_carries<A>(sc, aggs, t, first, last);   // (barriers inside)
@@ -849,7 +843,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
 #pragma unroll
         for (int k = CP_ITEMS - 1; k >= 0; --k) {    // reference at item 7
           const int z = cpz(i0 + k);
-          A::inject_at(X.M, E.ch[z], uc[k], E.a[z], E.ea[z], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], E.ea[z], D, Ee);
           D += E.d[z];
           Ee *= E.e[z];
         }
@@ -882,7 +876,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
           for (int k = 0; k < CP_ITEMS; ++k) {
             const int z = cpz(i0 + k);
             A::advance_all(M, E.d[z], E.e[z]);
-            const int ch = E.ch[z];
+            const int ch = E.rc[z] >> 30;
             const double a = E.a[z], ea = E.ea[z];
             of[k] = A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
@@ -900,7 +894,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
           const int z = cpz(i0 + k);
           D += E.d[z];
           Ee *= E.e[z];
-          A::inject_at(X.M, E.ch[z], uc[k], E.a[z], E.ea[z], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], E.ea[z], D, Ee);
         }
         X.D = D; X.E = Ee;
 #pragma unroll 1
@@ -931,13 +925,14 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
 #pragma unroll
           for (int k = CP_ITEMS - 1; k >= 0; --k) {
             const int z = cpz(i0 + k);
-            const int ch = E.ch[z];
+            const unsigned rcz = E.rc[z];
+            const int ch = rcz >> 30;
             const double a = E.a[z], ea = E.ea[z];
             const double val = of[k] + A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
             A::advance_all(M, E.d[z], E.e[z]);
-            const int r = E.r[z];
-            if (r >= 0) slot[r] = val;
+            const unsigned r = rcz & CP_RMASK;
+            if (r != CP_RMASK) slot[r] = val;
           }
         }
       }
@@ -946,7 +941,8 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
     // stage sidx is free: load tile item + 2G into it
     if (tid == 0 && item + 2 * G < total) {
       fence_proxy_async_smem();
-      cp_issue(hpbase, descs, s_item0, npass, item + 2 * G, E, &bar[sidx]);
+      p_iss = cp_pass_at(descs, npass, p_iss, item + 2 * G);
+      cp_issue(hpbase, descs, p_iss, item + 2 * G, E, &bar[sidx]);
     }
   }
 }
@@ -1044,7 +1040,6 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     GPM_TRY(pl.hpdesc.alloc(sizeof(HpDesc) * dv.size()));
     GPM_CUDA(cudaMemcpy(pl.hpdesc.ptr, dv.data(), sizeof(HpDesc) * dv.size(), cudaMemcpyHostToDevice));
     pl.hp_npass = (int)dv.size();
-    if (pl.hp_npass > CP_MAXPASS) return fail(GP_ERR_UNSUPPORTED, "too many carried passes");
     pl.hp_maxtiles = mt;
   }
   LvArgs g = lv_base_args(pl);
@@ -1118,13 +1113,20 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
           GPM_CUDA(cudaMemsetAsync(g.part + c * g.part_stride + (int64_t)p * n, 0,
                                    sizeof(double) * n, s));
     const HpDesc* dd = pl.hpdesc.as<HpDesc>();
-    const int grid = std::min(pl.hp_items, 3 * 148);   // persistent: 3 CTAs per SM
-    k_cp<A, 1><<<grid, CP_BLOCK, sizeof(CpSmem), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
-                                                      pl.hp_npass, pl.hp_items, pl.hp_maxtiles,
-                                                      nrhs);
-    k_cp<A, 2><<<grid, CP_BLOCK, sizeof(CpSmem), s>>>(g, pl.hpbuf.as<unsigned char>(), dd,
-                                                      pl.hp_npass, pl.hp_items, pl.hp_maxtiles,
-                                                      nrhs);
+    static int grid1 = 0, grid2 = 0;   // persistent: as many CTAs as fit (per instantiation)
+    if (!grid1) {
+      int dev = 0, sms = 0, o1 = 0, o2 = 0;
+      GPM_CUDA(cudaGetDevice(&dev));
+      GPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmem)));
+      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmem)));
+      grid1 = std::max(1, o1) * sms;
+      grid2 = std::max(1, o2) * sms;
+    }
+    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmem), s>>>(
+        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
+    k_cp<A, 2><<<std::min(pl.hp_items, grid2), CP_BLOCK, sizeof(CpSmem), s>>>(
+        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
     *launches += 2;
     GPM_CUDA(cudaGetLastError());
   }
