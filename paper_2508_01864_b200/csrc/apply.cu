@@ -103,7 +103,10 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
                    std::max(1, pl.hp_npass);
   if (pl.aggs.bytes < ag) GPM_TRY(pl.aggs.alloc(ag));
   const size_t pb = sizeof(double) * (size_t)std::max(1, level_nparts(pl)) * pl.n * nrhs;
-  if (pl.part.bytes < pb) GPM_TRY(pl.part.alloc(pb));
+  if (pl.part.bytes < pb) {
+    GPM_TRY(pl.part.alloc(pb));
+    pl.part_zero_cols = 0;
+  }
   return GP_OK;
 }
 

@@ -1017,6 +1017,11 @@ static LvArgs lv_base_args(const Plan& pl) {
 // the caller packs first)
 gp_status level_setup(Plan& pl, cudaStream_t s) {
   if (pl.d < 2) return GP_OK;
+  if (!pl.s2) {
+    GPM_CUDA(cudaStreamCreateWithFlags(&pl.s2, cudaStreamNonBlocking));
+    GPM_CUDA(cudaEventCreateWithFlags(&pl.ev_fork, cudaEventDisableTiming));
+    GPM_CUDA(cudaEventCreateWithFlags(&pl.ev_join, cudaEventDisableTiming));
+  }
   const std::vector<HPass> hp = high_passes(pl);
   size_t total = 0;
   for (const HPass& h : hp) total += hp_bytes(h.nact);
@@ -1092,6 +1097,35 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   g.npass = pl.hp_npass;
   g.part_stride = (int64_t)level_nparts(pl) * n;
   const dim3 gt(tiles, nrhs);
+  const bool hp = pl.hp_npass > 0;
+  const HpDesc* dd = pl.hpdesc.as<HpDesc>();
+  static int grid1 = 0, grid2 = 0;   // persistent k_cp: as many CTAs as fit (per instantiation)
+  if (hp && !grid1) {
+    int dev = 0, sms = 0, o1 = 0, o2 = 0;
+    GPM_CUDA(cudaGetDevice(&dev));
+    GPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmem)));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmem)));
+    grid1 = std::max(1, o1) * sms;
+    grid2 = std::max(1, o2) * sms;
+  }
+  if (hp) {
+    // ranks past a pass's active range are never written: zero those slots once per buffer
+    for (int c = pl.part_zero_cols; c < nrhs; ++c)
+      for (int p = 0; p < pl.hp_npass; ++p)
+        if (pl.hp_tail[p])
+          GPM_CUDA(cudaMemsetAsync(g.part + c * g.part_stride + (int64_t)p * n, 0,
+                                   sizeof(double) * n, s));
+    pl.part_zero_cols = std::max(pl.part_zero_cols, nrhs);
+    // the carried-pass tile aggregates do not depend on the low levels: side stream
+    GPM_CUDA(cudaEventRecord(pl.ev_fork, s));
+    GPM_CUDA(cudaStreamWaitEvent(pl.s2, pl.ev_fork, 0));
+    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmem), pl.s2>>>(
+        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
+    GPM_CUDA(cudaGetLastError());
+    GPM_CUDA(cudaEventRecord(pl.ev_join, pl.s2));
+    *launches += 1;
+  }
   // fused low levels (writes acc for every point: no memset needed)
   if (pl.d == 2)
     k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
@@ -1105,29 +1139,11 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     *launches += 1;
     GPM_CUDA(cudaGetLastError());
   }
-  // every carried pass in one aggregate launch + one apply launch (staged structure)
-  if (pl.hp_npass > 0) {
-    for (int p = 0; p < pl.hp_npass; ++p)   // ranks past n_act get no write: zero the slot
-      if (pl.hp_tail[p])
-        for (int c = 0; c < nrhs; ++c)
-          GPM_CUDA(cudaMemsetAsync(g.part + c * g.part_stride + (int64_t)p * n, 0,
-                                   sizeof(double) * n, s));
-    const HpDesc* dd = pl.hpdesc.as<HpDesc>();
-    static int grid1 = 0, grid2 = 0;   // persistent: as many CTAs as fit (per instantiation)
-    if (!grid1) {
-      int dev = 0, sms = 0, o1 = 0, o2 = 0;
-      GPM_CUDA(cudaGetDevice(&dev));
-      GPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmem)));
-      GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmem)));
-      grid1 = std::max(1, o1) * sms;
-      grid2 = std::max(1, o2) * sms;
-    }
-    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmem), s>>>(
-        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
+  if (hp) {   // carried-pass apply (needs the aggregates)
+    GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     k_cp<A, 2><<<std::min(pl.hp_items, grid2), CP_BLOCK, sizeof(CpSmem), s>>>(
         g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
-    *launches += 2;
+    *launches += 1;
     GPM_CUDA(cudaGetLastError());
   }
   return GP_OK;

@@ -79,6 +79,10 @@ struct Plan {
   DevBuf hpbuf;                     // d>=2: staged structure of the carried passes (setup)
   DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)
   int hp_npass = 0, hp_maxtiles = 0, hp_items = 0;   // carried passes, max tiles, total tiles
+  // d >= 2: side stream for the carried-pass aggregates (independent of the low levels)
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int part_zero_cols = 0;   // columns of `part` whose never-written tail slots are zeroed
   std::vector<char> hp_tail;        // carried pass has an inactive tail (slot must be zeroed)
   DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
   int near_lb2 = 4, near_lb3 = 8, near_lb3m = 5;   // near-field block log2 sizes (tuned)

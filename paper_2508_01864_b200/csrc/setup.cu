@@ -102,6 +102,11 @@ void plan_free(Plan& pl) {
   for (DevBuf* b : {&pl.x_raw, &pl.perm, &pl.t, &pl.ord2, &pl.ord3, &pl.u, &pl.acc, &pl.w,
                     &pl.aggs, &pl.bar, &pl.stage_in, &pl.stage_out, &pl.dbg, &pl.pts, &pl.hpbuf, &pl.hpdesc, &pl.part})
     b->release();
+  if (pl.ev_fork) cudaEventDestroy(pl.ev_fork);
+  if (pl.ev_join) cudaEventDestroy(pl.ev_join);
+  if (pl.s2) cudaStreamDestroy(pl.s2);
+  pl.ev_fork = pl.ev_join = nullptr;
+  pl.s2 = nullptr;
 }
 
 static gp_status sort_pairs_u64(void* tmp, size_t tmp_bytes, const unsigned long long* kin,
