@@ -265,6 +265,8 @@ gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
     p->pl.d1_shape = (int)value;
   } else if (option == 2) {
     p->pl.d1_pdl = value != 0;
+  } else if (option == 3) {
+    p->pl.d1_prefetch = value != 0;
   } else {
     return fail(GP_ERR_INVALID_ARG, "unknown option");
   }

@@ -34,6 +34,7 @@ struct DFArgs {
   int64_t n, n_src, tgt_off, chunk;
   int user_order;
   int nrhs;               // columns processed in this launch (multi-RHS, §8(f) f1)
+  int prefetch;           // user order: L2 prefetch of v slices
   int64_t vstride, ostride;
   double os2;
   D1Agg* chunk_aggs;      // D1Pub[2][grid] (see below; double-buffered per column)
@@ -187,6 +188,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
       if (u_tma && nu) tma_load_1d(s_u + lo, a.v + c0 + lo, nu * 8, &mbar[p]);
     }
   }
+  // user order: the random gathers of v hit L2 if v was streamed in first -- each CTA
+  // prefetches an equal slice of the first column (L2 is coherent: safe under PDL)
+  auto prefetch_v = [&](int col) {
+    const int64_t lo = min((int64_t)blockIdx.x * ((a.n_src + gridDim.x - 1) / gridDim.x), a.n_src);
+    const int64_t hi = min(lo + (a.n_src + gridDim.x - 1) / gridDim.x, a.n_src);
+    if (hi > lo) prefetch_l2_range(a.v + col * a.vstride + lo, (size_t)(hi - lo) * 8);
+  };
+  if (a.user_order && a.prefetch && tid == 32) prefetch_v(0);
   const int j0 = tid * ITEMS;
   const int mypart = tid / PT;
   double tprev = 0.0, tlast = 0.0;
@@ -220,6 +229,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   const double* vcol = a.v + col * a.vstride;
   double* ocol = a.out + col * a.ostride;
   D1Pub* pubc = pub + (col & 1) * gridDim.x;   // slots alternate: a CTA runs <= 1 sync ahead
+  if (a.user_order && a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
   {
     if (col > 0) __syncthreads();   // s_u of the previous column fully consumed
     if (!a.user_order) {
@@ -503,6 +513,7 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   a.chunk = pl.d1_chunk;
   a.user_order = user_order ? 1 : 0;
   a.nrhs = nrhs;
+  a.prefetch = pl.d1_prefetch;
   a.vstride = user_order ? pl.n_src : pl.n;
   a.ostride = user_order ? pl.n - pl.tgt_off : pl.n;
   a.os2 = pl.os2;

@@ -89,6 +89,7 @@ struct Plan {
   // d = 1 launch geometry
   int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;
   int d1_pdl = 1;                   // programmatic dependent launch for back-to-back applies
+  int d1_prefetch = 1;    // d = 1 user order: L2 prefetch of v before the gathers (option 3)
   int64_t d1_chunk = 0;
   int64_t struct_bytes = 0;
   int launches_per_apply = 0;

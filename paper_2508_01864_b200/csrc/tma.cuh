@@ -42,6 +42,15 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
       "l"(src), "r"(bytes), "r"(smem_u32(m))
       : "memory");
 }
+// L2 prefetch of [p, p + bytes) rounded inward to 16-byte boundaries (a hint: no data moves
+// to the SM; skipped when the rounded range is empty)
+__device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes) {
+  const uintptr_t lo = (reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + bytes) & ~uintptr_t(15);
+  if (hi > lo)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo))
+                 : "memory");
+}
 // order this thread's earlier generic-proxy shared accesses before later bulk copies
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
