@@ -161,6 +161,23 @@ void oracle_dense(int two_nu, int form, int d, const double *ell, double outputs
                                                           a + (size_t)i * d, b + (size_t)j * d);
 }
 
+/* Dense block of the lengthscale derivative, Kout[i*n + j] = l dKtilde(a_i, b_j)/dl (L1). */
+void oracle_dense_d(int two_nu, int form, int d, const double *ell, double outputscale,
+                    const double *a, int64_t m, const double *b, int64_t n, double *Kout,
+                    int nthreads)
+{
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j)
+            Kout[(size_t)i * n + j] = oracle_dkernel_value(two_nu, form, d, ell, outputscale,
+                                                           a + (size_t)i * d, b + (size_t)j * d);
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

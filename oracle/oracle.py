@@ -15,7 +15,7 @@ import numpy as np
 
 __all__ = [
     "build_oracle", "kernel_value", "dkernel_value", "kmvm_rows", "dkmvm_rows", "dkzx_rows", "kzx_rows", "dense_kernel",
-    "ols", "gp_dense", "max_threads", "FORMS",
+    "ols", "gp_dense", "max_threads", "FORMS", "dense_dkernel",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -56,6 +56,8 @@ def _load():
         lib.oracle_dense.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp,
                                      ctypes.c_double, dp, ctypes.c_int64, dp, ctypes.c_int64,
                                      dp, ctypes.c_int]
+        lib.oracle_dense_d.restype = None
+        lib.oracle_dense_d.argtypes = lib.oracle_dense.argtypes
         lib.oracle_max_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -138,6 +140,15 @@ def dense_kernel(a, b, two_nu: int, form: str, ell, outputscale: float = 1.0, nt
     out = np.empty((a.shape[0], b.shape[0]))
     _load().oracle_dense(two_nu, FORMS[form], a.shape[1], _dp(ell), float(outputscale),
                          _dp(a), a.shape[0], _dp(b), b.shape[0], _dp(out), int(nthreads))
+    return out
+
+
+def dense_dkernel(a, b, two_nu: int, form: str, ell, outputscale: float = 1.0, nthreads=0):
+    """Dense block [l dKtilde(a_i, b_j)/dl] (L1 form; PAPER.md L1314 times l); small sizes."""
+    a = _f64(a, 2); b = _f64(b, 2); ell = _f64(np.atleast_1d(ell))
+    out = np.empty((a.shape[0], b.shape[0]))
+    _load().oracle_dense_d(two_nu, FORMS[form], a.shape[1], _dp(ell), float(outputscale),
+                           _dp(a), a.shape[0], _dp(b), b.shape[0], _dp(out), int(nthreads))
     return out
 
 
