@@ -71,6 +71,19 @@ typedef struct {
 
 typedef struct gp_plan_s *gp_plan;    /* opaque: the stored sort / D&C structure of x */
 typedef struct gp_cross_s *gp_cross;  /* opaque: structure of the union x U z for K_zx */
+typedef struct gp_precond_s *gp_precond;  /* opaque: pivoted-Cholesky preconditioner */
+
+/* Result of gp_lml (log-marginal likelihood estimate and its gradient). */
+typedef struct {
+  double lml;             /* -1/2 quad - 1/2 logdet - N/2 log(2 pi) */
+  double quad;            /* r^T A^-1 r */
+  double logdet;          /* estimate of log det A (+ log det P when preconditioned) */
+  double logdet_precond;  /* log det P, 0 without preconditioner */
+  double grad[3];         /* dL/d outputscale, dL/d log(c) (all lengthscales scaled by c;
+                             = l dL/dl for one l; NaN for product forms), dL/d sigma */
+  int cg_iters;           /* iterations of the A^-1 r solve */
+  int lanczos_iters;      /* Lanczos steps per probe (max over probes) */
+} gp_lml_result;
 
 /* gp_setup -- build the stored structure of P:191 [§1], P:338 [§2.1], P:539 [§2.2.3]:
  * scale coordinates t_k = sqrt(2 nu) x_k / l_k, radix-sort each dimension, and for
@@ -154,6 +167,69 @@ GP_API void gp_kzx_destroy(gp_cross c);
 GP_API gp_status gp_cg_solve(gp_plan p, double sigma2, const double *y, int mean_kind,
                       const double *H, int L, double rtol, int max_iter, double *alpha,
                       double *beta, gp_cg_info *info, void *stream);
+
+/* gp_cg_solve_pc -- gp_cg_solve preconditioned by pc (P = L L^T + sigma2 I,
+ * applied by the Woodbury formula; pc = NULL is gp_cg_solve).  Same arguments, semantics
+ * and stopping rule (true residual, restarts from it when the recursion drifted). */
+GP_API gp_status gp_cg_solve_pc(gp_plan p, gp_precond pc, double sigma2, const double *y,
+                                int mean_kind, const double *H, int L, double rtol,
+                                int max_iter, double *alpha, double *beta, gp_cg_info *info,
+                                void *stream);
+
+/* ---- the likelihood machinery of PAPER.md App A ---------------------- */
+
+/* gp_precond_create -- rank-k pivoted Cholesky K ~ L L^T of the plan's kernel matrix
+ * (Harbrecht et al.): k greedy steps, pivot = largest remaining diagonal (ties:
+ * smallest x1-rank), one kernel column per step.  1 <= rank <= min(n, 1024).  L is held on
+ * the device (n x rank, 8 n rank bytes).  Errors: INVALID_ARG if rank exceeds the numerical
+ * rank of K (a non-positive pivot). */
+GP_API gp_status gp_precond_create(gp_plan p, int rank, void *stream, gp_precond *out);
+
+/* gp_precond_factor -- copies of the factor: pivots (host int64[rank], user indices, in
+ * pivot order) and/or L (device, n x rank column-major, user order); either may be NULL. */
+GP_API gp_status gp_precond_factor(gp_precond pc, int64_t *pivots, double *L, void *stream);
+
+/* gp_precond_solve -- z = P^-1 r, P = L L^T + sigma2 I, by the Woodbury formula
+ * (P:1080-1083).  r, z: n x nb column-major (device, user order), may not alias. */
+GP_API gp_status gp_precond_solve(gp_precond pc, double sigma2, const double *r, int nb,
+                                  double *z, void *stream);
+
+/* gp_precond_logdet -- log det P = N log sigma2 + log det(I + L^T L / sigma2) (Sylvester,
+ * P:1087-1095); host result. */
+GP_API gp_status gp_precond_logdet(gp_precond pc, double sigma2, double *logdet, void *stream);
+GP_API void gp_precond_destroy(gp_precond pc);
+
+/* gp_mbcg -- Algorithm 2: CG on A = K + sigma2 I with nb right-hand sides B,
+ * zero initial guess, preconditioner pc (NULL: identity), per-column stop at
+ *   ||b_c - A x_c||_2 <= rtol ||b_c||_2 (on the recursive residual; rtol = 0: exactly
+ *   max_iter iterations -- the Lanczos mode used for log-determinants).
+ *   B, X          : n x nb column-major (device, user order).
+ *   alpha_hist,
+ *   beta_hist     : (host, may be NULL) max_iter x nb, entry [it * nb + c]: the CG
+ *                   coefficients alpha_{it+1}, beta_{it+1} of column c; the Lanczos
+ *                   tridiagonal of column c has diagonal 1/alpha_j + beta_{j-1}/alpha_{j-1}
+ *                   and off-diagonal sqrt(beta_j)/alpha_j.
+ *   iters_done    : (host, may be NULL) number of alpha's recorded per column.
+ * Errors: BREAKDOWN (p^T A p <= 0).  Synchronises `stream`. */
+GP_API gp_status gp_mbcg(gp_plan p, gp_precond pc, double sigma2, const double *B, int nb,
+                         int max_iter, double rtol, double *X, double *alpha_hist,
+                         double *beta_hist, int *iters_done, void *stream);
+
+/* gp_lml -- log-marginal likelihood and its gradient (eq gp_log_likelihood; eq
+ * gp_log_likelihood_derivative) for the centred response r (the fixed effects
+ * removed first), as the paper estimates them (App A):
+ *   r^T A^-1 r by CG to cg_rtol; log det A by N/l sum_i e1^T log(T_i) e1 over l probes and
+ *   `lanczos_iters` Lanczos steps each, + log det P with a preconditioner;
+ *   tr(A^-1 dA/dth) by Hutchinson from the probes' CG solutions.
+ *   G : n x nprobe (device, user order) standard normal draws; W: rank x nprobe (device)
+ *       standard normal draws, required iff pc != NULL: the probes are z = L w + sigma g
+ *       ~ N(0, P) (reading R12), z = g without a preconditioner.
+ * The caller supplies the random numbers (the library draws none).  Synchronises `stream`.
+ * Errors: BREAKDOWN (CG breakdown or a non-positive Lanczos eigenvalue),
+ * NOT_CONVERGED (the r solve). */
+GP_API gp_status gp_lml(gp_plan p, gp_precond pc, double sigma2, const double *r,
+                        const double *G, const double *W, int nprobe, int lanczos_iters,
+                        double cg_rtol, gp_lml_result *out, void *stream);
 
 /* gp_predict -- posterior mean mu(z_q) = h(z_q)^T beta + sum_i K(z_q, x_i) alpha_i
  * (P:86 [eq gp_mean], P:149 [eq gp_mean_2]).

@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "load_library", "Kernel", "Plan", "Cross", "GPError", "setup", "kmvm", "cg_solve",
+    "load_library", "Kernel", "Plan", "Cross", "Precond", "GPError", "setup", "kmvm", "cg_solve",
     "predict", "FORM_L1", "FORM_PRODUCT", "MEAN_NONE", "MEAN_AFFINE", "MEAN_BASIS",
     "LIB_PATH",
 ]
@@ -43,6 +43,13 @@ class _CGInfo(ctypes.Structure):
                 ("failed_column", ctypes.c_int), ("restarts", ctypes.c_int)]
 
 
+class _LmlResult(ctypes.Structure):
+    _fields_ = [("lml", ctypes.c_double), ("quad", ctypes.c_double),
+                ("logdet", ctypes.c_double), ("logdet_precond", ctypes.c_double),
+                ("grad", ctypes.c_double * 3), ("cg_iters", ctypes.c_int),
+                ("lanczos_iters", ctypes.c_int)]
+
+
 def load_library(path: str | None = None):
     """Load libgpmatern.so (built in-tree by build.py).  Raises if missing."""
     global _lib
@@ -64,6 +71,14 @@ def load_library(path: str | None = None):
         "gp_kzx_setup": [vp, vp, i64, vp, ctypes.POINTER(vp)],
         "gp_kzx": [vp, vp, ci, vp, vp],
         "gp_cg_solve": [vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, ctypes.POINTER(_CGInfo), vp],
+        "gp_cg_solve_pc": [vp, vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, ctypes.POINTER(_CGInfo),
+                           vp],
+        "gp_precond_create": [vp, ci, vp, ctypes.POINTER(vp)],
+        "gp_precond_factor": [vp, vp, vp, vp],
+        "gp_precond_solve": [vp, cd, vp, ci, vp, vp],
+        "gp_precond_logdet": [vp, cd, ctypes.POINTER(cd), vp],
+        "gp_mbcg": [vp, vp, cd, vp, ci, ci, cd, vp, vp, vp, vp, vp],
+        "gp_lml": [vp, vp, cd, vp, vp, vp, ci, ci, cd, ctypes.POINTER(_LmlResult), vp],
         "gp_predict": [vp, vp, i64, vp, vp, vp, ci, vp, vp],
         "gp_plan_query": [vp, ci, ctypes.POINTER(i64)],
         "gp_plan_set_option": [vp, ci, i64],
@@ -74,6 +89,7 @@ def load_library(path: str | None = None):
         f.restype = ctypes.c_int
     lib.gp_destroy.argtypes = [vp]; lib.gp_destroy.restype = None
     lib.gp_kzx_destroy.argtypes = [vp]; lib.gp_kzx_destroy.restype = None
+    lib.gp_precond_destroy.argtypes = [vp]; lib.gp_precond_destroy.restype = None
     lib.gp_last_error.argtypes = []; lib.gp_last_error.restype = ctypes.c_char_p
     lib.gp_version.argtypes = []; lib.gp_version.restype = ctypes.c_char_p
     _lib = lib
@@ -211,8 +227,9 @@ class Plan:
         return Cross(self, z, stream)
 
     def cg_solve(self, y, sigma2: float, mean: int = MEAN_AFFINE, H=None, rtol: float = 1e-8,
-                 max_iter: int = 20000, stream=None):
-        """alpha, beta, info of (K + sigma^2 I) CG with GLS fixed effects (gp_cg_solve)."""
+                 max_iter: int = 20000, stream=None, precond=None):
+        """alpha, beta, info of (K + sigma^2 I) CG with GLS fixed effects (gp_cg_solve_pc;
+        precond: a Precond of this plan or None)."""
         import torch
         alpha = torch.empty(self.n, dtype=torch.float64, device=y.device)
         nb = 1 + self.d if mean == MEAN_AFFINE else (H.shape[0] if mean == MEAN_BASIS else 0)
@@ -220,9 +237,10 @@ class Plan:
         info = _CGInfo()
         Hp = _dev(H, "H") if mean == MEAN_BASIS else ctypes.c_void_p(0)
         L = H.shape[0] if mean == MEAN_BASIS else 0
-        st = _lib.gp_cg_solve(self._h, float(sigma2), _dev(y, "y", (self.n,)), mean, Hp, L,
-                              float(rtol), int(max_iter), _dev(alpha, "alpha"), beta,
-                              ctypes.byref(info), _stream(stream))
+        st = _lib.gp_cg_solve_pc(self._h, precond._h if precond is not None else None,
+                                 float(sigma2), _dev(y, "y", (self.n,)), mean, Hp, L,
+                                 float(rtol), int(max_iter), _dev(alpha, "alpha"), beta,
+                                 ctypes.byref(info), _stream(stream))
         res = {"iters": info.iters, "relres_max": info.relres_max,
                "failed_column": info.failed_column, "restarts": info.restarts}
         if st != 0:
@@ -231,6 +249,42 @@ class Plan:
             err.alpha = alpha
             raise err
         return alpha, [beta[i] for i in range(nb)], res
+
+    def mbcg(self, B, sigma2: float, max_iter: int, rtol: float = 0.0, precond=None,
+             stream=None):
+        """Algorithm 2 (gp_mbcg): B (nb, n) user order -> X (nb, n), alpha/beta histories
+        (max_iter, nb) and iterations done per column."""
+        import numpy as np
+        import torch
+        B2 = B if B.dim() == 2 else B.reshape(1, -1)
+        nb = B2.shape[0]
+        X = torch.empty_like(B2)
+        ah = np.zeros((max_iter, nb)); bh = np.zeros((max_iter, nb))
+        it = (ctypes.c_int * nb)()
+        _check(_lib.gp_mbcg(self._h, precond._h if precond is not None else None, float(sigma2),
+                            _dev(B2, "B", (nb, self.n)), nb, int(max_iter), float(rtol),
+                            _dev(X, "X"), ah.ctypes.data_as(ctypes.c_void_p),
+                            bh.ctypes.data_as(ctypes.c_void_p), it, _stream(stream)))
+        return X, ah, bh, [it[i] for i in range(nb)]
+
+    def lml(self, r, sigma2: float, G, W=None, lanczos_iters: int = 30, cg_rtol: float = 1e-8,
+            precond=None, stream=None):
+        """Log-marginal likelihood and gradient (gp_lml); G (nprobe, n) standard normals,
+        W (nprobe, rank) standard normals with a preconditioner."""
+        l = G.shape[0]
+        res = _LmlResult()
+        Wp = None
+        if precond is not None:
+            if W is None or tuple(W.shape) != (l, precond.rank):
+                raise ValueError("W must be (nprobe, rank) with a preconditioner")
+            Wp = _dev(W, "W")
+        _check(_lib.gp_lml(self._h, precond._h if precond is not None else None, float(sigma2),
+                           _dev(r, "r", (self.n,)), _dev(G, "G", (l, self.n)), Wp, l,
+                           int(lanczos_iters), float(cg_rtol), ctypes.byref(res),
+                           _stream(stream)))
+        return {"lml": res.lml, "quad": res.quad, "logdet": res.logdet,
+                "logdet_precond": res.logdet_precond, "grad": [res.grad[i] for i in range(3)],
+                "cg_iters": res.cg_iters, "lanczos_iters": res.lanczos_iters}
 
     def predict(self, z, alpha, beta=None, Hz=None, stream=None):
         import torch
@@ -295,6 +349,52 @@ def setup(x, kernel: Kernel, stream=None) -> Plan:
 
 def kmvm(plan: Plan, v, out=None, stream=None):
     return plan.kmvm(v, out, stream)
+
+
+class Precond:
+    """Rank-k pivoted-Cholesky preconditioner P = L L^T + sigma^2 I of a plan's K
+    (gp_precond_create)."""
+
+    def __init__(self, plan: Plan, rank: int, stream=None):
+        self.plan = plan
+        self.rank = int(rank)
+        h = ctypes.c_void_p()
+        _check(_lib.gp_precond_create(plan._h, self.rank, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    def factor(self, stream=None):
+        """(pivots as user indices, L as a (rank, n) tensor in user order)."""
+        import numpy as np
+        import torch
+        piv = np.zeros(self.rank, dtype=np.int64)
+        L = torch.empty((self.rank, self.plan.n), dtype=torch.float64, device="cuda")
+        _check(_lib.gp_precond_factor(self._h, piv.ctypes.data_as(ctypes.c_void_p), _dev(L, "L"),
+                                      _stream(stream)))
+        return piv, L
+
+    def solve(self, sigma2: float, r, stream=None):
+        import torch
+        r2 = r if r.dim() == 2 else r.reshape(1, -1)
+        z = torch.empty_like(r2)
+        _check(_lib.gp_precond_solve(self._h, float(sigma2), _dev(r2, "r"), r2.shape[0],
+                                     _dev(z, "z"), _stream(stream)))
+        return z if r.dim() == 2 else z[0]
+
+    def logdet(self, sigma2: float, stream=None) -> float:
+        out = ctypes.c_double()
+        _check(_lib.gp_precond_logdet(self._h, float(sigma2), ctypes.byref(out), _stream(stream)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.gp_precond_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def cg_solve(plan: Plan, y, sigma2, **kw):

@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpmatern.so")
 OBJDIR = os.path.join(HERE, "build")
-SOURCES = ["api.cu", "setup.cu", "apply.cu", "apply_d1.cu", "apply_d1_fast.cu", "apply_level.cu", "solve.cu"]
+SOURCES = ["api.cu", "setup.cu", "apply.cu", "apply_d1.cu", "apply_d1_fast.cu", "apply_level.cu",
+           "solve.cu", "lml.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -59,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _newer(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
-               "-lcudart"]
+               "-lcudart", "-lcublas"]
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
     return LIB

@@ -181,7 +181,15 @@ void gp_kzx_destroy(gp_cross c) {
 gp_status gp_cg_solve(gp_plan p, double sigma2, const double* y, int mean_kind,
                       const double* H, int L, double rtol, int max_iter, double* alpha,
                       double* beta, gp_cg_info* info, void* stream) {
+  return gp_cg_solve_pc(p, nullptr, sigma2, y, mean_kind, H, L, rtol, max_iter, alpha, beta,
+                        info, stream);
+}
+
+gp_status gp_cg_solve_pc(gp_plan p, gp_precond pc, double sigma2, const double* y, int mean_kind,
+                         const double* H, int L, double rtol, int max_iter, double* alpha,
+                         double* beta, gp_cg_info* info, void* stream) {
   if (!p || !y || !alpha) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (pc && pc->owner != p) return fail(GP_ERR_INVALID_ARG, "preconditioner built on another plan");
   if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
   if (!(rtol > 0)) return fail(GP_ERR_INVALID_ARG, "rtol must be > 0");
   if (max_iter < 1) return fail(GP_ERR_INVALID_ARG, "max_iter must be >= 1");
@@ -190,7 +198,134 @@ gp_status gp_cg_solve(gp_plan p, double sigma2, const double* y, int mean_kind,
   if (mean_kind == GP_MEAN_BASIS && (!H || L < 1 || L > 16))
     return fail(GP_ERR_INVALID_ARG, "BASIS mean needs H and 1 <= L <= 16");
   return cg_solve(p->pl, sigma2, y, mean_kind, H, L, rtol, max_iter, alpha, beta, info,
-                  static_cast<cudaStream_t>(stream));
+                  static_cast<cudaStream_t>(stream), pc ? &pc->pc : nullptr);
+}
+
+// ---- §8(f) f3: preconditioner, Algorithm 2, likelihood
+gp_status gp_precond_create(gp_plan p, int rank, void* stream, gp_precond* out) {
+  if (!p || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (rank < 1 || rank > 1024 || rank > p->pl.n)
+    return fail(GP_ERR_INVALID_ARG, "rank must be in [1, min(n, 1024)]");
+  gp_precond c = new (std::nothrow) gp_precond_s();
+  if (!c) return fail(GP_ERR_OOM, "host allocation failed");
+  c->owner = p;
+  gp_status st = precond_build(c->pc, p->pl, rank, static_cast<cudaStream_t>(stream));
+  if (st != GP_OK) {
+    precond_free(c->pc);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return GP_OK;
+}
+
+gp_status gp_precond_factor(gp_precond pc, int64_t* pivots, double* L, void* stream) {
+  if (!pc) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  Plan& pl = pc->owner->pl;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pivots) {
+    std::vector<int> perm(pl.n);
+    GPM_CUDA(cudaMemcpy(perm.data(), pl.perm.ptr, 4 * (size_t)pl.n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < pc->pc.k; ++i) pivots[i] = perm[pc->pc.piv[i]];
+  }
+  if (L)
+    for (int c = 0; c < pc->pc.k; ++c)
+      GPM_TRY(permute_vec(pl, pc->pc.L.as<double>() + (size_t)c * pl.n, L + (size_t)c * pl.n,
+                          false, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return GP_OK;
+}
+
+gp_status gp_precond_solve(gp_precond pc, double sigma2, const double* r, int nb, double* z,
+                           void* stream) {
+  if (!pc || !r || !z) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (r == z) return fail(GP_ERR_INVALID_ARG, "z must not alias r");
+  if (nb < 1) return fail(GP_ERR_INVALID_ARG, "nb must be >= 1");
+  if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
+  Plan& pl = pc->owner->pl;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = (size_t)pl.n;
+  DevBuf a, b;
+  GPM_TRY(a.alloc(8 * n * nb));
+  GPM_TRY(b.alloc(8 * n * nb));
+  for (int c = 0; c < nb; ++c) GPM_TRY(permute_vec(pl, r + c * n, a.as<double>() + c * n, true, s));
+  GPM_TRY(precond_apply(pc->pc, sigma2, a.as<double>(), nb, b.as<double>(), s));
+  for (int c = 0; c < nb; ++c) GPM_TRY(permute_vec(pl, b.as<double>() + c * n, z + c * n, false, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return GP_OK;
+}
+
+gp_status gp_precond_logdet(gp_precond pc, double sigma2, double* logdet, void* stream) {
+  if (!pc || !logdet) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
+  return precond_logdet(pc->pc, sigma2, logdet, static_cast<cudaStream_t>(stream));
+}
+
+void gp_precond_destroy(gp_precond pc) {
+  if (!pc) return;
+  precond_free(pc->pc);
+  delete pc;
+}
+
+gp_status gp_mbcg(gp_plan p, gp_precond pc, double sigma2, const double* B, int nb, int max_iter,
+                  double rtol, double* X, double* alpha_hist, double* beta_hist, int* iters_done,
+                  void* stream) {
+  if (!p || !B || !X) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (pc && pc->owner != p) return fail(GP_ERR_INVALID_ARG, "preconditioner built on another plan");
+  if (nb < 1 || max_iter < 1) return fail(GP_ERR_INVALID_ARG, "nb and max_iter must be >= 1");
+  if (!(rtol >= 0)) return fail(GP_ERR_INVALID_ARG, "rtol must be >= 0");
+  if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
+  if (B == X) return fail(GP_ERR_INVALID_ARG, "X must not alias B");
+  Plan& pl = p->pl;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = (size_t)pl.n;
+  DevBuf rb, xb, ah, bh;
+  GPM_TRY(rb.alloc(8 * n * nb));
+  GPM_TRY(xb.alloc(8 * n * nb));
+  GPM_TRY(ah.alloc(8 * (size_t)max_iter * nb));
+  GPM_TRY(bh.alloc(8 * (size_t)max_iter * nb));
+  for (int c = 0; c < nb; ++c) GPM_TRY(permute_vec(pl, B + c * n, rb.as<double>() + c * n, true, s));
+  // tolerance levels from ||b_c||^2
+  std::vector<double> bn(nb), t2(nb);
+  {
+    std::vector<double> hb(n);
+    for (int c = 0; c < nb; ++c) {
+      GPM_CUDA(cudaMemcpyAsync(hb.data(), rb.as<double>() + c * n, 8 * n, cudaMemcpyDeviceToHost, s));
+      GPM_CUDA(cudaStreamSynchronize(s));
+      long double acc = 0.0L;
+      for (size_t i = 0; i < n; ++i) acc += (long double)hb[i] * hb[i];
+      t2[c] = rtol * rtol * (double)acc;
+    }
+  }
+  std::vector<int> it, st;
+  GPM_CUDA(cudaMemsetAsync(ah.ptr, 0, 8 * (size_t)max_iter * nb, s));
+  GPM_CUDA(cudaMemsetAsync(bh.ptr, 0, 8 * (size_t)max_iter * nb, s));
+  GPM_TRY(mbcg_rank(pl, pc ? &pc->pc : nullptr, sigma2, rb.as<double>(), nb, max_iter, t2,
+                    xb.as<double>(), ah.as<double>(), bh.as<double>(), it, st, nullptr, s));
+  for (int c = 0; c < nb; ++c) GPM_TRY(permute_vec(pl, xb.as<double>() + c * n, X + c * n, false, s));
+  if (alpha_hist)
+    GPM_CUDA(cudaMemcpyAsync(alpha_hist, ah.ptr, 8 * (size_t)max_iter * nb, cudaMemcpyDeviceToHost, s));
+  if (beta_hist)
+    GPM_CUDA(cudaMemcpyAsync(beta_hist, bh.ptr, 8 * (size_t)max_iter * nb, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  if (iters_done) for (int c = 0; c < nb; ++c) iters_done[c] = it[c];
+  for (int c = 0; c < nb; ++c)
+    if (st[c] == 2) return fail(GP_ERR_BREAKDOWN, "CG breakdown (p^T A p <= 0) in column " + std::to_string(c));
+  return GP_OK;
+}
+
+gp_status gp_lml(gp_plan p, gp_precond pc, double sigma2, const double* r, const double* G,
+                 const double* W, int nprobe, int lanczos_iters, double cg_rtol,
+                 gp_lml_result* out, void* stream) {
+  if (!p || !r || !G || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (pc && pc->owner != p) return fail(GP_ERR_INVALID_ARG, "preconditioner built on another plan");
+  if (pc && !W) return fail(GP_ERR_INVALID_ARG, "W (rank x nprobe normals) required with a preconditioner");
+  if (nprobe < 1 || lanczos_iters < 1) return fail(GP_ERR_INVALID_ARG, "nprobe and lanczos_iters must be >= 1");
+  if (!(cg_rtol > 0)) return fail(GP_ERR_INVALID_ARG, "cg_rtol must be > 0");
+  if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
+  return lml_eval(p->pl, pc ? &pc->pc : nullptr, sigma2, r, G, W, nprobe, lanczos_iters, cg_rtol,
+                  out, static_cast<cudaStream_t>(stream));
 }
 
 gp_status gp_predict(gp_plan p, const double* z, int64_t m, const double* alpha,

@@ -7,6 +7,8 @@
 
 #include "../../include/gpmatern.h"
 
+struct cublasContext;   // cuBLAS handle (lml.cu only includes cublas_v2.h)
+
 namespace gpm {
 
 // Error plumbing ------------------------------------------------------------
@@ -95,6 +97,34 @@ struct Plan {
   int launches_per_apply = 0;
 };
 
+// lml.cu -- pivoted-Cholesky preconditioner P = L L^T + sigma^2 I
+struct Precond {
+  Plan* pl = nullptr;
+  int k = 0;
+  int64_t n = 0;
+  DevBuf L;                    // n x k column-major, rank order
+  DevBuf Cinv, W, Y;           // (I + L^T L / s2)^-1 (k x k) for the cached s2; scratch
+  std::vector<int> piv;        // pivot ranks
+  std::vector<double> G;       // L^T L (k x k, host)
+  double s2 = -1.0, logdetC = 0.0;
+  ::cublasContext* h = nullptr;
+};
+gp_status precond_build(Precond& pc, Plan& pl, int k, cudaStream_t s);
+gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double* Z,
+                        cudaStream_t s);
+gp_status precond_sample(Precond& pc, double s2, const double* G, const double* W, int nb,
+                         double* Z, cudaStream_t s);
+gp_status precond_logdet(Precond& pc, double s2, double* out, cudaStream_t s);
+void precond_free(Precond& pc);
+gp_status mbcg_rank(Plan& pl, Precond* pc, double s2, const double* B, int nb, int max_iter,
+                    const std::vector<double>& tol2, double* X, double* ahist, double* bhist,
+                    std::vector<int>& iters, std::vector<int>& status, double* P0,
+                    cudaStream_t s);
+gp_status slq_column(const double* ah, const double* bh, int nb, int c, int m, double* q);
+gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const double* G_user,
+                   const double* W, int nprobe, int m, double cg_rtol, gp_lml_result* out,
+                   cudaStream_t s);
+
 // setup.cu
 gp_status plan_build(Plan& pl, const double* x_dev, int64_t n, int d, const gp_kernel& k,
                      cudaStream_t s);
@@ -116,7 +146,7 @@ int64_t apply_model_bytes(const Plan& pl);
 // solve.cu
 gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,
                    int Lb, double rtol, int max_iter, double* alpha, double* beta,
-                   gp_cg_info* info, cudaStream_t s);
+                   gp_cg_info* info, cudaStream_t s, Precond* pc = nullptr);
 gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
                                  const double* Hz, int Lb, double* out, cudaStream_t s);
 
@@ -124,6 +154,10 @@ gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double
 
 struct gp_plan_s {
   gpm::Plan pl;
+};
+struct gp_precond_s {
+  gpm::Precond pc;
+  gp_plan owner = nullptr;
 };
 struct gp_cross_s {
   gpm::Plan pl;        // structure of the union x U z

@@ -1,0 +1,763 @@
+// lml.cu -- SURVEY §8(f) f3: the likelihood machinery of PAPER.md App A on top of the
+// fast K.v apply.
+//   * Precond: rank-k pivoted Cholesky K ~ L L^T (greedy pivot on the largest
+//     remaining diagonal, ties -> smallest rank), P = L L^T + sigma^2 I applied by the
+//     Woodbury formula, log det P by Sylvester's theorem.
+//     L is n x k column-major in the plan's rank order; the plain GEMMs of the Woodbury
+//     solve (L^T R, C^-1 W, L Y) and the Gram matrix L^T L go through cuBLAS.
+//   * mbcg_rank: Algorithm 2 -- CG with several right-hand sides and the
+//     preconditioner solve, zero initial guess, recording alpha_j, beta_j per iteration
+//     (the Lanczos tridiagonals T_j); per-column stop (reading R8).
+//   * slq: eqn approximationLogDet, e1^T log(T) e1 from an implicit-shift QL
+//     eigen-decomposition of the small tridiagonal (first eigenvector components only).
+//   * lml: eq gp_log_likelihood / _derivative with Hutchinson traces
+//      -- probes z ~ N(0, P) (reading R12).
+// All n-vectors live in rank order; every reduction is a fixed-order two-stage tree.
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace gpm {
+
+namespace {
+
+constexpr int LB = 256;
+constexpr int LG = 296;   // reduction partials per column
+
+__device__ __forceinline__ double lblock_sum(double v, double* sh) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+  }
+  __syncthreads();
+  return t;
+}
+
+inline int lgrid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
+
+// ---- kernel matrix column K[:, p] (rank order) for the pivoted Cholesky
+// profile k(s) = sum_q a_q s^q e^{-s}, s = scaled distance; os2 = outputscale^2
+__device__ __forceinline__ double prof(int P, double s) {
+  const double e = exp(-s);
+  if (P == 0) return e;
+  if (P == 1) return e * (1.0 + s);
+  return e * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0);
+}
+
+// piv[i] holds the pivot rank; Lp[j] = L[j*n + piv] for j < i (gathered first)
+__global__ void k_pivrow(const double* __restrict__ L, int64_t n, const int* __restrict__ piv,
+                         int i, double* __restrict__ Lp) {
+  const int p = piv[i];
+  for (int j = threadIdx.x; j < i; j += blockDim.x) Lp[j] = L[(size_t)j * n + p];
+}
+
+// col[r] = os2 k(x_r, x_p)  (the GEMV correction is applied by cuBLAS afterwards)
+__global__ void k_kcol(const double* __restrict__ t, int64_t n, int d, int P, int prod, double os2,
+                       const int* __restrict__ piv, int i, double* __restrict__ col) {
+  const int p = piv[i];
+  double tp[3];
+  for (int k = 0; k < d; ++k) tp[k] = t[(size_t)k * n + p];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double v;
+    if (!prod) {
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) s += fabs(t[(size_t)k * n + r] - tp[k]);
+      v = prof(P, s);
+    } else {
+      v = 1.0;
+      for (int k = 0; k < d; ++k) v *= prof(P, fabs(t[(size_t)k * n + r] - tp[k]));
+    }
+    col[r] = os2 * v;
+  }
+}
+
+// L[:, i] = col / sqrt(dp); diag -= L[:, i]^2 ; dp = pivot's remaining diagonal (pivd[i])
+__global__ void k_pcupd(double* __restrict__ col, double* __restrict__ diag, int64_t n,
+                        const int* __restrict__ piv, const double* __restrict__ pivd, int i) {
+  const double inv = 1.0 / sqrt(pivd[i]);
+  const int p = piv[i];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double l = col[r] * inv;
+    col[r] = l;
+    diag[r] = r == p ? 0.0 : diag[r] - l * l;
+  }
+}
+
+// argmax of diag (ties -> smallest index): stage 1 per block, stage 2 one block
+__global__ void k_argmax1(const double* __restrict__ diag, int64_t n, double* __restrict__ pv,
+                          int* __restrict__ pi) {
+  __shared__ double sv[LB];
+  __shared__ int si[LB];
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = diag[r];
+    if (v > bv) { bv = v; bi = (int)r; }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int i2 = si[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { pv[blockIdx.x] = sv[0]; pi[blockIdx.x] = si[0]; }
+}
+__global__ void k_argmax2(const double* __restrict__ pv, const int* __restrict__ pi, int nb,
+                          int* __restrict__ piv, double* __restrict__ pivd, int i) {
+  __shared__ double sv[LB];
+  __shared__ int si[LB];
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const double v = pv[b];
+    if (v > bv || (v == bv && pi[b] < bi)) { bv = v; bi = pi[b]; }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int i2 = si[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { piv[i] = si[0]; pivd[i] = sv[0]; }
+}
+
+// ---- CG kernels (columns in blockIdx.y; vectors n x nb column-major)
+__global__ void k_dotp(const double* __restrict__ A, const double* __restrict__ B, int64_t n,
+                       double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  const double* a = A + (size_t)c * n;
+  const double* b = B + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc = fma(a[i], b[i], acc);
+  const double t = lblock_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+__global__ void k_sum(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(size_t)c * nb + b];
+  const double t = lblock_sum(acc, sh);
+  if (threadIdx.x == 0) out[c] = t;
+}
+// Q += s2 P; part = P.Q
+__global__ void k_mq(const double* __restrict__ P, double* __restrict__ Q, int64_t n, double s2,
+                     double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  const double* p = P + (size_t)c * n;
+  double* q = Q + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double pv = p[i];
+    const double qv = fma(s2, pv, q[i]);
+    q[i] = qv;
+    acc = fma(pv, qv, acc);
+  }
+  const double t = lblock_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+// alpha_c = zr_c / pq_c ; history ; breakdown
+__global__ void k_malpha(const double* __restrict__ part, int nb, const double* __restrict__ zr,
+                         double* __restrict__ alpha, int* __restrict__ status,
+                         double* __restrict__ ahist, int it, int ncol) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(size_t)c * nb + b];
+  const double pq = lblock_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    if (status[c] == 0) {
+      if (!(pq > 0.0) || !isfinite(pq)) status[c] = 2;
+      else a = zr[c] / pq;
+      if (ahist && status[c] == 0) ahist[(size_t)it * ncol + c] = a;
+    }
+    alpha[c] = a;
+  }
+}
+// X += a P ; R -= a Q ; part = R.R
+__global__ void k_mupd(double* __restrict__ X, double* __restrict__ R, const double* __restrict__ P,
+                       const double* __restrict__ Q, const double* __restrict__ alpha, int64_t n,
+                       double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y;
+  const double a = alpha[c];
+  double* x = X + (size_t)c * n;
+  double* r = R + (size_t)c * n;
+  const double* p = P + (size_t)c * n;
+  const double* q = Q + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    const double rv = fma(-a, q[i], r[i]);
+    r[i] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  const double t = lblock_sum(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+// beta_c = zr_new / zr ; convergence on ||R||^2 <= tol2_c ; history
+__global__ void k_mbeta(const double* __restrict__ part_rr, const double* __restrict__ part_zr,
+                        int nb, double* __restrict__ zr, const double* __restrict__ tol2,
+                        double* __restrict__ beta, int* __restrict__ status,
+                        int* __restrict__ iters, double* __restrict__ bhist, int it, int ncol) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double a1 = 0.0, a2 = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    a1 += part_rr[(size_t)c * nb + b];
+    a2 += part_zr[(size_t)c * nb + b];
+  }
+  const double rr = lblock_sum(a1, sh);
+  const double zn = lblock_sum(a2, sh);
+  if (threadIdx.x == 0) {
+    double bt = 0.0;
+    if (status[c] == 0) {
+      iters[c] = it + 1;
+      bt = zn / zr[c];
+      zr[c] = zn;
+      if (bhist) bhist[(size_t)it * ncol + c] = bt;
+      if (rr <= tol2[c]) status[c] = 1;
+    }
+    beta[c] = bt;
+  }
+}
+// P = Z + beta P (active columns)
+__global__ void k_mpupd(double* __restrict__ P, const double* __restrict__ Z,
+                        const double* __restrict__ beta, const int* __restrict__ status, int64_t n) {
+  const int c = blockIdx.y;
+  if (status[c] != 0) return;
+  const double b = beta[c];
+  double* p = P + (size_t)c * n;
+  const double* z = Z + (size_t)c * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], z[i]);
+}
+__global__ void k_fill(double* __restrict__ x, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+// out = a*X + b*Y (elementwise, n*nb)
+__global__ void k_lin(const double* __restrict__ X, const double* __restrict__ Y, double a,
+                      double b, int64_t nk, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * X[i] + (Y ? b * Y[i] : 0.0);
+}
+
+// symmetric k x k Cholesky (lower, in place, row-major); false if not SPD
+bool chol(std::vector<double>& A, int k) {
+  for (int j = 0; j < k; ++j) {
+    double s = A[j * k + j];
+    for (int q = 0; q < j; ++q) s -= A[j * k + q] * A[j * k + q];
+    if (!(s > 0.0)) return false;
+    const double d = std::sqrt(s);
+    A[j * k + j] = d;
+    for (int i = j + 1; i < k; ++i) {
+      double t = A[i * k + j];
+      for (int q = 0; q < j; ++q) t -= A[i * k + q] * A[j * k + q];
+      A[i * k + j] = t / d;
+    }
+  }
+  return true;
+}
+
+const char* cublas_msg(cublasStatus_t st) {
+  switch (st) {
+    case CUBLAS_STATUS_NOT_INITIALIZED: return "cuBLAS not initialised";
+    case CUBLAS_STATUS_ALLOC_FAILED: return "cuBLAS allocation failed";
+    case CUBLAS_STATUS_INVALID_VALUE: return "cuBLAS invalid value";
+    case CUBLAS_STATUS_EXECUTION_FAILED: return "cuBLAS execution failed";
+    default: return "cuBLAS error";
+  }
+}
+#define GPM_CUBLAS(x)                                                  \
+  do {                                                                 \
+    cublasStatus_t st_ = (x);                                          \
+    if (st_ != CUBLAS_STATUS_SUCCESS) return fail(GP_ERR_CUDA, cublas_msg(st_)); \
+  } while (0)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Preconditioner
+gp_status precond_build(Precond& pc, Plan& pl, int k, cudaStream_t s) {
+  const int64_t n = pl.n;
+  pc.pl = &pl;
+  pc.k = k;
+  pc.n = n;
+  GPM_CUBLAS(cublasCreate(&pc.h));
+  GPM_CUBLAS(cublasSetStream(pc.h, s));
+  GPM_CUBLAS(cublasSetPointerMode(pc.h, CUBLAS_POINTER_MODE_HOST));
+  GPM_TRY(pc.L.alloc(sizeof(double) * (size_t)n * k));
+  DevBuf diag, pv, pi, piv, pivd, Lp;
+  GPM_TRY(diag.alloc(8 * n));
+  GPM_TRY(pv.alloc(8 * LG));
+  GPM_TRY(pi.alloc(4 * LG));
+  GPM_TRY(piv.alloc(4 * (size_t)k));
+  GPM_TRY(pivd.alloc(8 * (size_t)k));
+  GPM_TRY(Lp.alloc(8 * (size_t)k + 8));
+  // diag K = outputscale^2 at every point (stationary kernel)
+  k_fill<<<lgrid(n), 256, 0, s>>>(diag.as<double>(), n, pl.os2);
+  double* L = pc.L.as<double>();
+  const int prod = pl.form == GP_FORM_PRODUCT ? 1 : 0;
+  for (int i = 0; i < k; ++i) {
+    k_argmax1<<<LG, LB, 0, s>>>(diag.as<double>(), n, pv.as<double>(), pi.as<int>());
+    k_argmax2<<<1, LB, 0, s>>>(pv.as<double>(), pi.as<int>(), LG, piv.as<int>(),
+                               pivd.as<double>(), i);
+    double* col = L + (size_t)i * n;
+    k_kcol<<<lgrid(n), 256, 0, s>>>(pl.t.as<double>(), n, pl.d, pl.P, prod, pl.os2,
+                                    piv.as<int>(), i, col);
+    if (i > 0) {
+      k_pivrow<<<1, 256, 0, s>>>(L, n, piv.as<int>(), i, Lp.as<double>());
+      const double m1 = -1.0, one = 1.0;
+      GPM_CUBLAS(cublasDgemv(pc.h, CUBLAS_OP_N, (int)n, i, &m1, L, (int)n, Lp.as<double>(), 1,
+                             &one, col, 1));
+    }
+    k_pcupd<<<lgrid(n), 256, 0, s>>>(col, diag.as<double>(), n, piv.as<int>(),
+                                     pivd.as<double>(), i);
+    GPM_CUDA(cudaGetLastError());
+  }
+  pc.piv.resize(k);
+  std::vector<double> hpd(k);
+  GPM_CUDA(cudaMemcpyAsync(pc.piv.data(), piv.ptr, 4 * (size_t)k, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(hpd.data(), pivd.ptr, 8 * (size_t)k, cudaMemcpyDeviceToHost, s));
+  // Gram matrix G = L^T L (k x k, symmetric)
+  DevBuf G;
+  GPM_TRY(G.alloc(8 * (size_t)k * k));
+  const double one = 1.0, zero = 0.0;
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_T, CUBLAS_OP_N, k, k, (int)n, &one, L, (int)n, L,
+                         (int)n, &zero, G.as<double>(), k));
+  pc.G.resize((size_t)k * k);
+  GPM_CUDA(cudaMemcpyAsync(pc.G.data(), G.ptr, 8 * (size_t)k * k, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < k; ++i)
+    if (!(hpd[i] > 0.0))
+      return fail(GP_ERR_INVALID_ARG, "pivoted Cholesky: rank " + std::to_string(k) +
+                                          " exceeds the numerical rank of K (pivot " +
+                                          std::to_string(i) + ")");
+  GPM_TRY(pc.Cinv.alloc(8 * (size_t)k * k));
+  return GP_OK;
+}
+
+// C = I + G / s2 ; Cinv (device) and log det C for this sigma^2
+static gp_status precond_sigma(Precond& pc, double s2, cudaStream_t s) {
+  if (pc.s2 == s2) return GP_OK;
+  const int k = pc.k;
+  std::vector<double> C((size_t)k * k);
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j)
+      C[(size_t)i * k + j] = 0.5 * (pc.G[(size_t)i * k + j] + pc.G[(size_t)j * k + i]) / s2 +
+                             (i == j ? 1.0 : 0.0);
+  if (!chol(C, k)) return fail(GP_ERR_INVALID_ARG, "Woodbury capacitance matrix not SPD");
+  double ld = 0.0;
+  for (int i = 0; i < k; ++i) ld += 2.0 * std::log(C[(size_t)i * k + i]);
+  // inverse from the Cholesky factor: solve C X = I column by column
+  std::vector<double> inv((size_t)k * k), y(k);
+  for (int c = 0; c < k; ++c) {
+    for (int i = 0; i < k; ++i) {
+      double t = i == c ? 1.0 : 0.0;
+      for (int q = 0; q < i; ++q) t -= C[(size_t)i * k + q] * y[q];
+      y[i] = t / C[(size_t)i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double t = y[i];
+      for (int q = i + 1; q < k; ++q) t -= C[(size_t)q * k + i] * inv[(size_t)q * k + c];
+      inv[(size_t)i * k + c] = t / C[(size_t)i * k + i];
+    }
+  }
+  // symmetric: row-major == column-major
+  GPM_CUDA(cudaMemcpyAsync(pc.Cinv.ptr, inv.data(), 8 * (size_t)k * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  pc.s2 = s2;
+  pc.logdetC = ld;
+  return GP_OK;
+}
+
+double precond_logdet_val(const Precond& pc) {
+  return (double)pc.n * std::log(pc.s2) + pc.logdetC;
+}
+
+gp_status precond_logdet(Precond& pc, double s2, double* out, cudaStream_t s) {
+  GPM_TRY(precond_sigma(pc, s2, s));
+  *out = precond_logdet_val(pc);
+  return GP_OK;
+}
+
+// Z = P^-1 R = R/s2 - L Cinv L^T R / s2^2   (rank order, nb columns)
+gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double* Z,
+                        cudaStream_t s) {
+  GPM_TRY(precond_sigma(pc, s2, s));
+  const int k = pc.k;
+  const int n = (int)pc.n;
+  if (pc.W.bytes < 8 * (size_t)k * nb) GPM_TRY(pc.W.alloc(8 * (size_t)k * nb));
+  if (pc.Y.bytes < 8 * (size_t)k * nb) GPM_TRY(pc.Y.alloc(8 * (size_t)k * nb));
+  GPM_CUBLAS(cublasSetStream(pc.h, s));
+  const double one = 1.0, zero = 0.0, a = -1.0 / (s2 * s2), b = 1.0 / s2;
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_T, CUBLAS_OP_N, k, nb, n, &one, pc.L.as<double>(), n, R,
+                         n, &zero, pc.W.as<double>(), k));
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_N, k, nb, k, &one, pc.Cinv.as<double>(), k,
+                         pc.W.as<double>(), k, &zero, pc.Y.as<double>(), k));
+  if (Z != R) GPM_CUDA(cudaMemcpyAsync(Z, R, 8 * (size_t)n * nb, cudaMemcpyDeviceToDevice, s));
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_N, n, nb, k, &a, pc.L.as<double>(), n,
+                         pc.Y.as<double>(), k, &b, Z, n));
+  return GP_OK;
+}
+
+// z = L w + sigma g  (a sample of N(0, P) from standard normals g (n) and w (k))
+gp_status precond_sample(Precond& pc, double s2, const double* G, const double* W, int nb,
+                         double* Z, cudaStream_t s) {
+  const int k = pc.k;
+  const int n = (int)pc.n;
+  GPM_CUBLAS(cublasSetStream(pc.h, s));
+  const double one = 1.0, sg = std::sqrt(s2);
+  k_lin<<<lgrid((int64_t)n * nb), 256, 0, s>>>(G, nullptr, sg, 0.0, (int64_t)n * nb, Z);
+  GPM_CUDA(cudaGetLastError());
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_N, n, nb, k, &one, pc.L.as<double>(), n, W,
+                         k, &one, Z, n));
+  return GP_OK;
+}
+
+void precond_free(Precond& pc) {
+  pc.L.release();
+  pc.Cinv.release();
+  pc.W.release();
+  pc.Y.release();
+  if (pc.h) cublasDestroy(pc.h);
+  pc.h = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// Algorithm 2 in rank order.  B, X: n x nb.  tol2[c]: absolute stop level for ||r_c||^2
+// (0: run max_iter iterations).  ahist/bhist: device, max_iter x nb (may be null).
+gp_status mbcg_rank(Plan& pl, Precond* pc, double s2, const double* B, int nb, int max_iter,
+                    const std::vector<double>& tol2, double* X, double* ahist, double* bhist,
+                    std::vector<int>& iters, std::vector<int>& status, double* P0,
+                    cudaStream_t s) {
+  const int64_t n = pl.n;
+  const size_t nk = (size_t)n * nb;
+  DevBuf bR, bP, bQ, bZ, bpart, bsc;
+  struct Guard {
+    DevBuf* b[6];
+    ~Guard() { for (auto* x : b) x->release(); }
+  } guard{{&bR, &bP, &bQ, &bZ, &bpart, &bsc}};
+  GPM_TRY(bR.alloc(8 * nk));
+  GPM_TRY(bP.alloc(8 * nk));
+  GPM_TRY(bQ.alloc(8 * nk));
+  if (pc) GPM_TRY(bZ.alloc(8 * nk));
+  GPM_TRY(bpart.alloc(8 * (size_t)LG * nb * 2));
+  GPM_TRY(bsc.alloc(8 * 4 * (size_t)nb + 4 * 2 * (size_t)nb + 64));
+  double* R = bR.as<double>();
+  double* Pm = bP.as<double>();
+  double* Q = bQ.as<double>();
+  double* Z = pc ? bZ.as<double>() : R;
+  double* part = bpart.as<double>();
+  double* part2 = part + (size_t)LG * nb;
+  double* zr = bsc.as<double>();
+  double* t2 = zr + nb;
+  double* al = t2 + nb;
+  double* be = al + nb;
+  int* st = reinterpret_cast<int*>(be + nb);
+  int* itc = st + nb;
+
+  GPM_CUDA(cudaMemsetAsync(X, 0, 8 * nk, s));
+  GPM_CUDA(cudaMemcpyAsync(R, B, 8 * nk, cudaMemcpyDeviceToDevice, s));
+  if (pc) GPM_TRY(precond_apply(*pc, s2, R, nb, Z, s));
+  GPM_CUDA(cudaMemcpyAsync(Pm, Z, 8 * nk, cudaMemcpyDeviceToDevice, s));
+  if (P0) GPM_CUDA(cudaMemcpyAsync(P0, Z, 8 * nk, cudaMemcpyDeviceToDevice, s));   // P^-1 b
+  k_dotp<<<dim3(LG, nb), LB, 0, s>>>(Z, R, n, part);
+  k_sum<<<nb, LB, 0, s>>>(part, LG, zr);
+  k_dotp<<<dim3(LG, nb), LB, 0, s>>>(R, R, n, part);
+  DevBuf brr;
+  GPM_TRY(brr.alloc(8 * (size_t)nb));
+  k_sum<<<nb, LB, 0, s>>>(part, LG, brr.as<double>());
+  GPM_CUDA(cudaGetLastError());
+  std::vector<double> hrr(nb), hzr(nb);
+  GPM_CUDA(cudaMemcpyAsync(hrr.data(), brr.ptr, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(hzr.data(), zr, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  brr.release();
+  status.assign(nb, 0);
+  iters.assign(nb, 0);
+  for (int c = 0; c < nb; ++c)
+    if (hrr[c] == 0.0 || hrr[c] <= tol2[c]) status[c] = 1;   // x = 0 already meets the level
+  GPM_CUDA(cudaMemcpyAsync(t2, tol2.data(), 8 * (size_t)nb, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(st, status.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemsetAsync(itc, 0, 4 * (size_t)nb, s));
+
+  std::vector<char> active(nb);
+  int it = 0;
+  bool any = false;
+  for (int c = 0; c < nb; ++c) { active[c] = status[c] == 0; any |= active[c] != 0; }
+  while (any && it < max_iter) {
+    for (int step = 0; step < 8 && it < max_iter; ++step, ++it) {
+      // T = A Pbar (active columns; maximal runs through one multi-RHS apply)
+      for (int c = 0; c < nb;) {
+        if (!active[c]) { ++c; continue; }
+        int e = c;
+        while (e < nb && active[e]) ++e;
+        GPM_TRY(apply_rank(pl, Pm + (size_t)c * n, Q + (size_t)c * n, e - c, s));
+        c = e;
+      }
+      k_mq<<<dim3(LG, nb), LB, 0, s>>>(Pm, Q, n, s2, part);
+      k_malpha<<<nb, LB, 0, s>>>(part, LG, zr, al, st, ahist, it, nb);
+      k_mupd<<<dim3(LG, nb), LB, 0, s>>>(X, R, Pm, Q, al, n, part);
+      if (pc) {
+        GPM_TRY(precond_apply(*pc, s2, R, nb, Z, s));
+        k_dotp<<<dim3(LG, nb), LB, 0, s>>>(Z, R, n, part2);
+      }
+      k_mbeta<<<nb, LB, 0, s>>>(part, pc ? part2 : part, LG, zr, t2, be, st, itc, bhist, it, nb);
+      k_mpupd<<<dim3(LG, nb), LB, 0, s>>>(Pm, Z, be, st, n);
+    }
+    GPM_CUDA(cudaGetLastError());
+    GPM_CUDA(cudaMemcpyAsync(status.data(), st, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    any = false;
+    for (int c = 0; c < nb; ++c) {
+      active[c] = status[c] == 0;
+      any |= active[c] != 0;
+      if (status[c] == 2) any = false;
+    }
+    bool broke = false;
+    for (int c = 0; c < nb; ++c) broke |= status[c] == 2;
+    if (broke) break;
+  }
+  GPM_CUDA(cudaMemcpyAsync(iters.data(), itc, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return GP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// e1^T f(T) e1 for the symmetric tridiagonal T (diag d[0..m-1], off e[0..m-2]) with
+// f = log: implicit-shift QL (Wilkinson shift), eigenvalues in d, first eigenvector
+// components in z.  Returns false on non-convergence or a non-positive eigenvalue.
+static bool tridiag_log_e1(std::vector<double> d, std::vector<double> e, double* out) {
+  const int m = (int)d.size();
+  e.resize(m, 0.0);
+  std::vector<double> z(m, 0.0);
+  z[0] = 1.0;
+  for (int l = 0; l < m; ++l) {
+    int iter = 0;
+    while (true) {
+      int mm = l;
+      for (; mm < m - 1; ++mm) {
+        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
+        if (std::fabs(e[mm]) <= 1e-16 * dd) break;
+      }
+      if (mm == l) break;
+      if (++iter > 200) return false;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = std::hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + std::copysign(r, g));
+      double sn = 1.0, cs = 1.0, p = 0.0;
+      int i = mm - 1;
+      bool early = false;
+      for (; i >= l; --i) {
+        double f = sn * e[i];
+        const double b = cs * e[i];
+        r = std::hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[mm] = 0.0;
+          early = true;
+          break;
+        }
+        sn = f / r;
+        cs = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * sn + 2.0 * cs * b;
+        p = sn * r;
+        d[i + 1] = g + p;
+        g = cs * r - b;
+        // rotate the first row of the eigenvector matrix (columns i, i+1)
+        f = z[i + 1];
+        z[i + 1] = sn * z[i] + cs * f;
+        z[i] = cs * z[i] - sn * f;
+      }
+      if (early) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+  double acc = 0.0;
+  for (int j = 0; j < m; ++j) {
+    if (!(d[j] > 0.0) || !std::isfinite(d[j])) return false;
+    acc += z[j] * z[j] * std::log(d[j]);
+  }
+  *out = acc;
+  return true;
+}
+
+// Lanczos tridiagonal of column c from the CG coefficients (Alg 2)
+gp_status slq_column(const double* ah, const double* bh, int nb, int c, int m, double* q) {
+  if (m < 1) return fail(GP_ERR_BREAKDOWN, "Lanczos quadrature: no iteration recorded");
+  std::vector<double> d(m), e(std::max(m - 1, 0));
+  for (int j = 0; j < m; ++j) {
+    const double a = ah[(size_t)j * nb + c];
+    d[j] = 1.0 / a + (j > 0 ? bh[(size_t)(j - 1) * nb + c] / ah[(size_t)(j - 1) * nb + c] : 0.0);
+    if (j + 1 < m) e[j] = std::sqrt(bh[(size_t)j * nb + c]) / a;
+  }
+  if (!tridiag_log_e1(d, e, q))
+    return fail(GP_ERR_BREAKDOWN, "Lanczos tridiagonal has a non-positive or unresolved "
+                                  "eigenvalue (loss of orthogonality, P:713)");
+  return GP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// gp_lml: value and gradient of the log-marginal likelihood (App A).
+gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const double* G_user,
+                   const double* W, int nprobe, int m, double cg_rtol, gp_lml_result* out,
+                   cudaStream_t s) {
+  const int64_t n = pl.n;
+  const int l = nprobe;
+  const int nc = 1 + l;                    // column 0: the response, 1..l: the probes
+  DevBuf bB, bX, bP0, bK, bD, bpart, bdots, bah, bbh;
+  struct Guard {
+    DevBuf* b[9];
+    ~Guard() { for (auto* x : b) x->release(); }
+  } guard{{&bB, &bX, &bP0, &bK, &bD, &bpart, &bdots, &bah, &bbh}};
+  GPM_TRY(bB.alloc(8 * (size_t)n * nc));
+  GPM_TRY(bX.alloc(8 * (size_t)n * nc));
+  GPM_TRY(bP0.alloc(8 * (size_t)n * nc));
+  GPM_TRY(bK.alloc(8 * (size_t)n * nc));
+  GPM_TRY(bD.alloc(8 * (size_t)n * nc));
+  GPM_TRY(bpart.alloc(8 * (size_t)LG * nc));
+  GPM_TRY(bdots.alloc(8 * (size_t)nc * 4));
+  GPM_TRY(bah.alloc(8 * (size_t)m * l));
+  GPM_TRY(bbh.alloc(8 * (size_t)m * l));
+  double* B = bB.as<double>();
+  double* X = bX.as<double>();
+  double* P0 = bP0.as<double>();
+  double* KP = bK.as<double>();
+  double* DP = bD.as<double>();
+  double* dots = bdots.as<double>();
+  // rank-order right-hand sides
+  GPM_TRY(permute_vec(pl, r_user, B, true, s));
+  for (int c = 0; c < l; ++c)
+    GPM_TRY(permute_vec(pl, G_user + (size_t)c * n, P0 + (size_t)c * n, true, s));
+  if (pc) {
+    GPM_TRY(precond_sample(*pc, s2, P0, W, l, B + n, s));   // z = L w + sigma g ~ N(0, P)
+  } else {
+    GPM_CUDA(cudaMemcpyAsync(B + n, P0, 8 * (size_t)n * l, cudaMemcpyDeviceToDevice, s));
+  }
+  // (1) a = A^-1 r to cg_rtol
+  std::vector<int> it1, st1, itl, stl;
+  {
+    k_dotp<<<dim3(LG, 1), LB, 0, s>>>(B, B, n, bpart.as<double>());
+    k_sum<<<1, LB, 0, s>>>(bpart.as<double>(), LG, dots);
+    double rr = 0.0;
+    GPM_CUDA(cudaMemcpyAsync(&rr, dots, 8, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> t2(1, cg_rtol * cg_rtol * rr);
+    const int cap = (int)std::min<int64_t>(std::max<int64_t>(1000, 20 * n), 200000);
+    GPM_TRY(mbcg_rank(pl, pc, s2, B, 1, cap, t2, X, nullptr, nullptr, it1, st1, nullptr, s));
+    if (st1[0] == 2) return fail(GP_ERR_BREAKDOWN, "CG breakdown in the r solve");
+    if (st1[0] != 1) return fail(GP_ERR_NOT_CONVERGED, "CG for A^-1 r did not reach cg_rtol");
+  }
+  // (2) probes: m Lanczos steps (rtol 0); P0 = P^-1 z
+  {
+    std::vector<double> t2(l, 0.0);
+    GPM_TRY(mbcg_rank(pl, pc, s2, B + n, l, m, t2, X + n, bah.as<double>(), bbh.as<double>(),
+                      itl, stl, P0 + n, s));
+    for (int c = 0; c < l; ++c)
+      if (stl[c] == 2) return fail(GP_ERR_BREAKDOWN, "CG breakdown on probe " + std::to_string(c));
+  }
+  if (!pc) GPM_CUDA(cudaMemcpyAsync(P0 + n, B + n, 8 * (size_t)n * l, cudaMemcpyDeviceToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(P0, X, 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));   // col 0: a
+  // (3) K [a, P^-1 z] and l dK/dl [a, P^-1 z]
+  GPM_TRY(apply_rank(pl, P0, KP, nc, s, 0));
+  const bool has_dl = pl.d == 1 || pl.form == GP_FORM_L1;
+  if (has_dl) GPM_TRY(apply_rank(pl, P0, DP, nc, s, 1));
+  // (4) dots: col 0: a.Ka, a.dKa, a.a, r.a ; probe c: x_c.K p_c, x_c.dK p_c, x_c.p_c
+  //     (x_c = A^-1 z_c from Lanczos, p_c = P^-1 z_c)
+  std::vector<double> hk(nc), hd(nc, 0.0), hp(nc), hq(1);
+  auto dotcols = [&](const double* Aa, const double* Bb, std::vector<double>& h) -> gp_status {
+    k_dotp<<<dim3(LG, nc), LB, 0, s>>>(Aa, Bb, n, bpart.as<double>());
+    k_sum<<<nc, LB, 0, s>>>(bpart.as<double>(), LG, dots);
+    GPM_CUDA(cudaGetLastError());
+    GPM_CUDA(cudaMemcpyAsync(h.data(), dots, 8 * (size_t)nc, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+    return GP_OK;
+  };
+  GPM_TRY(dotcols(X, KP, hk));
+  if (has_dl) GPM_TRY(dotcols(X, DP, hd));
+  GPM_TRY(dotcols(X, P0, hp));
+  {
+    k_dotp<<<dim3(LG, 1), LB, 0, s>>>(B, X, n, bpart.as<double>());
+    k_sum<<<1, LB, 0, s>>>(bpart.as<double>(), LG, dots);
+    GPM_CUDA(cudaMemcpyAsync(hq.data(), dots, 8, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaStreamSynchronize(s));
+  }
+  // (5) log det by Lanczos quadrature
+  std::vector<double> ah((size_t)m * l), bh((size_t)m * l);
+  GPM_CUDA(cudaMemcpyAsync(ah.data(), bah.ptr, 8 * (size_t)m * l, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(bh.data(), bbh.ptr, 8 * (size_t)m * l, cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  double acc = 0.0;
+  int mmax = 0;
+  for (int c = 0; c < l; ++c) {
+    double q = 0.0;
+    GPM_TRY(slq_column(ah.data(), bh.data(), l, c, itl[c], &q));
+    acc += q;
+    mmax = std::max(mmax, itl[c]);
+  }
+  double ldP = 0.0;
+  if (pc) GPM_TRY(precond_logdet(*pc, s2, &ldP, s));
+  const double N = (double)n;
+  const double logdet = N / l * acc + ldP;
+  // (6) assemble; Hutchinson: tr(A^-1 M) ~ 1/l sum_c x_c^T M p_c
+  double trK = 0.0, trD = 0.0, trI = 0.0;
+  for (int c = 1; c <= l; ++c) { trK += hk[c]; trD += hd[c]; trI += hp[c]; }
+  trK /= l; trD /= l; trI /= l;
+  const double os = std::sqrt(pl.os2), sg = std::sqrt(s2);
+  out->quad = hq[0];
+  out->logdet = logdet;
+  out->logdet_precond = ldP;
+  out->lml = -0.5 * hq[0] - 0.5 * logdet - 0.5 * N * std::log(2.0 * M_PI);
+  out->grad[0] = (hk[0] - trK) / os;                       // 1/2 (2/s) (a'Ka - tr(A^-1 K))
+  out->grad[1] = has_dl ? 0.5 * (hd[0] - trD) : NAN;
+  out->grad[2] = sg * (hp[0] - trI);                        // 1/2 (2 sigma) (a'a - tr A^-1)
+  out->cg_iters = it1[0];
+  out->lanczos_iters = mmax;
+  return GP_OK;
+}
+
+}  // namespace gpm

@@ -169,6 +169,13 @@ __global__ void k_resid(const double* __restrict__ B, const double* __restrict__
     R[i] = B[i] - fma(sigma2, X[i], Q[i]);
 }
 
+// X += D
+__global__ void k_add(double* __restrict__ X, const double* __restrict__ D, int64_t nk) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk;
+       i += (int64_t)gridDim.x * blockDim.x)
+    X[i] += D[i];
+}
+
 // B columns in rank order: col 0 = y[perm], cols 1.. = H (affine from x_raw, or basis)
 __global__ void k_build_rhs(const int* __restrict__ perm, const double* __restrict__ y,
                             const double* __restrict__ xraw, int d, const double* __restrict__ H,
@@ -294,7 +301,7 @@ gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double
 
 gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,
                    int Lb, double rtol, int max_iter, double* alpha, double* beta,
-                   gp_cg_info* info, cudaStream_t s) {
+                   gp_cg_info* info, cudaStream_t s, Precond* pc) {
   const int64_t n = pl.n;
   const int nh = mean_kind == GP_MEAN_AFFINE ? 1 + pl.d : mean_kind == GP_MEAN_BASIS ? Lb : 0;
   const int k = 1 + nh;
@@ -351,7 +358,63 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
   int it = 0, restarts = 0;
   gp_status result = GP_OK;
   std::vector<double> relres(k, 0.0);
-  while (true) {
+  if (pc) {
+    // preconditioned (Alg 2 with s_P = Woodbury): solve, then the true
+    // residual; restart on it (solve A D = R, X += D) while the recursion drifted
+    std::vector<double> t2(k);
+    for (int c = 0; c < k; ++c) t2[c] = htol2[c];
+    std::vector<int> iters, st;
+    DevBuf bD;
+    GPM_TRY(bD.alloc(8 * nk));
+    const double* rhs = B;
+    double* sol = X;
+    while (true) {
+      GPM_TRY(mbcg_rank(pl, pc, sigma2, rhs, k, std::max(1, max_iter - it), t2, sol, nullptr,
+                        nullptr, iters, st, nullptr, s));
+      int mx = 0;
+      for (int c = 0; c < k; ++c) mx = std::max(mx, iters[c]);
+      it += mx;
+      if (sol != X) {   // X += D
+        k_add<<<g1((int64_t)nk), 256, 0, s>>>(X, sol, (int64_t)nk);
+        GPM_CUDA(cudaGetLastError());
+      }
+      bool broke = false;
+      for (int c = 0; c < k; ++c) { hst[c] = st[c]; broke |= st[c] == 2; }
+      GPM_TRY(apply_rank(pl, X, Q, k, s));
+      k_resid<<<g1((int64_t)nk), 256, 0, s>>>(B, Q, X, sigma2, (int64_t)nk, R);
+      k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(R, n, part);
+      k_finish_sum<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr);
+      GPM_CUDA(cudaGetLastError());
+      GPM_CUDA(cudaMemcpyAsync(hrr.data(), rr, 8 * k, cudaMemcpyDeviceToHost, s));
+      GPM_CUDA(cudaStreamSynchronize(s));
+      bool need = false;
+      int bad = -1;
+      for (int c = 0; c < k; ++c) {
+        relres[c] = hb2[c] > 0 ? std::sqrt(hrr[c] / hb2[c]) : 0.0;
+        if (relres[c] > rtol || st[c] == 2) { need = true; if (bad < 0) bad = c; }
+      }
+      if (broke) {
+        result = fail(GP_ERR_BREAKDOWN, "preconditioned CG breakdown (p^T A p <= 0) in column " +
+                                            std::to_string(bad) +
+                                            ": K + sigma^2 I is not positive definite");
+        break;
+      }
+      if (!need) break;
+      if (it >= max_iter || restarts >= 5) {
+        result = fail(GP_ERR_NOT_CONVERGED, "preconditioned CG did not reach rtol in " +
+                                                std::to_string(it) + " iterations (column " +
+                                                std::to_string(bad) + ", relres " +
+                                                std::to_string(relres[bad]) + ")");
+        break;
+      }
+      ++restarts;
+      rhs = R;                  // solve A D = R_true, same absolute levels
+      sol = bD.as<double>();
+      GPM_CUDA(cudaMemcpyAsync(Pm, R, 8 * nk, cudaMemcpyDeviceToDevice, s));   // (keep R)
+      rhs = Pm;
+    }
+  }
+  while (!pc) {
     std::vector<char> active(k, 0);
     for (int c = 0; c < k; ++c) active[c] = hst[c] == 0;
     bool any = false;
