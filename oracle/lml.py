@@ -29,7 +29,7 @@ from . import oracle as _o
 __all__ = [
     "cov_matrix", "dcov_matrices", "lml_exact", "lml_grad_exact", "mbcg", "lanczos_T",
     "slq_logdet", "hutchinson_trace", "pivoted_cholesky", "woodbury_solve",
-    "sylvester_logdet", "lml_stochastic",
+    "sylvester_logdet", "lml_stochastic", "adam_step", "sigma_update", "alg1_fit",
 ]
 
 
@@ -196,3 +196,78 @@ def lml_stochastic(A, dAs, r, Z, m, sP=None, logdet_P=0.0):
     lml = -0.5 * quad - 0.5 * logdet - 0.5 * N * math.log(2 * math.pi)
     return {"lml": lml, "quad": quad, "logdet": logdet, "grad": grad, "XZ": XZ, "T": T,
             "nI": nI}
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 1: successive gradient descents with the sigma update and
+# the GLS / beta-average loop.  GradDescStep is one ADAM step (Kingma & Ba, the optimiser
+# the paper uses, L713-714) on theta = (log s, log c) -- c scales every lengthscale --
+# ascending the stochastic LML (lml_stochastic with fixed probes).  Reading R13:
+# log-parameters, ADAM defaults beta1 = 0.9, beta2 = 0.999, eps = 1e-8, gradNorm =
+# ||grad_theta L|| / N.
+
+def adam_step(theta, g, state, lr, b1=0.9, b2=0.999, eps=1e-8):
+    """One ADAM ascent step (bias-corrected moments); state = (m, v, t)."""
+    m, v, t = state
+    t += 1
+    m = b1 * m + (1 - b1) * g
+    v = b2 * v + (1 - b2) * g * g
+    mh = m / (1 - b1 ** t)
+    vh = v / (1 - b2 ** t)
+    return theta + lr * mh / (np.sqrt(vh) + eps), (m, v, t)
+
+
+def sigma_update(x, yc, two_nu, form, ell, s, sigma_prev):
+    """(sigma)^2 = 1/N y^T (Ktilde + I)^-1 y, Ktilde = K(s / sigma_prev, l)  (Alg 1)."""
+    A, _ = cov_matrix(x, two_nu, form, ell, s / sigma_prev, 1.0)
+    return math.sqrt(float(yc @ np.linalg.solve(A, yc)) / len(yc))
+
+
+def alg1_fit(x, y, H, two_nu, form, ell0, s0, sigma0, Z, m, lr=0.05, max_steps=50,
+             max_outer=3, grad_tol=1e-4, beta_tol=1e-3, trace=None):
+    """Algorithm 1 with the stochastic LML of lml_stochastic (probes Z, m Lanczos steps).
+    Returns dict(s, c, sigma, beta, steps, outer)."""
+    N = len(y)
+    ell0 = np.asarray(ell0, dtype=np.float64)
+    beta_ols = _o.ols(H, y)                                  # OLS estimate
+    theta = np.array([math.log(s0), 0.0])
+    state = (np.zeros(2), np.zeros(2), 0)
+    sigma = sigma0
+    steps = 0
+
+    def descent(yc):
+        nonlocal theta, state, sigma, steps
+        while True:
+            s, c = math.exp(theta[0]), math.exp(theta[1])
+            A, K = cov_matrix(x, two_nu, form, ell0 * c, s, sigma ** 2)
+            dK = _o.dense_dkernel(x, x, two_nu, form, ell0 * c, s)
+            st = lml_stochastic(A, [2.0 / s * K, dK], yc, Z, m)
+            g = np.array([st["grad"][0] * s, st["grad"][1]])  # d/dlog s, d/dlog c
+            theta, state = adam_step(theta, g, state, lr)
+            steps += 1
+            s, c = math.exp(theta[0]), math.exp(theta[1])
+            sigma = sigma_update(x, yc, two_nu, form, ell0 * c, s, sigma)
+            if trace is not None:
+                trace.append((s, c, sigma))
+            if np.linalg.norm(g) / N <= grad_tol or steps >= max_steps * (outer + 1):
+                return
+
+    outer = 0
+    descent(y - H @ beta_ols)                                # descent with OLS-centred y
+    beta_avg = np.zeros(H.shape[1])
+    beta_old = beta_ols
+    beta_gls = beta_ols
+    while outer < max_outer:
+        s, c = math.exp(theta[0]), math.exp(theta[1])
+        A, _ = cov_matrix(x, two_nu, form, ell0 * c, s, sigma ** 2)
+        AiH = np.linalg.solve(A, H)
+        beta_gls = np.linalg.solve(H.T @ AiH, AiH.T @ y)    # L808-812
+        outer += 1
+        beta_avg = (outer - 1) / outer * beta_avg + beta_gls / outer
+        descent(y - H @ beta_avg)
+        change = np.linalg.norm(beta_gls - beta_old)
+        beta_old = beta_gls
+        if change <= beta_tol:
+            break
+    return {"s": math.exp(theta[0]), "c": math.exp(theta[1]), "sigma": sigma,
+            "beta": beta_gls, "steps": steps, "outer": outer}

@@ -63,17 +63,28 @@ static double dprofile(int two_nu, double r)
     }
 }
 
-/* Lengthscale derivative of Ktilde(a, b), L1 form only (form != 0 returns NAN): with every
- * l_k = c l_k0, d Ktilde / d log c at c = 1 is
- *   l dK/dl = -s^2 r k'_nu(r),   r = sum_k |a_k - b_k| / l_k
- * (PAPER.md L1314 [eq dkernel_dl] multiplied by l; one l: divide by l for dK/dl). */
+/* Lengthscale derivative of Ktilde(a, b): with every l_k = c l_k0, d Ktilde / d log c at
+ * c = 1 (PAPER.md L1314 [eq dkernel_dl] multiplied by l; one l: divide by l for dK/dl):
+ *   L1:      -s^2 r k'_nu(r),   r = sum_k |a_k - b_k| / l_k
+ *   product: -s^2 sum_k r_k k'_nu(r_k) prod_{j != k} k_nu(r_j),   r_k = |a_k - b_k| / l_k
+ * (the product rule; each factor's r_k scales with 1/c). */
 double oracle_dkernel_value(int two_nu, int form, int d, const double *ell, double outputscale,
                             const double *a, const double *b)
 {
-    if (form != 0) return NAN;
-    double r = 0.0;
-    for (int k = 0; k < d; ++k) r += fabs(a[k] - b[k]) / ell[k];
-    return -outputscale * outputscale * r * dprofile(two_nu, r);
+    if (form == 0) {
+        double r = 0.0;
+        for (int k = 0; k < d; ++k) r += fabs(a[k] - b[k]) / ell[k];
+        return -outputscale * outputscale * r * dprofile(two_nu, r);
+    }
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) {
+        const double rk = fabs(a[k] - b[k]) / ell[k];
+        double term = -rk * dprofile(two_nu, rk);
+        for (int j = 0; j < d; ++j)
+            if (j != k) term *= profile(two_nu, fabs(a[j] - b[j]) / ell[j]);
+        acc += term;
+    }
+    return outputscale * outputscale * acc;
 }
 
 /* Ktilde(a, b) for one pair of d-dimensional points (form 0 = L1, 1 = product). */

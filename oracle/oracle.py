@@ -86,8 +86,8 @@ def kernel_value(two_nu: int, form: str, ell, outputscale: float, a, b) -> float
 
 
 def dkernel_value(two_nu: int, form: str, ell, outputscale: float, a, b) -> float:
-    """l dKtilde/dl = -s^2 r k'_nu(r) (L1 form, every l_k scaled together)
-    [eq dkernel_dl] times l, with the L1320-1322 derivative profiles."""
+    """l dKtilde/dl, every l_k scaled together: L1 -s^2 r k'(r); product: the product rule
+    (PAPER.md L1314 [eq dkernel_dl] times l, with the L1320-1322 derivative profiles)."""
     a = _f64(np.atleast_1d(a)); b = _f64(np.atleast_1d(b)); ell = _f64(np.atleast_1d(ell))
     return float(_load().oracle_dkernel_value(two_nu, FORMS[form], a.size, _dp(ell),
                                               outputscale, _dp(a), _dp(b)))
@@ -95,7 +95,7 @@ def dkernel_value(two_nu: int, form: str, ell, outputscale: float, a, b) -> floa
 
 def dkzx_rows(x, v, z, two_nu: int, form: str, ell, outputscale: float = 1.0, rows=None,
               nthreads: int = 0, return_abs: bool = False):
-    """(l dK_zx/dl v)_q = sum_i v_i l dKtilde(x_i, z_q)/dl for q in rows (L1 form)."""
+    """(l dK_zx/dl v)_q = sum_i v_i l dKtilde(x_i, z_q)/dl for q in rows."""
     return kzx_rows(x, v, z, two_nu, form, ell, outputscale, rows, nthreads, return_abs,
                     _kind=1)
 
@@ -144,7 +144,7 @@ def dense_kernel(a, b, two_nu: int, form: str, ell, outputscale: float = 1.0, nt
 
 
 def dense_dkernel(a, b, two_nu: int, form: str, ell, outputscale: float = 1.0, nthreads=0):
-    """Dense block [l dKtilde(a_i, b_j)/dl] (L1 form; PAPER.md L1314 times l); small sizes."""
+    """Dense block [l dKtilde(a_i, b_j)/dl] (PAPER.md L1314 times l); small sizes."""
     a = _f64(a, 2); b = _f64(b, 2); ell = _f64(np.atleast_1d(ell))
     out = np.empty((a.shape[0], b.shape[0]))
     _load().oracle_dense_d(two_nu, FORMS[form], a.shape[1], _dp(ell), float(outputscale),

@@ -382,4 +382,29 @@ def test_dkmvm_bruteforce_lengthscale_derivative(two_nu, d):
     e = np.zeros(n); e[1] = 1.0
     col = oracle.dkmvm_rows(x, e, two_nu, "l1", ell, sig)
     assert col[1] == 0.0 and col[3] == 0.0
-    assert np.isnan(oracle.dkernel_value(two_nu, "product", ell, 1.0, x[0], x[2]))
+
+
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("d", [2, 3])
+def test_dkmvm_product_form_lengthscale_derivative(two_nu, d):
+    """Product form: 40-digit d/dc of prod_k k(|dx_k| / (c l_k)) on the Bessel definition."""
+    rng = np.random.default_rng(400 + 10 * d + two_nu)
+    n = 7
+    x = rng.random((n, d))
+    v = rng.standard_normal(n)
+    ell = [0.3, 0.5, 0.2][:d]
+    got, ab = oracle.dkmvm_rows(x, v, two_nu, "product", ell, 0.9, return_abs=True)
+    with mp.workdps(40):
+        ref = []
+        for j in range(n):
+            def f(c):
+                tot = mp.mpf(0)
+                for i in range(n):
+                    kv = mp.mpf(1)
+                    for k in range(d):
+                        kv *= bessel_profile(two_nu, abs(mp.mpf(x[i, k]) - mp.mpf(x[j, k])) /
+                                             (c * mp.mpf(ell[k])), 120)
+                    tot += mp.mpf(v[i]) * mp.mpf(0.9) ** 2 * kv
+                return tot
+            ref.append(float(mp.diff(f, mp.mpf(1))))
+    assert np.max(np.abs(got - np.array(ref))) <= 1e-14 * np.max(ab) * np.max(np.abs(v))

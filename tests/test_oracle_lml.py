@@ -180,3 +180,54 @@ def test_preconditioned_stochastic_lml_exact_with_structured_probes():
     assert st["logdet"] == pytest.approx(logdet, rel=1e-9, abs=1e-9)
     assert st["lml"] == pytest.approx(ex, rel=1e-9)
     assert np.allclose(st["grad"], ol.lml_grad_exact(A, dAs, r), rtol=1e-8, atol=1e-9)
+
+
+def test_adam_first_step_and_quadratic_convergence():
+    """ADAM: the bias-corrected first step moves each coordinate by lr * sign(g); on a
+    concave quadratic the iterates converge to the maximiser."""
+    th, st = ol.adam_step(np.zeros(2), np.array([3.0, -0.2]), (np.zeros(2), np.zeros(2), 0), 0.1)
+    assert np.allclose(th, [0.1, -0.1], atol=1e-7)
+    th = np.array([2.0, -1.0]); st = (np.zeros(2), np.zeros(2), 0)
+    for _ in range(3000):
+        th, st = ol.adam_step(th, -2.0 * (th - np.array([0.5, 0.25])), st, 0.01)
+    assert np.allclose(th, [0.5, 0.25], atol=1e-3)
+
+
+def test_sigma_update_maximises_lml_along_the_ratio():
+    """Alg 1's closed form (L846): with s/sigma fixed, sigma^2 = y^T (Ktilde + I)^-1 y / N
+    maximises the LML over sigma."""
+    rng = np.random.default_rng(14)
+    x = rng.random((150, 2)); y = rng.standard_normal(150)
+    ell, s, sig0 = [0.2, 0.3], 1.1, 0.4
+    sig = ol.sigma_update(x, y, 3, "product", ell, s, sig0)
+    ratio = s / sig0
+
+    def L(sg):
+        A, _ = ol.cov_matrix(x, 3, "product", ell, ratio * sg, sg ** 2)
+        return ol.lml_exact(A, y)[0]
+    assert L(sig) >= max(L(sig * 0.98), L(sig * 1.02))
+
+
+def test_alg1_recovers_simulated_parameters():
+    """Data simulated from the model (affine mean + GP + noise, dense Cholesky sampler):
+    Alg 1 recovers beta and sigma closely and increases the exact LML."""
+    rng = np.random.default_rng(15)
+    n = 500
+    x = rng.random((n, 2))
+    H = np.hstack([np.ones((n, 1)), x])
+    beta_true = np.array([1.0, 0.5, -0.3])
+    s_true, ell_true, sig_true = 1.0, np.array([0.2, 0.2]), 0.3
+    K = oracle.dense_kernel(x, x, 1, "l1", ell_true, s_true)
+    f = np.linalg.cholesky(K + 1e-10 * np.eye(n)) @ rng.standard_normal(n)
+    y = H @ beta_true + f + sig_true * rng.standard_normal(n)
+    Z = rng.standard_normal((n, 16))
+    res = ol.alg1_fit(x, y, H, 1, "l1", ell_true * 1.5, 0.7, 0.6, Z, 25, lr=0.05,
+                      max_steps=60, max_outer=3)
+    assert abs(res["sigma"] - sig_true) < 0.05
+    A0, _ = ol.cov_matrix(x, 1, "l1", ell_true * 1.5, 0.7, 0.36)
+    A1, _ = ol.cov_matrix(x, 1, "l1", ell_true * 1.5 * res["c"], res["s"], res["sigma"] ** 2)
+    # beta within 4 GLS standard errors, cov(beta_GLS) = (H^T A^-1 H)^-1
+    se = np.sqrt(np.diag(np.linalg.inv(H.T @ np.linalg.solve(A1, H))))
+    assert np.all(np.abs(res["beta"] - beta_true) <= 4 * se)
+    r = y - H @ res["beta"]
+    assert ol.lml_exact(A1, r)[0] > ol.lml_exact(A0, r)[0]
