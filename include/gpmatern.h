@@ -80,7 +80,8 @@ typedef struct {
   double logdet;          /* estimate of log det A (+ log det P when preconditioned) */
   double logdet_precond;  /* log det P, 0 without preconditioner */
   double grad[3];         /* dL/d outputscale, dL/d log(c) (all lengthscales scaled by c;
-                             = l dL/dl for one l; NaN for product forms), dL/d sigma */
+                             = l dL/dl for one l; NaN where gp_kmvm_dlengthscale is
+                             unsupported), dL/d sigma */
   int cg_iters;           /* iterations of the A^-1 r solve */
   int lanczos_iters;      /* Lanczos steps per probe (max over probes) */
 } gp_lml_result;
@@ -125,8 +126,9 @@ GP_API gp_status gp_kmvm_rank(gp_plan p, const double *v_rank, int nrhs, double 
  * (eq dkernel_dvarsigma) and needs no extra MVM.  Computed by the same decomposition with
  * one more moment (g(s) = (s, s^2, (s^2 + s^3)/3) e^{-s} for nu = 1/2, 3/2, 5/2 in scaled
  * distance s = sqrt(2 nu) r): exact like gp_kmvm, no nugget, zero diagonal.
- * Supported: d = 1 (n <= 148 x 6912 = 1022976 points) and the L1 form for d = 2, 3;
- * the product form returns GP_ERR_UNSUPPORTED.  v_order: 0 = user order (layout as
+ * Supported: d = 1 (n <= 148 x 6912 = 1022976 points), the L1 form for d = 2, 3 and the
+ * product form for d = 2 with nu <= 3/2 (product rule g(r1) k(r2) + k(r1) g(r2), (p+2)^2
+ * moments per channel); other product forms return GP_ERR_UNSUPPORTED.  v_order: 0 = user order (layout as
  * gp_kmvm), 1 = the plan's stored order (as gp_kmvm_rank). */
 GP_API gp_status gp_kmvm_dlengthscale(gp_plan p, const double *v, int nrhs, double *out,
                                       int v_order, void *stream);

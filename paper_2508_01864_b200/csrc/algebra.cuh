@@ -148,7 +148,7 @@ template <int P_, int NCH_, bool PROD_, int KIND_ = 0>
 struct Alg {
   static constexpr int P = P_;          // moment order (gradient: nu - 1/2 + 1)
   static constexpr int NCH = NCH_;
-  static constexpr bool PROD = PROD_;   // product form (KIND 0 only)
+  static constexpr bool PROD = PROD_;   // product form
   static constexpr int KIND = KIND_;
   static constexpr int NQ = P + 1;
   static constexpr int NM = PROD ? NQ * NQ : NQ;
@@ -218,12 +218,22 @@ struct Alg {
     double v;
     if constexpr (!PROD) {
       v = readc_poly<P, KIND>(Ms, beta);
-    } else {
+    } else if constexpr (KIND == 0) {
       // k(alpha+beta) k(s): e^{-beta} sum_a a_a sum_{m<=a} C(a,m) beta^{a-m} (sum_q a_q M[m][q])
       double G[NQ];
 #pragma unroll
       for (int m = 0; m < NQ; ++m) G[m] = read0<P>(Ms + m * NQ);
       v = read_poly<P>(G, beta);
+    } else {
+      // lengthscale gradient of k(r1) k(r2) (product rule): g(r1) k(r2) + k(r1) g(r2), with
+      // k of order P - 1 (coefficients a) and g = -s k'(s) of order P (coefficients b)
+      double Ga[NQ], Gb[NQ];
+#pragma unroll
+      for (int m = 0; m < NQ; ++m) {
+        Ga[m] = readc0<P - 1, 0>(Ms + m * NQ);
+        Gb[m] = readc0<P, 1>(Ms + m * NQ);
+      }
+      v = readc_poly<P, 1>(Ga, beta) + readc_poly<P - 1, 0>(Gb, beta);
     }
     return eb * v;
   }

@@ -105,9 +105,14 @@ __device__ __forceinline__ double kval(double d1, double d2, double d3, const do
     }
   } else {
     const double e = fexp_neg(d1 + d2, tab);
-    if constexpr (P == 0) return e;
-    else if constexpr (P == 1) return e * ((1.0 + d1) * (1.0 + d2));
-    else return e * (fma(d1, fma(d1, 1.0 / 3.0, 1.0), 1.0) * fma(d2, fma(d2, 1.0 / 3.0, 1.0), 1.0));
+    if constexpr (A::KIND == 0) {
+      if constexpr (P == 0) return e;
+      else if constexpr (P == 1) return e * ((1.0 + d1) * (1.0 + d2));
+      else return e * (fma(d1, fma(d1, 1.0 / 3.0, 1.0), 1.0) * fma(d2, fma(d2, 1.0 / 3.0, 1.0), 1.0));
+    } else {   // product rule: g(d1) k(d2) + k(d1) g(d2); nu = 1/2 (P = 1) or 3/2 (P = 2)
+      if constexpr (P == 1) return e * (d1 + d2);
+      else return e * ((d1 * d1) * (1.0 + d2) + (1.0 + d1) * (d2 * d2));
+    }
   }
 }
 
@@ -1190,8 +1195,13 @@ size_t level_pt_bytes() { return sizeof(Pt4); }
 
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
-  if (kind != 0) {   // lengthscale gradient (L1 form only): moment order p + 1
-    if (prod) return fail(GP_ERR_UNSUPPORTED, "lengthscale-gradient MVM needs the L1 form");
+  if (kind != 0) {   // lengthscale gradient: moment order p + 1
+    if (prod) {        // d = 2 product form, nu <= 3/2 ((p+2)^2 moments per channel)
+      if (pl.d != 2 || pl.P > 1)
+        return fail(GP_ERR_UNSUPPORTED, "product-form lengthscale gradient: d = 2, nu <= 3/2 only");
+      if (pl.P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
+      return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
+    }
     if (pl.d == 2) {
       if (pl.P == 0) return lv_run<Alg<1, 2, false, 1>>(pl, nrhs, s, launches);
       if (pl.P == 1) return lv_run<Alg<2, 2, false, 1>>(pl, nrhs, s, launches);

@@ -83,9 +83,34 @@ def test_l1_grad_multi_level_sampled(gpm, d):
                    what=f"grad d{d} sampled rhs {r}")
 
 
+@pytest.mark.parametrize("two_nu", [1, 3])
+@pytest.mark.parametrize("n", [3, 64, 2049, 5000])
+def test_product_grad_all_rows(gpm, two_nu, n):
+    """d = 2 product form (nu <= 3/2): the product rule through (p+2)^2 moments."""
+    x = _pts(n, 2, 13 * n + two_nu, ties=(n % 2 == 1))
+    v = np.random.default_rng(n + 7).standard_normal(n)
+    ell = (0.1, 0.2)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.1, form=1))
+    out = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "product", ell, 1.1, grad=True,
+               what=f"grad product nu={two_nu}/2 n={n}")
+
+
+def test_product_grad_multi_level_sampled(gpm):
+    n = 300000
+    x = _pts(n, 2, 1234)
+    V = np.random.default_rng(5).standard_normal((2, n))
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.1), form=1))
+    out = plan.kmvm_dlengthscale(to_dev(V)).cpu().numpy()
+    rows = W.sample_rows(x, 256)
+    for r in range(2):
+        check_rows(out[r], x, V[r], 3, "product", (0.1, 0.1), 1.0, rows=rows, grad=True,
+                   what=f"grad product sampled rhs {r}")
+
+
 def test_grad_unsupported_and_errors(gpm):
     x = _pts(500, 2, 1)
-    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.1), form=1))
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, (0.1, 0.1), form=1))
     with pytest.raises(gpm.GPError) as e:
         plan.kmvm_dlengthscale(to_dev(np.ones(500)))
     assert e.value.name == "UNSUPPORTED"
