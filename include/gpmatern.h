@@ -233,6 +233,45 @@ GP_API gp_status gp_lml(gp_plan p, gp_precond pc, double sigma2, const double *r
                         const double *G, const double *W, int nprobe, int lanczos_iters,
                         double cg_rtol, gp_lml_result *out, void *stream);
 
+/* Options / result of gp_fit (Algorithm 1).  Zero-initialise the options struct and set
+ * what you need: zero fields take the defaults in brackets. */
+typedef struct {
+  double lr;            /* ADAM step on log(outputscale), log(c) [0.05] */
+  int max_steps;        /* gradient steps per descent [50] */
+  int max_outer;        /* GLS rounds after the OLS descent [3] */
+  double grad_tol;      /* end a descent at ||grad_theta L|| / N <= grad_tol [1e-4] */
+  double beta_tol;      /* end at ||beta_GLS - beta_old|| <= beta_tol [1e-3] */
+  int lanczos_iters;    /* Lanczos steps per probe [25] */
+  int precond_rank;     /* pivoted-Cholesky rank of every solve, 0 = none [0] */
+  double cg_rtol;       /* relative residual of every CG solve [1e-8] */
+} gp_fit_opts;
+
+typedef struct {
+  gp_kernel kernel;     /* fitted outputscale and lengthscales (l_k = c * l0_k) */
+  double sigma;         /* fitted noise standard deviation */
+  double beta[4];       /* GLS fixed effects for h(x) = [1, x] */
+  int steps;            /* gradient steps taken */
+  int outer;            /* GLS rounds taken */
+  double lml;           /* stochastic LML at the last gradient evaluation */
+  double grad_norm;     /* last ||grad_theta L|| / N */
+} gp_fit_result;
+
+/* gp_fit -- Algorithm 1: OLS fixed effects, then gradient descents on
+ * theta = (log outputscale, log c) (c scales every lengthscale; GradDescStep = one ADAM
+ * ascent step on the gp_lml estimate) with the closed-form sigma update
+ *   sigma^2 = 1/N y^T (K(s / sigma_prev, l) + I)^-1 y
+ * after each step; then rounds of GLS beta, a running average beta_AVG and a
+ * descent on y - H beta_AVG, until successive beta_GLS differ by <= beta_tol (reading R13
+ * in DESIGN.md: log-parameters, ADAM defaults, gradient norm per observation).
+ *   x  : n x d row-major (device); k0: initial kernel (form, nu fixed); sigma0 > 0.
+ *   y  : n (device, user order).  G: n x nprobe standard normals (device, user order),
+ *   W  : precond_rank x nprobe standard normals (device) iff opts->precond_rank > 0.
+ * The probes are the same at every step (common random numbers).  One plan setup per
+ * gradient step (the lengthscale changes).  Synchronises `stream`. */
+GP_API gp_status gp_fit(const double *x, int64_t n, int d, const gp_kernel *k0, double sigma0,
+                        const double *y, const double *G, const double *W, int nprobe,
+                        const gp_fit_opts *opts, gp_fit_result *out, void *stream);
+
 /* gp_predict -- posterior mean mu(z_q) = h(z_q)^T beta + sum_i K(z_q, x_i) alpha_i
  * (P:86 [eq gp_mean], P:149 [eq gp_mean_2]).
  *   z      : m x d row-major (device); alpha: n (device, user order);

@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "load_library", "Kernel", "Plan", "Cross", "Precond", "GPError", "setup", "kmvm", "cg_solve",
+    "load_library", "Kernel", "Plan", "Cross", "Precond", "GPError", "setup", "kmvm", "cg_solve", "fit",
     "predict", "FORM_L1", "FORM_PRODUCT", "MEAN_NONE", "MEAN_AFFINE", "MEAN_BASIS",
     "LIB_PATH",
 ]
@@ -41,6 +41,19 @@ class _Kernel(ctypes.Structure):
 class _CGInfo(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int), ("relres_max", ctypes.c_double),
                 ("failed_column", ctypes.c_int), ("restarts", ctypes.c_int)]
+
+
+class _FitOpts(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("max_steps", ctypes.c_int),
+                ("max_outer", ctypes.c_int), ("grad_tol", ctypes.c_double),
+                ("beta_tol", ctypes.c_double), ("lanczos_iters", ctypes.c_int),
+                ("precond_rank", ctypes.c_int), ("cg_rtol", ctypes.c_double)]
+
+
+class _FitResult(ctypes.Structure):
+    _fields_ = [("kernel", _Kernel), ("sigma", ctypes.c_double), ("beta", ctypes.c_double * 4),
+                ("steps", ctypes.c_int), ("outer", ctypes.c_int), ("lml", ctypes.c_double),
+                ("grad_norm", ctypes.c_double)]
 
 
 class _LmlResult(ctypes.Structure):
@@ -79,6 +92,8 @@ def load_library(path: str | None = None):
         "gp_precond_logdet": [vp, cd, ctypes.POINTER(cd), vp],
         "gp_mbcg": [vp, vp, cd, vp, ci, ci, cd, vp, vp, vp, vp, vp],
         "gp_lml": [vp, vp, cd, vp, vp, vp, ci, ci, cd, ctypes.POINTER(_LmlResult), vp],
+        "gp_fit": [vp, i64, ci, ctypes.POINTER(_Kernel), cd, vp, vp, vp, ci,
+                   ctypes.POINTER(_FitOpts), ctypes.POINTER(_FitResult), vp],
         "gp_predict": [vp, vp, i64, vp, vp, vp, ci, vp, vp],
         "gp_plan_query": [vp, ci, ctypes.POINTER(i64)],
         "gp_plan_set_option": [vp, ci, i64],
@@ -395,6 +410,30 @@ class Precond:
             self.close()
         except Exception:
             pass
+
+
+def fit(x, kernel: Kernel, sigma0: float, y, G, W=None, stream=None, **opts):
+    """Algorithm 1 hyperparameter fit (gp_fit).  x (n, d), y (n,), G (nprobe, n) standard
+    normals, W (nprobe, precond_rank) standard normals if precond_rank > 0.  opts: lr,
+    max_steps, max_outer, grad_tol, beta_tol, lanczos_iters, precond_rank, cg_rtol.
+    Returns dict(kernel=Kernel, sigma, beta, steps, outer, lml, grad_norm)."""
+    load_library()
+    if x.dim() == 1:
+        x = x.reshape(-1, 1)
+    n, d = x.shape
+    o = _FitOpts()
+    for k, v in opts.items():
+        setattr(o, k, v)
+    res = _FitResult()
+    kc = kernel.c()
+    Wp = _dev(W, "W") if W is not None else None
+    _check(_lib.gp_fit(_dev(x, "x"), n, d, ctypes.byref(kc), float(sigma0), _dev(y, "y", (n,)),
+                       _dev(G, "G", (G.shape[0], n)), Wp, G.shape[0], ctypes.byref(o),
+                       ctypes.byref(res), _stream(stream)))
+    k = Kernel(res.kernel.two_nu, tuple(res.kernel.lengthscale[i] for i in range(d)),
+               res.kernel.outputscale, res.kernel.form)
+    return {"kernel": k, "sigma": res.sigma, "beta": [res.beta[i] for i in range(1 + d)],
+            "steps": res.steps, "outer": res.outer, "lml": res.lml, "grad_norm": res.grad_norm}
 
 
 def cg_solve(plan: Plan, y, sigma2, **kw):

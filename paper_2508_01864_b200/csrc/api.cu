@@ -315,6 +315,32 @@ gp_status gp_mbcg(gp_plan p, gp_precond pc, double sigma2, const double* B, int 
   return GP_OK;
 }
 
+gp_status gp_fit(const double* x, int64_t n, int d, const gp_kernel* k0, double sigma0,
+                 const double* y, const double* G, const double* W, int nprobe,
+                 const gp_fit_opts* opts, gp_fit_result* out, void* stream) {
+  if (!x || !k0 || !y || !G || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (n < 2) return fail(GP_ERR_INVALID_ARG, "n must be >= 2");
+  if (n >= (int64_t(1) << 30)) return fail(GP_ERR_UNSUPPORTED, "n >= 2^30 not supported");
+  GPM_TRY(check_kernel(k0, d));
+  GPM_TRY(check_device());
+  if (!(sigma0 > 0) || !std::isfinite(sigma0)) return fail(GP_ERR_INVALID_ARG, "sigma0 must be > 0");
+  if (nprobe < 1) return fail(GP_ERR_INVALID_ARG, "nprobe must be >= 1");
+  gp_fit_opts o{};
+  if (opts) o = *opts;
+  if (o.lr == 0) o.lr = 0.05;
+  if (o.max_steps == 0) o.max_steps = 50;
+  if (o.max_outer == 0) o.max_outer = 3;
+  if (o.grad_tol == 0) o.grad_tol = 1e-4;
+  if (o.beta_tol == 0) o.beta_tol = 1e-3;
+  if (o.lanczos_iters == 0) o.lanczos_iters = 25;
+  if (o.cg_rtol == 0) o.cg_rtol = 1e-8;
+  if (!(o.lr > 0) || o.max_steps < 1 || o.max_outer < 0 || o.lanczos_iters < 1 ||
+      !(o.cg_rtol > 0) || o.precond_rank < 0 || o.precond_rank > 1024 || o.precond_rank > n)
+    return fail(GP_ERR_INVALID_ARG, "invalid gp_fit_opts");
+  if (o.precond_rank > 0 && !W) return fail(GP_ERR_INVALID_ARG, "W required with precond_rank > 0");
+  return fit_alg1(x, n, d, *k0, sigma0, y, G, W, nprobe, o, out, static_cast<cudaStream_t>(stream));
+}
+
 gp_status gp_lml(gp_plan p, gp_precond pc, double sigma2, const double* r, const double* G,
                  const double* W, int nprobe, int lanczos_iters, double cg_rtol,
                  gp_lml_result* out, void* stream) {

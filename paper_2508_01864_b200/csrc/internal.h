@@ -125,6 +125,10 @@ gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const
                    const double* W, int nprobe, int m, double cg_rtol, gp_lml_result* out,
                    cudaStream_t s);
 
+gp_status fit_alg1(const double* x, int64_t n, int d, const gp_kernel& k0, double sigma0,
+                   const double* y, const double* G, const double* W, int nprobe,
+                   const gp_fit_opts& o, gp_fit_result* out, cudaStream_t s);
+
 // setup.cu
 gp_status plan_build(Plan& pl, const double* x_dev, int64_t n, int d, const gp_kernel& k,
                      cudaStream_t s);

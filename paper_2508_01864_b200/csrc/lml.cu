@@ -761,3 +761,215 @@ gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const
 }
 
 }  // namespace gpm
+
+// ---------------------------------------------------------------------------
+// gp_fit: Algorithm 1 with GradDescStep = one ADAM ascent step on
+// theta = (log s, log c) (reading R13).
+namespace gpm {
+
+namespace {
+
+// y - H beta for H = [1, x] (host)
+std::vector<double> centre(const std::vector<double>& y, const std::vector<double>& x, int d,
+                           const std::vector<double>& beta) {
+  const size_t n = y.size();
+  std::vector<double> r(n);
+  for (size_t i = 0; i < n; ++i) {
+    double m = beta[0];
+    for (int k = 0; k < d; ++k) m += beta[1 + k] * x[i * d + k];
+    r[i] = y[i] - m;
+  }
+  return r;
+}
+
+bool solve_small(std::vector<double> G, std::vector<double> g, int k, std::vector<double>& x) {
+  for (int c = 0; c < k; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < k; ++r)
+      if (std::fabs(G[r * k + c]) > std::fabs(G[piv * k + c])) piv = r;
+    if (G[piv * k + c] == 0.0) return false;
+    if (piv != c) {
+      for (int j = 0; j < k; ++j) std::swap(G[c * k + j], G[piv * k + j]);
+      std::swap(g[c], g[piv]);
+    }
+    for (int r = c + 1; r < k; ++r) {
+      const double f = G[r * k + c] / G[c * k + c];
+      for (int j = c; j < k; ++j) G[r * k + j] -= f * G[c * k + j];
+      g[r] -= f * g[c];
+    }
+  }
+  x.assign(k, 0.0);
+  for (int c = k - 1; c >= 0; --c) {
+    double s = g[c];
+    for (int j = c + 1; j < k; ++j) s -= G[c * k + j] * x[j];
+    x[c] = s / G[c * k + c];
+  }
+  return true;
+}
+
+struct FitState {
+  const double* x;
+  int64_t n;
+  int d;
+  gp_kernel k0;
+  double s, c, sigma;           // outputscale, lengthscale scale, noise sd
+  double m[2] = {0, 0}, v[2] = {0, 0};
+  int t = 0;
+  Plan pl;
+  bool built = false;
+  Precond pc;
+  bool has_pc = false;
+};
+
+gp_kernel cur_kernel(const FitState& F) {
+  gp_kernel k = F.k0;
+  k.outputscale = F.s;
+  for (int j = 0; j < 3; ++j) k.lengthscale[j] = F.k0.lengthscale[j] * F.c;
+  return k;
+}
+
+gp_status rebuild(FitState& F, int rank, cudaStream_t s) {
+  if (F.has_pc) { precond_free(F.pc); F.pc = Precond(); F.has_pc = false; }
+  if (F.built) { plan_free(F.pl); F.pl = Plan(); F.built = false; }
+  GPM_TRY(plan_build(F.pl, F.x, F.n, F.d, cur_kernel(F), s));
+  F.built = true;
+  if (rank > 0) {
+    GPM_TRY(precond_build(F.pc, F.pl, rank, s));
+    F.has_pc = true;
+  }
+  return GP_OK;
+}
+
+}  // namespace
+
+gp_status fit_alg1(const double* x, int64_t n, int d, const gp_kernel& k0, double sigma0,
+                   const double* y, const double* G, const double* W, int nprobe,
+                   const gp_fit_opts& o, gp_fit_result* out, cudaStream_t s) {
+  FitState F;
+  F.x = x; F.n = n; F.d = d; F.k0 = k0;
+  F.s = k0.outputscale; F.c = 1.0; F.sigma = sigma0;
+  struct Cleanup {
+    FitState* f;
+    ~Cleanup() {
+      if (f->has_pc) precond_free(f->pc);
+      if (f->built) plan_free(f->pl);
+    }
+  } cleanup{&F};
+  // host copies: x (n x d) and y for OLS / centring
+  std::vector<double> hx((size_t)n * d), hy((size_t)n);
+  GPM_CUDA(cudaMemcpyAsync(hx.data(), x, 8 * hx.size(), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaMemcpyAsync(hy.data(), y, 8 * hy.size(), cudaMemcpyDeviceToHost, s));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  const int nh = 1 + d;
+  std::vector<double> beta_ols;
+  {
+    std::vector<long double> G2(nh * nh, 0.0L), g2(nh, 0.0L);
+    for (int64_t i = 0; i < n; ++i) {
+      double h[4] = {1.0, 0, 0, 0};
+      for (int k = 0; k < d; ++k) h[1 + k] = hx[(size_t)i * d + k];
+      for (int a = 0; a < nh; ++a) {
+        g2[a] += (long double)h[a] * hy[i];
+        for (int b = 0; b < nh; ++b) G2[a * nh + b] += (long double)h[a] * h[b];
+      }
+    }
+    std::vector<double> Gd(nh * nh), gd(nh);
+    for (int a = 0; a < nh * nh; ++a) Gd[a] = (double)G2[a];
+    for (int a = 0; a < nh; ++a) gd[a] = (double)g2[a];
+    if (!solve_small(Gd, gd, nh, beta_ols))
+      return fail(GP_ERR_INVALID_ARG, "OLS: H^T H is singular");
+  }
+  DevBuf byc, ba;
+  GPM_TRY(byc.alloc(8 * (size_t)n));
+  GPM_TRY(ba.alloc(8 * (size_t)n));
+  GPM_TRY(rebuild(F, o.precond_rank, s));
+  int steps = 0;
+  double last_lml = 0.0, last_norm = 0.0;
+
+  auto descent = [&](const std::vector<double>& yc_host, int cap) -> gp_status {
+    GPM_CUDA(cudaMemcpyAsync(byc.ptr, yc_host.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+    int local = 0;
+    while (true) {
+      // GradDescStep: gradient of the LML at (s, c, sigma), ADAM ascent on (log s, log c)
+      gp_lml_result r{};
+      GPM_TRY(lml_eval(F.pl, F.has_pc ? &F.pc : nullptr, F.sigma * F.sigma, byc.as<double>(), G,
+                       W, nprobe, o.lanczos_iters, o.cg_rtol, &r, s));
+      if (!std::isfinite(r.grad[1]))
+        return fail(GP_ERR_UNSUPPORTED, "gp_fit needs the lengthscale gradient of this kernel");
+      last_lml = r.lml;
+      const double g[2] = {r.grad[0] * F.s, r.grad[1]};
+      ++F.t;
+      double th[2] = {std::log(F.s), std::log(F.c)};
+      for (int q = 0; q < 2; ++q) {
+        F.m[q] = 0.9 * F.m[q] + 0.1 * g[q];
+        F.v[q] = 0.999 * F.v[q] + 0.001 * g[q] * g[q];
+        const double mh = F.m[q] / (1.0 - std::pow(0.9, F.t));
+        const double vh = F.v[q] / (1.0 - std::pow(0.999, F.t));
+        th[q] += o.lr * mh / (std::sqrt(vh) + 1e-8);
+      }
+      F.s = std::exp(th[0]);
+      F.c = std::exp(th[1]);
+      last_norm = std::sqrt(g[0] * g[0] + g[1] * g[1]) / (double)n;
+      ++steps;
+      ++local;
+      // sigma update at the new (s, l): 1/N y^T (K(s/sigma_prev) + I)^-1 y
+      //   = sigma_prev^2 / N  y^T (K(s) + sigma_prev^2 I)^-1 y
+      GPM_TRY(rebuild(F, o.precond_rank, s));
+      {
+        std::vector<double> t2(1);
+        double yy = 0.0;
+        for (double v : yc_host) yy += v * v;
+        t2[0] = o.cg_rtol * o.cg_rtol * yy;
+        std::vector<double> hr(n);
+        DevBuf rb;
+        GPM_TRY(rb.alloc(8 * (size_t)n));
+        GPM_TRY(permute_vec(F.pl, byc.as<double>(), rb.as<double>(), true, s));
+        std::vector<int> it, st;
+        const int capcg = (int)std::min<int64_t>(std::max<int64_t>(1000, 20 * n), 200000);
+        GPM_TRY(mbcg_rank(F.pl, F.has_pc ? &F.pc : nullptr, F.sigma * F.sigma, rb.as<double>(), 1,
+                          capcg, t2, ba.as<double>(), nullptr, nullptr, it, st, nullptr, s));
+        if (st[0] != 1) return fail(GP_ERR_NOT_CONVERGED, "gp_fit: sigma-update CG failed");
+        std::vector<double> ha(n), hrr(n);
+        GPM_CUDA(cudaMemcpyAsync(ha.data(), ba.ptr, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+        GPM_CUDA(cudaMemcpyAsync(hrr.data(), rb.ptr, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+        GPM_CUDA(cudaStreamSynchronize(s));
+        long double q = 0.0L;
+        for (int64_t i = 0; i < n; ++i) q += (long double)hrr[i] * ha[i];
+        F.sigma = std::sqrt(F.sigma * F.sigma * (double)q / (double)n);
+      }
+      if (last_norm <= o.grad_tol || local >= cap) return GP_OK;
+    }
+  };
+
+  GPM_TRY(descent(centre(hy, hx, d, beta_ols), o.max_steps));
+  std::vector<double> beta_avg(nh, 0.0), beta_old = beta_ols, beta_gls = beta_ols;
+  int outer = 0;
+  while (outer < o.max_outer) {
+    // beta_GLS at the current parameters
+    DevBuf al;
+    GPM_TRY(al.alloc(8 * (size_t)n));
+    double bb[4] = {0, 0, 0, 0};
+    gp_cg_info info{};
+    GPM_TRY(cg_solve(F.pl, F.sigma * F.sigma, y, GP_MEAN_AFFINE, nullptr, 0, o.cg_rtol,
+                     (int)std::min<int64_t>(std::max<int64_t>(1000, 20 * n), 200000), al.as<double>(),
+                     bb, &info, s, F.has_pc ? &F.pc : nullptr));
+    for (int a = 0; a < nh; ++a) beta_gls[a] = bb[a];
+    ++outer;
+    for (int a = 0; a < nh; ++a)
+      beta_avg[a] = (double)(outer - 1) / outer * beta_avg[a] + beta_gls[a] / outer;
+    GPM_TRY(descent(centre(hy, hx, d, beta_avg), o.max_steps));
+    double ch = 0.0;
+    for (int a = 0; a < nh; ++a) ch += (beta_gls[a] - beta_old[a]) * (beta_gls[a] - beta_old[a]);
+    beta_old = beta_gls;
+    if (std::sqrt(ch) <= o.beta_tol) break;
+  }
+  out->kernel = cur_kernel(F);
+  out->sigma = F.sigma;
+  for (int a = 0; a < 4; ++a) out->beta[a] = a < nh ? beta_gls[a] : 0.0;
+  out->steps = steps;
+  out->outer = outer;
+  out->lml = last_lml;
+  out->grad_norm = last_norm;
+  return GP_OK;
+}
+
+}  // namespace gpm

@@ -34,7 +34,7 @@ def test_header_declares_the_boundary():
                  "gp_plan_set_option", "gp_version", "gp_kmvm_rank", "gp_permute",
                  "gp_kmvm_dlengthscale", "gp_cg_solve_pc", "gp_precond_create",
                  "gp_precond_factor", "gp_precond_solve", "gp_precond_logdet",
-                 "gp_precond_destroy", "gp_mbcg", "gp_lml"]:
+                 "gp_precond_destroy", "gp_mbcg", "gp_lml", "gp_fit"]:
         assert must in names, must
 
 

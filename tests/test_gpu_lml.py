@@ -211,3 +211,28 @@ def test_lml_errors(gpm):
     other = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1,)))
     with pytest.raises(gpm.GPError):
         other.cg_solve(to_dev(np.ones(200)), 0.1, precond=pc)
+
+
+@pytest.mark.parametrize("d,two_nu,form", [(1, 3, "l1"), (2, 1, "l1"), (2, 3, "product")])
+def test_fit_alg1_matches_oracle_trajectory(gpm, d, two_nu, form):
+    """Algorithm 1 with the same probes: a few ADAM steps, one GLS round -- the GPU and the
+    oracle follow the same trajectory (gradients agree to ~1e-7, ADAM is smooth in them)."""
+    rng = np.random.default_rng(60 + d)
+    n = 400
+    x = rng.random((n, d))
+    H = np.hstack([np.ones((n, 1)), x])
+    y = H @ np.array([1.0, 0.5, -0.3][:1 + d]) + np.sin(5 * x[:, 0]) + 0.2 * rng.standard_normal(n)
+    G = rng.standard_normal((8, n))
+    ell0 = [0.02, 0.2][:d] if d == 1 else [0.05, 0.05]
+    ro = _rank_order(x)
+    kw = dict(lr=0.05, max_steps=4, max_outer=1, grad_tol=1e-300, beta_tol=1e-300,
+              lanczos_iters=20, cg_rtol=1e-12)
+    got = gpm.fit(to_dev(x), gpm.Kernel(two_nu, tuple(ell0), 0.8, form=0 if form == "l1" else 1),
+                  0.5, to_dev(y), to_dev(G), **kw)
+    ref = ol.alg1_fit(x[ro], y[ro], H[ro], two_nu, form, ell0, 0.8, 0.5, G[:, ro].T, 20,
+                      lr=0.05, max_steps=4, max_outer=1, grad_tol=1e-300, beta_tol=1e-300)
+    assert got["steps"] == ref["steps"] == 8 and got["outer"] == ref["outer"] == 1
+    assert got["kernel"].outputscale == pytest.approx(ref["s"], rel=1e-6)
+    assert got["kernel"].lengthscale[0] == pytest.approx(ell0[0] * ref["c"], rel=1e-6)
+    assert got["sigma"] == pytest.approx(ref["sigma"], rel=1e-6)
+    assert np.allclose(got["beta"], ref["beta"], rtol=1e-6, atol=1e-8)
