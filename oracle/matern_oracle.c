@@ -21,7 +21,7 @@
  *   k_{3/2}(r) = (1 + sqrt3 r) exp(-sqrt3 r)
  *   k_{5/2}(r) = (1 + sqrt5 r + 5/3 r^2) exp(-sqrt5 r)
  *
- * and the two multivariate forms (PAPER.md L414-422 [eq product_kernel,
+ * (and k_{7/2}, k_{9/2} of L1276-1277) and the two multivariate forms (PAPER.md L414-422 [eq product_kernel,
  * L1_kernel]; §2.3):
  *
  *   L1:      Ktilde(x,x') = s^2 k( sum_k |x_k - x'_k| / l_k )
@@ -47,18 +47,33 @@ static double profile(int two_nu, double r)
     case 1: return exp(-r);
     case 3: { const double s = sqrt(3.0) * r; return (1.0 + s) * exp(-s); }
     case 5: { const double s = sqrt(5.0) * r; return (1.0 + s + (5.0 / 3.0) * r * r) * exp(-s); }
+    case 7: {   /* PAPER.md L1276 [eq matern_7_2] */
+        const double s = sqrt(7.0) * r;
+        return (1.0 + s + (14.0 / 5.0) * r * r + (7.0 * sqrt(7.0) / 15.0) * r * r * r) * exp(-s);
+    }
+    case 9: {   /* PAPER.md L1277 [eq matern_9_2] */
+        const double s = 3.0 * r;
+        return (1.0 + 3.0 * r + (27.0 / 7.0) * r * r + (18.0 / 7.0) * r * r * r +
+                (27.0 / 35.0) * r * r * r * r) * exp(-s);
+    }
     default: return NAN;
     }
 }
 
-/* k'_nu(r), the first derivative of the profile (PAPER.md L1320-1322 [eq dmatern12_dl,
- * dmatern32_dl, dmatern52_dl]). */
+/* k'_nu(r), the first derivative of the profile (PAPER.md L1320-1324 [eq dmatern12_dl ..
+ * dmatern92_dl]). */
 static double dprofile(int two_nu, double r)
 {
     switch (two_nu) {
     case 1: return -exp(-r);
     case 3: return -(3.0 * r) * exp(-sqrt(3.0) * r);
     case 5: return -((5.0 / 3.0) * r + (5.0 * sqrt(5.0) / 3.0) * r * r) * exp(-sqrt(5.0) * r);
+    case 7:   /* PAPER.md L1323 [eq dmatern72_dl] */
+        return -((7.0 / 5.0) * r + (7.0 * sqrt(7.0) / 5.0) * r * r + (49.0 / 15.0) * r * r * r) *
+               exp(-sqrt(7.0) * r);
+    case 9:   /* PAPER.md L1324 [eq dmatern92_dl] */
+        return -((9.0 / 7.0) * r + (27.0 / 7.0) * r * r + (162.0 / 35.0) * r * r * r +
+                 (81.0 / 35.0) * r * r * r * r) * exp(-3.0 * r);
     default: return NAN;
     }
 }

@@ -89,9 +89,11 @@ def test_explicit_coeffs_match_paper_table():
     assert explicit_coeffs(2) == [1, 1, Fraction(1, 3)]
     # k_{7/2}: 1 + sqrt7 u + 14/5 u^2 + 7 sqrt7/15 u^3 -> in s = sqrt7 u: 1, 1, 2/5, 1/15
     assert explicit_coeffs(3) == [1, 1, Fraction(2, 5), Fraction(1, 15)]
+    # k_{9/2}: 1 + 3u + 27/7 u^2 + 18/7 u^3 + 27/35 u^4 -> in s = 3u: 1, 1, 3/7, 2/21, 1/105
+    assert explicit_coeffs(4) == [1, 1, Fraction(3, 7), Fraction(2, 21), Fraction(1, 105)]
 
 
-@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
 def test_profile_against_bessel_definition(two_nu):
     for r in [0.0, 1e-3, 0.05, 0.3, 1.0, 2.5, 7.0, 30.0]:
         ref = float(bessel_profile(two_nu, r))
@@ -167,7 +169,7 @@ def test_product_kronecker_tensor_grid(two_nu, d):
 
 
 @pytest.mark.parametrize("form", ["l1", "product"])
-@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
 @pytest.mark.parametrize("d", [1, 2, 3])
 def test_bruteforce_mpmath(form, two_nu, d):
     """Tiny N: oracle vs a 40-digit dense sum built on the Bessel definition."""
@@ -343,7 +345,7 @@ def bessel_dprofile_scaled(two_nu, r, dps=50):
         return -r * mp.diff(lambda t: bessel_profile(two_nu, t, 3 * dps), r)
 
 
-@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
 def test_dprofile_against_bessel_derivative(two_nu):
     for r in [0.0, 1e-3, 0.05, 0.3, 1.0, 2.5, 7.0, 30.0]:
         ref = float(bessel_dprofile_scaled(two_nu, r))
@@ -352,7 +354,7 @@ def test_dprofile_against_bessel_derivative(two_nu):
         assert got == pytest.approx(ref, rel=rel, abs=1e-300), (two_nu, r)
 
 
-@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
 @pytest.mark.parametrize("d", [1, 2, 3])
 def test_dkmvm_bruteforce_lengthscale_derivative(two_nu, d):
     """Tiny N: l dK/dl v (every l_k scaled together) vs the 40-digit derivative
