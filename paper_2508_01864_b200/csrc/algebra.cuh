@@ -12,7 +12,7 @@
 //   read target    e^{-beta} sum_q a_q sum_{m<=q} C(q,m) beta^{q-m} M_m
 //
 // with the profile k(s) = sum_q a_q s^q e^{-s} of nu = P + 1/2 in scaled coordinates
-// (P:1282 [eq matern_explicit]: a = [1], [1,1], [1,1,1/3]).  Advances compose,
+// (P:1282 [eq matern_explicit]: a = [1], [1,1], [1,1,1/3], ...).  Advances compose,
 // S(a)S(b) = S(a+b), so (span, moments) is an associative scan monoid; this is the
 // "fast sum updating" of P:326-337 [§2.1] evaluated in a numerically safe basis.
 //
@@ -23,22 +23,41 @@
 
 namespace gpm {
 
-template <int P> struct Prof;
-template <> struct Prof<0> { __host__ __device__ static constexpr double a(int) { return 1.0; } };
-template <> struct Prof<1> { __host__ __device__ static constexpr double a(int) { return 1.0; } };
-template <> struct Prof<2> {
-  __host__ __device__ static constexpr double a(int q) { return q == 2 ? (1.0 / 3.0) : 1.0; }
-};
-
-__host__ __device__ constexpr double binom(int q, int m) {
-  // q <= 2 in this library
-  return (m == 0 || m == q) ? 1.0 : (q == 2 && m == 1 ? 2.0 : 1.0);
+// Small exact tables (literal constants, no loops or divisions at run time: every use sits
+// in a fully unrolled loop, so each call folds to one immediate).
+// Binomial C(q, m), q <= 6.
+__host__ __device__ __forceinline__ constexpr double binom(int q, int m) {
+  return (m < 0 || m > q) ? 0.0
+         : (m == 0 || m == q) ? 1.0
+         : (m == 1 || m == q - 1) ? double(q)
+         : q == 4 ? 6.0
+         : q == 5 ? 10.0
+         : (m == 3 ? 20.0 : 15.0);   // q == 6
+}
+// Matern coefficients of nu = p + 1/2 in scaled distance s = sqrt(2p+1) |u| (P:1282
+// [eq matern_explicit]: a_q = C(p,q) (2p-q)! / (2p)! 2^q), p <= 4: [1], [1,1], [1,1,1/3],
+// [1,1,2/5,1/15], [1,1,3/7,2/21,1/105]; zero outside 0..p.
+__host__ __device__ __forceinline__ constexpr double mcoef(int p, int q) {
+  return (q < 0 || q > p) ? 0.0
+         : q <= 1 ? 1.0
+         : p == 2 ? 1.0 / 3.0
+         : p == 3 ? (q == 2 ? 2.0 / 5.0 : 1.0 / 15.0)
+         : (q == 2 ? 3.0 / 7.0 : q == 3 ? 2.0 / 21.0 : 1.0 / 105.0);   // p == 4
 }
 
-// Advance a (P+1)-moment vector by D (E = e^{-D}).  In place, high q first.  P <= 3.
+// Advance a (P+1)-moment vector by D (E = e^{-D}).  In place, high q first.
 template <int P>
 __device__ __forceinline__ void advance(double* M, double D, double E) {
-  if constexpr (P == 3) {
+  if constexpr (P > 3) {
+    // M'_q = E sum_{m<=q} C(q,m) D^{q-m} M_m, Horner in D; q descending keeps M_m (m < q)
+#pragma unroll
+    for (int q = P; q >= 0; --q) {
+      double acc = M[0];
+#pragma unroll
+      for (int m = 1; m <= q; ++m) acc = fma(acc, D, binom(q, m) * M[m]);
+      M[q] = E * acc;
+    }
+  } else if constexpr (P == 3) {
     // M3 + 3D M2 + 3D^2 M1 + D^3 M0 = M3 + D (3 M2 + D (3 M1 + D M0))
     const double a = fma(D, M[0], M[1]);
     const double b = fma(D, fma(D, M[0], 3.0 * M[1]), 3.0 * M[2]);
@@ -71,7 +90,20 @@ __device__ __forceinline__ void advance_add(double* A, double D, double E, const
 // sum_q a_q sum_{m<=q} C(q,m) beta^{q-m} R_m   (without the e^{-beta} factor)
 template <int P>
 __device__ __forceinline__ double read_poly(const double* R, double beta) {
-  if constexpr (P == 2) {
+  if constexpr (P > 2) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q <= P; ++q) {
+      double t = 0.0, bp = 1.0;
+#pragma unroll
+      for (int m = q; m >= 0; --m) {
+        t = fma(binom(q, m) * bp, R[m], t);
+        bp *= beta;
+      }
+      acc = fma(mcoef(P, q), t, acc);
+    }
+    return acc;
+  } else if constexpr (P == 2) {
     // a0 R0 + a1 (R1 + b R0) + a2 (R2 + 2 b R1 + b^2 R0)
     const double b = beta;
     return R[0] + (R[1] + b * R[0]) + (1.0 / 3.0) * fma(b * b, R[0], fma(2.0 * b, R[1], R[2]));
@@ -85,7 +117,12 @@ __device__ __forceinline__ double read_poly(const double* R, double beta) {
 // sum_q a_q R_q  (beta = 0)
 template <int P>
 __device__ __forceinline__ double read0(const double* R) {
-  if constexpr (P == 2) return fma(1.0 / 3.0, R[2], R[0] + R[1]);
+  if constexpr (P > 2) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = P; q >= 0; --q) acc = fma(mcoef(P, q), R[q], acc);
+    return acc;
+  } else if constexpr (P == 2) return fma(1.0 / 3.0, R[2], R[0] + R[1]);
   else if constexpr (P == 1) return R[0] + R[1];
   else return R[0];
 }
@@ -96,14 +133,9 @@ __device__ __forceinline__ double read0(const double* R) {
 //   g(s) = -s k'(s) = sum_m b_m s^m e^{-s},  b_m = a_{m-1} - m a_m   (moments m <= PM),
 // so that dK/d(log l) = varsigma^2 g(s): P:1309 [eq dkernel_dl] with the closed forms
 // P:1321-1323 (nu=1/2: s e^{-s}; 3/2: s^2 e^{-s}; 5/2: (s^2 + s^3)/3 e^{-s}).
-__host__ __device__ constexpr double rcoef(int PM, int KIND, int q) {
-  return KIND == 0 ? (q == 2 && PM == 2 ? 1.0 / 3.0 : (q <= PM ? 1.0 : 0.0))
-                   : (PM == 1 ? (q == 1 ? 1.0 : 0.0)
-                      : PM == 2 ? (q == 2 ? 1.0 : 0.0)
-                                : (q >= 2 ? 1.0 / 3.0 : 0.0));
-}
-__host__ __device__ constexpr double binom3(int q, int m) {
-  return (m == 0 || m == q) ? 1.0 : (q == 2 ? 2.0 : (q == 3 ? 3.0 : 1.0));
+// KIND 0: a_q of nu = PM + 1/2; KIND 1: b_q = a_{q-1} - q a_q of nu = PM - 1/2 (g = -s k'(s))
+__host__ __device__ __forceinline__ constexpr double rcoef(int PM, int KIND, int q) {
+  return KIND == 0 ? mcoef(PM, q) : mcoef(PM - 1, q - 1) - q * mcoef(PM - 1, q);
 }
 // sum_q c_q R_q
 template <int PM, int KIND>
@@ -113,7 +145,14 @@ __device__ __forceinline__ double readc0(const double* R) {
   } else {
     if constexpr (PM == 1) return R[1];
     else if constexpr (PM == 2) return R[2];
-    else return (1.0 / 3.0) * (R[2] + R[3]);
+    else if constexpr (PM == 3) return (1.0 / 3.0) * (R[2] + R[3]);
+    else {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = PM; q >= 0; --q)
+        if (rcoef(PM, 1, q) != 0.0) acc = fma(rcoef(PM, 1, q), R[q], acc);
+      return acc;
+    }
   }
 }
 // sum_q c_q sum_{m<=q} C(q,m) beta^{q-m} R_m   (without e^{-beta})
@@ -129,7 +168,7 @@ __device__ __forceinline__ double readc_poly(const double* R, double beta) {
         double t = 0.0, bp = 1.0;
 #pragma unroll
         for (int m = q; m >= 0; --m) {   // sum_m C(q,m) beta^{q-m} R_m
-          t = fma(binom3(q, m) * bp, R[m], t);
+          t = fma(binom(q, m) * bp, R[m], t);
           bp *= beta;
         }
         acc = fma(rcoef(PM, KIND, q), t, acc);

@@ -506,7 +506,7 @@ gp_status d1_prepare(Plan& pl) {
       pl.d1_grid = (int)g;
       pl.d1_chunk = chunk;
       pl.d1_path = 1;
-      GPM_TRY(pl.aggs.alloc(96 * 2 * (size_t)g));   // D1Pub records x 2 (apply_d1_fast.cu)
+      GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)g));   // D1Pub records x 2 (apply_d1_fast.cu)
       GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
       GPM_TRY(pl.bar.alloc(64));
       GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));
@@ -548,6 +548,8 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   if (pl.d1_path == 1) return df_launch(pl, v, out, nrhs, user_order, s, kind);
   if (kind != 0)
     return fail(GP_ERR_UNSUPPORTED, "lengthscale-gradient MVM for d=1 needs n <= #SMs x 6912");
+  if (pl.P > 2)
+    return fail(GP_ERR_UNSUPPORTED, "nu >= 7/2 in d=1 needs n <= #SMs x 6912 (single-sub-tile path)");
   const int64_t vs = user_order ? pl.n_src : pl.n, os = user_order ? pl.n - pl.tgt_off : pl.n;
   for (int c = 0; c + 1 < nrhs; ++c)
     GPM_TRY(d1_launch(pl, v + c * vs, out + c * os, 1, user_order, s, 0));

@@ -118,8 +118,8 @@ __device__ __forceinline__ SF<P> sf_ld(const double* p) {
 }
 
 // Published chunk aggregate: D, E, F[3], B[3] and the launch epoch (written last).
-struct __align__(16) D1Pub {   // 96 B (apply_d1.cu allocates 96 x 2 x grid)
-  double v[10];   // D, E, F[4], B[4]
+struct __align__(16) D1Pub {   // 128 B (apply_d1.cu allocates 128 x 2 x grid)
+  double v[14];   // D, E, F[6], B[6]  (moment order <= 5)
   unsigned long long epoch;
   unsigned long long pad;
 };
@@ -151,10 +151,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
   int* s_pi = reinterpret_cast<int*>(s_e + SUB);       // SUB + 8
   __shared__ uint64_t mbar[DF_NPART];
   __shared__ double s_tab[64];
-  __shared__ double s_wf[NW][6], s_wb[NW][6];
-  __shared__ double s_tot[2][6];
-  __shared__ double s_part[2][8][6];
-  __shared__ double s_carry[2][4];
+  constexpr int NSF = P + 3;   // D, E, M[0..P]
+  __shared__ double s_wf[NW][NSF], s_wb[NW][NSF];
+  __shared__ double s_tot[2][NSF];
+  __shared__ double s_part[2][8][NSF];
+  __shared__ double s_carry[2][P + 1];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * a.chunk;
@@ -268,16 +269,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
       const double dl = s_t[j], e = s_e[j], u = s_u[j];
       Dc += dl;
       Ec *= e;
-      const double w = u * Ec;
-      B.M[0] += w;
-      if (P >= 1) {
-        const double wd = w * Dc;
-        B.M[P >= 1 ? 1 : 0] += wd;
-        if (P >= 2) {
-          const double wdd = wd * Dc;
-          B.M[P >= 2 ? 2 : 0] += wdd;
-          if (P >= 3) B.M[P >= 3 ? 3 : 0] = fma(wdd, Dc, B.M[P >= 3 ? 3 : 0]);
-        }
+      double wq = u * Ec;                  // u Dc^q e^{-Dc}, q = 0..P
+#pragma unroll
+      for (int q = 0; q <= P; ++q) {
+        B.M[q] += wq;
+        wq *= Dc;
       }
       advance<P>(F.M, dl, e);
       F.M[0] += u;
@@ -326,9 +322,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
     me->v[0] = s_tot[0][0];
     me->v[1] = s_tot[0][1];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      me->v[2 + q] = q <= P ? s_tot[0][2 + q] : 0.0;
-      me->v[6 + q] = q <= P ? s_tot[1][2 + q] : 0.0;
+    for (int q = 0; q <= P; ++q) {
+      me->v[2 + q] = s_tot[0][2 + q];
+      me->v[8 + q] = s_tot[1][2 + q];
     }
     __threadfence();
   }
@@ -352,7 +348,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
         X.D = __ldcg(&o->v[0]);
         X.E = __ldcg(&o->v[1]);
 #pragma unroll
-        for (int q = 0; q <= P; ++q) X.M[q] = __ldcg(&o->v[(fw ? 2 : 6) + q]);
+        for (int q = 0; q <= P; ++q) X.M[q] = __ldcg(&o->v[(fw ? 2 : 8) + q]);
       }
 #pragma unroll 1
       for (int off = 1; off < 32; off <<= 1) {
@@ -446,7 +442,7 @@ static size_t df_smem() {
 
 struct DFShape {
   int block, items;
-  const void* fn[6];   // [KIND * 3 + p]: KIND 0 moment order p, KIND 1 moment order p + 1
+  const void* fn[10];  // [KIND * 5 + p]: KIND 0 moment order p, KIND 1 moment order p + 1
   size_t smem;
 };
 
@@ -458,9 +454,13 @@ static DFShape make_shape() {
   s.fn[0] = (const void*)k_d1_fast<0, 0, BLOCK, ITEMS>;
   s.fn[1] = (const void*)k_d1_fast<1, 0, BLOCK, ITEMS>;
   s.fn[2] = (const void*)k_d1_fast<2, 0, BLOCK, ITEMS>;
-  s.fn[3] = (const void*)k_d1_fast<1, 1, BLOCK, ITEMS>;
-  s.fn[4] = (const void*)k_d1_fast<2, 1, BLOCK, ITEMS>;
-  s.fn[5] = (const void*)k_d1_fast<3, 1, BLOCK, ITEMS>;
+  s.fn[3] = (const void*)k_d1_fast<3, 0, BLOCK, ITEMS>;
+  s.fn[4] = (const void*)k_d1_fast<4, 0, BLOCK, ITEMS>;
+  s.fn[5] = (const void*)k_d1_fast<1, 1, BLOCK, ITEMS>;
+  s.fn[6] = (const void*)k_d1_fast<2, 1, BLOCK, ITEMS>;
+  s.fn[7] = (const void*)k_d1_fast<3, 1, BLOCK, ITEMS>;
+  s.fn[8] = (const void*)k_d1_fast<4, 1, BLOCK, ITEMS>;
+  s.fn[9] = (const void*)k_d1_fast<5, 1, BLOCK, ITEMS>;
   s.smem = df_smem<BLOCK, ITEMS>();
   return s;
 }
@@ -476,7 +476,7 @@ static gp_status df_init() {
   g_shapes[2] = make_shape<768, 9>();
   g_shapes[3] = make_shape<1024, 7>();
   for (auto& s : g_shapes)
-    for (int p = 0; p < 6; ++p)
+    for (int p = 0; p < 10; ++p)
       GPM_CUDA(cudaFuncSetAttribute(s.fn[p], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)s.smem));
   if (const char* e = getenv("GPM_D1_SHAPE")) g_default_shape = std::max(0, std::min(3, atoi(e)));
@@ -533,7 +533,7 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   cfg.attrs = at;
   cfg.numAttrs = pl.d1_pdl ? 2 : 1;
   void* args[] = {&a};
-  GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[kind * 3 + pl.P], args));
+  GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[kind * 5 + pl.P], args));
   return GP_OK;
 }
 

@@ -92,17 +92,14 @@ template <class A, int D>
 __device__ __forceinline__ double kval(double d1, double d2, double d3, const double* tab) {
   constexpr int P = A::P;
   if constexpr (!A::PROD) {
+    // L1: sum_q c_q s^q e^{-s} with the read coefficients of the algebra (Matern a_q for
+    // KIND 0, gradient b_q = a_{q-1} - q a_q for KIND 1), Horner in s
     const double s = D == 3 ? (d1 + d2) + d3 : d1 + d2;
     const double e = fexp_neg(s, tab);
-    if constexpr (A::KIND == 0) {
-      if constexpr (P == 0) return e;
-      else if constexpr (P == 1) return e * (1.0 + s);
-      else return e * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0);
-    } else {   // gradient profile g(s) = -s k'(s) (algebra.cuh rcoef)
-      if constexpr (P == 1) return e * s;
-      else if constexpr (P == 2) return e * (s * s);
-      else return e * ((1.0 / 3.0) * (s * s) * (1.0 + s));
-    }
+    double poly = rcoef(P, A::KIND, P);
+#pragma unroll
+    for (int q = P - 1; q >= 0; --q) poly = fma(poly, s, rcoef(P, A::KIND, q));
+    return e * poly;
   } else {
     const double e = fexp_neg(d1 + d2, tab);
     if constexpr (A::KIND == 0) {
@@ -960,12 +957,15 @@ template <class A>
 static cudaError_t lv_set_attrs() {
   cudaError_t e;
   const int fused = (int)lv_smem_fused();
-  if ((e = cudaFuncSetAttribute(k_low2<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_low3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_mid3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
-    return e;
+  if constexpr (A::NCH == 2) {   // d = 2
+    if ((e = cudaFuncSetAttribute(k_low2<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
+      return e;
+  } else {                       // d = 3
+    if ((e = cudaFuncSetAttribute(k_low3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
+      return e;
+    if ((e = cudaFuncSetAttribute(k_mid3<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused)))
+      return e;
+  }
   if ((e = cudaFuncSetAttribute(k_cp<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(CpSmem))))
     return e;
@@ -1132,17 +1132,20 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     *launches += 1;
   }
   // fused low levels (writes acc for every point: no memset needed)
-  if (pl.d == 2)
+  if constexpr (A::NCH == 2) {
     k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
-  else
-    k_low3<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
-  *launches += 1;
-  GPM_CUDA(cudaGetLastError());
-  if (pl.d == 3 && L > LV_LOGTILE) {   // d = 3: every outer level l1 > 10 (inner l2 <= 10)
-    g.l1 = LV_LOGTILE + 1;
-    k_mid3<A><<<dim3(tiles, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), s>>>(g);
     *launches += 1;
     GPM_CUDA(cudaGetLastError());
+  } else {
+    k_low3<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
+    *launches += 1;
+    GPM_CUDA(cudaGetLastError());
+    if (L > LV_LOGTILE) {   // d = 3: every outer level l1 > 10 (inner l2 <= 10)
+      g.l1 = LV_LOGTILE + 1;
+      k_mid3<A><<<dim3(tiles, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), s>>>(g);
+      *launches += 1;
+      GPM_CUDA(cudaGetLastError());
+    }
   }
   if (hp) {   // carried-pass apply (needs the aggregates)
     GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
@@ -1195,35 +1198,53 @@ size_t level_pt_bytes() { return sizeof(Pt4); }
 
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
+  const int P = pl.P;
   if (kind != 0) {   // lengthscale gradient: moment order p + 1
     if (prod) {        // d = 2 product form, nu <= 3/2 ((p+2)^2 moments per channel)
-      if (pl.d != 2 || pl.P > 1)
+      if (pl.d != 2 || P > 1)
         return fail(GP_ERR_UNSUPPORTED, "product-form lengthscale gradient: d = 2, nu <= 3/2 only");
-      if (pl.P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
+      if (P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
       return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
     }
     if (pl.d == 2) {
-      if (pl.P == 0) return lv_run<Alg<1, 2, false, 1>>(pl, nrhs, s, launches);
-      if (pl.P == 1) return lv_run<Alg<2, 2, false, 1>>(pl, nrhs, s, launches);
-      return lv_run<Alg<3, 2, false, 1>>(pl, nrhs, s, launches);
+      switch (P) {
+        case 0: return lv_run<Alg<1, 2, false, 1>>(pl, nrhs, s, launches);
+        case 1: return lv_run<Alg<2, 2, false, 1>>(pl, nrhs, s, launches);
+        case 2: return lv_run<Alg<3, 2, false, 1>>(pl, nrhs, s, launches);
+        case 3: return lv_run<Alg<4, 2, false, 1>>(pl, nrhs, s, launches);
+        default: return lv_run<Alg<5, 2, false, 1>>(pl, nrhs, s, launches);
+      }
     }
-    if (pl.P == 0) return lv_run<Alg<1, 4, false, 1>>(pl, nrhs, s, launches);
-    if (pl.P == 1) return lv_run<Alg<2, 4, false, 1>>(pl, nrhs, s, launches);
-    return lv_run<Alg<3, 4, false, 1>>(pl, nrhs, s, launches);
+    switch (P) {
+      case 0: return lv_run<Alg<1, 4, false, 1>>(pl, nrhs, s, launches);
+      case 1: return lv_run<Alg<2, 4, false, 1>>(pl, nrhs, s, launches);
+      case 2: return lv_run<Alg<3, 4, false, 1>>(pl, nrhs, s, launches);
+      case 3: return lv_run<Alg<4, 4, false, 1>>(pl, nrhs, s, launches);
+      default:
+        return fail(GP_ERR_UNSUPPORTED, "d=3 lengthscale gradient: nu <= 7/2 (4 x 5 moments)");
+    }
   }
   if (pl.d == 2) {
     if (!prod) {
-      if (pl.P == 0) return lv_run<Alg<0, 2, false>>(pl, nrhs, s, launches);
-      if (pl.P == 1) return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
-      return lv_run<Alg<2, 2, false>>(pl, nrhs, s, launches);
+      switch (P) {
+        case 0: return lv_run<Alg<0, 2, false>>(pl, nrhs, s, launches);
+        case 1: return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
+        case 2: return lv_run<Alg<2, 2, false>>(pl, nrhs, s, launches);
+        case 3: return lv_run<Alg<3, 2, false>>(pl, nrhs, s, launches);
+        default: return lv_run<Alg<4, 2, false>>(pl, nrhs, s, launches);
+      }
     }
-    if (pl.P == 0) return lv_run<Alg<0, 2, true>>(pl, nrhs, s, launches);
-    if (pl.P == 1) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
+    if (P == 0) return lv_run<Alg<0, 2, true>>(pl, nrhs, s, launches);
+    if (P == 1) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
     return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
   }
-  if (pl.P == 0) return lv_run<Alg<0, 4, false>>(pl, nrhs, s, launches);
-  if (pl.P == 1) return lv_run<Alg<1, 4, false>>(pl, nrhs, s, launches);
-  return lv_run<Alg<2, 4, false>>(pl, nrhs, s, launches);
+  switch (P) {
+    case 0: return lv_run<Alg<0, 4, false>>(pl, nrhs, s, launches);
+    case 1: return lv_run<Alg<1, 4, false>>(pl, nrhs, s, launches);
+    case 2: return lv_run<Alg<2, 4, false>>(pl, nrhs, s, launches);
+    case 3: return lv_run<Alg<3, 4, false>>(pl, nrhs, s, launches);
+    default: return lv_run<Alg<4, 4, false>>(pl, nrhs, s, launches);
+  }
 }
 
 int64_t level_tiles(int64_t n) { return (n + LV_TILE - 1) / LV_TILE; }

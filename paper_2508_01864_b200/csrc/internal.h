@@ -43,10 +43,11 @@ struct D1Agg {
   double B[3];      // backward moments, referenced one point before its first point
 };
 
-// Level-pass tile aggregate (one direction), up to 4 channels x 4 moments.
+// Level-pass tile aggregate (one direction): up to 4 channels x 5 moments (L1, d = 3,
+// nu = 9/2 or the nu = 7/2 gradient) or 2 channels x 9 mixed moments (product, d = 2).
 struct LvAgg {
   double D, E;
-  double M[18];
+  double M[20];
   int flag;
   int pad;
 };

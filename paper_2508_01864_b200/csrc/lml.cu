@@ -19,6 +19,7 @@
 #include <cmath>
 #include <vector>
 
+#include "algebra.cuh"
 #include "internal.h"
 
 namespace gpm {
@@ -48,9 +49,9 @@ inline int lgrid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>
 // profile k(s) = sum_q a_q s^q e^{-s}, s = scaled distance; os2 = outputscale^2
 __device__ __forceinline__ double prof(int P, double s) {
   const double e = exp(-s);
-  if (P == 0) return e;
-  if (P == 1) return e * (1.0 + s);
-  return e * fma(s, fma(s, 1.0 / 3.0, 1.0), 1.0);
+  double poly = 0.0;
+  for (int q = P; q >= 0; --q) poly = fma(poly, s, mcoef(P, q));
+  return e * poly;
 }
 
 // piv[i] holds the pivot rank; Lp[j] = L[j*n + piv] for j < i (gathered first)
@@ -704,7 +705,9 @@ gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const
   GPM_CUDA(cudaMemcpyAsync(P0, X, 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));   // col 0: a
   // (3) K [a, P^-1 z] and l dK/dl [a, P^-1 z]
   GPM_TRY(apply_rank(pl, P0, KP, nc, s, 0));
-  const bool has_dl = pl.d == 1 || pl.form == GP_FORM_L1 || (pl.d == 2 && pl.P <= 1);
+  const bool has_dl = (pl.d == 1 || (pl.d == 2 && pl.form == GP_FORM_L1)) ||
+                      (pl.d == 3 && pl.form == GP_FORM_L1 && pl.P <= 3) ||
+                      (pl.d == 2 && pl.form == GP_FORM_PRODUCT && pl.P <= 1);
   if (has_dl) GPM_TRY(apply_rank(pl, P0, DP, nc, s, 1));
   // (4) dots: col 0: a.Ka, a.dKa, a.a, r.a ; probe c: x_c.K p_c, x_c.dK p_c, x_c.p_c
   //     (x_c = A^-1 z_c from Lanczos, p_c = P^-1 z_c)

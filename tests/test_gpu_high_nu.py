@@ -1,0 +1,69 @@
+"""GPU parity for nu = 7/2, 9/2: the same
+decomposition with p = 3, 4 moments (generic binomial advance / read), L1 form for
+d = 1..3; gradients (p + 1 moments) for d = 1, 2 and d = 3 up to nu = 7/2."""
+import numpy as np
+import pytest
+
+import workloads as W
+from gpu_helpers import check_rows, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _pts(n, d, seed, ties=False):
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, d))
+    if ties:
+        x = np.floor(x * 17) / 17
+        if n > 4:
+            x[n // 2] = x[1]
+    return x
+
+
+@pytest.mark.parametrize("two_nu", [7, 9])
+@pytest.mark.parametrize("d,n", [(1, 1), (1, 7), (1, 1000), (1, 7681), (1, 20000), (2, 3),
+                                 (2, 2049), (2, 5000), (3, 64), (3, 2049), (3, 5000)])
+@pytest.mark.parametrize("grad", [False, True])
+def test_high_nu_all_rows(gpm, two_nu, d, n, grad):
+    x = _pts(n, d, 31 * n + two_nu + d, ties=(n % 2 == 1))
+    v = np.random.default_rng(n + two_nu).standard_normal(n)
+    ell = (0.08, 0.2, 0.15)[:d]
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.2, form=0))
+    if grad and d == 3 and two_nu == 9:
+        with pytest.raises(gpm.GPError) as e:
+            plan.kmvm_dlengthscale(to_dev(v))
+        assert e.value.name == "UNSUPPORTED"
+        return
+    out = (plan.kmvm_dlengthscale(to_dev(v)) if grad else plan.kmvm(to_dev(v))).cpu().numpy()
+    check_rows(out, x, v, two_nu, "l1", ell, 1.2, grad=grad,
+               what=f"nu={two_nu}/2 d={d} n={n} grad={grad}")
+
+
+@pytest.mark.parametrize("two_nu", [7, 9])
+def test_high_nu_config2_and_multilevel(gpm, two_nu):
+    c = W.CONFIGS[2]
+    x = W.config_points(c)
+    v = W.config_vector(c, 0)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, c.ell))
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    rows = W.sample_rows(x, 256)
+    check_rows(out, x, v, two_nu, "l1", c.ell, 1.0, rows=rows, what=f"config2 nu={two_nu}/2")
+    x3 = _pts(150000, 3, 9 + two_nu)
+    v3 = np.random.default_rng(two_nu).standard_normal(150000)
+    p3 = gpm.Plan(to_dev(x3), gpm.Kernel(two_nu, (0.1, 0.1, 0.1)))
+    o3 = p3.kmvm(to_dev(v3)).cpu().numpy()
+    check_rows(o3, x3, v3, two_nu, "l1", (0.1, 0.1, 0.1), 1.0, rows=W.sample_rows(x3, 128),
+               what=f"d3 multilevel nu={two_nu}/2")
+
+
+def test_high_nu_unsupported(gpm):
+    x = _pts(300, 2, 1)
+    with pytest.raises(gpm.GPError) as e:
+        gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1), form=1))
+    assert e.value.name == "UNSUPPORTED"
+    x1 = _pts(60000, 1, 2)
+    p1 = gpm.Plan(to_dev(x1), gpm.Kernel(7, (0.02,)))
+    p1.set_option(0, 2)            # multi-sub-tile path: nu <= 5/2 only
+    with pytest.raises(gpm.GPError) as e:
+        p1.kmvm(to_dev(np.ones(60000)))
+    assert e.value.name == "UNSUPPORTED"
