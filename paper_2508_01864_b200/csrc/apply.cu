@@ -99,7 +99,8 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
   const size_t need = (size_t)nrhs * pl.n;
   if (pl.acc.bytes < sizeof(double) * need) GPM_TRY(pl.acc.alloc(sizeof(double) * need));
   if (pl.pts.bytes < level_pt_bytes() * need) GPM_TRY(pl.pts.alloc(level_pt_bytes() * need));
-  const size_t ag = sizeof(LvAgg) * 2 * (size_t)level_tiles(pl.n) * nrhs *
+  // tile aggregates and (k_cp_carry) tile carries, same layout
+  const size_t ag = 2 * sizeof(LvAgg) * 2 * (size_t)level_tiles(pl.n) * nrhs *
                    std::max(1, pl.hp_npass);
   if (pl.aggs.bytes < ag) GPM_TRY(pl.aggs.alloc(ag));
   const size_t pb = sizeof(double) * (size_t)std::max(1, level_nparts(pl)) * pl.n * nrhs;

@@ -175,6 +175,15 @@ __device__ __forceinline__ CSt<NS> cs_shfl(const CSt<NS>& s, int off, bool up) {
   return r;
 }
 template <int NS>
+__device__ __forceinline__ CSt<NS> cs_bcast(const CSt<NS>& s, int src) {
+  CSt<NS> r;
+  r.D = __shfl_sync(0xffffffffu, s.D, src);
+  r.E = __shfl_sync(0xffffffffu, s.E, src);
+#pragma unroll
+  for (int i = 0; i < NS; ++i) r.M[i] = __shfl_sync(0xffffffffu, s.M[i], src);
+  return r;
+}
+template <int NS>
 __device__ __forceinline__ void cs_put(LvAgg* g, const CSt<NS>& s) {
   g->D = s.D; g->E = s.E;
 #pragma unroll
@@ -700,44 +709,57 @@ struct CpSmem {
 };
 constexpr unsigned CP_STAGE_BYTES = 36u * LV_TILE;
 
-// Tile carries of one column: warps 0-1 fold the forward aggregates of the node's tiles
-// before tile t, warps 2-3 the backward aggregates after it (each lane a contiguous run,
-// then an ordered warp fold).  Result in sc.cf / sc.cb.  Ends with a barrier.
+// Tile carries of every node, once per (column, pass, direction): an exclusive scan of the
+// tile aggregates of k_cp<1> (forward: tiles in order; backward: reversed), one warp per
+// node, 32 tiles per step (Kogge-Stone with the same combine as the tile scans).  k_cp<2>
+// then loads one record per direction instead of folding up to #tiles aggregates per column.
 template <class A>
-__device__ __forceinline__ void cp_carries(CpScratch<A>& sc, const LvAgg* aggs, int t, int first,
-                                           int last) {
+__global__ void __launch_bounds__(32) k_cp_carry(LvAgg* aggs, LvAgg* carr, const HpDesc* descs,
+                                                 int npass, int max_tiles) {
   using S = CSt<A::NS>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool fw = warp < 2;
-  const int lo = fw ? first : t + 1;
-  const int hi = fw ? t : last + 1;
-  const int cnt = max(0, hi - lo);
-  const int span = (cnt + 1) / 2;                   // tiles per warp
-  const int per = (span + 31) / 32;                 // tiles per lane
-  const int wlo = lo + (warp & 1) * span;
-  const int whi = min(hi, wlo + span);
-  S X = cs_id<A>();
+  const int p = blockIdx.y;
+  const int c = blockIdx.z >> 1, dir = blockIdx.z & 1;
+  const HpDesc hd = descs[p];
+  const int tps = 1 << (hd.lseg - LV_LOGTILE);
+  const int first = blockIdx.x * tps;
+  if (first >= hd.ntiles) return;
+  const int last = min(first + tps, hd.ntiles) - 1;
+  const int64_t base = ((int64_t)c * npass + p) * 2 * max_tiles;
+  const LvAgg* ag = aggs + base;
+  LvAgg* cr = carr + base;
+  const int lane = threadIdx.x;
+  S cin = cs_id<A>();
+  if (dir == 0) {
 #pragma unroll 1
-  for (int k0 = 0; k0 < per; k0 += 2) {             // two loads in flight per step
-    S y[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int j = wlo + lane * per + k0 + k;
-      y[k] = (k0 + k < per && j < whi) ? cs_get<A::NS>(aggs + 2 * j + (fw ? 0 : 1)) : cs_id<A>();
+    for (int b0 = first; b0 <= last; b0 += 32) {
+      const int t = b0 + lane;
+      S x = t <= last ? cs_get<A::NS>(ag + 2 * t) : cs_id<A>();
+#pragma unroll 1
+      for (int off = 1; off < 32; off <<= 1) {
+        const S y = cs_shfl<A::NS>(x, off, true);
+        if (lane >= off) x = cs_fw<A>(y, x);
+      }
+      S ex = cs_shfl<A::NS>(x, 1, true);
+      if (lane == 0) ex = cs_id<A>();
+      if (t <= last) cs_put<A::NS>(cr + 2 * t, cs_fw<A>(cin, ex));
+      cin = cs_fw<A>(cin, cs_bcast<A::NS>(x, 31));   // + lane 31's inclusive
     }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) X = fw ? cs_fw<A>(X, y[k]) : cs_bw<A>(X, y[k]);
-  }
+  } else {
 #pragma unroll 1
-  for (int off = 1; off < 32; off <<= 1) {
-    S Y = cs_shfl<A::NS>(X, off, false);
-    if (lane + off < 32) X = fw ? cs_fw<A>(X, Y) : cs_bw<A>(X, Y);
+    for (int b0 = last; b0 >= first; b0 -= 32) {
+      const int t = b0 - lane;
+      S x = t >= first ? cs_get<A::NS>(ag + 2 * t + 1) : cs_id<A>();
+#pragma unroll 1
+      for (int off = 1; off < 32; off <<= 1) {
+        const S y = cs_shfl<A::NS>(x, off, true);
+        if (lane >= off) x = cs_bw<A>(x, y);
+      }
+      S ex = cs_shfl<A::NS>(x, 1, true);
+      if (lane == 0) ex = cs_id<A>();
+      if (t >= first) cs_put<A::NS>(cr + 2 * t + 1, cs_bw<A>(ex, cin));
+      cin = cs_bw<A>(cs_bcast<A::NS>(x, 31), cin);
+    }
   }
-  if (lane == 0) sc.part[warp] = X;
-  __syncthreads();
-  if (threadIdx.x == 0) sc.cf = cs_fw<A>(sc.part[0], sc.part[1]);
-  if (threadIdx.x == 1) sc.cb = cs_bw<A>(sc.part[2], sc.part[3]);
-  __syncthreads();
 }
 
 // flattened work item -> pass: items are visited in increasing order, so each CTA keeps a
@@ -764,7 +786,7 @@ __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDe
 template <class A, int MODE>
 __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned char* hpbase,
                                                    const HpDesc* descs, int npass, int total,
-                                                   int max_tiles, int nrhs) {
+                                                   int max_tiles, int nrhs, int64_t carr_off) {
   using S = CSt<A::NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
@@ -835,7 +857,12 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
           un[k] = r != CP_RMASK ? g.pts[r].u : 0.0;
         }
       }
-      if (MODE == 2) cp_carries<A>(sc, aggs, t, first, last);   // (barriers inside)
+      if (MODE == 2) {   // tile carries (k_cp_carry); read after the next barrier
+        const double* cr = reinterpret_cast<const double*>(aggs + carr_off + 2 * t);
+        if (tid < A::NS + 2) reinterpret_cast<double*>(&sc.cf)[tid] = __ldcg(cr + tid);
+        if (tid >= 32 && tid < 32 + A::NS + 2)
+          reinterpret_cast<double*>(&sc.cb)[tid - 32] = __ldcg(cr + sizeof(LvAgg) / 8 + tid - 32);
+      }
       // ---- forward: per-thread aggregate (direct form), warp scan, block carry, apply.
       {
         S X;
@@ -1125,11 +1152,16 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     // the carried-pass tile aggregates do not depend on the low levels: side stream
     GPM_CUDA(cudaEventRecord(pl.ev_fork, s));
     GPM_CUDA(cudaStreamWaitEvent(pl.s2, pl.ev_fork, 0));
+    const int64_t carr_off = (int64_t)g.agg_stride * nrhs;   // carries after the aggregates
     k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmem), pl.s2>>>(
-        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
+        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
+        carr_off);
+    GPM_CUDA(cudaGetLastError());
+    k_cp_carry<A><<<dim3(pl.hp_maxtiles, pl.hp_npass, 2 * nrhs), 32, 0, pl.s2>>>(
+        g.aggs, g.aggs + carr_off, dd, pl.hp_npass, pl.hp_maxtiles);
     GPM_CUDA(cudaGetLastError());
     GPM_CUDA(cudaEventRecord(pl.ev_join, pl.s2));
-    *launches += 1;
+    *launches += 2;
   }
   // fused low levels (writes acc for every point: no memset needed)
   if constexpr (A::NCH == 2) {
@@ -1150,7 +1182,8 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   if (hp) {   // carried-pass apply (needs the aggregates)
     GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     k_cp<A, 2><<<std::min(pl.hp_items, grid2), CP_BLOCK, sizeof(CpSmem), s>>>(
-        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs);
+        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
+        (int64_t)g.agg_stride * nrhs);
     *launches += 1;
     GPM_CUDA(cudaGetLastError());
   }
