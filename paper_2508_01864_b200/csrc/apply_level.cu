@@ -200,7 +200,7 @@ __device__ __forceinline__ CSt<NS> cs_get(const LvAgg* g) {
 
 template <class A>
 struct CpScratch {
-  CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS], part[CP_WARPS], cf, cb;
+  CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS], cf, cb;
 };
 
 // ---------------------------------------------------------------------------
