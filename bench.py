@@ -311,11 +311,26 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     barrier(ws)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # (a) one call per MVM (copy in, apply, copy out, synchronise)
     e0.record(stream)
     for k in range(e2e_steps):
         st = lib.gp_kmvm_host(plan._h, ctypes.c_void_p(vh[k % nv].data_ptr()), 1,
                               ctypes.c_void_p(oh[k % nv].data_ptr()), s)
         assert st == 0
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e2e_single_sec = max_over_ranks(e0.elapsed_time(e1) / 1e3, ws)
+    # (b) one call for all the step's vectors (pinned buffers: the library pipelines the
+    # host->device copy of column c+1, the apply of c and the device->host copy of c-1)
+    lib.gp_kmvm_host(plan._h, ctypes.c_void_p(vh[0].data_ptr()), 3,
+                     ctypes.c_void_p(oh[0].data_ptr()), s)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0.record(stream)
+    st = lib.gp_kmvm_host(plan._h, ctypes.c_void_p(vh[0].data_ptr()), e2e_steps,
+                          ctypes.c_void_p(oh[0].data_ptr()), s)
+    assert st == 0
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(ws)
@@ -360,7 +375,10 @@ def run_ours(args, ws, rank, local):
         },
         "e2e": {"value": e2e_value, "unit": "MVM/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "steps": e2e_steps,
-                "api": "gp_kmvm_host (pinned host v/out, copies + apply + sync per step)"},
+                "api": (f"gp_kmvm_host, {e2e_steps} pinned host vectors in one call (copies "
+                        "pipelined with the applies, synchronised at the end)"),
+                "per_call": {"value": sum_over_ranks(e2e_steps, ws) / e2e_single_sec,
+                             "api": "gp_kmvm_host once per MVM (copy in, apply, copy out, sync)"}},
     }
     plan.close()
 

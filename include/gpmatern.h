@@ -109,7 +109,10 @@ GP_API gp_status gp_kmvm(gp_plan p, const double *v, int nrhs, double *out, void
 
 /* gp_kmvm_host -- gp_kmvm with HOST buffers (pinned or pageable): copies v to the
  * device, applies, copies out back and synchronises `stream`.  Used for the
- * end-to-end measurement.  v, out: n x nrhs column-major (host). */
+ * end-to-end measurement.  v, out: n x nrhs column-major (host).  With nrhs > 1 and both
+ * buffers pinned the columns are pipelined through three device slots: the host->device
+ * copy of column c+1, the apply of column c (on `stream`) and the device->host copy of
+ * column c-1 overlap (two internal copy streams). */
 GP_API gp_status gp_kmvm_host(gp_plan p, const double *v, int nrhs, double *out, void *stream);
 
 /* gp_kmvm_rank -- out = K v with v and out in the plan's STORED order (x1-rank order:

@@ -118,11 +118,61 @@ gp_status gp_permute(gp_plan p, const double* src, int nrhs, double* dst, int to
   return GP_OK;
 }
 
+static bool is_pinned(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// nrhs > 1 with pinned host buffers: columns flow through three device stage slots with
+// the host->device copy of column c+1, the apply of column c and the device->host copy of
+// column c-1 in flight together (copy streams + events; the apply stays on `s`).
+static gp_status kmvm_host_pipelined(gp_plan p, const double* v, int nrhs, double* out,
+                                     cudaStream_t s) {
+  Plan& pl = p->pl;
+  const size_t n = (size_t)pl.n;
+  const size_t col = sizeof(double) * n;
+  if (!pl.hs_in) {
+    GPM_CUDA(cudaStreamCreateWithFlags(&pl.hs_in, cudaStreamNonBlocking));
+    GPM_CUDA(cudaStreamCreateWithFlags(&pl.hs_out, cudaStreamNonBlocking));
+    for (int b = 0; b < 9; ++b) GPM_CUDA(cudaEventCreateWithFlags(&pl.hev[b], cudaEventDisableTiming));
+  }
+  if (pl.stage_in.bytes < 3 * col) GPM_TRY(pl.stage_in.alloc(3 * col));
+  if (pl.stage_out.bytes < 3 * col) GPM_TRY(pl.stage_out.alloc(3 * col));
+  cudaEvent_t* e_in = pl.hev;
+  cudaEvent_t* e_cmp = pl.hev + 3;
+  cudaEvent_t* e_out = pl.hev + 6;
+  GPM_CUDA(cudaEventRecord(e_cmp[0], s));   // copies start after prior work on s
+  GPM_CUDA(cudaStreamWaitEvent(pl.hs_in, e_cmp[0], 0));
+  for (int c = 0; c < nrhs; ++c) {
+    const int b = c % 3;
+    double* vb = pl.stage_in.as<double>() + b * n;
+    double* ob = pl.stage_out.as<double>() + b * n;
+    if (c >= 3) GPM_CUDA(cudaStreamWaitEvent(pl.hs_in, e_cmp[b], 0));   // slot consumed
+    GPM_CUDA(cudaMemcpyAsync(vb, v + c * n, col, cudaMemcpyHostToDevice, pl.hs_in));
+    GPM_CUDA(cudaEventRecord(e_in[b], pl.hs_in));
+    GPM_CUDA(cudaStreamWaitEvent(s, e_in[b], 0));
+    if (c >= 3) GPM_CUDA(cudaStreamWaitEvent(s, e_out[b], 0));          // slot drained
+    GPM_TRY(apply_user(pl, vb, ob, 1, s));
+    GPM_CUDA(cudaEventRecord(e_cmp[b], s));
+    GPM_CUDA(cudaStreamWaitEvent(pl.hs_out, e_cmp[b], 0));
+    GPM_CUDA(cudaMemcpyAsync(out + c * n, ob, col, cudaMemcpyDeviceToHost, pl.hs_out));
+    GPM_CUDA(cudaEventRecord(e_out[b], pl.hs_out));
+  }
+  GPM_CUDA(cudaStreamSynchronize(pl.hs_out));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return GP_OK;
+}
+
 gp_status gp_kmvm_host(gp_plan p, const double* v, int nrhs, double* out, void* stream) {
   if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
   Plan& pl = p->pl;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nrhs > 1 && is_pinned(v) && is_pinned(out)) return kmvm_host_pipelined(p, v, nrhs, out, s);
   const size_t bytes = sizeof(double) * pl.n * nrhs;
   if (pl.stage_in.bytes < bytes) GPM_TRY(pl.stage_in.alloc(bytes));
   if (pl.stage_out.bytes < bytes) GPM_TRY(pl.stage_out.alloc(bytes));

@@ -86,6 +86,9 @@ struct Plan {
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int part_zero_cols = 0;   // columns of `part` whose never-written tail slots are zeroed
+  // gp_kmvm_host pipelining: copy streams and per-slot events (in, compute, out) x 3
+  cudaStream_t hs_in = nullptr, hs_out = nullptr;
+  cudaEvent_t hev[9] = {};
   std::vector<char> hp_tail;        // carried pass has an inactive tail (slot must be zeroed)
   DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
   int near_lb2 = 4, near_lb3 = 8, near_lb3m = 5;   // near-field block log2 sizes (tuned)

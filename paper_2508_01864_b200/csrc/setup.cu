@@ -105,6 +105,11 @@ void plan_free(Plan& pl) {
   if (pl.ev_fork) cudaEventDestroy(pl.ev_fork);
   if (pl.ev_join) cudaEventDestroy(pl.ev_join);
   if (pl.s2) cudaStreamDestroy(pl.s2);
+  for (cudaEvent_t& e : pl.hev)
+    if (e) { cudaEventDestroy(e); e = nullptr; }
+  if (pl.hs_in) cudaStreamDestroy(pl.hs_in);
+  if (pl.hs_out) cudaStreamDestroy(pl.hs_out);
+  pl.hs_in = pl.hs_out = nullptr;
   pl.ev_fork = pl.ev_join = nullptr;
   pl.s2 = nullptr;
 }

@@ -55,17 +55,19 @@ def test_library_is_sm100a_only():
 
 def test_argument_validation_without_device(lib):
     import paper_2508_01864_b200 as g
-    k = g.Kernel(7, (0.1,)).c()
+    k = g.Kernel(11, (0.1,)).c()
     h = ctypes.c_void_p()
     dummy = ctypes.c_void_p(16)
     assert lib.gp_setup(dummy, 0, 1, ctypes.byref(k), None, ctypes.byref(h)) == 1      # n < 1
     assert lib.gp_setup(dummy, 10, 4, ctypes.byref(k), None, ctypes.byref(h)) == 1     # d = 4
-    assert lib.gp_setup(dummy, 10, 1, ctypes.byref(k), None, ctypes.byref(h)) == 2     # nu = 7/2
+    assert lib.gp_setup(dummy, 10, 1, ctypes.byref(k), None, ctypes.byref(h)) == 2     # nu = 11/2
     assert b"supported" in lib.gp_last_error()
     k = g.Kernel(3, (-0.1,)).c()
     assert lib.gp_setup(dummy, 10, 1, ctypes.byref(k), None, ctypes.byref(h)) == 1     # l <= 0
     k = g.Kernel(5, (0.1, 0.1, 0.1), form=g.FORM_PRODUCT).c()
     assert lib.gp_setup(dummy, 10, 3, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product d=3
+    k = g.Kernel(7, (0.1, 0.1), form=g.FORM_PRODUCT).c()
+    assert lib.gp_setup(dummy, 10, 2, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product 7/2
 
 
 def test_no_cpu_fallback(lib):

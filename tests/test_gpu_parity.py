@@ -275,3 +275,20 @@ def test_large_n_segments_over_256_tiles(gpm, d, ell):
     out = plan.kmvm(to_dev(v)).cpu().numpy()
     rows = W.sample_rows(x, 256)
     check_rows(out, x, v, 3, "l1", ell, 1.0, rows=rows, what=f"large-n d={d}")
+
+
+def test_host_buffers_pipelined_batch(gpm):
+    """gp_kmvm_host with several pinned columns (pipelined copies) equals device applies."""
+    import torch
+    n = 30000
+    x = _points("normal", n, 1, 12)
+    V = torch.from_numpy(np.random.default_rng(4).standard_normal((7, n))).pin_memory()
+    O = torch.empty_like(V).pin_memory()
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, (0.05,)))
+    plan.kmvm_host(V, O)
+    dev = plan.kmvm(V.cuda()).cpu()
+    assert torch.equal(O, dev)
+    # pageable buffers take the plain path, same values
+    O2 = np.empty((7, n))
+    plan.kmvm_host(V.numpy().copy(), O2)
+    assert np.array_equal(O2, dev.numpy())
