@@ -21,6 +21,7 @@
  */
 #ifndef GPMATERN_H
 #define GPMATERN_H
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -71,6 +72,12 @@ typedef struct {
     int restarts;          /* residual-replacement restarts taken */
 } gp_cg_info;
 
+/* Device-memory hook: alloc(bytes, stream, ctx) returns a device pointer (or NULL), free(ptr,
+ * stream, ctx) releases it (stream is always NULL: the library synchronises the device
+ * before a release). */
+typedef void *(*gp_alloc_fn)(size_t bytes, void *stream, void *ctx);
+typedef void (*gp_free_fn)(void *ptr, void *stream, void *ctx);
+
 typedef struct gp_plan_s *gp_plan;    /* opaque: the stored sort / D&C structure of x */
 typedef struct gp_cross_s *gp_cross;  /* opaque: structure of the union x U z for K_zx */
 typedef struct gp_precond_s *gp_precond;  /* opaque: pivoted-Cholesky preconditioner */
@@ -96,6 +103,12 @@ typedef struct {
  *   out : receives the plan (host).
  * Errors: INVALID_ARG, UNSUPPORTED, NONFINITE (first bad row), OOM, CUDA.
  * Synchronises `stream` once (finiteness check). */
+/* gp_set_allocator -- route every device allocation of the library (plan structure,
+ * scratch, solver buffers) through alloc/free, e.g. the PyTorch caching allocator
+ * (SURVEY §8(b)).  Process-wide; buffers keep the hook they were allocated with.  Both NULL:
+ * back to cudaMalloc / cudaFree (the default).  Errors: INVALID_ARG if only one is NULL. */
+GP_API gp_status gp_set_allocator(gp_alloc_fn alloc, gp_free_fn free, void *ctx);
+
 GP_API gp_status gp_setup(const double *x, int64_t n, int d, const gp_kernel *k, void *stream,
                    gp_plan *out);
 

@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass
 
 __all__ = [
-    "load_library", "Kernel", "Plan", "Cross", "Precond", "GPError", "setup", "kmvm", "cg_solve", "fit",
+    "load_library", "Kernel", "Plan", "Cross", "Precond", "GPError", "setup", "kmvm", "cg_solve", "fit", "use_torch_allocator",
     "predict", "FORM_L1", "FORM_PRODUCT", "MEAN_NONE", "MEAN_AFFINE", "MEAN_BASIS",
     "LIB_PATH",
 ]
@@ -102,6 +102,7 @@ def load_library(path: str | None = None):
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    lib.gp_set_allocator.argtypes = [vp, vp, vp]; lib.gp_set_allocator.restype = ctypes.c_int
     lib.gp_destroy.argtypes = [vp]; lib.gp_destroy.restype = None
     lib.gp_kzx_destroy.argtypes = [vp]; lib.gp_kzx_destroy.restype = None
     lib.gp_precond_destroy.argtypes = [vp]; lib.gp_precond_destroy.restype = None
@@ -410,6 +411,34 @@ class Precond:
             self.close()
         except Exception:
             pass
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+_alloc_hooks = None
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's device allocations through PyTorch's caching allocator
+    (gp_set_allocator); enable=False restores cudaMalloc/cudaFree.  Marshalling only: the
+    callbacks call torch.cuda.caching_allocator_alloc / _delete."""
+    global _alloc_hooks
+    lib = load_library()
+    if not enable:
+        _check(lib.gp_set_allocator(None, None, None))
+        _alloc_hooks = None
+        return
+    import torch
+
+    def _alloc(nbytes, stream, ctx):
+        return torch.cuda.caching_allocator_alloc(int(nbytes))
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    _alloc_hooks = (_ALLOC_FN(_alloc), _FREE_FN(_free))   # keep the thunks alive
+    _check(lib.gp_set_allocator(ctypes.cast(_alloc_hooks[0], ctypes.c_void_p),
+                                ctypes.cast(_alloc_hooks[1], ctypes.c_void_p), None))
 
 
 def fit(x, kernel: Kernel, sigma0: float, y, G, W=None, stream=None, **opts):

@@ -58,6 +58,13 @@ using namespace gpm;
 extern "C" {
 
 const char* gp_last_error(void) { return g_err.c_str(); }
+
+gp_status gp_set_allocator(gp_alloc_fn alloc, gp_free_fn free_fn, void* ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr))
+    return fail(GP_ERR_INVALID_ARG, "alloc and free must both be set or both be NULL");
+  set_allocator(alloc, free_fn, ctx);
+  return GP_OK;
+}
 const char* gp_version(void) { return "gpmatern 0.1 sm_100a"; }
 
 gp_status gp_setup(const double* x, int64_t n, int d, const gp_kernel* k, void* stream,

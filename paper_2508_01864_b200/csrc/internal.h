@@ -31,6 +31,8 @@ gp_status fail(gp_status st, const std::string& msg);
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  gp_free_fn fr = nullptr;   // allocator hook that owns ptr (gp_set_allocator), else cudaFree
+  void* fctx = nullptr;
   gp_status alloc(size_t b);
   void release();
   template <class T> T* as() const { return static_cast<T*>(ptr); }
@@ -134,6 +136,7 @@ gp_status fit_alg1(const double* x, int64_t n, int d, const gp_kernel& k0, doubl
                    const gp_fit_opts& o, gp_fit_result* out, cudaStream_t s);
 
 // setup.cu
+void set_allocator(gp_alloc_fn a, gp_free_fn f, void* ctx);
 gp_status plan_build(Plan& pl, const double* x_dev, int64_t n, int d, const gp_kernel& k,
                      cudaStream_t s);
 void plan_free(Plan& pl);

@@ -78,9 +78,28 @@ inline int grid_for(int64_t n) {
 
 }  // namespace
 
+// allocator hook (gp_set_allocator); process-wide, captured per buffer at allocation
+static gp_alloc_fn g_alloc = nullptr;
+static gp_free_fn g_free = nullptr;
+static void* g_actx = nullptr;
+
+void set_allocator(gp_alloc_fn a, gp_free_fn f, void* ctx) {
+  g_alloc = a;
+  g_free = f;
+  g_actx = ctx;
+}
+
 gp_status DevBuf::alloc(size_t b) {
   release();
   if (b == 0) b = 16;
+  if (g_alloc) {
+    ptr = g_alloc(b, nullptr, g_actx);
+    if (!ptr) return fail(GP_ERR_OOM, "allocator hook returned NULL for " + std::to_string(b) + " bytes");
+    fr = g_free;
+    fctx = g_actx;
+    bytes = b;
+    return GP_OK;
+  }
   cudaError_t e = cudaMalloc(&ptr, b);
   if (e != cudaSuccess) {
     ptr = nullptr;
@@ -93,9 +112,18 @@ gp_status DevBuf::alloc(size_t b) {
 }
 
 void DevBuf::release() {
-  if (ptr) cudaFree(ptr);
+  if (ptr) {
+    if (fr) {
+      cudaDeviceSynchronize();   // the hook's pool may hand the block out at once
+      fr(ptr, nullptr, fctx);
+    } else {
+      cudaFree(ptr);
+    }
+  }
   ptr = nullptr;
   bytes = 0;
+  fr = nullptr;
+  fctx = nullptr;
 }
 
 void plan_free(Plan& pl) {

@@ -34,7 +34,7 @@ def test_header_declares_the_boundary():
                  "gp_plan_set_option", "gp_version", "gp_kmvm_rank", "gp_permute",
                  "gp_kmvm_dlengthscale", "gp_cg_solve_pc", "gp_precond_create",
                  "gp_precond_factor", "gp_precond_solve", "gp_precond_logdet",
-                 "gp_precond_destroy", "gp_mbcg", "gp_lml", "gp_fit"]:
+                 "gp_precond_destroy", "gp_mbcg", "gp_lml", "gp_fit", "gp_set_allocator"]:
         assert must in names, must
 
 
@@ -81,3 +81,9 @@ def test_no_cpu_fallback(lib):
     assert lib.gp_setup(ctypes.c_void_p(16), 10, 1, ctypes.byref(k), None, ctypes.byref(h)) == 7
     assert b"no CUDA device" in lib.gp_last_error()
     assert lib.gp_kmvm(None, None, 1, None, None) == 1
+
+
+def test_set_allocator_validation(lib):
+    import ctypes as C
+    assert lib.gp_set_allocator(C.c_void_p(16), None, None) == 1   # only one hook
+    assert lib.gp_set_allocator(None, None, None) == 0             # default restored

@@ -292,3 +292,21 @@ def test_host_buffers_pipelined_batch(gpm):
     O2 = np.empty((7, n))
     plan.kmvm_host(V.numpy().copy(), O2)
     assert np.array_equal(O2, dev.numpy())
+
+
+def test_torch_allocator_hook(gpm):
+    """gp_set_allocator through PyTorch's caching allocator: same results, memory from torch."""
+    import torch
+    x = _points("uniform", 20000, 2, 5)
+    v = to_dev(np.random.default_rng(5).standard_normal(20000))
+    ref = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.1))).kmvm(v)
+    before = torch.cuda.memory_allocated()
+    gpm.use_torch_allocator(True)
+    try:
+        plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.1)))
+        out = plan.kmvm(v)
+        assert torch.cuda.memory_allocated() > before + 20000 * 8
+        assert torch.equal(out, ref)
+        plan.close()
+    finally:
+        gpm.use_torch_allocator(False)
