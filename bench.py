@@ -199,9 +199,11 @@ def time_applies(applier, steps, warmup, stream, ws):
     return max_over_ranks(sec, ws), sec
 
 
-def time_graph(make_applier, steps, warmup, ws):
-    """Capture `steps` applies in one CUDA graph (on a side stream) and time one replay.
-    Returns (max-over-ranks seconds, local seconds) or None if capture is unsupported."""
+def time_graph(make_applier, steps, warmup, ws, reps=1, stats=None):
+    """Capture `steps` applies in one CUDA graph (on a side stream) and time `reps` replays
+    (each bracketed by barrier + synchronize); returns the median replay as (max-over-ranks
+    seconds, local seconds) or None if capture is unsupported.  stats (dict) receives the
+    per-apply p10 / p50 / p90 over the replays (SURVEY §8(d) timing protocol)."""
     import torch
     cs = torch.cuda.Stream()
     try:
@@ -219,17 +221,25 @@ def time_graph(make_applier, steps, warmup, ws):
     except Exception as e:          # pragma: no cover - reported in the JSON line
         print(f"graph capture failed: {e}", file=sys.stderr)
         return None
-    barrier(ws)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(cs):
-        e0.record(cs)
-        graph.replay()
-        e1.record(cs)
-    torch.cuda.synchronize()
-    barrier(ws)
-    sec = e0.elapsed_time(e1) / 1e3
-    return max_over_ranks(sec, ws), sec
+    secs = []
+    for _ in range(reps):
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            e0.record(cs)
+            graph.replay()
+            e1.record(cs)
+        torch.cuda.synchronize()
+        barrier(ws)
+        secs.append(max_over_ranks(e0.elapsed_time(e1) / 1e3, ws))
+    order = sorted(secs)
+    med = order[len(order) // 2]
+    if stats is not None:
+        q = lambda f: order[min(len(order) - 1, int(f * (len(order) - 1) + 0.5))] / steps * 1e3
+        stats.update({"replays": reps, "apply_ms_p10": q(0.1), "apply_ms_p50": q(0.5),
+                      "apply_ms_p90": q(0.9)})
+    return med, med
 
 
 def per_launch(applier, steps, stream):
@@ -266,27 +276,33 @@ def run_ours(args, ws, rank, local):
     hbm, peak_kind = peaks()
     result = {}
 
-    def measure(two_nu, steps, warmup, sampler=None, vin=None, rank_order=False):
+    def measure(two_nu, steps, warmup, sampler=None, vin=None, rank_order=False, reps=1):
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter()
         plan = g.Plan(x, g.Kernel(two_nu, cfg.ell), stream)
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter() - t_setup
+        gstats = {"setup_s": t_setup}
         VV = V if vin is None else vin(plan)
         ap = Applier(g, plan, VV, OUT, stream, rank_order=rank_order)
         mk = lambda st: Applier(g, plan, VV, OUT, st, rank_order=rank_order)
         import contextlib
         with (sampler if sampler else contextlib.nullcontext()):
-            gr = None if args.no_graph else time_graph(mk, steps, warmup, ws)
+            gr = None if args.no_graph else time_graph(mk, steps, warmup, ws, reps, gstats)
             if gr is None:
                 sec_max, sec = time_applies(ap, steps, warmup, stream, ws)
             else:
                 sec_max, sec = gr
         loop_max, _ = time_applies(ap, min(steps, 500), 3, stream, ws)
         mean_l, med_l, min_l = per_launch(ap, min(steps, 200), stream)
-        info = {"graph": gr is not None, "stream_loop_ms_per_step": loop_max / min(steps, 500) * 1e3}
+        info = {"graph": gr is not None, "stream_loop_ms_per_step": loop_max / min(steps, 500) * 1e3,
+                **gstats}
         return plan, ap, sec_max, sec, mean_l, med_l, min_l, info
 
     sampler = ClockSampler(local)
     two_nu = 5
     plan, ap, sec_max, sec, mean_l, med_l, min_l, tinfo = measure(two_nu, args.steps, args.warmup,
-                                                                   sampler)
+                                                                   sampler, reps=5)
     total = sum_over_ranks(args.steps, ws)
     value = total / sec_max
     model_bytes = plan.model_bytes
@@ -355,9 +371,13 @@ def run_ours(args, ws, rank, local):
             "n": n, "d": 1, "nu": "5/2", "lengthscale": cfg.ell[0], "form": "L1(=product, d=1)",
             "setup": "once (sort + stored structure), outside the timed region",
             "l2": "inputs larger than L2: 100 distinct v and out buffers (1.6 GB) cycled",
-            "launch": ("CUDA graph of K gp_kmvm calls (one cooperative kernel each), one replay"
+            "launch": ("CUDA graph of K gp_kmvm calls (one cooperative kernel each), median of 5 replays"
                        if tinfo["graph"] else "gp_kmvm through ctypes, stream loop"),
             "stream_loop_ms_per_step": tinfo["stream_loop_ms_per_step"],
+            "graph_replays": tinfo.get("replays", 1),
+            "apply_ms_p10_p50_p90": [tinfo.get("apply_ms_p10"), tinfo.get("apply_ms_p50"),
+                                     tinfo.get("apply_ms_p90")],
+            "setup_s": tinfo["setup_s"],
             "parallelism": f"replicas x{ws}",
         },
         "gpu_launches": int(args.steps * launches),
@@ -468,6 +488,28 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
 
     c3 = W.CONFIGS[3]
     out["config3_d2_n2e5_nu32_l1"] = apply_stats(W.config_points(c3), g.Kernel(3, c3.ell), 20)
+    # config 3's rectangular product K_zx v (20,000 queries): union setup + applies
+    x3 = torch.from_numpy(W.config_points(c3)).to(dev)
+    z3 = torch.from_numpy(W.config_queries(c3)).to(dev)
+    p3 = g.Plan(x3, g.Kernel(3, c3.ell), stream)
+    v3 = torch.randn(c3.n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cr = p3.cross(z3, stream)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    cr.kzx(v3, stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(10):
+        cr.kzx(v3, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    out["config3_kzx_m2e4"] = {"union_setup_s": t1 - t0, "apply_ms": e0.elapsed_time(e1) / 10,
+                               "n": c3.n, "m": int(z3.shape[0])}
+    cr.close()
+    p3.close()
     out["config3_d2_n2e5_nu32_l1_dlengthscale"] = apply_stats(
         W.config_points(c3), g.Kernel(3, c3.ell), 20, grad=True)
     c2 = W.CONFIGS[2]
@@ -509,6 +551,13 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
                                      "relres_max": info2["relres_max"], "rhs": 4,
                                      "beta": beta2, "preconditioner": f"pivoted Cholesky rank {rank}",
                                      "ms_per_iter": (t2 - t1) / max(info2["iters"], 1) * 1e3}
+        # posterior mean at the 10,000 queries (union setup + K_zx alpha + h(z)^T beta)
+        z5 = torch.from_numpy(W.config_queries(c5)).to(dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan.predict(z5, alpha2, beta2, stream=stream)
+        torch.cuda.synchronize()
+        out["config5_predict"] = {"predict_s": time.perf_counter() - t0, "m": int(z5.shape[0])}
         pc.close()
         plan.close()
     return out
