@@ -506,7 +506,7 @@ gp_status d1_prepare(Plan& pl) {
       pl.d1_grid = (int)g;
       pl.d1_chunk = chunk;
       pl.d1_path = 1;
-      GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)g));   // D1Pub records x 2 (apply_d1_fast.cu)
+      GPM_TRY(pl.aggs.alloc(128 * 2 * 4 * (size_t)g));   // D1Pub [2 parities][4 replicas][g] (apply_d1_fast.cu)
       GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
       GPM_TRY(pl.bar.alloc(64));
       GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));

@@ -432,8 +432,443 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Host side.  Shapes (BLOCK, ITEMS): 0 = (512, 15), 1 = (640, 11), 2 = (768, 9),
-// 3 = (1024, 7).  The default is chosen by measurement.
+// k_d1_ov: the same scan with the grid-wide exchange taken off the critical path
+// (measured on B200, tools/micro/{lat,xchg}.cu: one grid-wide exchange of per-CTA records
+// costs ~2.5 us whatever the mechanism -- cg grid.sync, counter, per-slot flags -- and
+// a 24-warp shuffle scan of (span, moments) is bound by the one-shuffle-per-clock pipe):
+//   1. t (+perm) by bulk copies at launch; after griddepcontrol.wait v by bulk copies
+//      (rank order) or the random gathers (user order);
+//   2. pass 1: each thread's forward / backward aggregates (as k_d1_fast);
+//   3. the CHUNK aggregate is a plain sum: each thread shifts its aggregates to the chunk's
+//      reference points (one e^{-x} each, x from the sorted t directly), warp xor-sums,
+//      one warp adds the warp sums in a fixed order (deterministic);
+//   4. thread 0 publishes it and arrives on a monotone counter (red.release.gpu) -- a
+//      split barrier: the wait comes only after steps 5-6;
+//   5. meanwhile: the block scan (warp shuffles) for the within-chunk prefixes and
+//   6. the local pass 2: both recurrences from the within-chunk prefixes only, storing
+//      loc_j = u_j + read_F + read_B;
+//   7. wait (thread 0 polls, fence.acq_rel, __syncthreads), fold the other chunks'
+//      records into the carries C_F, C_B;
+//   8. carry pass: the carries' contribution at a point Delta after their reference is
+//      e^{-Delta} sum_r beta_r Delta^r (beta from C once per CTA), Delta and e^{-Delta}
+//      as running sums / products of the stored gaps: P + 1 FMAs per point and direction;
+//      out = os2 (loc + both contributions), stored per warp (rank order) or scattered.
+// Counter: bar[4..5] (u64) counts published columns x CTAs over the plan's life (zeroed at
+// prepare); a CTA's record holds its own published-column count, so every CTA derives
+// the same target (base + col + 1) x grid at kernel start.
+constexpr int DF_REPL = 4;   // k_d1_ov record replicas (readers spread over 4 lines per record)
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int P, int KIND, int BLOCK, int ITEMS, bool USER>
+__global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
+  constexpr int SUB = BLOCK * ITEMS;
+  constexpr int NW = BLOCK / 32;
+  constexpr int PT = BLOCK / DF_NPART;
+  constexpr int PSZ = PT * ITEMS;
+  constexpr int NM = 2 * (P + 1);   // chunk-sum values: forward and backward moments
+  static_assert(PSZ % 4 == 0, "load parts must stay 16-byte aligned");
+  static_assert(NW <= 32 && NM <= 32, "one warp adds the warp sums");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* s_t = reinterpret_cast<double*>(smem_raw);   // SUB + 8: t, then gaps
+  double* s_u = s_t + SUB + 8;                         // SUB: u, then loc, then out
+  double* s_e = s_u + SUB;                             // SUB: e^{-gap}
+  int* s_pi = reinterpret_cast<int*>(s_e + SUB);       // SUB + 8 (user order)
+  __shared__ uint64_t mbar[DF_NPART], mbar_v[DF_NPART];
+  __shared__ double s_tab[64];
+  constexpr int NSF = P + 3;
+  __shared__ double s_wf[NW][NSF], s_wb[NW][NSF];
+  __shared__ double s_wsum[NW][NM];
+  __shared__ double s_beta[2][P + 1];
+  __shared__ double s_part[2][8][NSF];
+  __shared__ unsigned long long s_base;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * a.chunk;
+  const int cnt = (int)max((int64_t)0, min(a.chunk, a.n - c0));
+  const int G = gridDim.x, b = blockIdx.x;
+  D1Pub* pub = reinterpret_cast<D1Pub*>(a.chunk_aggs);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(a.bar + 8);
+
+  DF_STAMP(0);
+  fexp_table_init(s_tab);
+  if (tid == 0) {
+    for (int p = 0; p < DF_NPART; ++p) {
+      mbar_init(&mbar[p], 1);
+      mbar_init(&mbar_v[p], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < DF_NPART && cnt > 0) {   // plan data: before griddepcontrol.wait
+    const int lo = tid * PSZ, hi = min(cnt, lo + PSZ);
+    if (lo < hi) {
+      const unsigned nt = (unsigned)(((hi - lo) + 1) & ~1);   // padded plan arrays
+      const unsigned np = (unsigned)(((hi - lo) + 3) & ~3);
+      mbar_expect_tx(&mbar[tid], nt * 8 + (USER ? np * 4 : 0));
+      tma_load_1d(s_t + lo, a.ts + c0 + lo, nt * 8, &mbar[tid]);
+      if (USER) tma_load_1d(s_pi + lo, a.perm + c0 + lo, np * 4, &mbar[tid]);
+    }
+  }
+  auto prefetch_v = [&](int col) {
+    const int64_t per = (a.n_src + G - 1) / G;
+    const int64_t lo = min((int64_t)b * per, a.n_src);
+    const int64_t hi = min(lo + per, a.n_src);
+    if (hi > lo) prefetch_l2_range(a.v + col * a.vstride + lo, (size_t)(hi - lo) * 8);
+  };
+  if (USER && a.prefetch && tid == 32) prefetch_v(0);
+  const int j0 = tid * ITEMS;
+  const int mypart = tid / PT;
+  const bool part_live = mypart * PSZ < cnt;
+  // reference points: chunk forward ref = its last point; chunk backward ref = the point
+  // before its first point (t[0] for chunk 0: the first gap is 0); thread likewise
+  double tprev = 0.0, tlast = 0.0, tcref = 0.0, tmy = 0.0;
+  if (cnt > 0) {
+    tlast = __ldg(a.ts + c0 + cnt - 1);
+    tcref = c0 > 0 ? __ldg(a.ts + c0 - 1) : __ldg(a.ts);
+    const int64_t gp = c0 + min(j0, cnt) - 1;
+    tprev = gp >= 0 ? __ldg(a.ts + gp) : __ldg(a.ts);
+    if (j0 >= cnt) tprev = tlast;
+    tmy = j0 + ITEMS - 1 < cnt ? __ldg(a.ts + c0 + j0 + ITEMS - 1) : tlast;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // v, records, counter of the previous apply
+  if (tid == 0) {
+    const unsigned long long b0 = __ldcg(&pub[b].epoch), b1 = __ldcg(&pub[DF_REPL * G + b].epoch);
+    s_base = b0 > b1 ? b0 : b1;
+  }
+  const bool v_bulk = !USER && ((reinterpret_cast<uintptr_t>(a.v + c0) & 15) == 0) &&
+                      (a.vstride % 2 == 0 || a.nrhs == 1);
+  auto issue_v = [&](int col) {   // rank order: every column by bulk copy, or none
+    const double* vcol = a.v + col * a.vstride + c0;
+    if (v_bulk && tid < DF_NPART && cnt > 0) {
+      const int lo = tid * PSZ, hi = min(cnt, lo + PSZ);
+      const unsigned nu = (unsigned)((hi - lo) & ~1);   // never over-read v
+      if (lo < hi) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&mbar_v[tid], nu * 8);
+        if (nu) tma_load_1d(s_u + lo, vcol + lo, nu * 8, &mbar_v[tid]);
+      }
+    }
+  };
+  if (!USER) issue_v(0);
+  if (part_live) mbar_wait(&mbar[mypart], 0);
+  DF_STAMP(1);
+  {   // independent per point: unrolled for ILP
+    double tv[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) tv[k] = j0 + k < cnt ? s_t[j0 + k] : tlast;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const double dl = tv[k] - (k ? tv[k - 1] : tprev);   // neutral (0) past the chunk end
+      s_t[j0 + k] = dl;
+      s_e[j0 + k] = fexp_neg(dl, s_tab);
+    }
+  }
+  // shifts of this thread's aggregates to the chunk references (plan data only)
+  const double dF = tlast - tmy, eF = fexp_neg(dF, s_tab);
+  const double dB = tprev - tcref, eB = fexp_neg(dB, s_tab);
+  const double dC = tlast - tcref, eC = fexp_neg(dC, s_tab);
+  __syncthreads();   // s_base
+
+#pragma unroll 1
+  for (int col = 0; col < a.nrhs; ++col) {
+    const double* vcol = a.v + col * a.vstride;
+    double* ocol = a.out + col * a.ostride;
+    D1Pub* pubc = pub + (col & 1) * DF_REPL * G;   // [parity][replica][chunk]
+    const unsigned long long mycount = s_base + (unsigned long long)col + 1ull;
+    if (USER && a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
+    if (USER) {
+      double uu[ITEMS];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int j = j0 + k;
+        const int pi = j < cnt ? s_pi[j] : INT_MAX;
+        uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = uu[k];
+    } else {
+      if (v_bulk) {
+        if (part_live) mbar_wait(&mbar_v[mypart], (unsigned)(col & 1));
+        const int lo = mypart * PSZ, hi = min(cnt, lo + PSZ);
+        if (lo < hi && ((hi - lo) & 1) && tid == (hi - 1) / ITEMS)   // odd tail element
+          s_u[hi - 1] = __ldg(vcol + c0 + hi - 1);
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int j = j0 + k;
+        if (!v_bulk) s_u[j] = j < cnt ? __ldg(vcol + c0 + j) : 0.0;
+        else if (j >= cnt) s_u[j] = 0.0;
+      }
+    }
+    // ---- pass 1: this thread's aggregates by direct accumulation (short dependency
+    // chains: a running span and e^{-span} per direction), forward from the suffix spans
+    // (referenced at my last point), backward from the prefix spans (referenced at tprev)
+    SF<P> F = sf_id<P>(), B = sf_id<P>();
+    {
+      double Dc = 0.0, Ec = 1.0, Ds = 0.0, Es = 1.0;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int jb = j0 + k, jf = j0 + ITEMS - 1 - k;
+        Dc += s_t[jb];
+        Ec *= s_e[jb];
+        double wb = s_u[jb] * Ec, wf = s_u[jf] * Es;
+#pragma unroll
+        for (int q = 0; q <= P; ++q) {
+          B.M[q] += wb;
+          F.M[q] += wf;
+          wb *= Dc;
+          wf *= Ds;
+        }
+        Ds += s_t[jf];
+        Es *= s_e[jf];
+      }
+      F.D = B.D = Dc;
+      F.E = B.E = Ec;
+    }
+    DF_STAMP(2);
+    // ---- chunk aggregate = sum of the shifted thread aggregates (fixed order)
+    {
+      double m[NM];
+#pragma unroll
+      for (int q = 0; q <= P; ++q) {
+        m[q] = F.M[q];
+        m[P + 1 + q] = B.M[q];
+      }
+      advance<P>(m, dF, eF);
+      advance<P>(m + P + 1, dB, eB);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < NM; ++q) m[q] += __shfl_xor_sync(0xffffffffu, m[q], off);
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NM; ++q) s_wsum[warp][q] = m[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+      if (lane < NM)
+#pragma unroll 1
+        for (int w = 0; w < NW; ++w) s += s_wsum[w][lane];
+      __syncwarp();
+      if (lane < NM) s_wsum[0][lane] = s;
+      __syncwarp();
+      if (lane == 0) {   // publish (all replicas), then arrive: the release orders them
+#pragma unroll 1
+        for (int r = 0; r < DF_REPL; ++r) {
+          D1Pub* me = pubc + r * G + b;
+          me->v[0] = dC;
+          me->v[1] = eC;
+#pragma unroll
+          for (int q = 0; q <= P; ++q) {
+            me->v[2 + q] = s_wsum[0][q];
+            me->v[8 + q] = s_wsum[0][P + 1 + q];
+          }
+          me->epoch = mycount;
+        }
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+      }
+    }
+    DF_STAMP(3);
+    // ---- overlapped with the exchange: block scan for the within-chunk prefixes
+    SF<P> fi = F, bi = B;
+#pragma unroll 1
+    for (int off = 1; off < 32; off <<= 1) {
+      SF<P> l = sf_shfl<P>(fi, off, true);
+      SF<P> r = sf_shfl<P>(bi, off, false);
+      if (lane >= off) fi = sf_cf<P>(l, fi);
+      if (lane + off < 32) bi = sf_cb<P>(bi, r);
+    }
+    if (lane == 31) sf_st<P>(s_wf[warp], fi);
+    if (lane == 0) sf_st<P>(s_wb[warp], bi);
+    SF<P> fe = sf_shfl<P>(fi, 1, true);
+    SF<P> be = sf_shfl<P>(bi, 1, false);
+    if (lane == 0) fe = sf_id<P>();
+    if (lane == 31) be = sf_id<P>();
+    __syncthreads();
+    if (warp < 2) {
+      const bool fw = warp == 0;
+      SF<P> x = lane < NW ? sf_ld<P>(fw ? s_wf[lane] : s_wb[lane]) : sf_id<P>();
+#pragma unroll 1
+      for (int off = 1; off < NW; off <<= 1) {
+        SF<P> y = sf_shfl<P>(x, off, fw);
+        if (fw && lane >= off) x = sf_cf<P>(y, x);
+        if (!fw && lane + off < 32) x = sf_cb<P>(x, y);
+      }
+      SF<P> xe = sf_shfl<P>(x, 1, fw);
+      if ((fw && lane == 0) || (!fw && lane >= NW - 1)) xe = sf_id<P>();
+      __syncwarp();
+      if (lane < NW) sf_st<P>(fw ? s_wf[lane] : s_wb[lane], xe);
+    }
+    __syncthreads();
+    const SF<P> Fx = sf_cf<P>(sf_ld<P>(s_wf[warp]), fe);   // chunk ref -> my ref (forward)
+    const SF<P> Bx = sf_cb<P>(be, sf_ld<P>(s_wb[warp]));   // my last point -> chunk last
+    // ---- local pass 2: both recurrences (without the other chunks) interleaved in one
+    // loop, forward over k and backward over ITEMS-1-k: two independent chains
+    {
+      double MF[P + 1], MB[P + 1], rf[ITEMS], rb[ITEMS];
+#pragma unroll
+      for (int q = 0; q <= P; ++q) {
+        MF[q] = Fx.M[q];
+        MB[q] = Bx.M[q];
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int jf = j0 + k, jb = j0 + ITEMS - 1 - k;
+        advance<P>(MF, s_t[jf], s_e[jf]);
+        rf[k] = readc0<P, KIND>(MF);
+        MF[0] += s_u[jf];
+        rb[ITEMS - 1 - k] = readc0<P, KIND>(MB);
+        MB[0] += s_u[jb];
+        advance<P>(MB, s_t[jb], s_e[jb]);
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int j = j0 + k;
+        s_u[j] = (KIND == 0 ? s_u[j] : 0.0) + (rf[k] + rb[k]);
+      }
+    }
+    // ---- wait for every chunk's record of this column
+    if (tid == 0) {
+      const unsigned long long target = mycount * (unsigned long long)G;
+      while (ld_acquire_u64(ctr) < target) {
+      }
+    }
+    __syncthreads();
+    DF_STAMP(4);
+    {   // one record per lane (replica b % DF_REPL), all loads in flight at once; each
+        // warp folds its 32 records both ways, two threads fold the warp partials
+      const int ngroups = (G + 31) / 32;
+      const D1Pub* rep = pubc + (b % DF_REPL) * G;
+#pragma unroll 1
+      for (int grp = warp; grp < ngroups; grp += NW) {
+        const int jj = grp * 32 + lane;
+        const bool tf = jj < b, tb = jj > b && jj < G;
+        SF<P> XF = sf_id<P>(), XB = sf_id<P>();
+        if (tf || tb) {
+          const double* o = rep[jj].v;
+          const double2 de = __ldcg(reinterpret_cast<const double2*>(o));
+          const double* m = o + (tf ? 2 : 8);
+          double mv[P + 1];
+#pragma unroll
+          for (int q = 0; q + 1 <= P; q += 2) {
+            const double2 w = __ldcg(reinterpret_cast<const double2*>(m + q));
+            mv[q] = w.x;
+            mv[q + 1] = w.y;
+          }
+          if ((P + 1) & 1) mv[P] = __ldcg(m + P);
+          SF<P> Y;
+          Y.D = de.x;
+          Y.E = de.y;
+#pragma unroll
+          for (int q = 0; q <= P; ++q) Y.M[q] = mv[q];
+          if (tf) XF = Y;
+          else XB = Y;
+        }
+#pragma unroll 1
+        for (int off = 1; off < 32; off <<= 1) {
+          SF<P> YF = sf_shfl<P>(XF, off, false);
+          SF<P> YB = sf_shfl<P>(XB, off, false);
+          if (lane + off < 32) {
+            XF = sf_cf<P>(XF, YF);
+            XB = sf_cb<P>(XB, YB);
+          }
+        }
+        if (lane == 0) {
+          sf_st<P>(s_part[0][grp], XF);
+          sf_st<P>(s_part[1][grp], XB);
+        }
+      }
+      __syncthreads();
+      if (tid < 2) {   // fold the partials in order; the carry's read polynomial coefficients
+        const bool fw = tid == 0;
+        SF<P> X = sf_id<P>();
+#pragma unroll 1
+        for (int gi = 0; gi < ngroups; ++gi) {
+          const SF<P> y = sf_ld<P>(s_part[tid][gi]);
+          X = fw ? sf_cf<P>(X, y) : sf_cb<P>(X, y);
+        }
+        // read(S(Delta) C) = e^{-Delta} sum_r beta_r Delta^r,
+        // beta_r = sum_{q >= r} c_q C(q, q - r) C_{q - r}
+#pragma unroll
+        for (int r = 0; r <= P; ++r) {
+          double br = 0.0;
+#pragma unroll
+          for (int q = r; q <= P; ++q) br = fma(rcoef(P, KIND, q) * binom(q, q - r), X.M[q - r], br);
+          s_beta[tid][r] = br;
+        }
+      }
+    }
+    __syncthreads();
+    DF_STAMP(5);
+    // ---- carry pass and output
+    {
+      double bF[P + 1], bB[P + 1];
+#pragma unroll
+      for (int r = 0; r <= P; ++r) {
+        bF[r] = s_beta[0][r];
+        bB[r] = s_beta[1][r];
+      }
+      double D = Fx.D, E = Fx.E;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int j = j0 + k;
+        D += s_t[j];
+        E *= s_e[j];
+        double h = bF[P];
+#pragma unroll
+        for (int r = P - 1; r >= 0; --r) h = fma(h, D, bF[r]);
+        s_u[j] = fma(E, h, s_u[j]);
+      }
+      D = Bx.D;
+      E = Bx.E;
+#pragma unroll
+      for (int k = ITEMS - 1; k >= 0; --k) {
+        const int j = j0 + k;
+        double h = bB[P];
+#pragma unroll
+        for (int r = P - 1; r >= 0; --r) h = fma(h, D, bB[r]);
+        const double val = a.os2 * fma(E, h, s_u[j]);
+        D += s_t[j];
+        E *= s_e[j];
+        if (USER) {
+          if (j < cnt) {
+            const int pi = s_pi[j];
+            if (pi >= a.tgt_off) ocol[pi - a.tgt_off] = val;
+          }
+        } else {
+          s_u[j] = val;
+        }
+      }
+    }
+    if (!USER) {   // this warp's contiguous outputs
+      __syncwarp();
+      const int wb = warp * 32 * ITEMS;
+      const int we = min(cnt, wb + 32 * ITEMS);
+#pragma unroll 1
+      for (int j = wb + lane; j < we; j += 32) ocol[c0 + j] = s_u[j];
+    }
+    if (col + 1 < a.nrhs) {
+      __syncthreads();   // s_u / s_beta / s_wsum of this column consumed
+      if (!USER) issue_v(col + 1);
+    }
+  }   // column loop
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (a.dbg) {
+    __syncthreads();
+    DF_STAMP(6);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side.  Shapes (BLOCK, ITEMS): k_d1_fast 0 = (512, 15), 1 = (640, 11), 2 = (768, 9),
+// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (384, 19), 6 = (512, 15), 7 = (768, 9).
+// The default is chosen by measurement.
 template <int BLOCK, int ITEMS>
 static size_t df_smem() {
   constexpr int SUB = BLOCK * ITEMS;
@@ -442,7 +877,8 @@ static size_t df_smem() {
 
 struct DFShape {
   int block, items;
-  const void* fn[10];  // [KIND * 5 + p]: KIND 0 moment order p, KIND 1 moment order p + 1
+  // [user order][KIND * 5 + p]: KIND 0 moment order p, KIND 1 moment order p + 1
+  const void* fn[2][10];
   size_t smem;
 };
 
@@ -451,23 +887,45 @@ static DFShape make_shape() {
   DFShape s;
   s.block = BLOCK;
   s.items = ITEMS;
-  s.fn[0] = (const void*)k_d1_fast<0, 0, BLOCK, ITEMS>;
-  s.fn[1] = (const void*)k_d1_fast<1, 0, BLOCK, ITEMS>;
-  s.fn[2] = (const void*)k_d1_fast<2, 0, BLOCK, ITEMS>;
-  s.fn[3] = (const void*)k_d1_fast<3, 0, BLOCK, ITEMS>;
-  s.fn[4] = (const void*)k_d1_fast<4, 0, BLOCK, ITEMS>;
-  s.fn[5] = (const void*)k_d1_fast<1, 1, BLOCK, ITEMS>;
-  s.fn[6] = (const void*)k_d1_fast<2, 1, BLOCK, ITEMS>;
-  s.fn[7] = (const void*)k_d1_fast<3, 1, BLOCK, ITEMS>;
-  s.fn[8] = (const void*)k_d1_fast<4, 1, BLOCK, ITEMS>;
-  s.fn[9] = (const void*)k_d1_fast<5, 1, BLOCK, ITEMS>;
+  const void* f[10] = {
+      (const void*)k_d1_fast<0, 0, BLOCK, ITEMS>, (const void*)k_d1_fast<1, 0, BLOCK, ITEMS>,
+      (const void*)k_d1_fast<2, 0, BLOCK, ITEMS>, (const void*)k_d1_fast<3, 0, BLOCK, ITEMS>,
+      (const void*)k_d1_fast<4, 0, BLOCK, ITEMS>, (const void*)k_d1_fast<1, 1, BLOCK, ITEMS>,
+      (const void*)k_d1_fast<2, 1, BLOCK, ITEMS>, (const void*)k_d1_fast<3, 1, BLOCK, ITEMS>,
+      (const void*)k_d1_fast<4, 1, BLOCK, ITEMS>, (const void*)k_d1_fast<5, 1, BLOCK, ITEMS>};
+  for (int p = 0; p < 10; ++p) s.fn[0][p] = s.fn[1][p] = f[p];
   s.smem = df_smem<BLOCK, ITEMS>();
   return s;
 }
 
-static DFShape g_shapes[4];
+template <int BLOCK, int ITEMS, bool USER>
+static void flag_fns(const void** f) {
+  f[0] = (const void*)k_d1_ov<0, 0, BLOCK, ITEMS, USER>;
+  f[1] = (const void*)k_d1_ov<1, 0, BLOCK, ITEMS, USER>;
+  f[2] = (const void*)k_d1_ov<2, 0, BLOCK, ITEMS, USER>;
+  f[3] = (const void*)k_d1_ov<3, 0, BLOCK, ITEMS, USER>;
+  f[4] = (const void*)k_d1_ov<4, 0, BLOCK, ITEMS, USER>;
+  f[5] = (const void*)k_d1_ov<1, 1, BLOCK, ITEMS, USER>;
+  f[6] = (const void*)k_d1_ov<2, 1, BLOCK, ITEMS, USER>;
+  f[7] = (const void*)k_d1_ov<3, 1, BLOCK, ITEMS, USER>;
+  f[8] = (const void*)k_d1_ov<4, 1, BLOCK, ITEMS, USER>;
+  f[9] = (const void*)k_d1_ov<5, 1, BLOCK, ITEMS, USER>;
+}
+template <int BLOCK, int ITEMS>
+static DFShape make_shape_flag() {
+  DFShape s;
+  s.block = BLOCK;
+  s.items = ITEMS;
+  flag_fns<BLOCK, ITEMS, false>(s.fn[0]);
+  flag_fns<BLOCK, ITEMS, true>(s.fn[1]);
+  s.smem = df_smem<BLOCK, ITEMS>();
+  return s;
+}
+
+constexpr int DF_NSHAPE = 8;
+static DFShape g_shapes[DF_NSHAPE];
 static int g_shapes_ready = 0;
-static int g_default_shape = 2;   // 768 x 9: best measured (profiles/)
+static int g_default_shape = 4;   // k_d1_ov 256 x 27: best measured (tools/sweep_d1.py)
 
 static gp_status df_init() {
   if (g_shapes_ready) return GP_OK;
@@ -475,11 +933,17 @@ static gp_status df_init() {
   g_shapes[1] = make_shape<640, 11>();
   g_shapes[2] = make_shape<768, 9>();
   g_shapes[3] = make_shape<1024, 7>();
+  g_shapes[4] = make_shape_flag<256, 27>();
+  g_shapes[5] = make_shape_flag<384, 19>();
+  g_shapes[6] = make_shape_flag<512, 15>();
+  g_shapes[7] = make_shape_flag<768, 9>();
   for (auto& s : g_shapes)
-    for (int p = 0; p < 10; ++p)
-      GPM_CUDA(cudaFuncSetAttribute(s.fn[p], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)s.smem));
-  if (const char* e = getenv("GPM_D1_SHAPE")) g_default_shape = std::max(0, std::min(3, atoi(e)));
+    for (int u = 0; u < 2; ++u)
+      for (int p = 0; p < 10; ++p)
+        GPM_CUDA(cudaFuncSetAttribute(s.fn[u][p], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)s.smem));
+  if (const char* e = getenv("GPM_D1_SHAPE"))
+    g_default_shape = std::max(0, std::min(DF_NSHAPE - 1, atoi(e)));
   g_shapes_ready = 1;
   return GP_OK;
 }
@@ -493,7 +957,7 @@ gp_status df_shape_info(int shape, int* capacity, int* max_grid) {
   int dev = 0, nsm = 0, occ = 0;
   GPM_CUDA(cudaGetDevice(&dev));
   GPM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s.fn[2], s.block, s.smem));
+  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s.fn[1][2], s.block, s.smem));
   *capacity = s.block * s.items;
   *max_grid = occ * nsm;
   return GP_OK;
@@ -533,7 +997,7 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   cfg.attrs = at;
   cfg.numAttrs = pl.d1_pdl ? 2 : 1;
   void* args[] = {&a};
-  GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[kind * 5 + pl.P], args));
+  GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[user_order ? 1 : 0][kind * 5 + pl.P], args));
   return GP_OK;
 }
 

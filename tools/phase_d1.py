@@ -10,7 +10,7 @@ c = W.CONFIGS[2]
 names = ["tma+load", "pass1", "scan", "grid.sync", "carries", "pass2+store"]
 for n in (10000, 1000000):
     x = torch.from_numpy(W.config_points(c)[:n]).cuda()
-    for shape in (2,):
+    for shape in (int(os.environ.get("GPM_D1_SHAPE", "2")),):
         plan = g.Plan(x, g.Kernel(int(os.environ.get("NU2", "5")), c.ell))
         plan.set_option(1, shape)
         V = torch.randn((64, n), dtype=torch.float64, device="cuda")   # fresh v (> L2)
