@@ -50,6 +50,16 @@ def peaks():
         return FALLBACK_HBM, "fallback"
 
 
+def d1_kernel_name(shape):
+    """Name of the d = 1 kernel (nu = 5/2, user order) of a plan's thread-block shape
+    (gp_plan_set_option option 1)."""
+    shapes = {0: "k_d1_fast<2,0,512,15>", 1: "k_d1_fast<2,0,640,11>", 2: "k_d1_fast<2,0,768,9>",
+              3: "k_d1_fast<2,0,1024,7>", 4: "k_d1_ov<2,0,256,27,user>",
+              5: "k_d1_ov<2,0,384,19,user>", 6: "k_d1_ov<2,0,512,15,user>",
+              7: "k_d1_ov<2,0,768,9,user>"}
+    return shapes.get(shape, f"d1 shape {shape}")
+
+
 def ncu_traffic(key):
     try:
         with open(TRAFFIC_PATH) as f:
@@ -383,7 +393,7 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": int(args.steps * launches),
         "clocks": clocks,
         "roofline": {
-            "bound": "hbm", "kernel": "k_d1_fast<2,768,9>",
+            "bound": "hbm", "kernel": d1_kernel_name(plan.query(7)),
             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
             "frac": achieved / hbm,
             "traffic": ncu_traffic("d1_nu52_n1e6"),
