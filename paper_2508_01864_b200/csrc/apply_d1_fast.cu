@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
   __shared__ double s_wf[NW][NSF], s_wb[NW][NSF];
   __shared__ double s_wsum[NW][NM];
   __shared__ double s_beta[2][P + 1];
-  __shared__ double s_part[2][8][NSF];
+  __shared__ double s_part[2][16][NSF];   // warp partials of the record fold (grid <= 512)
   __shared__ unsigned long long s_base;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -867,7 +867,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
 
 // ---------------------------------------------------------------------------
 // Host side.  Shapes (BLOCK, ITEMS): k_d1_fast 0 = (512, 15), 1 = (640, 11), 2 = (768, 9),
-// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (384, 19), 6 = (512, 15), 7 = (768, 9).
+// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (384, 19), 6 = (512, 15), 7 = (128, 27) (two CTAs
+// per SM).
 // The default is chosen by measurement.
 template <int BLOCK, int ITEMS>
 static size_t df_smem() {
@@ -936,7 +937,7 @@ static gp_status df_init() {
   g_shapes[4] = make_shape_flag<256, 27>();
   g_shapes[5] = make_shape_flag<384, 19>();
   g_shapes[6] = make_shape_flag<512, 15>();
-  g_shapes[7] = make_shape_flag<768, 9>();
+  g_shapes[7] = make_shape_flag<128, 27>();   // 97 KB: two CTAs per SM
   for (auto& s : g_shapes)
     for (int u = 0; u < 2; ++u)
       for (int p = 0; p < 10; ++p)
