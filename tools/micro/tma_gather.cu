@@ -36,6 +36,35 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = threadIdx.x; j < cnt; j += blockDim.x) out[c0 + j] = __ldg(v + s_p[j]);
     return;
   }
+  if (MODE == 3) {   // split: TMA gather4 for [0, h) issued by warp 0, LDG for [h, cnt)
+    const int h = (cnt / 2) & ~3;
+    if (threadIdx.x == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mbar)),
+                   "r"((unsigned)(h / 4) * 64u));
+    if (threadIdx.x < 32) {
+      for (int g = threadIdx.x; g * 4 < h; g += 32) {
+        int r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r[q] = s_p[g * 4 + q] >> 1;
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(s_v + g * 16)),
+            "l"(tm), "r"(su32(&mbar)), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+            : "memory");
+      }
+    } else {
+      for (int j = h + threadIdx.x - 32; j < cnt; j += blockDim.x - 32) out[c0 + j] = __ldg(v + s_p[j]);
+    }
+    unsigned ok = 0;
+    while (!ok)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(su32(&mbar)));
+    for (int j = threadIdx.x; j < h; j += blockDim.x)
+      out[c0 + j] = s_v[(j >> 2) * 16 + (j & 3) * 2 + (s_p[j] & 1)];
+    return;
+  }
   const unsigned bytes = MODE == 1 ? ((cnt + 3) / 4) * 64u : cnt * 16u;
   if (threadIdx.x == 0)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mbar)),
@@ -111,22 +140,24 @@ int main() {
   cudaMalloc(&dm, sizeof(CUtensorMap) * NV);
   cudaMemcpy(dm, hm.data(), sizeof(CUtensorMap) * NV, cudaMemcpyHostToDevice);
 
-  const int grid = 296, chunk = (n + grid - 1) / grid;
-  const size_t smem = ((chunk * 4 + 127) / 128) * 128 + ((chunk + 3) / 4) * 128 + 256;
+  const int grid = 148, chunk = (n + grid - 1) / grid;
+  const size_t smem = ((chunk * 4 + 127) / 128) * 128 + ((chunk / 2 + 3) / 4) * 128 + 256;
   cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[] = {"LDG gather", "TMA gather4", "bulk 16B"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char* names[] = {"LDG gather", "TMA gather4", "bulk 16B", "split TMA+LDG"};
+  for (int mode : {0, 3}) {
     auto run = [&](int r) {
       const double* v = dv + (size_t)(r % NV) * n;
       double* o = dout + (size_t)(r % NV) * n;
       if (mode == 0) k<0><<<grid, 256, smem>>>(dm + r % NV, dp, v, o, n, chunk);
       if (mode == 1) k<1><<<grid, 256, smem>>>(dm + r % NV, dp, v, o, n, chunk);
       if (mode == 2) k<2><<<grid, 256, smem>>>(dm + r % NV, dp, v, o, n, chunk);
+      if (mode == 3) k<3><<<grid, 256, smem>>>(dm + r % NV, dp, v, o, n, chunk);
     };
     for (int r = 0; r < 10; ++r) run(r);
     if (cudaGetLastError() != cudaSuccess) { printf("launch error\n"); }
