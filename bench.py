@@ -55,7 +55,7 @@ def d1_kernel_name(shape):
     (gp_plan_set_option option 1)."""
     shapes = {0: "k_d1_fast<2,0,512,15>", 1: "k_d1_fast<2,0,640,11>", 2: "k_d1_fast<2,0,768,9>",
               3: "k_d1_fast<2,0,1024,7>", 4: "k_d1_ov<2,0,256,27,user>",
-              5: "k_d1_ov<2,0,384,19,user>", 6: "k_d1_ov<2,0,512,15,user>",
+              5: "k_d1_ov<2,0,192,37,user>", 6: "k_d1_ov<2,0,512,15,user>",
               7: "k_d1_ov<2,0,128,27,user>"}
     return shapes.get(shape, f"d1 shape {shape}")
 

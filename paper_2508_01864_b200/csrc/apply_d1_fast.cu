@@ -708,10 +708,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
     __syncthreads();
     const SF<P> Fx = sf_cf<P>(sf_ld<P>(s_wf[warp]), fe);   // chunk ref -> my ref (forward)
     const SF<P> Bx = sf_cb<P>(be, sf_ld<P>(s_wb[warp]));   // my last point -> chunk last
-    // ---- local pass 2: both recurrences (without the other chunks) interleaved in one
-    // loop, forward over k and backward over ITEMS-1-k: two independent chains
+    // ---- local pass 2: both recurrences (without the other chunks) interleaved, forward
+    // over item k and backward over item ITEMS-1-k (two independent chains); an item's
+    // first read waits in r1[] until the other direction reaches it, then
+    // loc = u + read_F + read_B replaces u (about ITEMS values live at once, not 2 ITEMS)
     {
-      double MF[P + 1], MB[P + 1], rf[ITEMS], rb[ITEMS];
+      double MF[P + 1], MB[P + 1], r1[ITEMS];
 #pragma unroll
       for (int q = 0; q <= P; ++q) {
         MF[q] = Fx.M[q];
@@ -719,18 +721,20 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
       }
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const int jf = j0 + k, jb = j0 + ITEMS - 1 - k;
-        advance<P>(MF, s_t[jf], s_e[jf]);
-        rf[k] = readc0<P, KIND>(MF);
-        MF[0] += s_u[jf];
-        rb[ITEMS - 1 - k] = readc0<P, KIND>(MB);
-        MB[0] += s_u[jb];
-        advance<P>(MB, s_t[jb], s_e[jb]);
-      }
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const int j = j0 + k;
-        s_u[j] = (KIND == 0 ? s_u[j] : 0.0) + (rf[k] + rb[k]);
+        const int kf = k, kb = ITEMS - 1 - k;
+        advance<P>(MF, s_t[j0 + kf], s_e[j0 + kf]);
+        const double rfk = readc0<P, KIND>(MF);
+        const double uf = s_u[j0 + kf];
+        MF[0] += uf;
+        if (kb < kf) s_u[j0 + kf] = (KIND == 0 ? uf : 0.0) + (rfk + r1[kf]);   // B came first
+        else if (kb > kf) r1[kf] = rfk;
+        const double rbk = readc0<P, KIND>(MB);
+        const double ub = s_u[j0 + kb];
+        MB[0] += ub;
+        advance<P>(MB, s_t[j0 + kb], s_e[j0 + kb]);
+        if (kb < kf) s_u[j0 + kb] = (KIND == 0 ? ub : 0.0) + (r1[kb] + rbk);   // F came first
+        else if (kb > kf) r1[kb] = rbk;
+        else s_u[j0 + kb] = (KIND == 0 ? ub : 0.0) + (rfk + rbk);              // middle item
       }
     }
     // ---- wait for every chunk's record of this column
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
 
 // ---------------------------------------------------------------------------
 // Host side.  Shapes (BLOCK, ITEMS): k_d1_fast 0 = (512, 15), 1 = (640, 11), 2 = (768, 9),
-// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (384, 19), 6 = (512, 15), 7 = (128, 27) (two CTAs
+// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (192, 37), 6 = (512, 15), 7 = (128, 27) (two CTAs
 // per SM).
 // The default is chosen by measurement.
 template <int BLOCK, int ITEMS>
@@ -935,7 +939,7 @@ static gp_status df_init() {
   g_shapes[2] = make_shape<768, 9>();
   g_shapes[3] = make_shape<1024, 7>();
   g_shapes[4] = make_shape_flag<256, 27>();
-  g_shapes[5] = make_shape_flag<384, 19>();
+  g_shapes[5] = make_shape_flag<192, 37>();
   g_shapes[6] = make_shape_flag<512, 15>();
   g_shapes[7] = make_shape_flag<128, 27>();   // 97 KB: two CTAs per SM
   for (auto& s : g_shapes)
