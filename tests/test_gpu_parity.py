@@ -264,6 +264,31 @@ def test_multi_rhs_batches(gpm, d):
     assert np.max(np.abs(KZ[9].cpu().numpy() - ref)) < 1e-9 * np.abs(ref).max() * 50
 
 
+@pytest.mark.parametrize("n", [3000, 3001, 200_003])
+@pytest.mark.parametrize("nrhs", [2, 5])
+def test_rank_order_multi_rhs_pipeline(gpm, n, nrhs):
+    """d = 1 rank order with several columns in one launch: every column equals its
+    single-column apply bitwise, over repeated launches (the exchange's record counts
+    carry across launches); odd n exercises the non-bulk-copy loads."""
+    import torch
+    x = _points("normal", n, 1, 90 + nrhs)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, (0.05,)))
+    V = to_dev(np.random.default_rng(n + nrhs).standard_normal((nrhs, n)))
+    VR = torch.stack([plan.to_rank(V[c].contiguous()) for c in range(nrhs)])
+    for rep in range(3):   # repeated launches: the record counts carry across launches
+        KR = plan.kmvm_rank(VR)
+        for c in range(nrhs):
+            assert torch.equal(KR[c], plan.kmvm_rank(VR[c].contiguous())), (rep, c)
+    rows = workloads_rows(n)
+    check_rows(plan.from_rank(KR[nrhs - 1]).cpu().numpy(), x, V[nrhs - 1].cpu().numpy(), 5, "l1",
+               (0.05,), 1.0, rows=rows, what=f"pipeline n={n} nrhs={nrhs}")
+
+
+def workloads_rows(n):
+    return np.unique(np.concatenate([np.arange(0, min(n, 64)), np.arange(n - min(n, 64), n),
+                                     np.random.default_rng(5).choice(n, min(n, 256), replace=False)]))
+
+
 @pytest.mark.parametrize("d,ell", [(2, (0.6, 0.9)), (3, (0.7, 0.8, 0.9))])
 def test_large_n_segments_over_256_tiles(gpm, d, ell):
     """N > 2^18: the top D&C node spans > 256 tiles (carry folds over many tile
