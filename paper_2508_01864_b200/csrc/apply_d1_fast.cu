@@ -884,7 +884,7 @@ struct DFShape {
   int block, items;
   // [user order][KIND * 5 + p]: KIND 0 moment order p, KIND 1 moment order p + 1
   const void* fn[2][10];
-  size_t smem;
+  size_t smem[2];   // [user order]: k_d1_ov in rank order has no permutation in smem
 };
 
 template <int BLOCK, int ITEMS>
@@ -899,7 +899,7 @@ static DFShape make_shape() {
       (const void*)k_d1_fast<2, 1, BLOCK, ITEMS>, (const void*)k_d1_fast<3, 1, BLOCK, ITEMS>,
       (const void*)k_d1_fast<4, 1, BLOCK, ITEMS>, (const void*)k_d1_fast<5, 1, BLOCK, ITEMS>};
   for (int p = 0; p < 10; ++p) s.fn[0][p] = s.fn[1][p] = f[p];
-  s.smem = df_smem<BLOCK, ITEMS>();
+  s.smem[0] = s.smem[1] = df_smem<BLOCK, ITEMS>();
   return s;
 }
 
@@ -923,7 +923,8 @@ static DFShape make_shape_flag() {
   s.items = ITEMS;
   flag_fns<BLOCK, ITEMS, false>(s.fn[0]);
   flag_fns<BLOCK, ITEMS, true>(s.fn[1]);
-  s.smem = df_smem<BLOCK, ITEMS>();
+  s.smem[0] = sizeof(double) * (3 * BLOCK * ITEMS + 8);   // t, u, e (a larger L1 carve-out)
+  s.smem[1] = df_smem<BLOCK, ITEMS>();
   return s;
 }
 
@@ -946,7 +947,7 @@ static gp_status df_init() {
     for (int u = 0; u < 2; ++u)
       for (int p = 0; p < 10; ++p)
         GPM_CUDA(cudaFuncSetAttribute(s.fn[u][p], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)s.smem));
+                                      (int)s.smem[u]));
   if (const char* e = getenv("GPM_D1_SHAPE"))
     g_default_shape = std::max(0, std::min(DF_NSHAPE - 1, atoi(e)));
   g_shapes_ready = 1;
@@ -962,7 +963,7 @@ gp_status df_shape_info(int shape, int* capacity, int* max_grid) {
   int dev = 0, nsm = 0, occ = 0;
   GPM_CUDA(cudaGetDevice(&dev));
   GPM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s.fn[1][2], s.block, s.smem));
+  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s.fn[1][2], s.block, s.smem[1]));
   *capacity = s.block * s.items;
   *max_grid = occ * nsm;
   return GP_OK;
@@ -992,7 +993,7 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.d1_grid);
   cfg.blockDim = dim3(sh.block);
-  cfg.dynamicSmemBytes = sh.smem;
+  cfg.dynamicSmemBytes = sh.smem[user_order ? 1 : 0];
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
