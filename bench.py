@@ -468,13 +468,24 @@ def run_ours(args, ws, rank, local):
     return line
 
 
+def ncu_fp64(key):
+    """FP64 FLOPs per apply of a workload (profiles/ncu_fp64.json, ncu instruction counts)
+    and the derived FP64 peak (TFLOP/s), or (None, None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fp64.json")) as f:
+            d = json.load(f)
+        return d.get(key), d.get("peak_fp64_tflops")
+    except (OSError, ValueError):
+        return None, None
+
+
 def extra_configs(g, dev, stream, ws, rank, hbm, args):
     """d = 2 (config 3) and d = 3 (config 4) K.v; d=1,2,3 at N = 2^20 (the metric's
     'N=1e6, d=1..3'); config-5 CG solve time with --cg."""
     import torch
     out = {}
 
-    def apply_stats(x_np, kern, reps, vecs=4, grad=False):
+    def apply_stats(x_np, kern, reps, vecs=4, grad=False, fp64_key=None):
         x = torch.from_numpy(x_np).to(dev)
         t0 = time.perf_counter()
         plan = g.Plan(x, kern, stream)
@@ -493,11 +504,18 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
                "model_gbs": plan.model_bytes / mean_l / 1e9,
                "frac_hbm": plan.model_bytes / mean_l / 1e9 / hbm,
                "struct_mb": plan.struct_bytes / 1e6}
+        flop, peak = ncu_fp64(fp64_key) if fp64_key else (None, None)
+        if flop:   # d >= 2 is bound by FP64 issue, not HBM: the ALU roofline
+            tf = flop / (sec_max / reps) / 1e12
+            res["alu_roofline"] = {"bound": "alu", "fp64_flop_per_apply": flop,
+                                   "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                                   "frac": tf / peak}
         plan.close()
         return res
 
     c3 = W.CONFIGS[3]
-    out["config3_d2_n2e5_nu32_l1"] = apply_stats(W.config_points(c3), g.Kernel(3, c3.ell), 20)
+    out["config3_d2_n2e5_nu32_l1"] = apply_stats(W.config_points(c3), g.Kernel(3, c3.ell), 20,
+                                                 fp64_key="config3_d2_nu32_l1")
     # config 3's rectangular product K_zx v (20,000 queries): union setup + applies
     x3 = torch.from_numpy(W.config_points(c3)).to(dev)
     z3 = torch.from_numpy(W.config_queries(c3)).to(dev)
@@ -526,7 +544,8 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
     out["config2_d1_n1e6_nu52_dlengthscale"] = apply_stats(
         W.config_points(c2), g.Kernel(5, c2.ell), 50, grad=True)
     c4 = W.CONFIGS[4]
-    out["config4_d3_n5e5_nu52_l1"] = apply_stats(W.config_points(c4), g.Kernel(5, c4.ell), 5)
+    out["config4_d3_n5e5_nu52_l1"] = apply_stats(W.config_points(c4), g.Kernel(5, c4.ell), 5,
+                                                 fp64_key="config4_d3_nu52_l1")
     for d, reps in [(2, 10), (3, 3)]:
         xn = W.uniform_points(1 << 20, d, 1000 + d)
         out[f"sweep_d{d}_n2^20_nu32_l1"] = apply_stats(xn, g.Kernel(3, (0.1,) * d), reps)
@@ -545,6 +564,12 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
                              "relres_max": info["relres_max"], "rhs": 4, "beta": beta,
                              "ms_per_iter": cg_s / max(info["iters"], 1) * 1e3,
                              "preconditioner": "none (Alg 2 with s_P = I)"}
+        flop, peak = ncu_fp64("config5_d2_prod32_nrhs4")
+        if flop:   # one 4-column apply per iteration dominates (vector updates are O(N))
+            tf = flop * info["iters"] / cg_s / 1e12
+            out["config5_cg"]["alu_roofline"] = {"bound": "alu", "fp64_flop_per_iter": flop,
+                                                 "achieved": tf, "peak": peak,
+                                                 "unit": "TFLOP/s", "frac": tf / peak}
         # the paper's preconditioned CG (App A: rank-k pivoted Cholesky + Woodbury), f3
         rank = 400
         torch.cuda.synchronize()
