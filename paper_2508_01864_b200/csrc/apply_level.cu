@@ -620,13 +620,14 @@ __device__ __forceinline__ double lv_y(const LvArgs& g, int64_t pos) {
 }
 
 // Structure of one carried (multi-tile) pass, precomputed at setup (it does not depend on
-// v): per position the gap to the previous position of its node, e^{-gap}, the split
-// offset alpha, e^{-alpha}, the rank and the channel.  37 B per position, read coalesced.
+// v): per position the gap to the previous position of its node, the split offset alpha,
+// the rank and the channel: 20 B per position, read coalesced.  e^{-gap} and e^{-alpha}
+// are recomputed per tile in k_cp (two branch-free fexp_neg per position and launch: the
+// same values bit for bit, 16 B per position less DRAM traffic -- config 4 moves 2.1 GB of
+// staged structure per apply at 36 B per position).
 struct HpView {
   const double* d;
-  const double* e;
   const double* a;
-  const double* ea;
   const unsigned* rc;   // rank | channel << 30; CP_NONE: padding
 };
 constexpr unsigned CP_RMASK = 0x3FFFFFFFu;
@@ -637,28 +638,21 @@ __host__ __device__ inline int64_t hp_padded(int64_t nact) {
   return (nact + LV_TILE - 1) / LV_TILE * LV_TILE;
 }
 __host__ __device__ inline size_t hp_bytes(int64_t nact) {
-  return ((size_t)hp_padded(nact) * 36 + 255) & ~size_t(255);
+  return ((size_t)hp_padded(nact) * 20 + 255) & ~size_t(255);
 }
 __host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nact) {
   const int64_t np = hp_padded(nact);
   HpView v;
   v.d = reinterpret_cast<const double*>(base);
-  v.e = v.d + np;
-  v.a = v.e + np;
-  v.ea = v.a + np;
-  v.rc = reinterpret_cast<const unsigned*>(v.ea + np);
+  v.a = v.d + np;
+  v.rc = reinterpret_cast<const unsigned*>(v.a + np);
   return v;
 }
 
 __global__ void k_hp_prep(LvArgs g, unsigned char* base) {
-  __shared__ double tab[64];
-  fexp_table_init(tab);
-  __syncthreads();
   HpView v = hp_view(base, g.n_act);
   double* d = const_cast<double*>(v.d);
-  double* e = const_cast<double*>(v.e);
   double* a = const_cast<double*>(v.a);
-  double* ea = const_cast<double*>(v.ea);
   unsigned* rc = const_cast<unsigned*>(v.rc);
   const int64_t smask = (int64_t(1) << g.lseg) - 1;
   const int64_t np = hp_padded(g.n_act);
@@ -669,12 +663,10 @@ __global__ void k_hp_prep(LvArgs g, unsigned char* base) {
       const Elem el = lv_elem(g, pos);
       const double dl = (pos & smask) == 0 ? 0.0 : el.y - lv_y(g, pos - 1);
       d[w] = dl;
-      e[w] = fexp_neg(dl, tab);
       a[w] = el.a;
-      ea[w] = fexp_neg(el.a, tab);
       rc[w] = (unsigned)el.r | ((unsigned)el.ch << 30);
-    } else {
-      d[w] = 0.0; e[w] = 1.0; a[w] = 0.0; ea[w] = 0.0; rc[w] = CP_NONE;
+    } else {   // identity: no gap; alpha = 800 makes e^{-alpha} exactly 0 (fexp_neg: d >= 708)
+      d[w] = 0.0; a[w] = 800.0; rc[w] = CP_NONE;
     }
   }
 }
@@ -701,13 +693,13 @@ struct HpDesc {
 //   MODE 1: tile aggregates (forward, backward) -> aggs;
 //   MODE 2: apply, with the tile carries folded from MODE 1's aggregates of the node.
 struct CpStage {
-  double d[LV_TILE], e[LV_TILE], a[LV_TILE], ea[LV_TILE];
+  double d[LV_TILE], a[LV_TILE];
   unsigned rc[LV_TILE];   // rank | channel << 30
 };
 struct CpSmem {
   CpStage st[2];
 };
-constexpr unsigned CP_STAGE_BYTES = 36u * LV_TILE;
+constexpr unsigned CP_STAGE_BYTES = 20u * LV_TILE;
 
 // Tile carries of every node, once per (column, pass, direction): an exclusive scan of the
 // tile aggregates of k_cp<1> (forward: tiles in order; backward: reversed), one warp per
@@ -777,9 +769,7 @@ __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDe
   const HpView v = hp_view(hpbase + hd.off, hd.nact);
   mbar_expect_tx(bar, CP_STAGE_BYTES);
   tma_load_1d(st.d, v.d + T0, 8 * LV_TILE, bar);
-  tma_load_1d(st.e, v.e + T0, 8 * LV_TILE, bar);
   tma_load_1d(st.a, v.a + T0, 8 * LV_TILE, bar);
-  tma_load_1d(st.ea, v.ea + T0, 8 * LV_TILE, bar);
   tma_load_1d(st.rc, v.rc + T0, 4 * LV_TILE, bar);
 }
 
@@ -792,10 +782,12 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
   CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
   __shared__ CpScratch<A> sc;
   __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double s_tab[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = tid * CP_ITEMS;
   const int G = gridDim.x;
   int p_iss = 0;   // pass of the last issued tile (thread 0)
+  fexp_table_init(s_tab);
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -834,6 +826,14 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
     const int tps = 1 << (hd.lseg - LV_LOGTILE);    // tiles per node
     const int first = t & ~(tps - 1);
     const int last = min(first + tps, hd.ntiles) - 1;
+    // e^{-gap}, e^{-alpha} of my positions (not staged: recomputed, shared by the columns)
+    double ek[CP_ITEMS], eak[CP_ITEMS];
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      const int z = cpz(i0 + k);
+      ek[k] = fexp_neg(E.d[z], s_tab);
+      eak[k] = fexp_neg(E.a[z], s_tab);
+    }
 #pragma unroll 1
     for (int c = 0; c < nrhs; ++c) {
       LvAgg* aggs = g.aggs + ((int64_t)c * npass + p) * 2 * max_tiles;
@@ -872,9 +872,9 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
 #pragma unroll
         for (int k = CP_ITEMS - 1; k >= 0; --k) {    // reference at item 7
           const int z = cpz(i0 + k);
-          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], E.ea[z], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], D, Ee);
           D += E.d[z];
-          Ee *= E.e[z];
+          Ee *= ek[k];
         }
         X.D = D; X.E = Ee;
 #pragma unroll 1
@@ -904,9 +904,9 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
 #pragma unroll
           for (int k = 0; k < CP_ITEMS; ++k) {
             const int z = cpz(i0 + k);
-            A::advance_all(M, E.d[z], E.e[z]);
+            A::advance_all(M, E.d[z], ek[k]);
             const int ch = E.rc[z] >> 30;
-            const double a = E.a[z], ea = E.ea[z];
+            const double a = E.a[z], ea = eak[k];
             of[k] = A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
           }
@@ -922,8 +922,8 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
         for (int k = 0; k < CP_ITEMS; ++k) {         // reference just before item 0
           const int z = cpz(i0 + k);
           D += E.d[z];
-          Ee *= E.e[z];
-          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], E.ea[z], D, Ee);
+          Ee *= ek[k];
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], D, Ee);
         }
         X.D = D; X.E = Ee;
 #pragma unroll 1
@@ -956,10 +956,10 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
             const int z = cpz(i0 + k);
             const unsigned rcz = E.rc[z];
             const int ch = rcz >> 30;
-            const double a = E.a[z], ea = E.ea[z];
+            const double a = E.a[z], ea = eak[k];
             const double val = of[k] + A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
-            A::advance_all(M, E.d[z], E.e[z]);
+            A::advance_all(M, E.d[z], ek[k]);
             const unsigned r = rcz & CP_RMASK;
             if (r != CP_RMASK) slot[r] = val;
           }

@@ -49,10 +49,14 @@ def test_d1_grad_config2_full_size(gpm, two_nu):
     for r in range(3):
         check_rows(out[r], x, V[r], two_nu, "l1", c.ell, 1.0, rows=rows, grad=True,
                    what=f"grad config2 nu={two_nu}/2 rhs {r}")
-    # rank-order entry point and single-column calls agree bitwise with the batch
+    # a single-column call of the same entry point agrees bitwise with the batch column;
+    # the rank-order entry point is a separately compiled kernel (user/rank template
+    # flag): the same arithmetic, so equal up to the compiler's FMA contraction choices
+    one = plan.kmvm_dlengthscale(to_dev(V[1])).cpu()
+    assert torch.equal(one, torch.from_numpy(out[1]))
     vr = plan.to_rank(to_dev(V[1]))
-    o_r = plan.kmvm_dlengthscale(vr, rank_order=True)
-    assert torch.equal(plan.from_rank(o_r).cpu(), torch.from_numpy(out[1]))
+    o_r = plan.from_rank(plan.kmvm_dlengthscale(vr, rank_order=True)).cpu().numpy()
+    assert np.max(np.abs(o_r - out[1])) <= 1e-14 * np.abs(out[1]).max()
 
 
 @pytest.mark.parametrize("d", [2, 3])
