@@ -536,6 +536,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
     tmy = j0 + ITEMS - 1 < cnt ? __ldg(a.ts + c0 + j0 + ITEMS - 1) : tlast;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");   // v, records, counter of the previous apply
+  // the next launch may be scheduled now: its CTAs only get an SM when one of ours exits,
+  // and its griddepcontrol.wait still waits for this whole grid (memory included)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) {
     const unsigned long long b0 = __ldcg(&pub[b].epoch), b1 = __ldcg(&pub[DF_REPL * G + b].epoch);
     s_base = b0 > b1 ? b0 : b1;
@@ -862,7 +865,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
       if (!USER) issue_v(col + 1);
     }
   }   // column loop
-  asm volatile("griddepcontrol.launch_dependents;");
   if (a.dbg) {
     __syncthreads();
     DF_STAMP(6);
