@@ -55,7 +55,7 @@ def d1_kernel_name(shape):
     (gp_plan_set_option option 1)."""
     shapes = {0: "k_d1_fast<2,0,512,15>", 1: "k_d1_fast<2,0,640,11>", 2: "k_d1_fast<2,0,768,9>",
               3: "k_d1_fast<2,0,1024,7>", 4: "k_d1_ov<2,0,256,27,user>",
-              5: "k_d1_ov<2,0,192,37,user>", 6: "k_d1_ov<2,0,512,15,user>",
+              5: "k_d1_ov<2,0,256,31,user>", 6: "k_d1_ov<2,0,512,15,user>",
               7: "k_d1_ov<2,0,128,27,user>"}
     return shapes.get(shape, f"d1 shape {shape}")
 
@@ -546,6 +546,9 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
     c4 = W.CONFIGS[4]
     out["config4_d3_n5e5_nu52_l1"] = apply_stats(W.config_points(c4), g.Kernel(5, c4.ell), 5,
                                                  fp64_key="config4_d3_nu52_l1")
+    for n1 in (1 << 20, 1 << 22):   # d = 1 above the single-chunk capacity (k_d1_coop)
+        out[f"sweep_d1_n2^{n1.bit_length() - 1}_nu32"] = apply_stats(
+            W.uniform_points(n1, 1, 1001), g.Kernel(3, (0.1,)), 50)
     for d, reps in [(2, 10), (3, 3)]:
         xn = W.uniform_points(1 << 20, d, 1000 + d)
         out[f"sweep_d{d}_n2^20_nu32_l1"] = apply_stats(xn, g.Kernel(3, (0.1,) * d), reps)

@@ -312,7 +312,7 @@ GP_API gp_status gp_plan_query(gp_plan p, int what, int64_t *value);
  *   option 0: force the d=1 apply path (0 auto, 1 single-sub-tile if it fits, 2 multi-sub-tile);
  *   option 1: thread-block shape of path 1: k_d1_fast (grid barrier) 0 = 512x15, 1 = 640x11,
  *             2 = 768x9, 3 = 1024x7; k_d1_ov (split-barrier exchange) 4 = 256x27,
- *             5 = 192x37, 6 = 512x15, 7 = 128x27 (two CTAs per SM)
+ *             5 = 256x31 (the default above 4's capacity), 6 = 512x15, 7 = 128x27 (two CTAs per SM)
  *             (threads x points per thread);
  *   option 2: programmatic dependent launch of the d=1 kernel (1 default, 0 off);
  *   option 3: L2 prefetch of v before the user-order gathers (1 default, 0 off). */

@@ -481,6 +481,8 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
                     cudaStream_t s, int kind);
 int df_default_shape();
 
+int df_large_shape();
+
 gp_status d1_prepare(Plan& pl) {
   static int attr_done = 0;
   if (!attr_done) {
@@ -496,7 +498,14 @@ gp_status d1_prepare(Plan& pl) {
   if (!coop) return fail(GP_ERR_UNSUPPORTED, "device does not support cooperative launch");
   // fast path: one shared-memory chunk per CTA (apply_d1_fast.cu)
   int fast_grid = 0, cap = 0;
-  if (pl.d1_shape < 0) pl.d1_shape = df_default_shape();
+  if (pl.d1_shape < 0) {
+    // default shape; above its capacity (#SMs x 6912) the 31-point-per-thread shape keeps
+    // the single-chunk kernel up to #SMs x 7936 (N = 2^20 and a little beyond)
+    pl.d1_shape = df_default_shape();
+    GPM_TRY(df_shape_info(pl.d1_shape, &cap, &fast_grid));
+    const int large = df_large_shape();
+    if (large >= 0 && pl.n > (int64_t)cap * fast_grid) pl.d1_shape = large;
+  }
   GPM_TRY(df_shape_info(pl.d1_shape, &cap, &fast_grid));
   if (pl.d1_force != 2 && fast_grid > 0) {
     int64_t g = std::min<int64_t>(fast_grid, std::max<int64_t>(1, (pl.n + 1023) / 1024));

@@ -873,7 +873,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
 
 // ---------------------------------------------------------------------------
 // Host side.  Shapes (BLOCK, ITEMS): k_d1_fast 0 = (512, 15), 1 = (640, 11), 2 = (768, 9),
-// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (192, 37), 6 = (512, 15), 7 = (128, 27) (two CTAs
+// 3 = (1024, 7); k_d1_ov 4 = (256, 27), 5 = (256, 31) (chosen above 4's capacity), 6 = (512, 15), 7 = (128, 27) (two CTAs
 // per SM).
 // The default is chosen by measurement.
 template <int BLOCK, int ITEMS>
@@ -942,7 +942,7 @@ static gp_status df_init() {
   g_shapes[2] = make_shape<768, 9>();
   g_shapes[3] = make_shape<1024, 7>();
   g_shapes[4] = make_shape_flag<256, 27>();
-  g_shapes[5] = make_shape_flag<192, 37>();
+  g_shapes[5] = make_shape_flag<256, 31>();   // larger chunks: N up to #SMs x 7936
   g_shapes[6] = make_shape_flag<512, 15>();
   g_shapes[7] = make_shape_flag<128, 27>();   // 97 KB: two CTAs per SM
   for (auto& s : g_shapes)
@@ -957,6 +957,7 @@ static gp_status df_init() {
 }
 
 int df_default_shape() { return g_default_shape; }
+int df_large_shape() { return g_default_shape == 4 ? 5 : -1; }
 
 // capacity per CTA and max co-resident grid for a shape
 gp_status df_shape_info(int shape, int* capacity, int* max_grid) {
