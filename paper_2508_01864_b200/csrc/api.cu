@@ -476,7 +476,7 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
 gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
   if (!p) return fail(GP_ERR_INVALID_ARG, "NULL plan");
   if (option == 0) {
-    if (value < 0 || value > 2) return fail(GP_ERR_INVALID_ARG, "bad value for option 0");
+    if (value < 0 || value > 3) return fail(GP_ERR_INVALID_ARG, "bad value for option 0");
     p->pl.d1_force = (int)value;
   } else if (option == 1) {
     if (value < 0 || value > 7) return fail(GP_ERR_INVALID_ARG, "bad value for option 1");

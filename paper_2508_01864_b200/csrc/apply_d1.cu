@@ -482,6 +482,9 @@ gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
 int df_default_shape();
 
 int df_large_shape();
+int db_capacity_sub();
+gp_status db_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
+                    cudaStream_t s, int kind);
 
 gp_status d1_prepare(Plan& pl) {
   static int attr_done = 0;
@@ -498,6 +501,14 @@ gp_status d1_prepare(Plan& pl) {
   if (!coop) return fail(GP_ERR_UNSUPPORTED, "device does not support cooperative launch");
   // fast path: one shared-memory chunk per CTA (apply_d1_fast.cu)
   int fast_grid = 0, cap = 0;
+  if (pl.d1_force == 3) {   // testing knob: the reduce-then-scan path at any size
+    const int64_t nsub = (pl.n + db_capacity_sub() - 1) / db_capacity_sub();
+    pl.d1_grid = (int)nsub;
+    pl.d1_chunk = db_capacity_sub();
+    pl.d1_path = 3;
+    GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)nsub));
+    return GP_OK;
+  }
   if (pl.d1_shape < 0) {
     // default shape; above its capacity (#SMs x 6912) the 31-point-per-thread shape keeps
     // the single-chunk kernel up to #SMs x 7936 (N = 2^20 and a little beyond)
@@ -525,6 +536,17 @@ gp_status d1_prepare(Plan& pl) {
       }
       return GP_OK;
     }
+  }
+  if (pl.d1_force != 2) {
+    // path 3: reduce-then-scan over sub-tiles in three plain launches (apply_d1_fast.cu
+    // k_d1_big), any N, every nu and the lengthscale gradient
+    const int64_t nsub = (pl.n + db_capacity_sub() - 1) / db_capacity_sub();
+    if (nsub > (int64_t)1 << 30) return fail(GP_ERR_UNSUPPORTED, "d=1 problem too large");
+    pl.d1_grid = (int)nsub;
+    pl.d1_chunk = db_capacity_sub();
+    pl.d1_path = 3;
+    GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)nsub));   // sub-tile records + carries
+    return GP_OK;
   }
   int occ = 0;
   GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_d1_coop<2>, D1_BLOCK,
@@ -555,6 +577,7 @@ gp_status d1_prepare(Plan& pl) {
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
                     cudaStream_t s, int kind) {
   if (pl.d1_path == 1) return df_launch(pl, v, out, nrhs, user_order, s, kind);
+  if (pl.d1_path == 3) return db_launch(pl, v, out, nrhs, user_order, s, kind);
   if (kind != 0)
     return fail(GP_ERR_UNSUPPORTED, "lengthscale-gradient MVM for d=1 needs n <= #SMs x 6912");
   if (pl.P > 2)

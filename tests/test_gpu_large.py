@@ -19,7 +19,7 @@ def test_large_n_sampled_rows(gpm, d, n, two_nu):
     ell = (0.05, 0.05, 0.1)[:d] if d > 1 else (0.01,)
     plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell))
     if d == 1:
-        assert plan.d1_path == 2                   # beyond 148 x 6912 points
+        assert plan.d1_path == 3                   # beyond 148 x 7936 points: reduce-then-scan
     out = plan.kmvm(to_dev(v)).cpu().numpy()
     rows = W.sample_rows(x, 96)
     check_rows(out, x, v, two_nu, "l1", ell, 1.0, rows=rows, what=f"large d={d} n={n}")

@@ -62,6 +62,41 @@ def test_d1_multi_subtile_path(gpm, two_nu):
     check_rows(out2, x, v, two_nu, "l1", (0.02,), 1.0, rows=rows, what="d1 coop")
 
 
+@pytest.mark.parametrize("n", [1, 7, 6912, 6913, 60001, 200_003])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7])
+def test_d1_reduce_then_scan_path(gpm, n, two_nu):
+    """The three-launch d = 1 path (sub-tile records, one-CTA carry scan, apply) forced at
+    small sizes: user order against the oracle, rank order equal to user order to rounding
+    (separately compiled kernels), multi-RHS columns bitwise equal to single columns."""
+    import torch
+    x = _points("normal" if n > 100 else "ties", n, 1, n + two_nu)
+    V = np.random.default_rng(n).standard_normal((2, n))
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, (0.02,)))
+    plan.set_option(0, 3)
+    assert plan.d1_path == 3
+    out = plan.kmvm(to_dev(V)).cpu().numpy()
+    rows = W.sample_rows(x, 600) if n > 600 else None
+    for c in range(2):
+        check_rows(out[c], x, V[c], two_nu, "l1", (0.02,), 1.0, rows=rows,
+                   what=f"d1 path 3 nu={two_nu}/2 n={n} col {c}")
+    assert np.array_equal(plan.kmvm(to_dev(V[1])).cpu().numpy(), out[1])
+    vr = plan.to_rank(to_dev(V[0]))
+    o_r = plan.from_rank(plan.kmvm_rank(vr)).cpu().numpy()
+    assert np.max(np.abs(o_r - out[0])) <= 1e-14 * max(np.abs(out[0]).max(), 1e-300)
+
+
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
+def test_d1_reduce_then_scan_gradient(gpm, two_nu):
+    n = 60001
+    x = _points("normal", n, 1, 77)
+    v = np.random.default_rng(78).standard_normal(n)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, (0.02,)))
+    plan.set_option(0, 3)
+    out = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "l1", (0.02,), 1.0, rows=W.sample_rows(x, 400), grad=True,
+               what=f"d1 path 3 grad nu={two_nu}/2")
+
+
 def test_config1_all_rows(gpm):
     c = W.CONFIGS[1]
     x = W.config_points(c)
