@@ -589,13 +589,20 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
                                      "relres_max": info2["relres_max"], "rhs": 4,
                                      "beta": beta2, "preconditioner": f"pivoted Cholesky rank {rank}",
                                      "ms_per_iter": (t2 - t1) / max(info2["iters"], 1) * 1e3}
-        # posterior mean at the 10,000 queries (union setup + K_zx alpha + h(z)^T beta)
+        pc.close()
+        # posterior mean at the 10,000 queries (union setup + K_zx alpha + h(z)^T beta), the
+        # first call (device allocations of the union structure included) and a repeat
         z5 = torch.from_numpy(W.config_queries(c5)).to(dev)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        plan.predict(z5, alpha2, beta2, stream=stream)
-        torch.cuda.synchronize()
-        out["config5_predict"] = {"predict_s": time.perf_counter() - t0, "m": int(z5.shape[0])}
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            plan.predict(z5, alpha2, beta2, stream=stream)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        out["config5_predict"] = {"predict_s": ts[0], "predict_s_repeat": min(ts[1:]),
+                                  "m": int(z5.shape[0]),
+                                  "note": "gp_predict builds the union x u z structure per call"}
         pc.close()
         plan.close()
     return out

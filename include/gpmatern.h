@@ -297,7 +297,8 @@ GP_API gp_status gp_fit(const double *x, int64_t n, int d, const gp_kernel *k0, 
  *            out = K_zx alpha exactly;
  *   Hz     : for a basis mean, the m x L column-major basis at z (device) and
  *            beta of length L; pass NULL and L = 0 for the affine mean.
- *   out    : m (device).  Builds and frees a union structure internally. */
+ *   out    : m (device).  Builds and frees a union structure internally (for repeated
+ *            predictions at the same z, gp_kzx_setup once + gp_kzx reuse it). */
 GP_API gp_status gp_predict(gp_plan p, const double *z, int64_t m, const double *alpha,
                      const double *beta, const double *Hz, int L, double *out, void *stream);
 
