@@ -79,3 +79,45 @@ def test_config5_gp_inference(gpm):
     # plausibility (not parity): the fit tracks the generating function
     f = 1 + 0.5 * z[:, 0] - 0.3 * z[:, 1] + np.sin(6 * z[:, 0]) * np.cos(4 * z[:, 1])
     assert np.sqrt(np.mean((mu - f) ** 2)) < 0.05
+
+
+@pytest.mark.parametrize("rank_order", [False, True])
+def test_config2_back_to_back_applies(gpm, rank_order):
+    """SURVEY §8(c) c2 #15 in the launch configuration bench.py times: 100 applies with
+    distinct v captured in one CUDA graph and replayed back to back (programmatic dependent
+    launch: each launch releases the next right after its own griddepcontrol.wait, the
+    split-barrier records carry their counts across launches). Every output equals the
+    isolated apply of the same v bitwise; applies 0, 1, 50, 99 are checked against the
+    oracle on sampled rows."""
+    import torch
+    c = W.CONFIGS[2]
+    x = W.config_points(c)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, c.ell))
+    nv = 100
+    V = torch.stack([to_dev(W.config_vector(c, r)) for r in range(nv)])
+    if rank_order:
+        V = torch.stack([plan.to_rank(V[r]) for r in range(nv)])
+    O = torch.empty_like(V)
+    f = plan.kmvm_rank if rank_order else plan.kmvm
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for r in range(3):
+            f(V[r], O[r], stream=s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        for r in range(nv):
+            f(V[r], O[r], stream=s)
+    O.zero_()
+    for _ in range(2):
+        with torch.cuda.stream(s):
+            graph.replay()
+    torch.cuda.synchronize()
+    for r in range(nv):
+        assert torch.equal(O[r], f(V[r].contiguous())), r
+    rows = W.sample_rows(x, 256)
+    for r in (0, 1, 50, 99):
+        out = (plan.from_rank(O[r]) if rank_order else O[r]).cpu().numpy()
+        check_rows(out, x, W.config_vector(c, r), 5, "l1", c.ell, 1.0, rows=rows,
+                   what=f"back-to-back apply {r}")
+    plan.close()
