@@ -15,6 +15,9 @@ for d, n, form, two_nu in [(1, 3000, 0, 5), (2, 3000, 0, 3), (2, 2500, 1, 3), (3
     plan.cross(z).kzx(V[0].contiguous())
     if d == 1:
         plan.set_option(0, 2); plan.kmvm(V[1].contiguous()); plan.set_option(0, 0)
+        plan.set_option(0, 3); plan.kmvm(V); plan.kmvm_rank(plan.to_rank(V[0]))   # path 3
+        plan.kmvm_dlengthscale(V[1].contiguous()); plan.set_option(0, 0)
+        plan.kmvm_dlengthscale(V)
     if form == 1 or d == 1:
         y = torch.randn(n, dtype=torch.float64, device="cuda")
         plan.cg_solve(y, 0.1, mean=g.MEAN_AFFINE, rtol=1e-6, max_iter=200)
