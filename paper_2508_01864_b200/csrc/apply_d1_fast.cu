@@ -447,22 +447,20 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_fast(DFArgs a) {
 //   5. meanwhile: the block scan (warp shuffles) for the within-chunk prefixes and
 //   6. the local pass 2: both recurrences from the within-chunk prefixes only, storing
 //      loc_j = u_j + read_F + read_B;
-//   7. wait (thread 0 polls, fence.acq_rel, __syncthreads), fold the other chunks'
-//      records into the carries C_F, C_B;
+//   7. wait (thread 0 polls the counter with ld.acquire.gpu, then __syncthreads; the
+//      records are read with ld.global.cg, i.e. from L2, the point of coherence), fold the
+//      other chunks' records (4 replicas, one record per lane, 16-byte loads) into the
+//      carries C_F, C_B;
 //   8. carry pass: the carries' contribution at a point Delta after their reference is
 //      e^{-Delta} sum_r beta_r Delta^r (beta from C once per CTA), Delta and e^{-Delta}
 //      as running sums / products of the stored gaps: P + 1 FMAs per point and direction;
 //      out = os2 (loc + both contributions), stored per warp (rank order) or scattered.
 // Counter: bar[4..5] (u64) counts published columns x CTAs over the plan's life (zeroed at
 // prepare); a CTA's record holds its own published-column count, so every CTA derives
-// the same target (base + col + 1) x grid at kernel start.
+// the same target (base + col + 1) x grid at kernel start (CUDA-graph safe: no host epoch).
+// The dependent launch is released right after griddepcontrol.wait: its CTAs get an SM
+// only when one of ours exits, and its own wait covers this whole grid.
 constexpr int DF_REPL = 4;   // k_d1_ov record replicas (readers spread over 4 lines per record)
-
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 template <int P, int KIND, int BLOCK, int ITEMS, bool USER>
 __global__ void __launch_bounds__(BLOCK, 1) k_d1_ov(DFArgs a) {
