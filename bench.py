@@ -564,15 +564,18 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
         plan = g.Plan(torch.from_numpy(x).to(dev), g.Kernel(3, c5.ell, form=g.FORM_PRODUCT), stream)
         yt = torch.from_numpy(y).to(dev)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        alpha, beta, info = plan.cg_solve(yt, c5.noise_sigma ** 2, mean=g.MEAN_AFFINE, rtol=1e-8,
-                                          max_iter=40000)
-        torch.cuda.synchronize()
-        cg_s = time.perf_counter() - t0
+        cg_clock = ClockSampler(dev.index if dev.index is not None else 0)
+        with cg_clock:   # a few seconds of sustained FP64 load: the SM clock is reported
+            t0 = time.perf_counter()
+            alpha, beta, info = plan.cg_solve(yt, c5.noise_sigma ** 2, mean=g.MEAN_AFFINE,
+                                              rtol=1e-8, max_iter=40000)
+            torch.cuda.synchronize()
+            cg_s = time.perf_counter() - t0
         out["config5_cg"] = {"cg_solve_s": cg_s, "iters": info["iters"],
                              "relres_max": info["relres_max"], "rhs": 4, "beta": beta,
                              "ms_per_iter": cg_s / max(info["iters"], 1) * 1e3,
-                             "preconditioner": "none (Alg 2 with s_P = I)"}
+                             "preconditioner": "none (Alg 2 with s_P = I)",
+                             "clocks": cg_clock.summary()}
         flop, peak = ncu_fp64("config5_d2_prod32_nrhs4")
         if flop:   # one 4-column apply per iteration dominates (vector updates are O(N))
             tf = flop * info["iters"] / cg_s / 1e12
