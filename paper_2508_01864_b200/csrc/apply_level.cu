@@ -441,6 +441,111 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low2(LvArgs g) {
   for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
 }
 
+// ---- fused low levels, d = 2, NC right-hand sides per CTA (nrhs >= 2, e.g. config 5's CG
+// with [y, 1, x1, x2]): the kernel values of the near field and each level's gaps,
+// e^{-gap}, alpha, e^{-alpha} do not depend on v -- computed once per tile and shared by the
+// columns (k_low2 recomputes them per column).  acc / pts of column c at c * n.
+template <int NC>
+struct LvPointsM {
+  double u[NC][LV_TILE], t1[LV_TILE], t2[LV_TILE], acc[NC][LV_TILE];
+};
+
+template <class A, int NC>
+__global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvPointsM<NC>& Pt = *reinterpret_cast<LvPointsM<NC>*>(smem_raw);
+  __shared__ TScratch<A> sc;
+  const int tid = threadIdx.x;
+  const int i0 = tid * CP_ITEMS;
+  const int c0 = blockIdx.y * NC;
+  const int nc = min(NC, nrhs - c0);
+  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
+  fexp_table_init(sc.tab);
+#pragma unroll 2
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) {
+    const Pt4 p = g.pts[T0 + i];
+    Pt.t1[i] = p.t1;
+    Pt.t2[i] = p.t2;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      Pt.u[c][i] = c < nc ? g.pts[(int64_t)(c0 + c) * g.n + T0 + i].u : 0.0;
+      Pt.acc[c][i] = 0.0;
+    }
+  }
+  __syncthreads();
+  const int lmax = min(LV_LOGTILE, g.L);
+  const int lb = min(lv_clamp_lb(g.lb, LV_LOGTILE), lmax);
+  if (lb > 0 && i0 < cnt) {   // near field: one kernel value per pair, NC columns
+    double ti1[CP_ITEMS], ti2[CP_ITEMS], acc[CP_ITEMS][NC];
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      const int i = min(i0 + k, cnt - 1);
+      ti1[k] = Pt.t1[i];
+      ti2[k] = Pt.t2[i];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[k][c] = 0.0;
+    }
+    const int bs = (i0 >> lb) << lb;
+    const int be = min(bs + (1 << lb), cnt);
+#pragma unroll 1
+    for (int j = bs; j < be; ++j) {
+      const double tj1 = Pt.t1[j], tj2 = Pt.t2[j];
+      double uj[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) uj[c] = Pt.u[c][j];
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k) {
+        const double v = (i0 + k != j) ? kval<A, 2>(fabs(ti1[k] - tj1), fabs(ti2[k] - tj2), 0.0, sc.tab)
+                                       : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[k][c] = fma(v, uj[c], acc[k][c]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k)
+      if (i0 + k < cnt)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) Pt.acc[c][i0 + k] += acc[k][c];
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int l = lb + 1; l <= lmax; ++l) {
+    const int* ord = g.ord2 + (size_t)(l - 1) * g.n + T0;
+    TItems it;
+    double y[CP_ITEMS];
+    load_ord8(ord, i0, cnt, (int)T0, it.o);
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      const int i = i0 + k;
+      const int r = it.o[k];
+      const int mid = ((i >> l) << l) + (1 << (l - 1));
+      const bool act = r >= 0 && T0 + mid < g.n;
+      y[k] = r >= 0 ? Pt.t2[r] : (k > 0 ? y[k - 1] : 0.0);
+      it.a[k] = act ? fabs(Pt.t1[r] - Pt.t1[mid]) : 0.0;
+      it.ch[k] = act ? (r >> (l - 1)) & 1 : -1;
+    }
+    const bool nstart = (i0 & ((1 << l) - 1)) == 0;
+    const double ypre = (!nstart && i0 <= cnt) ? Pt.t2[__ldg(ord + i0 - 1) - (int)T0] : 0.0;
+    titems_gaps(it, y, ypre, nstart, sc.tab);
+#pragma unroll 1
+    for (int c = 0; c < nc; ++c) {
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k) it.u[k] = it.o[k] >= 0 ? Pt.u[c][it.o[k]] : 0.0;
+      double of[CP_ITEMS];
+      seg_engine<A>(it, l, of, sc);
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[c][it.o[k]] += of[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int c = 0; c < nc; ++c)
+#pragma unroll 4
+    for (int i = tid; i < LV_TILE; i += CP_BLOCK)
+      if (i < cnt) g.acc[(int64_t)(c0 + c) * g.n + T0 + i] = Pt.acc[c][i];
+}
+
 // ---- fused low levels, d = 3: every (l1 <= min(10, L), l2 <= l1) of one tile
 template <class A>
 __global__ void __launch_bounds__(CP_BLOCK, 3) k_low3(LvArgs g) {
@@ -1165,7 +1270,19 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   }
   // fused low levels (writes acc for every point: no memset needed)
   if constexpr (A::NCH == 2) {
-    k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
+    if (nrhs >= 2 && !getenv("GPM_LOW2_PERCOL")) {   // columns share the v-independent work
+      constexpr int NC = 4;
+      static bool attr = false;
+      if (!attr) {
+        GPM_CUDA(cudaFuncSetAttribute(k_low2m<A, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(LvPointsM<NC>)));
+        attr = true;
+      }
+      k_low2m<A, NC><<<dim3(tiles, (nrhs + NC - 1) / NC), CP_BLOCK, sizeof(LvPointsM<NC>), s>>>(
+          g, nrhs);
+    } else {
+      k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
+    }
     *launches += 1;
     GPM_CUDA(cudaGetLastError());
   } else {
