@@ -272,6 +272,9 @@ def run_ours(args, ws, rank, local):
     import torch
     import paper_2508_01864_b200 as g
     g.load_library()
+    # plan / scratch allocations through PyTorch's caching allocator (gp_set_allocator):
+    # setups after the first reuse cached blocks instead of cudaMalloc / cudaFree
+    g.use_torch_allocator()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     cfg = W.CONFIGS[2]
