@@ -201,6 +201,7 @@ __device__ __forceinline__ CSt<NS> cs_get(const LvAgg* g) {
 template <class A>
 struct CpScratch {
   CSt<A::NS> wf[CP_WARPS], wb[CP_WARPS], cf, cb;
+  double wsp[CP_WARPS];   // k_cp<1>: warp sums of the thread spans
 };
 
 // ---------------------------------------------------------------------------
@@ -968,6 +969,75 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
         if (tid >= 32 && tid < 32 + A::NS + 2)
           reinterpret_cast<double*>(&sc.cb)[tid - 32] = __ldcg(cr + sizeof(LvAgg) / 8 + tid - 32);
       }
+      if constexpr (MODE == 1) {
+        // ---- tile aggregates only: each thread's aggregates (direct form) shifted to the
+        // tile's reference points and summed (a fixed-order reduction: no scan of the
+        // (span, moments) pairs needed -- the spans are prefix sums of scalars)
+        S XF, XB;
+        double D = 0.0, Ee = 1.0, Db = 0.0, Eb = 1.0;
+#pragma unroll
+        for (int q = 0; q < A::NS; ++q) XF.M[q] = XB.M[q] = 0.0;
+#pragma unroll
+        for (int k = CP_ITEMS - 1; k >= 0; --k) {    // forward: reference at item 7
+          const int z = cpz(i0 + k);
+          A::inject_at(XF.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], D, Ee);
+          D += E.d[z];
+          Ee *= ek[k];
+        }
+#pragma unroll
+        for (int k = 0; k < CP_ITEMS; ++k) {         // backward: reference before item 0
+          const int z = cpz(i0 + k);
+          Db += E.d[z];
+          Eb *= ek[k];
+          A::inject_at(XB.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], Db, Eb);
+        }
+        // spans after my last position / before my first one within the tile
+        double incl = D;   // inclusive prefix sum of the thread spans (warp)
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        if (lane == 31) sc.wsp[warp] = incl;
+        __syncthreads();
+        double before = incl - D, wtot = 0.0, tot = 0.0;
+#pragma unroll
+        for (int w = 0; w < CP_WARPS; ++w) {
+          const double sw = sc.wsp[w];
+          if (w < warp) wtot += sw;
+          tot += sw;
+        }
+        before = fmax(before + wtot, 0.0);
+        const double after = tot - before - D;
+        A::advance_all(XF.M, fmax(after, 0.0), fexp_neg(fmax(after, 0.0), s_tab));
+        A::advance_all(XB.M, before, fexp_neg(before, s_tab));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int q = 0; q < A::NS; ++q) {
+            XF.M[q] += __shfl_xor_sync(0xffffffffu, XF.M[q], off);
+            XB.M[q] += __shfl_xor_sync(0xffffffffu, XB.M[q], off);
+          }
+        if (lane == 0) {
+          sc.wf[warp] = XF;
+          sc.wb[warp] = XB;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          S TF = sc.wf[0], TB = sc.wb[0];
+#pragma unroll 1
+          for (int w = 1; w < CP_WARPS; ++w)
+#pragma unroll
+            for (int q = 0; q < A::NS; ++q) {
+              TF.M[q] += sc.wf[w].M[q];
+              TB.M[q] += sc.wb[w].M[q];
+            }
+          TF.D = TB.D = tot;
+          TF.E = TB.E = fexp_neg(tot, s_tab);
+          cs_put<A::NS>(aggs + 2 * t, TF);
+          cs_put<A::NS>(aggs + 2 * t + 1, TB);
+        }
+      } else {
       // ---- forward: per-thread aggregate (direct form), warp scan, block carry, apply.
       {
         S X;
@@ -1069,6 +1139,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
             if (r != CP_RMASK) slot[r] = val;
           }
         }
+      }
       }
       __syncthreads();                               // scratch reuse by the next column
     }
