@@ -55,7 +55,7 @@ enum { GP_MEAN_NONE = 0, GP_MEAN_AFFINE = 1, GP_MEAN_BASIS = 2 }; /* P:73-82 [eq
  * with k_nu the half-integer closed forms of P:1273-1275.  Supported:
  *   two_nu in {1,3,5,7,9} (nu = 7/2, 9/2: P:1276-1277; d = 1 needs
  *   n <= 1022976 for them); d in {1,2,3}; form L1 for every d and nu; form PRODUCT for
- *   d <= 2 and two_nu <= 5
+ *   d <= 2 and every nu ((p+1)^2 mixed moments per channel; d = 3 only for two_nu = 1)
  *   (for d == 1 or two_nu == 1 the two forms coincide, and form is ignored).
  * Per-dimension lengthscales are reading R2 (the paper uses one l). */
 typedef struct {
@@ -144,9 +144,9 @@ GP_API gp_status gp_kmvm_rank(gp_plan p, const double *v_rank, int nrhs, double 
  * (eq dkernel_dvarsigma) and needs no extra MVM.  Computed by the same decomposition with
  * one more moment (g(s) = (s, s^2, (s^2 + s^3)/3) e^{-s} for nu = 1/2, 3/2, 5/2 in scaled
  * distance s = sqrt(2 nu) r): exact like gp_kmvm, no nugget, zero diagonal.
- * Supported: d = 1 (n <= 148 x 6912 = 1022976 points), the L1 form for d = 2, 3 and the
- * product form for d = 2 with nu <= 3/2 (product rule g(r1) k(r2) + k(r1) g(r2), (p+2)^2
- * moments per channel); other product forms return GP_ERR_UNSUPPORTED.  v_order: 0 = user order (layout as
+ * Supported: d = 1 (any n), the L1 form for d = 2 and for d = 3 with nu <= 7/2, and the
+ * product form for d = 2 with nu <= 7/2 (product rule g(r1) k(r2) + k(r1) g(r2), (p+2)^2
+ * moments per channel); other kernels return GP_ERR_UNSUPPORTED.  v_order: 0 = user order (layout as
  * gp_kmvm), 1 = the plan's stored order (as gp_kmvm_rank). */
 GP_API gp_status gp_kmvm_dlengthscale(gp_plan p, const double *v, int nrhs, double *out,
                                       int v_order, void *stream);

@@ -100,7 +100,8 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
   if (pl.acc.bytes < sizeof(double) * need) GPM_TRY(pl.acc.alloc(sizeof(double) * need));
   if (pl.pts.bytes < level_pt_bytes() * need) GPM_TRY(pl.pts.alloc(level_pt_bytes() * need));
   // tile aggregates and (k_cp_carry) tile carries, same layout
-  const size_t ag = 2 * sizeof(LvAgg) * 2 * (size_t)level_tiles(pl.n) * nrhs *
+  const size_t ag = 2 * level_rec_bytes(pl.d, pl.form == GP_FORM_PRODUCT, pl.P) * 2 *
+                   (size_t)level_tiles(pl.n) * nrhs *
                    std::max(1, pl.hp_npass);
   if (pl.aggs.bytes < ag) GPM_TRY(pl.aggs.alloc(ag));
   const size_t pb = sizeof(double) * (size_t)std::max(1, level_nparts(pl)) * pl.n * nrhs;

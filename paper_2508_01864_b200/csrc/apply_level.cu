@@ -86,6 +86,15 @@ __device__ __forceinline__ void lv_col(LvArgs& g) {
 
 __device__ __forceinline__ int ord3_index(int l1, int l2) { return (l1 - 1) * l1 / 2 + (l2 - 1); }
 
+// sum_q c_q s^q of a read profile (rcoef: Matern a_q for KIND 0, gradient b_q for KIND 1)
+template <int PM, int KIND>
+__device__ __forceinline__ double kpoly(double s) {
+  double poly = rcoef(PM, KIND, PM);
+#pragma unroll
+  for (int q = PM - 1; q >= 0; --q) poly = fma(poly, s, rcoef(PM, KIND, q));
+  return poly;
+}
+
 // Kernel value from per-dimension distances d_k = |t_ik - t_jk| (scaled coordinates):
 // L1: k(d1+d2(+d3)); product (d = 2): k(d1) k(d2); k(s) = sum_q a_q s^q e^{-s}.
 template <class A, int D>
@@ -105,10 +114,14 @@ __device__ __forceinline__ double kval(double d1, double d2, double d3, const do
     if constexpr (A::KIND == 0) {
       if constexpr (P == 0) return e;
       else if constexpr (P == 1) return e * ((1.0 + d1) * (1.0 + d2));
-      else return e * (fma(d1, fma(d1, 1.0 / 3.0, 1.0), 1.0) * fma(d2, fma(d2, 1.0 / 3.0, 1.0), 1.0));
-    } else {   // product rule: g(d1) k(d2) + k(d1) g(d2); nu = 1/2 (P = 1) or 3/2 (P = 2)
+      else if constexpr (P == 2)
+        return e * (fma(d1, fma(d1, 1.0 / 3.0, 1.0), 1.0) * fma(d2, fma(d2, 1.0 / 3.0, 1.0), 1.0));
+      else return e * (kpoly<P, 0>(d1) * kpoly<P, 0>(d2));   // nu = 7/2, 9/2
+    } else {   // product rule: g(d1) k(d2) + k(d1) g(d2); k of order P - 1, g = -s k'(s) of order P
       if constexpr (P == 1) return e * (d1 + d2);
-      else return e * ((d1 * d1) * (1.0 + d2) + (1.0 + d1) * (d2 * d2));
+      else if constexpr (P == 2) return e * ((d1 * d1) * (1.0 + d2) + (1.0 + d1) * (d2 * d2));
+      else
+        return e * fma(kpoly<P, 1>(d1), kpoly<P - 1, 0>(d2), kpoly<P - 1, 0>(d1) * kpoly<P, 1>(d2));
     }
   }
 }
@@ -183,14 +196,14 @@ __device__ __forceinline__ CSt<NS> cs_bcast(const CSt<NS>& s, int src) {
   for (int i = 0; i < NS; ++i) r.M[i] = __shfl_sync(0xffffffffu, s.M[i], src);
   return r;
 }
-template <int NS>
-__device__ __forceinline__ void cs_put(LvAgg* g, const CSt<NS>& s) {
+template <int NS, class R>
+__device__ __forceinline__ void cs_put(R* g, const CSt<NS>& s) {
   g->D = s.D; g->E = s.E;
 #pragma unroll
   for (int i = 0; i < NS; ++i) g->M[i] = s.M[i];
 }
-template <int NS>
-__device__ __forceinline__ CSt<NS> cs_get(const LvAgg* g) {
+template <int NS, class R>
+__device__ __forceinline__ CSt<NS> cs_get(const R* g) {
   CSt<NS> s;
   s.D = __ldcg(&g->D); s.E = __ldcg(&g->E);
 #pragma unroll
@@ -812,9 +825,10 @@ constexpr unsigned CP_STAGE_BYTES = 20u * LV_TILE;
 // node, 32 tiles per step (Kogge-Stone with the same combine as the tile scans).  k_cp<2>
 // then loads one record per direction instead of folding up to #tiles aggregates per column.
 template <class A>
-__global__ void __launch_bounds__(32) k_cp_carry(LvAgg* aggs, LvAgg* carr, const HpDesc* descs,
-                                                 int npass, int max_tiles) {
+__global__ void __launch_bounds__(32) k_cp_carry(LvRecFor<A::NS>* aggs, LvRecFor<A::NS>* carr,
+                                                 const HpDesc* descs, int npass, int max_tiles) {
   using S = CSt<A::NS>;
+  using Rec = LvRecFor<A::NS>;
   const int p = blockIdx.y;
   const int c = blockIdx.z >> 1, dir = blockIdx.z & 1;
   const HpDesc hd = descs[p];
@@ -823,8 +837,8 @@ __global__ void __launch_bounds__(32) k_cp_carry(LvAgg* aggs, LvAgg* carr, const
   if (first >= hd.ntiles) return;
   const int last = min(first + tps, hd.ntiles) - 1;
   const int64_t base = ((int64_t)c * npass + p) * 2 * max_tiles;
-  const LvAgg* ag = aggs + base;
-  LvAgg* cr = carr + base;
+  const Rec* ag = aggs + base;
+  Rec* cr = carr + base;
   const int lane = threadIdx.x;
   S cin = cs_id<A>();
   if (dir == 0) {
@@ -942,7 +956,8 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
     }
 #pragma unroll 1
     for (int c = 0; c < nrhs; ++c) {
-      LvAgg* aggs = g.aggs + ((int64_t)c * npass + p) * 2 * max_tiles;
+      LvRecFor<A::NS>* aggs =
+          reinterpret_cast<LvRecFor<A::NS>*>(g.aggs) + ((int64_t)c * npass + p) * 2 * max_tiles;
       double uc[CP_ITEMS], of[CP_ITEMS];
 #pragma unroll
       for (int k = 0; k < CP_ITEMS; ++k) uc[k] = un[k];
@@ -967,7 +982,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
         const double* cr = reinterpret_cast<const double*>(aggs + carr_off + 2 * t);
         if (tid < A::NS + 2) reinterpret_cast<double*>(&sc.cf)[tid] = __ldcg(cr + tid);
         if (tid >= 32 && tid < 32 + A::NS + 2)
-          reinterpret_cast<double*>(&sc.cb)[tid - 32] = __ldcg(cr + sizeof(LvAgg) / 8 + tid - 32);
+          reinterpret_cast<double*>(&sc.cb)[tid - 32] = __ldcg(cr + sizeof(LvRecFor<A::NS>) / 8 + tid - 32);
       }
       if constexpr (MODE == 1) {
         // ---- tile aggregates only: each thread's aggregates (direct form) shifted to the
@@ -1333,8 +1348,9 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
         g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
         carr_off);
     GPM_CUDA(cudaGetLastError());
+    LvRecFor<A::NS>* recs = reinterpret_cast<LvRecFor<A::NS>*>(g.aggs);
     k_cp_carry<A><<<dim3(pl.hp_maxtiles, pl.hp_npass, 2 * nrhs), 32, 0, pl.s2>>>(
-        g.aggs, g.aggs + carr_off, dd, pl.hp_npass, pl.hp_maxtiles);
+        recs, recs + carr_off, dd, pl.hp_npass, pl.hp_maxtiles);
     GPM_CUDA(cudaGetLastError());
     GPM_CUDA(cudaEventRecord(pl.ev_join, pl.s2));
     *launches += 2;
@@ -1421,11 +1437,13 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
   const bool prod = pl.form == GP_FORM_PRODUCT;
   const int P = pl.P;
   if (kind != 0) {   // lengthscale gradient: moment order p + 1
-    if (prod) {        // d = 2 product form, nu <= 3/2 ((p+2)^2 moments per channel)
-      if (pl.d != 2 || P > 1)
-        return fail(GP_ERR_UNSUPPORTED, "product-form lengthscale gradient: d = 2, nu <= 3/2 only");
+    if (prod) {        // d = 2 product form, nu <= 7/2 ((p+2)^2 moments per channel)
+      if (pl.d != 2 || P > 3)
+        return fail(GP_ERR_UNSUPPORTED, "product-form lengthscale gradient: d = 2, nu <= 7/2 only");
       if (P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
-      return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
+      if (P == 1) return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
+      if (P == 2) return lv_run<Alg<3, 2, true, 1>>(pl, nrhs, s, launches);
+      return lv_run<Alg<4, 2, true, 1>>(pl, nrhs, s, launches);
     }
     if (pl.d == 2) {
       switch (P) {
@@ -1457,7 +1475,9 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
     }
     if (P == 0) return lv_run<Alg<0, 2, true>>(pl, nrhs, s, launches);
     if (P == 1) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
-    return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
+    if (P == 2) return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
+    if (P == 3) return lv_run<Alg<3, 2, true>>(pl, nrhs, s, launches);
+    return lv_run<Alg<4, 2, true>>(pl, nrhs, s, launches);
   }
   switch (P) {
     case 0: return lv_run<Alg<0, 4, false>>(pl, nrhs, s, launches);

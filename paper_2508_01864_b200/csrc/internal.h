@@ -46,13 +46,30 @@ struct D1Agg {
 };
 
 // Level-pass tile aggregate (one direction): up to 4 channels x 5 moments (L1, d = 3,
-// nu = 9/2 or the nu = 7/2 gradient) or 2 channels x 9 mixed moments (product, d = 2).
-struct LvAgg {
+// nu = 9/2 or the nu = 7/2 gradient) or 2 channels x 9 mixed moments (product, d = 2,
+// nu <= 5/2) in the 184 B record LvAgg; the wider product states (2 x 16 / 2 x 25 mixed
+// moments: product nu = 7/2, 9/2 and the nu = 5/2, 7/2 gradients) use LvRec<32> / LvRec<50>.
+template <int W>
+struct LvRec {
   double D, E;
-  double M[20];
+  double M[W];
   int flag;
   int pad;
 };
+using LvAgg = LvRec<20>;
+// record width of an algebra with NS state doubles
+template <int NS>
+using LvRecFor = LvRec<(NS > 20 ? NS : 20)>;
+// bytes of the widest record a plan's level passes can use (product d = 2: 2 (p+2)^2
+// for the gradient, capped at the widest supported state)
+inline size_t level_rec_bytes(int d, int form_product, int P) {
+  int ns = 20;
+  if (d == 2 && form_product) {
+    const int w = 2 * (P + 2) * (P + 2);
+    ns = w > 50 ? 50 : (w > 20 ? w : 20);
+  }
+  return sizeof(double) * (2 + (size_t)ns) + 2 * sizeof(int);
+}
 
 // The stored structure of P:191 [§1], P:338 [§2.1], P:539 [§2.2.3], in HBM.
 //   "rank" = x1-rank: position of a point in the stable (t1, index) order.

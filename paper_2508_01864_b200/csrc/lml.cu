@@ -707,7 +707,7 @@ gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const
   GPM_TRY(apply_rank(pl, P0, KP, nc, s, 0));
   const bool has_dl = (pl.d == 1 || (pl.d == 2 && pl.form == GP_FORM_L1)) ||
                       (pl.d == 3 && pl.form == GP_FORM_L1 && pl.P <= 3) ||
-                      (pl.d == 2 && pl.form == GP_FORM_PRODUCT && pl.P <= 1);
+                      (pl.d == 2 && pl.form == GP_FORM_PRODUCT && pl.P <= 3);
   if (has_dl) GPM_TRY(apply_rank(pl, P0, DP, nc, s, 1));
   // (4) dots: col 0: a.Ka, a.dKa, a.a, r.a ; probe c: x_c.K p_c, x_c.dK p_c, x_c.p_c
   //     (x_c = A^-1 z_c from Lanczos, p_c = P^-1 z_c)

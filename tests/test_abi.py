@@ -66,8 +66,8 @@ def test_argument_validation_without_device(lib):
     assert lib.gp_setup(dummy, 10, 1, ctypes.byref(k), None, ctypes.byref(h)) == 1     # l <= 0
     k = g.Kernel(5, (0.1, 0.1, 0.1), form=g.FORM_PRODUCT).c()
     assert lib.gp_setup(dummy, 10, 3, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product d=3
-    k = g.Kernel(7, (0.1, 0.1), form=g.FORM_PRODUCT).c()
-    assert lib.gp_setup(dummy, 10, 2, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product 7/2
+    k = g.Kernel(7, (0.1, 0.1, 0.1), form=g.FORM_PRODUCT).c()
+    assert lib.gp_setup(dummy, 10, 3, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product d=3 7/2
 
 
 def test_no_cpu_fallback(lib):

@@ -87,10 +87,11 @@ def test_l1_grad_multi_level_sampled(gpm, d):
                    what=f"grad d{d} sampled rhs {r}")
 
 
-@pytest.mark.parametrize("two_nu", [1, 3])
+@pytest.mark.parametrize("two_nu", [1, 3, 5])
 @pytest.mark.parametrize("n", [3, 64, 2049, 5000])
 def test_product_grad_all_rows(gpm, two_nu, n):
-    """d = 2 product form (nu <= 3/2): the product rule through (p+2)^2 moments."""
+    """d = 2 product form (nu <= 5/2 here, 7/2 in test_gpu_high_nu): the product rule
+    through (p+2)^2 moments."""
     x = _pts(n, 2, 13 * n + two_nu, ties=(n % 2 == 1))
     v = np.random.default_rng(n + 7).standard_normal(n)
     ell = (0.1, 0.2)
@@ -114,7 +115,7 @@ def test_product_grad_multi_level_sampled(gpm):
 
 def test_grad_unsupported_and_errors(gpm):
     x = _pts(500, 2, 1)
-    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, (0.1, 0.1), form=1))
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(9, (0.1, 0.1), form=1))
     with pytest.raises(gpm.GPError) as e:
         plan.kmvm_dlengthscale(to_dev(np.ones(500)))
     assert e.value.name == "UNSUPPORTED"

@@ -56,10 +56,50 @@ def test_high_nu_config2_and_multilevel(gpm, two_nu):
                what=f"d3 multilevel nu={two_nu}/2")
 
 
+@pytest.mark.parametrize("two_nu", [7, 9])
+@pytest.mark.parametrize("n", [3, 64, 2049, 5000])
+@pytest.mark.parametrize("grad", [False, True])
+def test_high_nu_product_d2_all_rows(gpm, two_nu, n, grad):
+    """d = 2 product form for nu = 7/2, 9/2: (p+1)^2 = 16 / 25 mixed
+    moments per channel (wide tile records); the gradient (product rule, (p+2)^2 = 25
+    moments) for nu = 7/2, UNSUPPORTED for nu = 9/2."""
+    x = _pts(n, 2, 17 * n + two_nu, ties=(n % 2 == 1))
+    v = np.random.default_rng(n + two_nu + 3).standard_normal(n)
+    ell = (0.1, 0.2)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.1, form=1))
+    if grad and two_nu == 9:
+        with pytest.raises(gpm.GPError) as e:
+            plan.kmvm_dlengthscale(to_dev(v))
+        assert e.value.name == "UNSUPPORTED"
+        return
+    out = (plan.kmvm_dlengthscale(to_dev(v)) if grad else plan.kmvm(to_dev(v))).cpu().numpy()
+    check_rows(out, x, v, two_nu, "product", ell, 1.1, grad=grad,
+               what=f"product nu={two_nu}/2 n={n} grad={grad}")
+
+
+@pytest.mark.parametrize("two_nu", [7, 9])
+def test_high_nu_product_d2_multilevel_multirhs(gpm, two_nu):
+    """Carried passes (k_cp, k_cp_carry on the wide records) at 2e5 points, 3 columns."""
+    n = 200000
+    x = _pts(n, 2, 4321 + two_nu)
+    V = np.random.default_rng(two_nu).standard_normal((3, n))
+    ell = (0.05, 0.08)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.0, form=1))
+    out = plan.kmvm(to_dev(V)).cpu().numpy()
+    rows = W.sample_rows(x, 128)
+    for r in range(3):
+        check_rows(out[r], x, V[r], two_nu, "product", ell, 1.0, rows=rows,
+                   what=f"product nu={two_nu}/2 multilevel rhs {r}")
+    if two_nu == 7:
+        g = plan.kmvm_dlengthscale(to_dev(V[:1])).cpu().numpy()
+        check_rows(g[0] if g.ndim == 2 else g, x, V[0], two_nu, "product", ell, 1.0, rows=rows,
+                   grad=True, what="product nu=7/2 multilevel grad")
+
+
 def test_high_nu_unsupported(gpm):
-    x = _pts(300, 2, 1)
+    x = _pts(300, 3, 1)
     with pytest.raises(gpm.GPError) as e:
-        gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1), form=1))
+        gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1, 0.1), form=1))
     assert e.value.name == "UNSUPPORTED"
     x1 = _pts(60000, 1, 2)
     p1 = gpm.Plan(to_dev(x1), gpm.Kernel(7, (0.02,)))
