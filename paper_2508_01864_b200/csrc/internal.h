@@ -127,6 +127,7 @@ struct Precond {
   int64_t n = 0;
   DevBuf L;                    // n x k column-major, rank order
   DevBuf Cinv, W, Y;           // (I + L^T L / s2)^-1 (k x k) for the cached s2; scratch
+  DevBuf Wp;                   // L^T R row-block partials (k_wlt), summed in order by k_wred
   std::vector<int> piv;        // pivot ranks
   std::vector<double> G;       // L^T L (k x k, host)
   double s2 = -1.0, logdetC = 0.0;

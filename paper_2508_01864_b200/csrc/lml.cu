@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "algebra.cuh"
@@ -421,6 +422,149 @@ gp_status precond_logdet(Precond& pc, double s2, double* out, cudaStream_t s) {
   return GP_OK;
 }
 
+// ---- Woodbury solve for a few columns (nb <= 8): the two passes over L (n x k, the
+// dominant traffic: 8 n k bytes each) as streaming kernels instead of the library's
+// tall-skinny GEMMs.  Both are HBM-bound: L is read once per pass, coalesced along n.
+template <int NB>
+__host__ __device__ constexpr int wb_rows() { return 256; }   // k_wlt: rows of L per CTA (~8 CTAs per SM)
+constexpr int WB_THREADS = 256;
+
+// k_wlt: partial[(c k + j) nblk + b] = sum_{i in row block b} L[j n + i] R[c n + i].
+// Each lane keeps its rows' R values in registers for the whole CTA; a warp takes 32 / NB
+// columns at a time (32 partial dot products per lane) and reduces them with one
+// reduce-scatter butterfly (31 shuffles instead of 5 per value), leaving lane l with value l.
+template <int NB>
+__global__ void __launch_bounds__(WB_THREADS) k_wlt(const double* __restrict__ L,
+                                                    const double* __restrict__ R, int64_t n,
+                                                    int k, int nb, double* __restrict__ part) {
+  constexpr int WB_ROWS = wb_rows<NB>();
+  constexpr int RPL = WB_ROWS / 32;   // rows per lane
+  constexpr int G = 32 / NB;          // columns per warp step
+  const int64_t i0 = (int64_t)blockIdx.x * WB_ROWS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x;
+  double rr[NB][RPL];
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int64_t i = i0 + lane + 32 * t;
+      rr[c][t] = (c < nb && i < n) ? __ldg(R + (int64_t)c * n + i) : 0.0;
+    }
+  for (int j0 = warp * G; j0 < k; j0 += (WB_THREADS / 32) * G) {
+    double vals[32];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int j = j0 + g;
+      const double* Lj = L + (int64_t)j * n + i0 + lane;
+      double l[RPL];
+#pragma unroll
+      for (int t = 0; t < RPL; ++t)
+        l[t] = (j < k && i0 + lane + 32 * t < n) ? __ldcs(Lj + 32 * t) : 0.0;
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) acc = fma(l[t], rr[c][t], acc);
+        vals[g * NB + c] = acc;
+      }
+    }
+    // reduce-scatter: after the step with offset s, a lane holds the half of the values
+    // selected by its bit s; at the end vals[0] is the warp total of value `lane`
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      const bool up = (lane & sft) != 0;
+#pragma unroll
+      for (int i = 0; i < sft; ++i) {
+        const double send = up ? vals[i] : vals[i + sft];
+        const double keep = up ? vals[i + sft] : vals[i];
+        vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      }
+    }
+    const int j = j0 + lane / NB, c = lane % NB;
+    if (j < k && j < j0 + G) part[((int64_t)c * k + j) * nblk + blockIdx.x] = vals[0];
+  }
+}
+
+// k_wred: W[o] = sum_b part[o nblk + b], o = c k + j (fixed order: lane-strided, then a
+// warp tree; one warp per output, coalesced along b)
+__global__ void k_wred(const double* __restrict__ part, int nblk, int kn,
+                       double* __restrict__ W) {
+  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (o >= kn) return;
+  double s = 0.0;
+  const double* po = part + (int64_t)o * nblk;
+  for (int b = lane; b < nblk; b += 32) s += po[b];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) W[o] = s;
+}
+
+// k_wly: Z[c n + i] = b R[c n + i] + a sum_j L[j n + i] Y[c k + j]  (Z may alias R)
+template <int NB>
+__global__ void __launch_bounds__(WB_THREADS) k_wly(const double* __restrict__ L,
+                                                    const double* R, int64_t n, int k, int nb,
+                                                    const double* __restrict__ Y, double a,
+                                                    double b, double* Z) {
+  extern __shared__ double Ys[];   // [k][NB]
+  for (int t = threadIdx.x; t < k * NB; t += WB_THREADS) {
+    const int j = t / NB, c = t % NB;
+    Ys[t] = c < nb ? __ldg(Y + (int64_t)c * k + j) : 0.0;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * WB_THREADS + threadIdx.x;
+  if (i >= n) return;
+  double acc[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+  const double* Li = L + i;
+  int j = 0;
+  for (; j + 8 <= k; j += 8) {
+    double l[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) l[u] = __ldcs(Li + (int64_t)(j + u) * n);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) acc[c] = fma(l[u], Ys[(j + u) * NB + c], acc[c]);
+  }
+  for (; j < k; ++j) {
+    const double l = __ldcs(Li + (int64_t)j * n);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = fma(l, Ys[j * NB + c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+    if (c < nb) Z[(int64_t)c * n + i] = fma(b, R[(int64_t)c * n + i], a * acc[c]);
+}
+
+template <int NB>
+static gp_status wood_stream(Precond& pc, const double* R, int nb, double* Z, double a, double b,
+                             cudaStream_t s) {
+  const int k = pc.k;
+  const int64_t n = pc.n;
+  const int nblk = (int)((n + wb_rows<NB>() - 1) / wb_rows<NB>());
+  const size_t pb = 8 * (size_t)nblk * NB * k;
+  if (pc.Wp.bytes < pb) GPM_TRY(pc.Wp.alloc(pb));
+  k_wlt<NB><<<nblk, WB_THREADS, 0, s>>>(pc.L.as<double>(), R, n, k, nb, pc.Wp.as<double>());
+  GPM_CUDA(cudaGetLastError());
+  const int kn = k * nb;   // W is k x nb column-major
+  k_wred<<<(kn + 7) / 8, 256, 0, s>>>(pc.Wp.as<double>(), nblk, kn, pc.W.as<double>());
+  GPM_CUDA(cudaGetLastError());
+  const double one = 1.0, zero = 0.0;
+  GPM_CUBLAS(cublasSetStream(pc.h, s));
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_N, k, nb, k, &one, pc.Cinv.as<double>(), k,
+                         pc.W.as<double>(), k, &zero, pc.Y.as<double>(), k));
+  const size_t ysm = 8 * (size_t)k * NB;
+  if (ysm > 48 * 1024)
+    GPM_CUDA(cudaFuncSetAttribute(k_wly<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm));
+  k_wly<NB><<<(int)((n + WB_THREADS - 1) / WB_THREADS), WB_THREADS, ysm, s>>>(
+      pc.L.as<double>(), R, n, k, nb, pc.Y.as<double>(), a, b, Z);
+  GPM_CUDA(cudaGetLastError());
+  return GP_OK;
+}
+
 // Z = P^-1 R = R/s2 - L Cinv L^T R / s2^2   (rank order, nb columns)
 gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double* Z,
                         cudaStream_t s) {
@@ -429,8 +573,14 @@ gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double*
   const int n = (int)pc.n;
   if (pc.W.bytes < 8 * (size_t)k * nb) GPM_TRY(pc.W.alloc(8 * (size_t)k * nb));
   if (pc.Y.bytes < 8 * (size_t)k * nb) GPM_TRY(pc.Y.alloc(8 * (size_t)k * nb));
-  GPM_CUBLAS(cublasSetStream(pc.h, s));
   const double one = 1.0, zero = 0.0, a = -1.0 / (s2 * s2), b = 1.0 / s2;
+  if (!getenv("GPM_WOODBURY_CUBLAS") && k * 8 * 8 <= 200 * 1024) {
+    if (nb == 1) return wood_stream<1>(pc, R, nb, Z, a, b, s);
+    if (nb == 2) return wood_stream<2>(pc, R, nb, Z, a, b, s);
+    if (nb <= 4) return wood_stream<4>(pc, R, nb, Z, a, b, s);
+    if (nb <= 8) return wood_stream<8>(pc, R, nb, Z, a, b, s);
+  }
+  GPM_CUBLAS(cublasSetStream(pc.h, s));
   GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_T, CUBLAS_OP_N, k, nb, n, &one, pc.L.as<double>(), n, R,
                          n, &zero, pc.W.as<double>(), k));
   GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_N, k, nb, k, &one, pc.Cinv.as<double>(), k,
@@ -460,6 +610,7 @@ void precond_free(Precond& pc) {
   pc.Cinv.release();
   pc.W.release();
   pc.Y.release();
+  pc.Wp.release();
   if (pc.h) cublasDestroy(pc.h);
   pc.h = nullptr;
 }

@@ -236,3 +236,24 @@ def test_fit_alg1_matches_oracle_trajectory(gpm, d, two_nu, form):
     assert got["kernel"].lengthscale[0] == pytest.approx(ell0[0] * ref["c"], rel=1e-6)
     assert got["sigma"] == pytest.approx(ref["sigma"], rel=1e-6)
     assert np.allclose(got["beta"], ref["beta"], rtol=1e-6, atol=1e-8)
+
+
+@pytest.mark.parametrize("nb", [1, 2, 3, 4, 5, 8, 9])
+def test_woodbury_streaming_kernels(gpm, nb, monkeypatch):
+    """P^-1 R by the streaming L^T R / L Y kernels (nb <= 8; nb = 9 takes the cuBLAS GEMMs)
+    vs the oracle's Woodbury solve, with n spanning several 1024-row blocks and a ragged
+    tail; and equal to the cuBLAS path to rounding (GPM_WOODBURY_CUBLAS)."""
+    n, k, s2 = 5000 + 37, 40, 0.05
+    x, ell, two_nu, _, os_ = _problem(n, 2, 400 + nb, ell=[0.1, 0.2])
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, tuple(ell), os_, form=1))
+    pc = gpm.Precond(plan, k)
+    _, L = pc.factor()
+    Lu = L.cpu().numpy().T                    # user order, n x k: P = L L^T + s2 I
+    r = np.random.default_rng(nb).standard_normal((nb, n))
+    z = pc.solve(s2, to_dev(r)).cpu().numpy()
+    zo = ol.woodbury_solve(Lu, s2, r.T).T
+    assert np.max(np.abs(z - zo)) <= 1e-9 * np.max(np.abs(zo))
+    monkeypatch.setenv("GPM_WOODBURY_CUBLAS", "1")
+    zc = pc.solve(s2, to_dev(r)).cpu().numpy()
+    assert np.max(np.abs(z - zc)) <= 1e-12 * np.max(np.abs(zc))
+    pc.close()

@@ -63,7 +63,7 @@ def test_d1_multi_subtile_path(gpm, two_nu):
 
 
 @pytest.mark.parametrize("n", [1, 7, 6912, 6913, 60001, 200_003])
-@pytest.mark.parametrize("two_nu", [1, 3, 5, 7])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
 def test_d1_reduce_then_scan_path(gpm, n, two_nu):
     """The three-launch d = 1 path (sub-tile records, one-CTA carry scan, apply) forced at
     small sizes: user order against the oracle, rank order equal to user order to rounding
@@ -85,7 +85,7 @@ def test_d1_reduce_then_scan_path(gpm, n, two_nu):
     assert np.max(np.abs(o_r - out[0])) <= 1e-14 * max(np.abs(out[0]).max(), 1e-300)
 
 
-@pytest.mark.parametrize("two_nu", [1, 3, 5])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
 def test_d1_reduce_then_scan_gradient(gpm, two_nu):
     n = 60001
     x = _points("normal", n, 1, 77)
