@@ -426,15 +426,16 @@ gp_status precond_logdet(Precond& pc, double s2, double* out, cudaStream_t s) {
 // dominant traffic: 8 n k bytes each) as streaming kernels instead of the library's
 // tall-skinny GEMMs.  Both are HBM-bound: L is read once per pass, coalesced along n.
 template <int NB>
-__host__ __device__ constexpr int wb_rows() { return 256; }   // k_wlt: rows of L per CTA (~8 CTAs per SM)
+__host__ __device__ constexpr int wb_rows() { return NB >= 8 ? 128 : 256; }   // k_wlt: rows of L per CTA
 constexpr int WB_THREADS = 256;
 
 // k_wlt: partial[(c k + j) nblk + b] = sum_{i in row block b} L[j n + i] R[c n + i].
 // Each lane keeps its rows' R values in registers for the whole CTA; a warp takes 32 / NB
 // columns at a time (32 partial dot products per lane) and reduces them with one
 // reduce-scatter butterfly (31 shuffles instead of 5 per value), leaving lane l with value l.
+constexpr int WT_THREADS = 128;   // k_wlt: 4 warps per CTA, 3 CTAs per SM
 template <int NB>
-__global__ void __launch_bounds__(WB_THREADS) k_wlt(const double* __restrict__ L,
+__global__ void __launch_bounds__(WT_THREADS, 3) k_wlt(const double* __restrict__ L,
                                                     const double* __restrict__ R, int64_t n,
                                                     int k, int nb, double* __restrict__ part) {
   constexpr int WB_ROWS = wb_rows<NB>();
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(WB_THREADS) k_wlt(const double* __restrict__ L
       const int64_t i = i0 + lane + 32 * t;
       rr[c][t] = (c < nb && i < n) ? __ldg(R + (int64_t)c * n + i) : 0.0;
     }
-  for (int j0 = warp * G; j0 < k; j0 += (WB_THREADS / 32) * G) {
+  for (int j0 = warp * G; j0 < k; j0 += (WT_THREADS / 32) * G) {
     double vals[32];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -547,7 +548,7 @@ static gp_status wood_stream(Precond& pc, const double* R, int nb, double* Z, do
   const int nblk = (int)((n + wb_rows<NB>() - 1) / wb_rows<NB>());
   const size_t pb = 8 * (size_t)nblk * NB * k;
   if (pc.Wp.bytes < pb) GPM_TRY(pc.Wp.alloc(pb));
-  k_wlt<NB><<<nblk, WB_THREADS, 0, s>>>(pc.L.as<double>(), R, n, k, nb, pc.Wp.as<double>());
+  k_wlt<NB><<<nblk, WT_THREADS, 0, s>>>(pc.L.as<double>(), R, n, k, nb, pc.Wp.as<double>());
   GPM_CUDA(cudaGetLastError());
   const int kn = k * nb;   // W is k x nb column-major
   k_wred<<<(kn + 7) / 8, 256, 0, s>>>(pc.Wp.as<double>(), nblk, kn, pc.W.as<double>());
