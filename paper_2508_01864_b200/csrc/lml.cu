@@ -3,8 +3,9 @@
 //   * Precond: rank-k pivoted Cholesky K ~ L L^T (greedy pivot on the largest
 //     remaining diagonal, ties -> smallest rank), P = L L^T + sigma^2 I applied by the
 //     Woodbury formula, log det P by Sylvester's theorem.
-//     L is n x k column-major in the plan's rank order; the plain GEMMs of the Woodbury
-//     solve (L^T R, C^-1 W, L Y) and the Gram matrix L^T L go through cuBLAS.
+//     L is n x k column-major in the plan's rank order; the Woodbury solve streams L twice
+//     (k_wlt: L^T R, k_wly: R/s2 - L Y/s2^2) for up to 8 columns; C^-1 W, the Gram matrix
+//     L^T L, the pivot GEMV and the solves with more columns go through cuBLAS.
 //   * mbcg_rank: Algorithm 2 -- CG with several right-hand sides and the
 //     preconditioner solve, zero initial guess, recording alpha_j, beta_j per iteration
 //     (the Lanczos tridiagonals T_j); per-column stop (reading R8).
