@@ -329,7 +329,11 @@ gp_status precond_build(Precond& pc, Plan& pl, int k, cudaStream_t s) {
   GPM_CUBLAS(cublasSetStream(pc.h, s));
   GPM_CUBLAS(cublasSetPointerMode(pc.h, CUBLAS_POINTER_MODE_HOST));
   GPM_TRY(pc.L.alloc(sizeof(double) * (size_t)n * k));
-  DevBuf diag, pv, pi, piv, pivd, Lp;
+  DevBuf diag, pv, pi, piv, pivd, Lp, G;
+  struct Guard {   // scratch released on every exit path
+    DevBuf* b[7];
+    ~Guard() { for (auto* x : b) x->release(); }
+  } guard{{&diag, &pv, &pi, &piv, &pivd, &Lp, &G}};
   GPM_TRY(diag.alloc(8 * n));
   GPM_TRY(pv.alloc(8 * LG));
   GPM_TRY(pi.alloc(4 * LG));
@@ -362,7 +366,6 @@ gp_status precond_build(Precond& pc, Plan& pl, int k, cudaStream_t s) {
   GPM_CUDA(cudaMemcpyAsync(pc.piv.data(), piv.ptr, 4 * (size_t)k, cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaMemcpyAsync(hpd.data(), pivd.ptr, 8 * (size_t)k, cudaMemcpyDeviceToHost, s));
   // Gram matrix G = L^T L (k x k, symmetric)
-  DevBuf G;
   GPM_TRY(G.alloc(8 * (size_t)k * k));
   const double one = 1.0, zero = 0.0;
   GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_T, CUBLAS_OP_N, k, k, (int)n, &one, L, (int)n, L,
@@ -391,22 +394,26 @@ static gp_status precond_sigma(Precond& pc, double s2, cudaStream_t s) {
   if (!chol(C, k)) return fail(GP_ERR_INVALID_ARG, "Woodbury capacitance matrix not SPD");
   double ld = 0.0;
   for (int i = 0; i < k; ++i) ld += 2.0 * std::log(C[(size_t)i * k + i]);
-  // inverse from the Cholesky factor: solve C X = I column by column
-  std::vector<double> inv((size_t)k * k), y(k);
-  for (int c = 0; c < k; ++c) {
-    for (int i = 0; i < k; ++i) {
-      double t = i == c ? 1.0 : 0.0;
-      for (int q = 0; q < i; ++q) t -= C[(size_t)i * k + q] * y[q];
-      y[i] = t / C[(size_t)i * k + i];
-    }
-    for (int i = k - 1; i >= 0; --i) {
-      double t = y[i];
-      for (int q = i + 1; q < k; ++q) t -= C[(size_t)q * k + i] * inv[(size_t)q * k + c];
-      inv[(size_t)i * k + c] = t / C[(size_t)i * k + i];
-    }
-  }
-  // symmetric: row-major == column-major
-  GPM_CUDA(cudaMemcpyAsync(pc.Cinv.ptr, inv.data(), 8 * (size_t)k * k, cudaMemcpyHostToDevice, s));
+  // C^-1 from the Cholesky factor C = F F^T (F lower, row-major in C, i.e. U = F^T upper
+  // in cuBLAS's column-major view): X = U^-1 by one triangular solve on the identity, then
+  // C^-1 = U^-1 U^-T = X X^T (device, O(k^3) flops off the host)
+  DevBuf Fd, Xd;
+  struct Guard {
+    DevBuf* b[2];
+    ~Guard() { for (auto* x : b) x->release(); }
+  } guard{{&Fd, &Xd}};
+  GPM_TRY(Fd.alloc(8 * (size_t)k * k));
+  GPM_TRY(Xd.alloc(8 * (size_t)k * k));
+  std::vector<double> I((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) I[(size_t)i * k + i] = 1.0;
+  GPM_CUDA(cudaMemcpyAsync(Fd.ptr, C.data(), 8 * (size_t)k * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(Xd.ptr, I.data(), 8 * (size_t)k * k, cudaMemcpyHostToDevice, s));
+  GPM_CUBLAS(cublasSetStream(pc.h, s));
+  const double one = 1.0, zero = 0.0;
+  GPM_CUBLAS(cublasDtrsm(pc.h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                         CUBLAS_DIAG_NON_UNIT, k, k, &one, Fd.as<double>(), k, Xd.as<double>(), k));
+  GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_T, k, k, k, &one, Xd.as<double>(), k,
+                         Xd.as<double>(), k, &zero, pc.Cinv.as<double>(), k));
   GPM_CUDA(cudaStreamSynchronize(s));
   pc.s2 = s2;
   pc.logdetC = ld;
