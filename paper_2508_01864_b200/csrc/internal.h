@@ -36,6 +36,22 @@ struct DevBuf {
   gp_status alloc(size_t b);
   void release();
   template <class T> T* as() const { return static_cast<T*>(ptr); }
+  // owning and move-only: scratch buffers are freed on every exit path
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), bytes(o.bytes), fr(o.fr), fctx(o.fctx) {
+    o.ptr = nullptr; o.bytes = 0; o.fr = nullptr; o.fctx = nullptr;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr = o.ptr; bytes = o.bytes; fr = o.fr; fctx = o.fctx;
+      o.ptr = nullptr; o.bytes = 0; o.fr = nullptr; o.fctx = nullptr;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
 };
 
 // d = 1 tile-aggregate record (both scan directions), P <= 2.
