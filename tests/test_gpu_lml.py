@@ -257,3 +257,28 @@ def test_woodbury_streaming_kernels(gpm, nb, monkeypatch):
     zc = pc.solve(s2, to_dev(r)).cpu().numpy()
     assert np.max(np.abs(z - zc)) <= 1e-12 * np.max(np.abs(zc))
     pc.close()
+
+
+def test_solver_entry_points_do_not_leak_device_memory(gpm):
+    """Repeated gp_precond_solve / gp_mbcg / preconditioned CG calls return their scratch:
+    free device memory is unchanged after 10 more rounds (library buffers are owning)."""
+    import torch
+    n = 20000
+    x, ell, two_nu, _, os_ = _problem(n, 2, 900, ell=[0.1, 0.2])
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, tuple(ell), os_, form=1))
+    pc = gpm.Precond(plan, 20)
+    r = to_dev(np.random.default_rng(1).standard_normal((3, n)))
+    y = to_dev(np.random.default_rng(2).standard_normal(n))
+
+    def one_round():
+        pc.solve(0.05, r)
+        plan.mbcg(r, 0.05, 30, 0.0)
+        plan.cg_solve(y, 0.05, mean=gpm.MEAN_AFFINE, rtol=1e-8, max_iter=5000, precond=pc)
+        torch.cuda.synchronize()
+
+    one_round()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(10):
+        one_round()
+    assert torch.cuda.mem_get_info()[0] >= free0 - (4 << 20)
+    pc.close()
