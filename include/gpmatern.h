@@ -209,7 +209,10 @@ GP_API gp_status gp_precond_create(gp_plan p, int rank, void *stream, gp_precond
 GP_API gp_status gp_precond_factor(gp_precond pc, int64_t *pivots, double *L, void *stream);
 
 /* gp_precond_solve -- z = P^-1 r, P = L L^T + sigma2 I, by the Woodbury formula
- * (P:1080-1083).  r, z: n x nb column-major (device, user order), may not alias. */
+ * (P:1080-1083): z = r / sigma2 - L C^-1 L^T r / sigma2^2, C = I + L^T L / sigma2 (C^-1
+ * formed once per sigma2 from a host Cholesky of C; nb <= 8 columns stream L twice, more
+ * go through cuBLAS GEMMs).  r, z: n x nb column-major (device, user order), may not
+ * alias.  Synchronises `stream`. */
 GP_API gp_status gp_precond_solve(gp_precond pc, double sigma2, const double *r, int nb,
                                   double *z, void *stream);
 
