@@ -107,3 +107,36 @@ def test_high_nu_unsupported(gpm):
     with pytest.raises(gpm.GPError) as e:
         p1.kmvm(to_dev(np.ones(60000)))
     assert e.value.name == "UNSUPPORTED"
+
+
+@pytest.mark.parametrize("two_nu", [5, 7, 9])
+def test_high_nu_product_d2_kzx_and_gp(gpm, two_nu):
+    """K_zx v on the union x U z (queries on top of data points included) and a CG + GLS
+    solve with the d = 2 product kernel of order two_nu/2, against the oracle's dense rows
+    and its dense-Cholesky GP (mean, alpha, beta)."""
+    import oracle
+    rng = np.random.default_rng(60 + two_nu)
+    n, m = 2500, 600
+    x = rng.random((n, 2))
+    z = rng.random((m, 2))
+    z[:40] = x[:40]
+    ell = (0.15, 0.25)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.0, form=1))
+    v = rng.standard_normal(n)
+    out = plan.cross(to_dev(z)).kzx(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "product", ell, 1.0, z=z, what=f"kzx product nu={two_nu}/2")
+    y = np.sin(4 * x[:, 0]) + x[:, 1] + 0.1 * rng.standard_normal(n)
+    s2 = 0.05
+    alpha, beta, info = plan.cg_solve(to_dev(y), s2, mean=gpm.MEAN_AFFINE, rtol=1e-10,
+                                      max_iter=20000)
+    ref = oracle.gp_dense(x, y, z, two_nu, "product", ell, 1.0, s2, mean="affine")
+    assert info["relres_max"] <= 1e-10
+    mu = plan.predict(to_dev(z), alpha, beta).cpu().numpy()
+    # the solve against dense Cholesky (CG-tolerance bound, as test_cg_gls_predict_small_vs_dense)
+    assert np.allclose(beta, ref["beta"], rtol=0, atol=1e-5)
+    assert np.max(np.abs(mu - ref["mu"])) <= 1e-5 * max(1.0, np.max(np.abs(ref["mu"])))
+    # the posterior mean given the GPU's alpha, beta: parity with the oracle's K_zx rows
+    a = alpha.cpu().numpy()
+    mu_or = oracle.kzx_rows(x, a, z, two_nu, "product", ell, 1.0) + \
+        np.hstack([np.ones((m, 1)), z]) @ np.array(beta)
+    assert np.max(np.abs(mu - mu_or)) <= 1e-9 * np.abs(a).max() * 50
