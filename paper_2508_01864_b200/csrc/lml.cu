@@ -56,12 +56,6 @@ __device__ __forceinline__ double prof(int P, double s) {
   return e * poly;
 }
 
-// piv[i] holds the pivot rank; Lp[j] = L[j*n + piv] for j < i (gathered first)
-__global__ void k_pivrow(const double* __restrict__ L, int64_t n, const int* __restrict__ piv,
-                         int i, double* __restrict__ Lp) {
-  const int p = piv[i];
-  for (int j = threadIdx.x; j < i; j += blockDim.x) Lp[j] = L[(size_t)j * n + p];
-}
 
 // col[r] = os2 k(x_r, x_p)  (the GEMV correction is applied by cuBLAS afterwards)
 __global__ void k_kcol(const double* __restrict__ t, int64_t n, int d, int P, int prod, double os2,
@@ -85,16 +79,41 @@ __global__ void k_kcol(const double* __restrict__ t, int64_t n, int d, int P, in
 }
 
 // L[:, i] = col / sqrt(dp); diag -= L[:, i]^2 ; dp = pivot's remaining diagonal (pivd[i])
-__global__ void k_pcupd(double* __restrict__ col, double* __restrict__ diag, int64_t n,
-                        const int* __restrict__ piv, const double* __restrict__ pivd, int i) {
+
+// k_pcupd followed by k_argmax1's stage 1 on the updated diagonal, in one pass (launched
+// <<<LG, LB>>> like k_argmax1: the same grid-stride partition, so the same partials)
+__global__ void k_pcupd_am(double* __restrict__ col, double* __restrict__ diag, int64_t n,
+                           const int* __restrict__ piv, const double* __restrict__ pivd, int i,
+                           double* __restrict__ pv, int* __restrict__ pi) {
+  __shared__ double sv[LB];
+  __shared__ int si[LB];
   const double inv = 1.0 / sqrt(pivd[i]);
   const int p = piv[i];
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     const double l = col[r] * inv;
     col[r] = l;
-    diag[r] = r == p ? 0.0 : diag[r] - l * l;
+    const double v = r == p ? 0.0 : diag[r] - l * l;
+    diag[r] = v;
+    if (v > bv) { bv = v; bi = (int)r; }
   }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int i2 = si[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { pv[blockIdx.x] = sv[0]; pi[blockIdx.x] = si[0]; }
 }
 
 // argmax of diag (ties -> smallest index): stage 1 per block, stage 2 one block
@@ -125,8 +144,10 @@ __global__ void k_argmax1(const double* __restrict__ diag, int64_t n, double* __
   }
   if (threadIdx.x == 0) { pv[blockIdx.x] = sv[0]; pi[blockIdx.x] = si[0]; }
 }
+// stage 2 also gathers the pivot's row of L (Lp[j] = L[j n + p], j < i; was k_pivrow)
 __global__ void k_argmax2(const double* __restrict__ pv, const int* __restrict__ pi, int nb,
-                          int* __restrict__ piv, double* __restrict__ pivd, int i) {
+                          int* __restrict__ piv, double* __restrict__ pivd, int i,
+                          const double* __restrict__ L, int64_t n, double* __restrict__ Lp) {
   __shared__ double sv[LB];
   __shared__ int si[LB];
   double bv = -INFINITY;
@@ -150,6 +171,8 @@ __global__ void k_argmax2(const double* __restrict__ pv, const int* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) { piv[i] = si[0]; pivd[i] = sv[0]; }
+  const int p = si[0];
+  for (int j = threadIdx.x; j < i; j += blockDim.x) Lp[j] = L[(size_t)j * n + p];
 }
 
 // ---- CG kernels (columns in blockIdx.y; vectors n x nb column-major)
@@ -345,20 +368,20 @@ gp_status precond_build(Precond& pc, Plan& pl, int k, cudaStream_t s) {
   double* L = pc.L.as<double>();
   const int prod = pl.form == GP_FORM_PRODUCT ? 1 : 0;
   for (int i = 0; i < k; ++i) {
-    k_argmax1<<<LG, LB, 0, s>>>(diag.as<double>(), n, pv.as<double>(), pi.as<int>());
+    // step i's argmax partials: k_argmax1 at i = 0, else step i-1's k_pcupd_am
+    if (i == 0) k_argmax1<<<LG, LB, 0, s>>>(diag.as<double>(), n, pv.as<double>(), pi.as<int>());
     k_argmax2<<<1, LB, 0, s>>>(pv.as<double>(), pi.as<int>(), LG, piv.as<int>(),
-                               pivd.as<double>(), i);
+                               pivd.as<double>(), i, L, n, Lp.as<double>());
     double* col = L + (size_t)i * n;
     k_kcol<<<lgrid(n), 256, 0, s>>>(pl.t.as<double>(), n, pl.d, pl.P, prod, pl.os2,
                                     piv.as<int>(), i, col);
     if (i > 0) {
-      k_pivrow<<<1, 256, 0, s>>>(L, n, piv.as<int>(), i, Lp.as<double>());
       const double m1 = -1.0, one = 1.0;
       GPM_CUBLAS(cublasDgemv(pc.h, CUBLAS_OP_N, (int)n, i, &m1, L, (int)n, Lp.as<double>(), 1,
                              &one, col, 1));
     }
-    k_pcupd<<<lgrid(n), 256, 0, s>>>(col, diag.as<double>(), n, piv.as<int>(),
-                                     pivd.as<double>(), i);
+    k_pcupd_am<<<LG, LB, 0, s>>>(col, diag.as<double>(), n, piv.as<int>(), pivd.as<double>(),
+                                 i, pv.as<double>(), pi.as<int>());
     GPM_CUDA(cudaGetLastError());
   }
   pc.piv.resize(k);
