@@ -213,7 +213,8 @@ def test_lml_errors(gpm):
         other.cg_solve(to_dev(np.ones(200)), 0.1, precond=pc)
 
 
-@pytest.mark.parametrize("d,two_nu,form", [(1, 3, "l1"), (2, 1, "l1"), (2, 3, "product")])
+@pytest.mark.parametrize("d,two_nu,form", [(1, 3, "l1"), (2, 1, "l1"), (2, 3, "product"),
+                                             (2, 5, "product")])
 def test_fit_alg1_matches_oracle_trajectory(gpm, d, two_nu, form):
     """Algorithm 1 with the same probes: a few ADAM steps, one GLS round -- the GPU and the
     oracle follow the same trajectory (gradients agree to ~1e-7, ADAM is smooth in them)."""
