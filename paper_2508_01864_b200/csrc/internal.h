@@ -150,8 +150,11 @@ struct Precond {
   ::cublasContext* h = nullptr;
 };
 gp_status precond_build(Precond& pc, Plan& pl, int k, cudaStream_t s);
+// zr_part (optional): when the streaming path runs, per-CTA partials of z_c . r_c are
+// written there ([nb][*zr_nblk]) and *zr_nblk is set; otherwise *zr_nblk = 0
 gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double* Z,
-                        cudaStream_t s);
+                        cudaStream_t s, double* zr_part = nullptr, int* zr_nblk = nullptr);
+inline int precond_zr_blocks(int64_t n) { return (int)((n + 255) / 256); }
 gp_status precond_sample(Precond& pc, double s2, const double* G, const double* W, int nb,
                          double* Z, cudaStream_t s);
 gp_status precond_logdet(Precond& pc, double s2, double* out, cudaStream_t s);

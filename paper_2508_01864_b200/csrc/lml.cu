@@ -257,17 +257,16 @@ __global__ void k_mupd(double* __restrict__ X, double* __restrict__ R, const dou
   if (threadIdx.x == 0) part[(size_t)c * gridDim.x + blockIdx.x] = t;
 }
 // beta_c = zr_new / zr ; convergence on ||R||^2 <= tol2_c ; history
-__global__ void k_mbeta(const double* __restrict__ part_rr, const double* __restrict__ part_zr,
-                        int nb, double* __restrict__ zr, const double* __restrict__ tol2,
+__global__ void k_mbeta(const double* __restrict__ part_rr, int nb,
+                        const double* __restrict__ part_zr, int nb2,
+                        double* __restrict__ zr, const double* __restrict__ tol2,
                         double* __restrict__ beta, int* __restrict__ status,
                         int* __restrict__ iters, double* __restrict__ bhist, int it, int ncol) {
   __shared__ double sh[32];
   const int c = blockIdx.x;
   double a1 = 0.0, a2 = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    a1 += part_rr[(size_t)c * nb + b];
-    a2 += part_zr[(size_t)c * nb + b];
-  }
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) a1 += part_rr[(size_t)c * nb + b];
+  for (int b = threadIdx.x; b < nb2; b += blockDim.x) a2 += part_zr[(size_t)c * nb2 + b];
   const double rr = lblock_sum(a1, sh);
   const double zn = lblock_sum(a2, sh);
   if (threadIdx.x == 0) {
@@ -538,15 +537,17 @@ template <int NB>
 __global__ void __launch_bounds__(WB_THREADS) k_wly(const double* __restrict__ L,
                                                     const double* R, int64_t n, int k, int nb,
                                                     const double* __restrict__ Y, double a,
-                                                    double b, double* Z) {
+                                                    double b, double* Z, double* zr_part) {
   extern __shared__ double Ys[];   // [k][NB]
+  __shared__ double wsum[NB][WB_THREADS / 32];
   for (int t = threadIdx.x; t < k * NB; t += WB_THREADS) {
     const int j = t / NB, c = t % NB;
     Ys[t] = c < nb ? __ldg(Y + (int64_t)c * k + j) : 0.0;
   }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * WB_THREADS + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i0 = (int64_t)blockIdx.x * WB_THREADS + threadIdx.x;
+  const bool live = i0 < n;
+  const int64_t i = live ? i0 : n - 1;   // dead lanes recompute the last row, write nothing
   double acc[NB];
 #pragma unroll
   for (int c = 0; c < NB; ++c) acc[c] = 0.0;
@@ -566,14 +567,37 @@ __global__ void __launch_bounds__(WB_THREADS) k_wly(const double* __restrict__ L
 #pragma unroll
     for (int c = 0; c < NB; ++c) acc[c] = fma(l, Ys[j * NB + c], acc[c]);
   }
+  double zr[NB];
 #pragma unroll
-  for (int c = 0; c < NB; ++c)
-    if (c < nb) Z[(int64_t)c * n + i] = fma(b, R[(int64_t)c * n + i], a * acc[c]);
+  for (int c = 0; c < NB; ++c) {
+    zr[c] = 0.0;
+    if (c < nb && live) {
+      const double rv = R[(int64_t)c * n + i];
+      const double zv = fma(b, rv, a * acc[c]);
+      Z[(int64_t)c * n + i] = zv;
+      zr[c] = zv * rv;
+    }
+  }
+  if (zr_part) {   // fixed-order block sums of z.r per column (Alg 2's z^T r)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) zr[c] += __shfl_down_sync(0xffffffffu, zr[c], off);
+      if (lane == 0) wsum[c][warp] = zr[c];
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      double t = 0.0;
+      for (int w = 0; w < WB_THREADS / 32; ++w) t += wsum[threadIdx.x][w];
+      zr_part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
 
 template <int NB>
 static gp_status wood_stream(Precond& pc, const double* R, int nb, double* Z, double a, double b,
-                             cudaStream_t s) {
+                             cudaStream_t s, double* zr_part, int* zr_nblk) {
   const int k = pc.k;
   const int64_t n = pc.n;
   const int nblk = (int)((n + wb_rows<NB>() - 1) / wb_rows<NB>());
@@ -592,14 +616,16 @@ static gp_status wood_stream(Precond& pc, const double* R, int nb, double* Z, do
   if (ysm > 48 * 1024)
     GPM_CUDA(cudaFuncSetAttribute(k_wly<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm));
   k_wly<NB><<<(int)((n + WB_THREADS - 1) / WB_THREADS), WB_THREADS, ysm, s>>>(
-      pc.L.as<double>(), R, n, k, nb, pc.Y.as<double>(), a, b, Z);
+      pc.L.as<double>(), R, n, k, nb, pc.Y.as<double>(), a, b, Z, zr_part);
   GPM_CUDA(cudaGetLastError());
+  if (zr_nblk) *zr_nblk = zr_part ? (int)((n + WB_THREADS - 1) / WB_THREADS) : 0;
   return GP_OK;
 }
 
 // Z = P^-1 R = R/s2 - L Cinv L^T R / s2^2   (rank order, nb columns)
 gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double* Z,
-                        cudaStream_t s) {
+                        cudaStream_t s, double* zr_part, int* zr_nblk) {
+  if (zr_nblk) *zr_nblk = 0;
   GPM_TRY(precond_sigma(pc, s2, s));
   const int k = pc.k;
   const int n = (int)pc.n;
@@ -607,10 +633,10 @@ gp_status precond_apply(Precond& pc, double s2, const double* R, int nb, double*
   if (pc.Y.bytes < 8 * (size_t)k * nb) GPM_TRY(pc.Y.alloc(8 * (size_t)k * nb));
   const double one = 1.0, zero = 0.0, a = -1.0 / (s2 * s2), b = 1.0 / s2;
   if (!getenv("GPM_WOODBURY_CUBLAS") && k * 8 * 8 <= 200 * 1024) {
-    if (nb == 1) return wood_stream<1>(pc, R, nb, Z, a, b, s);
-    if (nb == 2) return wood_stream<2>(pc, R, nb, Z, a, b, s);
-    if (nb <= 4) return wood_stream<4>(pc, R, nb, Z, a, b, s);
-    if (nb <= 8) return wood_stream<8>(pc, R, nb, Z, a, b, s);
+    if (nb == 1) return wood_stream<1>(pc, R, nb, Z, a, b, s, zr_part, zr_nblk);
+    if (nb == 2) return wood_stream<2>(pc, R, nb, Z, a, b, s, zr_part, zr_nblk);
+    if (nb <= 4) return wood_stream<4>(pc, R, nb, Z, a, b, s, zr_part, zr_nblk);
+    if (nb <= 8) return wood_stream<8>(pc, R, nb, Z, a, b, s, zr_part, zr_nblk);
   }
   GPM_CUBLAS(cublasSetStream(pc.h, s));
   GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_T, CUBLAS_OP_N, k, nb, n, &one, pc.L.as<double>(), n, R,
@@ -665,7 +691,8 @@ gp_status mbcg_rank(Plan& pl, Precond* pc, double s2, const double* B, int nb, i
   GPM_TRY(bP.alloc(8 * nk));
   GPM_TRY(bQ.alloc(8 * nk));
   if (pc) GPM_TRY(bZ.alloc(8 * nk));
-  GPM_TRY(bpart.alloc(8 * (size_t)LG * nb * 2));
+  // part: LG partials per column; part2: z.r partials (LG from k_dotp, or one per k_wly CTA)
+  GPM_TRY(bpart.alloc(8 * (size_t)nb * (LG + std::max(LG, precond_zr_blocks(n)))));
   GPM_TRY(bsc.alloc(8 * 4 * (size_t)nb + 4 * 2 * (size_t)nb + 64));
   double* R = bR.as<double>();
   double* Pm = bP.as<double>();
@@ -722,11 +749,16 @@ gp_status mbcg_rank(Plan& pl, Precond* pc, double s2, const double* B, int nb, i
       k_mq<<<dim3(LG, nb), LB, 0, s>>>(Pm, Q, n, s2, part);
       k_malpha<<<nb, LB, 0, s>>>(part, LG, zr, al, st, ahist, it, nb);
       k_mupd<<<dim3(LG, nb), LB, 0, s>>>(X, R, Pm, Q, al, n, part);
-      if (pc) {
-        GPM_TRY(precond_apply(*pc, s2, R, nb, Z, s));
-        k_dotp<<<dim3(LG, nb), LB, 0, s>>>(Z, R, n, part2);
+      int nzr = LG;
+      if (pc) {   // z.r comes out of the Woodbury kernel when it streams (else k_dotp)
+        GPM_TRY(precond_apply(*pc, s2, R, nb, Z, s, part2, &nzr));
+        if (nzr == 0) {
+          k_dotp<<<dim3(LG, nb), LB, 0, s>>>(Z, R, n, part2);
+          nzr = LG;
+        }
       }
-      k_mbeta<<<nb, LB, 0, s>>>(part, pc ? part2 : part, LG, zr, t2, be, st, itc, bhist, it, nb);
+      k_mbeta<<<nb, LB, 0, s>>>(part, LG, pc ? part2 : part, nzr, zr, t2, be, st, itc, bhist,
+                                it, nb);
       k_mpupd<<<dim3(LG, nb), LB, 0, s>>>(Pm, Z, be, st, n);
     }
     GPM_CUDA(cudaGetLastError());
