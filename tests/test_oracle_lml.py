@@ -231,3 +231,38 @@ def test_alg1_recovers_simulated_parameters():
     assert np.all(np.abs(res["beta"] - beta_true) <= 4 * se)
     r = y - H @ res["beta"]
     assert ol.lml_exact(A1, r)[0] > ol.lml_exact(A0, r)[0]
+
+
+def _schur_diag(K, sel):
+    """diag of the Schur complement K - K[:, S] K[S, S]^-1 K[S, :] (S = sel): the residual
+    variance after conditioning on the selected points, computed by a dense solve that
+    shares nothing with the pivoted-Cholesky loop."""
+    if not sel:
+        return np.diag(K).copy()
+    S = np.asarray(sel)
+    KS = K[:, S]
+    return np.diag(K) - np.einsum("ij,ji->i", KS, np.linalg.solve(K[np.ix_(S, S)], KS.T))
+
+
+def test_pivoted_cholesky_pivot_is_greedy_argmax_of_schur_diagonal():
+    """Harbrecht's greedy rule (cited at PAPER.md L1073 [App A.3]): step i pivots on the
+    largest diagonal entry of the Schur complement given the earlier pivots (ties: the
+    smallest index).  Fails for any other pivot order (e.g. the unpivoted p = i)."""
+    rng = np.random.default_rng(21)
+    x = rng.random((30, 2))
+    K = oracle.dense_kernel(x, x, 3, "product", [0.5, 0.5], 1.0)
+    _, piv = ol.pivoted_cholesky(K, 12)
+    for i in range(12):
+        d = _schur_diag(K, piv[:i].tolist())
+        assert d[piv[i]] >= d.max() * (1 - 1e-9), (i, piv[i], int(np.argmax(d)))
+
+
+def test_pivoted_cholesky_second_pivot_is_farthest_point():
+    """1-D, stationary kernel: the diagonal is constant, so the first pivot is index 0
+    (tie rule) and the residual variance after it is s^2 (1 - k(r)^2), largest at the
+    point farthest from x_0."""
+    x = np.array([[0.41], [0.40], [0.05], [0.95], [0.42], [0.60]])
+    K = oracle.dense_kernel(x, x, 1, "l1", [0.3], 1.0)
+    _, piv = ol.pivoted_cholesky(K, 2)
+    assert piv[0] == 0
+    assert piv[1] == int(np.argmax(np.abs(x[:, 0] - x[0, 0]))) == 3
