@@ -219,6 +219,8 @@ GP_API gp_status gp_precond_solve(gp_precond pc, double sigma2, const double *r,
 /* gp_precond_logdet -- log det P = N log sigma2 + log det(I + L^T L / sigma2) (Sylvester,
  * P:1087-1095); host result. */
 GP_API gp_status gp_precond_logdet(gp_precond pc, double sigma2, double *logdet, void *stream);
+/* gp_precond_destroy -- frees the preconditioner; if its plan's gp_destroy already ran
+ * (deferred, see gp_destroy), the plan is freed with its last preconditioner. */
 GP_API void gp_precond_destroy(gp_precond pc);
 
 /* gp_mbcg -- Algorithm 2: CG on A = K + sigma2 I with nb right-hand sides B,
@@ -324,6 +326,9 @@ GP_API gp_status gp_plan_query(gp_plan p, int what, int64_t *value);
  *   option 3: L2 prefetch of v before the user-order gathers (1 default, 0 off). */
 GP_API gp_status gp_plan_set_option(gp_plan p, int option, int64_t value);
 
+/* gp_destroy -- frees the plan and its device memory.  Preconditioners point into their
+ * plan: while any built on p is alive the free is deferred to the last gp_precond_destroy
+ * (p must not be used after gp_destroy either way). */
 GP_API void gp_destroy(gp_plan p);
 GP_API const char *gp_last_error(void);
 /* Library version string, e.g. "gpmatern 0.1 sm_100a". */

@@ -416,6 +416,9 @@ class Precond:
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 _FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 _alloc_hooks = None
+# every (alloc, free) thunk pair ever installed: buffers keep the free hook they were
+# allocated with (include/gpmatern.h), so a replaced pair must outlive them -- never cleared
+_all_hooks = []
 
 
 def use_torch_allocator(enable: bool = True):
@@ -436,7 +439,8 @@ def use_torch_allocator(enable: bool = True):
     def _free(ptr, stream, ctx):
         torch.cuda.caching_allocator_delete(ptr)
 
-    _alloc_hooks = (_ALLOC_FN(_alloc), _FREE_FN(_free))   # keep the thunks alive
+    _alloc_hooks = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    _all_hooks.append(_alloc_hooks)   # keep the thunks alive for the whole process
     _check(lib.gp_set_allocator(ctypes.cast(_alloc_hooks[0], ctypes.c_void_p),
                                 ctypes.cast(_alloc_hooks[1], ctypes.c_void_p), None))
 

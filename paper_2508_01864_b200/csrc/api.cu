@@ -273,6 +273,7 @@ gp_status gp_precond_create(gp_plan p, int rank, void* stream, gp_precond* out) 
     delete c;
     return st;
   }
+  ++p->live_preconds;
   *out = c;
   return GP_OK;
 }
@@ -321,8 +322,14 @@ gp_status gp_precond_logdet(gp_precond pc, double sigma2, double* logdet, void* 
 
 void gp_precond_destroy(gp_precond pc) {
   if (!pc) return;
+  gp_plan owner = pc->owner;
   precond_free(pc->pc);
   delete pc;
+  // a plan whose gp_destroy came first is freed with its last preconditioner
+  if (owner && --owner->live_preconds == 0 && owner->destroy_pending) {
+    plan_free(owner->pl);
+    delete owner;
+  }
 }
 
 gp_status gp_mbcg(gp_plan p, gp_precond pc, double sigma2, const double* B, int nb, int max_iter,
@@ -494,6 +501,10 @@ gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
 
 void gp_destroy(gp_plan p) {
   if (!p) return;
+  if (p->live_preconds > 0) {   // preconditioners point into the plan: defer
+    p->destroy_pending = true;
+    return;
+  }
   plan_free(p->pl);
   delete p;
 }

@@ -202,6 +202,8 @@ gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double
 
 struct gp_plan_s {
   gpm::Plan pl;
+  int live_preconds = 0;     // preconditioners built on this plan (they point into pl)
+  bool destroy_pending = false;   // gp_destroy called while preconditioners were alive
 };
 struct gp_precond_s {
   gpm::Precond pc;

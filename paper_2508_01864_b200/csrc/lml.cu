@@ -613,8 +613,14 @@ static gp_status wood_stream(Precond& pc, const double* R, int nb, double* Z, do
   GPM_CUBLAS(cublasDgemm(pc.h, CUBLAS_OP_N, CUBLAS_OP_N, k, nb, k, &one, pc.Cinv.as<double>(), k,
                          pc.W.as<double>(), k, &zero, pc.Y.as<double>(), k));
   const size_t ysm = 8 * (size_t)k * NB;
-  if (ysm > 48 * 1024)
-    GPM_CUDA(cudaFuncSetAttribute(k_wly<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm));
+  // opt in once per instantiation to the largest Y any rank can need (k <= 1024): the
+  // static wsum[][] adds to the dynamic size, so a 48 KB test on ysm alone is not enough
+  static bool attr_set = false;
+  if (!attr_set) {
+    GPM_CUDA(cudaFuncSetAttribute(k_wly<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(8 * 1024 * NB)));
+    attr_set = true;
+  }
   k_wly<NB><<<(int)((n + WB_THREADS - 1) / WB_THREADS), WB_THREADS, ysm, s>>>(
       pc.L.as<double>(), R, n, k, nb, pc.Y.as<double>(), a, b, Z, zr_part);
   GPM_CUDA(cudaGetLastError());

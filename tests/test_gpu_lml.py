@@ -283,3 +283,35 @@ def test_solver_entry_points_do_not_leak_device_memory(gpm):
         one_round()
     assert torch.cuda.mem_get_info()[0] >= free0 - (4 << 20)
     pc.close()
+
+
+def test_woodbury_streaming_rank768_five_columns(gpm):
+    """k_wly's dynamic Y (8 k NB bytes) plus its static partials crosses 48 KB at
+    k = 761..768 with NB = 8 (5..8 columns): the launch must opt in to the larger carve-out."""
+    n, k, s2 = 3000, 768, 0.05
+    x, ell, two_nu, _, os_ = _problem(n, 2, 777, ell=[0.1, 0.2])
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, tuple(ell), os_, form=1))
+    pc = gpm.Precond(plan, k)
+    _, L = pc.factor()
+    Lu = L.cpu().numpy().T
+    r = np.random.default_rng(5).standard_normal((5, n))
+    z = pc.solve(s2, to_dev(r)).cpu().numpy()
+    zo = ol.woodbury_solve(Lu, s2, r.T).T
+    assert np.max(np.abs(z - zo)) <= 1e-8 * np.max(np.abs(zo))
+    pc.close()
+    plan.close()
+
+
+def test_plan_destroyed_before_its_preconditioner(gpm):
+    """gp_destroy while a preconditioner is alive defers the free; the
+    preconditioner stays usable and frees the plan with itself."""
+    n = 2000
+    x, ell, two_nu, _, os_ = _problem(n, 2, 778, ell=[0.1, 0.2])
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, tuple(ell), os_, form=1))
+    pc = gpm.Precond(plan, 16)
+    r = np.random.default_rng(6).standard_normal((2, n))
+    z0 = pc.solve(0.1, to_dev(r)).cpu().numpy()
+    plan.close()
+    z1 = pc.solve(0.1, to_dev(r)).cpu().numpy()
+    assert np.array_equal(z0, z1)
+    pc.close()
