@@ -53,10 +53,8 @@ def peaks():
 def d1_kernel_name(shape):
     """Name of the d = 1 kernel (nu = 5/2, user order) of a plan's thread-block shape
     (gp_plan_set_option option 1)."""
-    shapes = {0: "k_d1_fast<2,0,512,15>", 1: "k_d1_fast<2,0,640,11>", 2: "k_d1_fast<2,0,768,9>",
-              3: "k_d1_fast<2,0,1024,7>", 4: "k_d1_ov<2,0,256,27,user>",
-              5: "k_d1_ov<2,0,256,31,user>", 6: "k_d1_ov<2,0,512,15,user>",
-              7: "k_d1_ov<2,0,128,27,user>"}
+    shapes = {0: "k_d1_lpc<2,0,512,15,user>", 1: "k_d1_lpc<2,0,384,19,user>",
+              2: "k_d1_lpc<2,0,256,27,user>"}
     return shapes.get(shape, f"d1 shape {shape}")
 
 

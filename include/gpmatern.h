@@ -309,19 +309,17 @@ GP_API gp_status gp_predict(gp_plan p, const double *z, int64_t m, const double 
 /* gp_plan_query -- introspection for tests and the bench (host value in *value):
  *   0 n, 1 d, 2 levels L, 3 bytes of device structure, 4 kernel launches per
  *   single-RHS gp_kmvm, 5 algorithmic HBM bytes per single-RHS gp_kmvm,
- *   6 d=1 apply path in use (1 = single-launch cooperative, 2 = multi-sub-tile cooperative,
- *     3 = three-launch reduce-then-scan),
+ *   6 d=1 apply path in use (1 = single-launch cooperative k_d1_lpc, 3 = three-launch
+ *     reduce-then-scan),
  *   7 d=1 thread-block shape of path 1 (see gp_plan_set_option). */
 GP_API gp_status gp_plan_query(gp_plan p, int what, int64_t *value);
 
 /* gp_plan_set_option -- tuning / testing knobs (d = 1 only; ignored otherwise):
- *   option 0: force the d=1 apply path (0 auto, 1 single-chunk if it fits, 2 the cooperative
- *             multi-sub-tile kernel, 3 the three-launch reduce-then-scan path -- the automatic
- *             choice above the single-chunk capacity);
- *   option 1: thread-block shape of path 1: k_d1_fast (grid barrier) 0 = 512x15, 1 = 640x11,
- *             2 = 768x9, 3 = 1024x7; k_d1_ov (split-barrier exchange) 4 = 256x27,
- *             5 = 256x31 (the default above 4's capacity), 6 = 512x15, 7 = 128x27 (two CTAs per SM)
- *             (threads x points per thread);
+ *   option 0: force the d=1 apply path (0 auto, 1 single-chunk k_d1_lpc if it fits, 3 the
+ *             three-launch reduce-then-scan path -- the automatic choice above the
+ *             single-chunk capacity; 2 is rejected: the multi-sub-tile kernel is gone);
+ *   option 1: thread-block shape of path 1 (threads x points per thread): 0 = 512x15
+ *             (default), 1 = 384x19, 2 = 256x27;
  *   option 2: programmatic dependent launch of the d=1 kernel (1 default, 0 off);
  *   option 3: L2 prefetch of v before the user-order gathers (1 default, 0 off). */
 GP_API gp_status gp_plan_set_option(gp_plan p, int option, int64_t value);

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpmatern.so")
 OBJDIR = os.path.join(HERE, "build")
-SOURCES = ["api.cu", "setup.cu", "apply.cu", "apply_d1.cu", "apply_d1_fast.cu", "apply_level.cu",
+SOURCES = ["api.cu", "setup.cu", "apply.cu", "apply_d1.cu", "apply_d1_big.cu", "apply_level.cu",
            "solve.cu", "lml.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",

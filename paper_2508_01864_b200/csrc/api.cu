@@ -448,34 +448,33 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
     case 5: *value = apply_model_bytes(pl); break;
     case 6: *value = pl.d == 1 ? pl.d1_path : 0; break;
     case 7: *value = pl.d == 1 ? pl.d1_shape : -1; break;
-    case 20: case 21: case 22: case 23: case 24: case 25: {
-      // debug (GPM_D1_TIMING): MAX over CTAs of stamp[what-19] - min stamp[0], ns
+    default: {
+      // debug (GPM_D1_TIMING, d = 1 single-chunk path, last launch): what = 100 + slot:
+      // mean over CTAs of stamp[slot] - min stamp[0] (ns); 200 + slot: the max over CTAs
+      if (what < 100 || what >= 216 || (what >= 116 && what < 200))
+        return fail(GP_ERR_INVALID_ARG, "unknown query");
       if (!pl.dbg.bytes) return fail(GP_ERR_INVALID_ARG, "GPM_D1_TIMING not enabled");
       std::vector<unsigned long long> h(pl.dbg.bytes / 8);
       if (cudaMemcpy(h.data(), pl.dbg.ptr, pl.dbg.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         return fail(GP_ERR_CUDA, "dbg copy failed");
+      const int slot = what % 100;
+      // per-warp stamps [cta][32 warps][16]; warps that never wrote slot 0 are unused
       unsigned long long t0 = ~0ull, mx = 0;
-      for (int b = 0; b < pl.d1_grid; ++b) t0 = std::min(t0, h[b * 8]);
-      const int slot = what == 25 ? 6 : what - 19;
-      for (int b = 0; b < pl.d1_grid; ++b) mx = std::max(mx, h[b * 8 + slot] - t0);
-      *value = (int64_t)mx;
-      break;
-    }
-    case 8: case 9: case 10: case 11: case 12: case 13: case 14: {
-      // debug (GPM_D1_TIMING): mean over CTAs of stamp[what-7] - stamp[0], ns, last launch
-      if (!pl.dbg.bytes) return fail(GP_ERR_INVALID_ARG, "GPM_D1_TIMING not enabled");
-      std::vector<unsigned long long> h(pl.dbg.bytes / 8);
-      if (cudaMemcpy(h.data(), pl.dbg.ptr, pl.dbg.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
-        return fail(GP_ERR_CUDA, "dbg copy failed");
-      unsigned long long t0 = ~0ull;
-      for (int b = 0; b < pl.d1_grid; ++b) t0 = std::min(t0, h[b * 8]);
       double acc = 0;
-      const int slot = what == 13 ? 6 : what - 7;
-      for (int b = 0; b < pl.d1_grid; ++b) acc += (double)(h[b * 8 + slot] - t0);
-      *value = (int64_t)(acc / pl.d1_grid);
-      break;
+      int cntw = 0;
+      for (int b = 0; b < pl.d1_grid * 32; ++b)
+        if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
+      for (int b = 0; b < pl.d1_grid * 32; ++b) {
+        if (!h[b * 16] || !h[b * 16 + slot]) continue;
+        const unsigned long long dt = h[b * 16 + slot] > t0 ? h[b * 16 + slot] - t0 : 0;
+        acc += (double)dt;
+        mx = std::max(mx, dt);
+        ++cntw;
+      }
+      if (!cntw) cntw = 1;
+      *value = what >= 200 ? (int64_t)mx : (int64_t)(acc / cntw);
+      return GP_OK;
     }
-    default: return fail(GP_ERR_INVALID_ARG, "unknown query");
   }
   return GP_OK;
 }
@@ -483,10 +482,11 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
 gp_status gp_plan_set_option(gp_plan p, int option, int64_t value) {
   if (!p) return fail(GP_ERR_INVALID_ARG, "NULL plan");
   if (option == 0) {
-    if (value < 0 || value > 3) return fail(GP_ERR_INVALID_ARG, "bad value for option 0");
+    if (value < 0 || value > 3 || value == 2)
+      return fail(GP_ERR_INVALID_ARG, "bad value for option 0 (0 auto, 1 single-chunk, 3 reduce-then-scan)");
     p->pl.d1_force = (int)value;
   } else if (option == 1) {
-    if (value < 0 || value > 7) return fail(GP_ERR_INVALID_ARG, "bad value for option 1");
+    if (value < 0 || value > 2) return fail(GP_ERR_INVALID_ARG, "bad value for option 1 (shapes 0..2)");
     p->pl.d1_shape = (int)value;
   } else if (option == 2) {
     p->pl.d1_pdl = value != 0;

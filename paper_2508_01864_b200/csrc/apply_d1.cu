@@ -1,611 +1,832 @@
-// apply_d1.cu -- d = 1 hot path: K v by the 1-D ECDF decomposition
-//   sum_i y_i k(|x_i - z|) = sum_p phi1_p(z) CDF_p(z) + phi1_p(-z) SURV_p(z)
-// (P:314-325 [eq fast_exact_decomposition_1d]) evaluated by "fast sum updating"
-// over the presorted data (P:326-340 [§2.1]) as two prefix scans -- a forward scan
-// (sources left of the target: the CDF part) and a backward scan (sources right of
-// it: the survival part) -- in the overflow-free moment basis of algebra.cuh.
+// apply_d1.cu -- the d = 1 hot path: K.v over the stored sort in
+// ONE cooperative launch when the sorted points fit one shared-memory chunk per CTA
+// (N <= #SMs x BLOCK x ITEMS; every BASELINE.json d = 1 config).  Method: the weighted
+// ECDF / survival-function decomposition of P:314-325 [eq fast_exact_decomposition_1d]
+// evaluated by "fast sum updating" over the presorted data (P:326-340 [§2.1]) in the
+// overflow-free moment basis of algebra.cuh (reading R5).
 //
-// B200 design: ONE cooperative launch, grid = 148 CTAs x 512 threads
-// (one per SM, every CTA co-resident).  CTA b owns a contiguous chunk of the sorted
-// order; the chunk's t, perm and the gathered v sit in 215 KB of shared memory.
-//   pass 1: per-thread sequential recurrences -> block scan of (span, moments) in both
-//           directions (warp shuffles) -> chunk aggregate published to global memory;
-//   barrier: self-resetting grid barrier (all CTAs resident, so no deadlock);
-//   carries: warp 0 folds the aggregates of chunks < b (forward), warp 1 those > b
-//           (backward) -- a decoupled look-back/look-ahead in one step;
-//   pass 2: re-run the per-thread recurrences from the carries, scatter out[perm].
-// The data is read from HBM exactly once: t (8 B) + perm (4 B) + v (8 B) + out (8 B).
-// Chunks larger than one shared-memory sub-tile stream through sub-tiles (re-read).
-#include <cooperative_groups.h>
-
+// B200 structure (k_d1_lpc, "local pass + correction"):
+//   0. the chunk's sorted t (+ perm, user order) arrive by 1-D bulk copies issued before
+//      griddepcontrol.wait (plan data); the gaps and e^{-gap} are computed into registers
+//      while v is still in flight;
+//   1. rank order: v by bulk copies; user order: the gathers v[perm] (after a 1/G-slice L2
+//      prefetch of v per CTA);
+//   2. LOCAL pass: each thread runs the forward and backward recurrences over its ITEMS
+//      consecutive points starting from zero state (two independent chains), keeping
+//      loc_j = self u_j + read_F + read_B in registers; the final states are the thread's
+//      aggregates;
+//   3. chunk aggregate = fixed-order plain sum of the thread aggregates shifted to the
+//      chunk's reference points (all shifts forward: e^{-x}, x >= 0), published as a
+//      self-validating record (every 8-byte word = 32 data bits + a 32-bit column tag,
+//      "LL" words: no fence, no flag, no barrier);
+//   4. while the other chunks publish: the block scan of the thread aggregates (warp
+//      shuffles) -> each thread's exclusive prefix / suffix inside the chunk;
+//   5. each thread folds the records it needs (one record per thread, poll until every
+//      word carries this column's tag; plain sums of forward shifts, fixed order);
+//   6. CORRECTION pass: the carry entering a thread adds e^{-D} sum_r beta_r D^r at a
+//      point D past the thread's reference (P + 3 FLOPs per point and direction);
+//      out = os2 (loc + both corrections), written back coalesced (rank order) or
+//      scattered to out[perm] (user order).
+// Determinism: every sum has a fixed order (no atomics on data), so repeated applies are
+// bitwise identical.
 #include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "algebra.cuh"
+#include "fexp.cuh"
 #include "internal.h"
+#include "tma.cuh"
 
 namespace gpm {
 
-__device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+namespace lpc {
 
-constexpr int D1_BLOCK = 512;
-constexpr int D1_ITEMS = 15;                 // odd: conflict-free strided 8-byte smem access
-constexpr int D1_SUB = D1_BLOCK * D1_ITEMS;  // 7680 points per shared-memory sub-tile
-constexpr int D1_WARPS = D1_BLOCK / 32;
-constexpr int D1_MAXSUB = 64;
+constexpr int NPART = 4;    // bulk-copy pipeline depth (parts of the chunk)
+constexpr int LL_W = 32;    // 8-byte words per record slot (<= 2 x 2 x 6 moments x 2 halves)
 
-template <int P>
-struct St {  // one-direction scan element: span D, E = e^{-D}, moments M
-  double D, E, M[P + 1];
-};
-
-template <int P>
-__device__ __forceinline__ St<P> st_identity() {
-  St<P> s;
-  s.D = 0.0; s.E = 1.0;
-#pragma unroll
-  for (int q = 0; q <= P; ++q) s.M[q] = 0.0;
-  return s;
-}
-
-// forward: A then B (A left of B): M = S(B.D) A.M + B.M
-template <int P>
-__device__ __forceinline__ St<P> comb_f(const St<P>& A, const St<P>& B) {
-  St<P> r;
-#pragma unroll
-  for (int q = 0; q <= P; ++q) r.M[q] = A.M[q];
-  advance<P>(r.M, B.D, B.E);
-#pragma unroll
-  for (int q = 0; q <= P; ++q) r.M[q] += B.M[q];
-  r.D = A.D + B.D; r.E = A.E * B.E;
-  return r;
-}
-
-// backward: A left of B: M = A.M + S(A.D) B.M
-template <int P>
-__device__ __forceinline__ St<P> comb_b(const St<P>& A, const St<P>& B) {
-  St<P> r;
-#pragma unroll
-  for (int q = 0; q <= P; ++q) r.M[q] = B.M[q];
-  advance<P>(r.M, A.D, A.E);
-#pragma unroll
-  for (int q = 0; q <= P; ++q) r.M[q] += A.M[q];
-  r.D = A.D + B.D; r.E = A.E * B.E;
-  return r;
-}
-
-template <int P>
-__device__ __forceinline__ St<P> shfl_st_up(const St<P>& s, int off) {
-  St<P> r;
-  r.D = __shfl_up_sync(0xffffffffu, s.D, off);
-  r.E = __shfl_up_sync(0xffffffffu, s.E, off);
-#pragma unroll
-  for (int q = 0; q <= P; ++q) r.M[q] = __shfl_up_sync(0xffffffffu, s.M[q], off);
-  return r;
-}
-template <int P>
-__device__ __forceinline__ St<P> shfl_st_down(const St<P>& s, int off) {
-  St<P> r;
-  r.D = __shfl_down_sync(0xffffffffu, s.D, off);
-  r.E = __shfl_down_sync(0xffffffffu, s.E, off);
-#pragma unroll
-  for (int q = 0; q <= P; ++q) r.M[q] = __shfl_down_sync(0xffffffffu, s.M[q], off);
-  return r;
-}
-
-template <int P>
-__device__ __forceinline__ St<P> agg_f(const D1Agg& a) {
-  St<P> s; s.D = a.D; s.E = a.E;
-#pragma unroll
-  for (int q = 0; q <= P; ++q) s.M[q] = a.F[q];
-  return s;
-}
-template <int P>
-__device__ __forceinline__ St<P> agg_b(const D1Agg& a) {
-  St<P> s; s.D = a.D; s.E = a.E;
-#pragma unroll
-  for (int q = 0; q <= P; ++q) s.M[q] = a.B[q];
-  return s;
-}
-__device__ __forceinline__ D1Agg ldcg_agg(const D1Agg* p) {
-  D1Agg a;
-  const double* s = reinterpret_cast<const double*>(p);
-  double* d = reinterpret_cast<double*>(&a);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) d[i] = __ldcg(s + i);
-  return a;
-}
-
-struct D1Smem {
-  double x[D1_SUB];   // t, then the gap Delta_j = t_j - t_{j-1}
-  double e[D1_SUB];   // e^{-Delta_j}
-  double u[D1_SUB];   // v[perm_j] (0 for non-sources)
-  int pi[D1_SUB];     // perm_j (user index)
-};
-
-struct D1Scratch {
-  double wf[D1_WARPS][5];  // warp totals, forward (D, E, M0..M2)
-  double wb[D1_WARPS][5];
-  double wfx[D1_WARPS][5]; // exclusive prefixes of the warp totals
-  double wbx[D1_WARPS][5];
-  double tot[2][5];        // sub-tile totals (forward, backward)
-  double carry[2][5];      // forward / backward carry of the current sub-tile
-  double subB[D1_MAXSUB][3];
-};
-
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
-    __threadfence();
-    const unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      unsigned cur;
-      do {
-        __nanosleep(32);
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
-      } while (cur == gen);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-struct D1Args {
-  const double* ts;   // sorted scaled coordinate (rank order)
-  const int* perm;    // rank -> user index, or nullptr (rank-space vectors)
-  const double* v;    // input (user order if perm, else rank order)
-  double* out;        // output (user order if perm, else rank order)
+struct Args {
+  const double* ts;    // sorted scaled coordinates (plan)
+  const int* perm;     // rank -> user index (plan, padded)
+  const double* v;     // input columns: user order or rank order
+  double* out;         // output columns: user order (targets only) or rank order
   int64_t n, n_src, tgt_off, chunk;
-  int nsub;
+  int nrhs;
+  int prefetch;        // user order: L2 prefetch of a 1/G slice of v per CTA
+  int64_t vstride, ostride;
   double os2;
-  D1Agg* chunk_aggs;  // [grid]
-  D1Agg* sub_aggs;    // [grid][D1_MAXSUB] (only when nsub > 1)
-  unsigned* bar;
+  unsigned long long* rec;   // [2 parities][G][LL_W] LL words
+  unsigned* ep;              // [G]: columns published by CTA b over the plan's life
+  unsigned long long* dbg;   // optional phase timestamps [G][16] (GPM_D1_TIMING)
+  int knob;                  // debug: skip phases (GPM_D1_KNOB; timing experiments only)
 };
 
-// Load sub-tile [g0, g0+cnt) into smem and convert t -> gaps; compute e^{-gap}.
-__device__ __forceinline__ void d1_load(const D1Args& a, D1Smem& sm, int64_t g0, int cnt) {
-  const int tid = threadIdx.x;
-  double tv[D1_ITEMS];
-  int pv[D1_ITEMS];
-#pragma unroll
-  for (int k = 0; k < D1_ITEMS; ++k) {
-    const int i = k * D1_BLOCK + tid;
-    if (i < cnt) {
-      tv[k] = __ldg(a.ts + g0 + i);
-      pv[k] = a.perm ? __ldg(a.perm + g0 + i) : static_cast<int>(g0 + i);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < D1_ITEMS; ++k) {
-    const int i = k * D1_BLOCK + tid;
-    if (i < cnt) {
-      sm.x[i] = tv[k];
-      sm.pi[i] = pv[k];
-      tv[k] = (pv[k] < a.n_src) ? __ldg(a.v + pv[k]) : 0.0;  // gather
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < D1_ITEMS; ++k) {
-    const int i = k * D1_BLOCK + tid;
-    if (i < cnt) sm.u[i] = tv[k];
-  }
-  __syncthreads();
-  const int i0 = tid * D1_ITEMS;
-  double tprev = 0.0;
-  if (i0 < cnt) {
-    if (i0 > 0) tprev = sm.x[i0 - 1];
-    else tprev = (g0 > 0) ? __ldg(a.ts + g0 - 1) : sm.x[0];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < D1_ITEMS; ++k) {
-    const int i = i0 + k;
-    if (i < cnt) {
-      const double t = sm.x[i];
-      const double dl = t - tprev;
-      tprev = t;
-      sm.x[i] = dl;
-      sm.e[i] = exp(-dl);
-    }
-  }
-  __syncthreads();
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// per-warp phase timestamps (lane 0 of every warp): dbg[(cta * 32 + warp) * 16 + slot]
+#define LPC_STAMP(k)                                                                      \
+  do {                                                                                    \
+    if (a.dbg && (threadIdx.x & 31) == 0)                                                 \
+      a.dbg[(blockIdx.x * 32 + (threadIdx.x >> 5)) * 16 + (k)] = gtimer();                \
+  } while (0)
+
+// LL words: 32 data bits in the low half, the column tag in the high half; each 8-byte
+// access is single-copy atomic, so a word with the expected tag carries valid data.
+__device__ __forceinline__ void st_ll2(unsigned long long* p, unsigned long long a,
+                                       unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b)
+               : "memory");
+}
+__device__ __forceinline__ void ld_ll2(const unsigned long long* p, unsigned long long& a,
+                                       unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long ll_word(unsigned tag, unsigned data) {
+  return ((unsigned long long)tag << 32) | data;
 }
 
-// Per-thread aggregates of its items (forward F, backward B, common D/E).
-template <int P>
-__device__ __forceinline__ void d1_thread_aggs(const D1Smem& sm, int cnt, St<P>& F, St<P>& B) {
-  const int i0 = threadIdx.x * D1_ITEMS;
-  F = st_identity<P>();
-  B = st_identity<P>();
+// scan element: span D, E = e^{-D}, NQ moments
+template <int NQ>
+struct Mon {
+  double D, E, M[NQ];
+};
+template <int NQ>
+__device__ __forceinline__ Mon<NQ> mon_id() {
+  Mon<NQ> r;
+  r.D = 0.0;
+  r.E = 1.0;
 #pragma unroll
-  for (int k = 0; k < D1_ITEMS; ++k) {
-    const int i = i0 + k;
-    if (i < cnt) {
-      const double dl = sm.x[i], e = sm.e[i];
-      advance<P>(F.M, dl, e);
-      F.M[0] += sm.u[i];
-      F.D += dl;
-      F.E *= e;
-    }
-  }
-#pragma unroll
-  for (int k = D1_ITEMS - 1; k >= 0; --k) {
-    const int i = i0 + k;
-    if (i < cnt) {
-      B.M[0] += sm.u[i];
-      advance<P>(B.M, sm.x[i], sm.e[i]);
-    }
-  }
-  B.D = F.D;
-  B.E = F.E;
+  for (int q = 0; q < NQ; ++q) r.M[q] = 0.0;
+  return r;
 }
-
-// Block-wide exclusive scans: Fx = combine of threads < me (forward),
-// Bx = combine of threads > me (backward); sub-tile totals returned in Ft / Bt.
-template <int P>
-__device__ __forceinline__ St<P> ld_st(const double* p) {
-  St<P> s; s.D = p[0]; s.E = p[1];
+// forward (A left of B): S(B.D) A + B
+template <int NQ>
+__device__ __forceinline__ Mon<NQ> mon_f(const Mon<NQ>& A, const Mon<NQ>& B) {
+  Mon<NQ> r;
 #pragma unroll
-  for (int q = 0; q <= P; ++q) s.M[q] = p[2 + q];
+  for (int q = 0; q < NQ; ++q) r.M[q] = A.M[q];
+  advance<NQ - 1>(r.M, B.D, B.E);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) r.M[q] += B.M[q];
+  r.D = A.D + B.D;
+  r.E = A.E * B.E;
+  return r;
+}
+// backward (A left of B): A + S(A.D) B
+template <int NQ>
+__device__ __forceinline__ Mon<NQ> mon_b(const Mon<NQ>& A, const Mon<NQ>& B) {
+  Mon<NQ> r;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) r.M[q] = B.M[q];
+  advance<NQ - 1>(r.M, A.D, A.E);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) r.M[q] += A.M[q];
+  r.D = A.D + B.D;
+  r.E = A.E * B.E;
+  return r;
+}
+template <int NQ>
+__device__ __forceinline__ Mon<NQ> mon_shfl(const Mon<NQ>& s, int off, bool up) {
+  Mon<NQ> r;
+  if (up) {
+    r.D = __shfl_up_sync(0xffffffffu, s.D, off);
+    r.E = __shfl_up_sync(0xffffffffu, s.E, off);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) r.M[q] = __shfl_up_sync(0xffffffffu, s.M[q], off);
+  } else {
+    r.D = __shfl_down_sync(0xffffffffu, s.D, off);
+    r.E = __shfl_down_sync(0xffffffffu, s.E, off);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) r.M[q] = __shfl_down_sync(0xffffffffu, s.M[q], off);
+  }
+  return r;
+}
+template <int NQ>
+__device__ __forceinline__ void mon_st(double* p, const Mon<NQ>& s) {
+  p[0] = s.D;
+  p[1] = s.E;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) p[2 + q] = s.M[q];
+}
+template <int NQ>
+__device__ __forceinline__ Mon<NQ> mon_ld(const double* p) {
+  Mon<NQ> s;
+  s.D = p[0];
+  s.E = p[1];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) s.M[q] = p[2 + q];
   return s;
 }
-template <int P>
-__device__ __forceinline__ void st_st(double* p, const St<P>& s) {
-  p[0] = s.D; p[1] = s.E;
-#pragma unroll
-  for (int q = 0; q <= P; ++q) p[2 + q] = s.M[q];
-}
 
-template <int P>
-__device__ __forceinline__ void d1_block_scan(D1Scratch& sc, const St<P>& F, const St<P>& B,
-                                              St<P>& Fx, St<P>& Bx, St<P>& Ft, St<P>& Bt) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  St<P> fi = F, bi = B;
+// read(S(D) C) = e^{-D} sum_r beta_r D^r with beta_r = sum_{q >= r} c_q C(q, q - r) C_{q-r}
+template <int P, int KIND>
+__device__ __forceinline__ void carry_beta(const double* C, double* beta) {
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    St<P> l = shfl_st_up<P>(fi, off);
-    if (lane >= off) fi = comb_f<P>(l, fi);
-    St<P> r = shfl_st_down<P>(bi, off);
-    if (lane + off < 32) bi = comb_b<P>(bi, r);
-  }
-  if (lane == 31) st_st<P>(sc.wf[warp], fi);
-  if (lane == 0) st_st<P>(sc.wb[warp], bi);
-  St<P> fe = shfl_st_up<P>(fi, 1);
-  if (lane == 0) fe = st_identity<P>();
-  St<P> be = shfl_st_down<P>(bi, 1);
-  if (lane == 31) be = st_identity<P>();
-  __syncthreads();
-  if (warp == 0) {          // exclusive scan of the forward warp totals
-    St<P> x = lane < D1_WARPS ? ld_st<P>(sc.wf[lane]) : st_identity<P>();
+  for (int r = 0; r <= P; ++r) {
+    double br = 0.0;
 #pragma unroll
-    for (int off = 1; off < D1_WARPS; off <<= 1) {
-      St<P> l = shfl_st_up<P>(x, off);
-      if (lane >= off) x = comb_f<P>(l, x);
-    }
-    St<P> xe = shfl_st_up<P>(x, 1);
-    if (lane == 0) xe = st_identity<P>();
-    if (lane < D1_WARPS) st_st<P>(sc.wfx[lane], xe);
-    if (lane == D1_WARPS - 1) st_st<P>(sc.tot[0], x);
-  } else if (warp == 1) {   // exclusive suffix scan of the backward warp totals
-    St<P> x = lane < D1_WARPS ? ld_st<P>(sc.wb[lane]) : st_identity<P>();
-#pragma unroll
-    for (int off = 1; off < D1_WARPS; off <<= 1) {
-      St<P> r = shfl_st_down<P>(x, off);
-      if (lane + off < 32) x = comb_b<P>(x, r);
-    }
-    St<P> xe = shfl_st_down<P>(x, 1);
-    if (lane >= D1_WARPS - 1) xe = st_identity<P>();
-    if (lane < D1_WARPS) st_st<P>(sc.wbx[lane], xe);
-    if (lane == 0) st_st<P>(sc.tot[1], x);
-  }
-  __syncthreads();
-  Fx = comb_f<P>(ld_st<P>(sc.wfx[warp]), fe);
-  Bx = comb_b<P>(be, ld_st<P>(sc.wbx[warp]));
-  Ft = ld_st<P>(sc.tot[0]);
-  Bt = ld_st<P>(sc.tot[1]);
-}
-
-// Pass 2 for one sub-tile: per-thread recurrences from carries, scatter.
-template <int P>
-__device__ __forceinline__ void d1_apply_items(const D1Args& a, const D1Smem& sm, int cnt,
-                                               const double* Fin, const double* Bin) {
-  const int i0 = threadIdx.x * D1_ITEMS;
-  double M[P + 1], rf[D1_ITEMS];
-#pragma unroll
-  for (int q = 0; q <= P; ++q) M[q] = Fin[q];
-#pragma unroll
-  for (int k = 0; k < D1_ITEMS; ++k) {
-    const int i = i0 + k;
-    rf[k] = 0.0;
-    if (i < cnt) {
-      advance<P>(M, sm.x[i], sm.e[i]);
-      rf[k] = read0<P>(M);
-      M[0] += sm.u[i];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q <= P; ++q) M[q] = Bin[q];
-#pragma unroll
-  for (int k = D1_ITEMS - 1; k >= 0; --k) {
-    const int i = i0 + k;
-    if (i < cnt) {
-      const double uu = sm.u[i];
-      const double val = a.os2 * (uu + (rf[k] + read0<P>(M)));
-      M[0] += uu;
-      advance<P>(M, sm.x[i], sm.e[i]);
-      const int pi = sm.pi[i];
-      if (pi >= a.tgt_off) a.out[pi - a.tgt_off] = val;
-    }
+    for (int q = r; q <= P; ++q)
+      if (rcoef(P, KIND, q) != 0.0) br = fma(rcoef(P, KIND, q) * binom(q, q - r), C[q - r], br);
+    beta[r] = br;
   }
 }
 
-template <int P>
-__global__ void __launch_bounds__(D1_BLOCK, 1) k_d1_coop(D1Args a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  D1Smem& sm = *reinterpret_cast<D1Smem*>(smem_raw);
-  __shared__ D1Scratch sc;
+constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
-  const int64_t c0 = blockIdx.x * a.chunk;
-  const int64_t c1 = min(a.n, c0 + a.chunk);
-  const int64_t len = lmax(0, c1 - c0);
-  St<P> F, B, Fx, Bx, Ft, Bt;
-  St<P> chF = st_identity<P>(), chB = st_identity<P>();
-
-  // ---- pass 1: chunk aggregate
-  for (int s = 0; s < a.nsub; ++s) {
-    const int64_t g0 = c0 + (int64_t)s * D1_SUB;
-    const int cnt = (int)lmax(0, lmin(D1_SUB, c1 - g0));
-    if (s > 0) __syncthreads();
-    d1_load(a, sm, g0, cnt);
-    d1_thread_aggs<P>(sm, cnt, F, B);
-    d1_block_scan<P>(sc, F, B, Fx, Bx, Ft, Bt);
-    if (a.nsub > 1 && threadIdx.x == 0) {
-      D1Agg g; g.D = Ft.D; g.E = Ft.E;
-      for (int q = 0; q < 3; ++q) { g.F[q] = q <= P ? Ft.M[q] : 0.0; g.B[q] = q <= P ? Bt.M[q] : 0.0; }
-      a.sub_aggs[(int64_t)blockIdx.x * D1_MAXSUB + s] = g;
+// Warp sum of NV values by a reduce-scatter butterfly (NP = NV rounded up to a power of
+// two): each round halves the values a lane keeps, so a warp moves NP - 1 + log2(32/NP)
+// doubles per lane instead of 5 NV.  Returns the warp total of value *idx (same on every
+// lane of a group of 32/NP lanes); fixed order, hence deterministic.
+template <int NV>
+__device__ __forceinline__ double warp_sum_scatter(const double* in, int lane, int* idx) {
+  constexpr int NP = pow2_at_least(NV);
+  static_assert(NP <= 32, "at most 32 values");
+  double v[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) v[i] = i < NV ? in[i] : 0.0;
+  int id = 0;
+#pragma unroll
+  for (int r = 0, cur = NP; r < 5; ++r) {
+    const int o = 16 >> r;
+    if (cur > 1) {
+      const int half = cur / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double keep = up ? v[i + half] : v[i];
+        const double send = up ? v[i] : v[i + half];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      if (up) id += half;
+      cur = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
     }
-    chF = comb_f<P>(chF, Ft);
-    chB = comb_b<P>(chB, Bt);   // sub-tiles are visited left to right
   }
-  (void)len;
-  if (threadIdx.x == 0) {
-    D1Agg g; g.D = chF.D; g.E = chF.E;
-    for (int q = 0; q < 3; ++q) { g.F[q] = q <= P ? chF.M[q] : 0.0; g.B[q] = q <= P ? chB.M[q] : 0.0; }
-    a.chunk_aggs[blockIdx.x] = g;
-  }
-  grid_barrier(a.bar, gridDim.x);
+  *idx = id;
+  return v[0];
+}
 
-  // ---- carries from the other chunks (warp 0: forward, warp 1: backward)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp < 2) {
-    const int b = blockIdx.x;
-    const int lo = warp == 0 ? 0 : b + 1;
-    const int hi = warp == 0 ? b : (int)gridDim.x;
-    const int cntc = max(0, hi - lo);
-    const int per = (cntc + 31) / 32;
-    St<P> X = st_identity<P>();
-    for (int k = 0; k < per; ++k) {
-      const int j = lo + lane * per + k;
-      if (j < hi) {
-        const D1Agg g = ldcg_agg(a.chunk_aggs + j);
-        X = warp == 0 ? comb_f<P>(X, agg_f<P>(g)) : comb_b<P>(X, agg_b<P>(g));
+// One scan element of a run of points (forward moments MF referenced at the run's last
+// point, backward moments MB referenced at the point before its first point, span D from
+// that point to the last point, E = e^{-D}).
+template <int NQ>
+struct Run {
+  double D, E, MF[NQ], MB[NQ];
+};
+
+// P: moment order (KIND 0: nu = P + 1/2; KIND 1: the lengthscale gradient of nu = P - 1/2)
+template <int P, int KIND, int BLOCK, int SEGS, int SL, bool USER>
+__global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
+  constexpr int ITEMS = SEGS * SL;    // my points: SEGS segments of SL consecutive points
+  constexpr int NQ = P + 1;
+  constexpr int SUB = BLOCK * ITEMS;
+  constexpr int NW = BLOCK / 32;
+  constexpr int PT = BLOCK / NPART;   // threads per load part
+  constexpr int PSZ = PT * ITEMS;     // points per load part
+  constexpr int NV = 2 * NQ;          // record values: forward + backward moments
+  constexpr double SELF = KIND == 0 ? 1.0 : 0.0;   // k(0) = 1; g(0) = 0
+  static_assert(PSZ % 4 == 0, "load parts must stay 16-byte aligned");
+  static_assert(2 * NV <= LL_W, "record slot too small");
+  static_assert(NW <= 32, "one warp scans the warp totals");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* s_t = reinterpret_cast<double*>(smem_raw);   // SUB + 8: t (clamped past the end)
+  double* s_e = s_t + SUB + 8;                         // SUB: e^{-gap}
+  double* s_u = s_e + SUB;                             // SUB: u, then out (rank order)
+  int* s_pi = reinterpret_cast<int*>(s_u + SUB);       // SUB + 8 (user order)
+  __shared__ uint64_t mbar[NPART], mbar_v[NPART], mbar_tab;
+  __shared__ __align__(16) double s_tab[64];
+  __shared__ double s_wf[NW][NQ + 2], s_wb[NW][NQ + 2];   // warp totals of the block scan
+  __shared__ double s_red[NW][NV];                        // warp sums (chunk sum / fold)
+  __shared__ double s_C[NV];                              // folded chunk carries
+  __shared__ double s_tl[160 + 1];                        // chunk-end t: s_tl[b + 1], s_tl[0] = t_0
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int64_t c0 = (int64_t)c * a.chunk;
+  const int cnt = (int)min(a.chunk, a.n - c0);   // >= 1 (host: every CTA owns points)
+  const int j0 = tid * ITEMS;
+  const int mypart = tid / PT;
+  const bool part_live = mypart * PSZ < cnt;
+  const bool v_bulk = !USER && ((reinterpret_cast<uintptr_t>(a.v + c0) & 15) == 0) &&
+                      (a.vstride % 2 == 0 || a.nrhs == 1);
+  // rank order: a column of v by bulk copies (thread 0 owns the barriers)
+  auto issue_v = [&](int col) {
+#pragma unroll 1
+    for (int p = 0; p < NPART; ++p) {
+      const int lo = p * PSZ, hi = min(cnt, lo + PSZ);
+      if (lo < hi) {
+        const unsigned nu = (unsigned)((hi - lo) & ~1);   // never over-read v
+        mbar_expect_tx(&mbar_v[p], nu * 8);
+        if (nu) tma_load_1d(s_u + lo, a.v + col * a.vstride + c0 + lo, nu * 8, &mbar_v[p]);
       }
     }
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      St<P> Y = shfl_st_down<P>(X, off);
-      if (lane + off < 32) X = warp == 0 ? comb_f<P>(X, Y) : comb_b<P>(X, Y);
-    }
-    if (lane == 0) {
-      for (int q = 0; q <= P; ++q) sc.carry[warp][2 + q] = X.M[q];
-    }
-  }
-  __syncthreads();
+  };
+  auto prefetch_v = [&](int col) {   // user order: this CTA's 1/G slice of v into L2
+    const int64_t per = (a.n_src + G - 1) / G;
+    const int64_t lo = min((int64_t)c * per, a.n_src);
+    const int64_t hi = min(lo + per, a.n_src);
+    if (hi > lo) prefetch_l2_range(a.v + col * a.vstride + lo, (size_t)(hi - lo) * 8);
+  };
 
-  if (a.nsub == 1) {
-    // data, thread aggregates and block scan are still live: apply directly
-    const int cnt = (int)len;
-    double Fin[P + 1], Bin[P + 1];
-#pragma unroll
-    for (int q = 0; q <= P; ++q) { Fin[q] = sc.carry[0][2 + q]; Bin[q] = sc.carry[1][2 + q]; }
-    // thread carry = combine(chunk carry, block-exclusive part)
-    advance<P>(Fin, Fx.D, Fx.E);
-    double tmp[P + 1];
-#pragma unroll
-    for (int q = 0; q <= P; ++q) { Fin[q] += Fx.M[q]; tmp[q] = Bin[q]; }
-    advance<P>(tmp, Bx.D, Bx.E);
-#pragma unroll
-    for (int q = 0; q <= P; ++q) Bin[q] = Bx.M[q] + tmp[q];
-    d1_apply_items<P>(a, sm, cnt, Fin, Bin);
-    return;
-  }
-
-  // ---- nsub > 1: backward carries of each sub-tile (thread 0, sequential)
-  if (threadIdx.x == 0) {
-    double Bc[P + 1];
-    for (int q = 0; q <= P; ++q) Bc[q] = sc.carry[1][2 + q];
-    for (int s = a.nsub - 1; s >= 0; --s) {
-      for (int q = 0; q <= P; ++q) sc.subB[s][q] = Bc[q];
-      const D1Agg g = ldcg_agg(a.sub_aggs + (int64_t)blockIdx.x * D1_MAXSUB + s);
-      St<P> A = agg_b<P>(g);
-      double t2[P + 1];
-      for (int q = 0; q <= P; ++q) t2[q] = Bc[q];
-      advance<P>(t2, A.D, A.E);
-      for (int q = 0; q <= P; ++q) Bc[q] = A.M[q] + t2[q];
+  LPC_STAMP(0);
+  // ---- prologue: the bulk copies go out first (thread 0 initialises and arms the
+  // barriers; the others meet them after the first __syncthreads); every global scalar
+  // goes to a register and is consumed late, so no load latency sits before the copies
+  if (tid == 0) {
+    for (int p = 0; p < NPART; ++p) {
+      mbar_init(&mbar[p], 1);
+      mbar_init(&mbar_v[p], 1);
+    }
+    mbar_init(&mbar_tab, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&mbar_tab, 64 * 8);
+    tma_load_1d(s_tab, g_fexp_tab, 64 * 8, &mbar_tab);
+#pragma unroll 1
+    for (int p = 0; p < NPART; ++p) {   // plan data: before griddepcontrol.wait
+      const int lo = p * PSZ, hi = min(cnt, lo + PSZ);
+      if (lo < hi) {
+        const unsigned nt = (unsigned)(((hi - lo) + 1) & ~1);   // padded plan arrays
+        const unsigned np = (unsigned)(((hi - lo) + 3) & ~3);
+        mbar_expect_tx(&mbar[p], nt * 8 + (USER ? np * 4 : 0));
+        tma_load_1d(s_t + lo, a.ts + c0 + lo, nt * 8, &mbar[p]);
+        if (USER) tma_load_1d(s_pi + lo, a.perm + c0 + lo, np * 4, &mbar[p]);
+      }
     }
   }
-  __syncthreads();
-  double Fc[P + 1];
+  // boundary coordinates (clamped to the chunk): the point before my first point, the
+  // last points of my segments, this chunk's reference (the point before its first point;
+  // t_0 for chunk 0: its first gap is 0) and last point, and one chunk end per thread
+  // for the fold's shift distances (-> s_tl)
+  const int64_t cl = c0 + cnt - 1;
+  const double tprev = __ldg(a.ts + (j0 < cnt ? (c0 + j0 > 0 ? c0 + j0 - 1 : 0) : cl));
+  double tseg[SEGS];   // the last point of each of my segments
 #pragma unroll
-  for (int q = 0; q <= P; ++q) Fc[q] = sc.carry[0][2 + q];
-  for (int s = 0; s < a.nsub; ++s) {
-    const int64_t g0 = c0 + (int64_t)s * D1_SUB;
-    const int cnt = (int)lmax(0, lmin(D1_SUB, c1 - g0));
+  for (int sg = 0; sg < SEGS; ++sg) tseg[sg] = __ldg(a.ts + min(c0 + j0 + (sg + 1) * SL - 1, cl));
+  const double tmye = tseg[SEGS - 1];
+  const double tref0 = __ldg(a.ts + (c0 > 0 ? c0 - 1 : 0));
+  const double tlast = __ldg(a.ts + cl);
+  const double my_tl = tid <= G ? __ldg(a.ts + (tid == 0 ? 0 : min((int64_t)tid * a.chunk, a.n) - 1))
+                                : 0.0;
+  __syncthreads();   // barrier initialisation visible
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // v, records and ep of earlier launches
+  asm volatile("griddepcontrol.launch_dependents;");
+  LPC_STAMP(8);
+  const unsigned base = *(volatile const unsigned*)(a.ep + c);   // columns published so far
+  if (tid == 0 && v_bulk) issue_v(0);
+  if (USER && a.prefetch && tid == 32) prefetch_v(0);
+  mbar_wait(&mbar_tab, 0);
+  LPC_STAMP(7);
+  if (part_live) mbar_wait(&mbar[mypart], 0);
+  LPC_STAMP(9);
+  // ---- my points' e^{-gap} (while v is in flight), neutral tails: t clamped to the last
+  // point (gap 0), u = 0, no source index
+  {
+    double tp = tprev;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int j = j0 + k;
+      double tk = tlast;
+      if (j < cnt) tk = s_t[j];
+      else s_t[j] = tlast;
+      s_e[j] = fexp_neg(tk - tp, s_tab);
+      tp = tk;
+      if (j >= cnt) s_u[j] = 0.0;
+      if (USER && j >= ((cnt + 3) & ~3)) s_pi[j] = INT_MAX;
+    }
+  }
+  double uu[USER ? ITEMS : 1];
+  if (USER) {   // the first column's gathers
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int pi = s_pi[j0 + k];
+      uu[k] = pi < a.n_src ? __ldg(a.v + pi) : 0.0;
+    }
+  }
+  // segment spans (the point before a segment -> its last point) for the scan elements
+  double DS[SEGS], ES[SEGS];
+#pragma unroll
+  for (int sg = 0; sg < SEGS; ++sg) {
+    DS[sg] = tseg[sg] - (sg ? tseg[sg - 1] : tprev);
+    ES[sg] = fexp_neg(DS[sg], s_tab);
+  }
+  LPC_STAMP(1);
+
+#pragma unroll 1
+  for (int col = 0; col < a.nrhs; ++col) {
+    const double* vcol = a.v + col * a.vstride;
+    double* ocol = a.out + col * a.ostride;
+    const unsigned tag = base + (unsigned)col + 1u;
+    unsigned long long* recp = a.rec + (size_t)(col & 1) * G * LL_W;
+    // ---- u of my points into s_u (own items only: no block barrier needed)
+    if (USER) {
+      if (col > 0) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+          const int pi = s_pi[j0 + k];
+          uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
+        }
+      }
+      if (a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = uu[k];
+    } else if (v_bulk) {
+      if (part_live) mbar_wait(&mbar_v[mypart], (unsigned)(col & 1));
+      const int lo = mypart * PSZ, hi = min(cnt, lo + PSZ);
+      if (lo < hi && ((hi - lo) & 1) && tid == (hi - 1) / ITEMS)   // odd tail element
+        s_u[hi - 1] = __ldg(vcol + c0 + hi - 1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = j0 + k < cnt ? __ldg(vcol + c0 + j0 + k) : 0.0;
+    }
+    LPC_STAMP(2);
+    // ---- local pass from zero state, segment by segment: the forward and backward
+    // recurrences over the segment's points interleaved (two chains), the segment's t, u
+    // and e^{-gap} loaded once into registers; loc_j = self u_j + read_F + read_B
+    double loc[ITEMS];
+    double FS[SEGS][NQ], BS[SEGS][NQ];   // segment aggregates (F at its last point, B at
+                                         // the point before its first point)
+#pragma unroll
+    for (int sg = 0; sg < SEGS; ++sg) {
+      const int i0 = sg * SL;
+      double tt[SL + 1], ee[SL], uu2[SL];
+      tt[0] = sg ? tseg[sg - 1] : tprev;
+#pragma unroll
+      for (int k = 0; k < SL; ++k) {
+        tt[k + 1] = s_t[j0 + i0 + k];
+        ee[k] = s_e[j0 + i0 + k];
+        uu2[k] = s_u[j0 + i0 + k];
+      }
+      double F[NQ], B[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) F[q] = B[q] = 0.0;
+#pragma unroll
+      for (int k = 0; k < SL; ++k) {
+        const int kf = k, kb = SL - 1 - k;   // forward point kf, backward point kb
+        if (k > 0) advance<P>(F, tt[kf + 1] - tt[kf], ee[kf]);
+        const double rf = fma(SELF, uu2[kf], k > 0 ? readc0<P, KIND>(F) : 0.0);
+        F[0] += uu2[kf];
+        if (k > 0) advance<P>(B, tt[kb + 2] - tt[kb + 1], ee[kb + 1]);
+        const double rb = k > 0 ? readc0<P, KIND>(B) : 0.0;
+        B[0] += uu2[kb];
+        // first touch assigns (the middle point is touched by both chains in one step)
+        if (kf <= kb) loc[i0 + kf] = rf; else loc[i0 + kf] += rf;
+        if (kb > kf) loc[i0 + kb] = rb; else loc[i0 + kb] += rb;
+      }
+      advance<P>(B, tt[1] - tt[0], ee[0]);   // -> the point before the segment
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        FS[sg][q] = F[q];
+        BS[sg][q] = B[q];
+      }
+    }
+    // my scan element = the segments in order
+    Run<NQ> me;
+    me.D = DS[0];
+    me.E = ES[0];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      me.MF[q] = FS[0][q];
+      me.MB[q] = BS[SEGS - 1][q];
+    }
+#pragma unroll
+    for (int sg = 1; sg < SEGS; ++sg) {
+      advance<P>(me.MF, DS[sg], ES[sg]);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) me.MF[q] += FS[sg][q];
+      me.D += DS[sg];
+      me.E *= ES[sg];
+    }
+#pragma unroll
+    for (int sg = SEGS - 2; sg >= 0; --sg) {
+      advance<P>(me.MB, DS[sg], ES[sg]);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) me.MB[q] += BS[sg][q];
+    }
+    LPC_STAMP(3);
+    // ---- chunk aggregate = fixed-order sum of the shifted thread aggregates -> record
+    {
+      double m[NV];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        m[q] = me.MF[q];
+        m[NQ + q] = me.MB[q];
+      }
+      const double dF = tlast - tmye;    // my last point -> chunk last point
+      const double dB = tprev - tref0;   // chunk reference -> my t_prev
+      advance<P>(m, dF, fexp_neg(dF, s_tab));
+      advance<P>(m + NQ, dB, fexp_neg(dB, s_tab));
+      if (col == 0 && tid <= G) s_tl[tid] = my_tl;   // read after the barrier below
+      int id;
+      const double sw = warp_sum_scatter<NV>(m, lane, &id);
+      if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp][id] = sw;
+    }
     __syncthreads();
-    d1_load(a, sm, g0, cnt);
-    d1_thread_aggs<P>(sm, cnt, F, B);
-    d1_block_scan<P>(sc, F, B, Fx, Bx, Ft, Bt);
-    double Fin[P + 1], Bin[P + 1], tmp[P + 1];
+    if (tid < NV) {   // one value per thread, warps summed in order, published as 2 words
+      double s = 0.0;
+#pragma unroll 1
+      for (int w = 0; w < NW; ++w) s += s_red[w][tid];
+      st_ll2(recp + (size_t)c * LL_W + 2 * tid, ll_word(tag, (unsigned)__double2loint(s)),
+             ll_word(tag, (unsigned)__double2hiint(s)));
+    }
+    LPC_STAMP(4);
+    // ---- the record this thread folds: loads issued now, checked after the block scan
+    const int b = tid;
+    const bool fold_me = b < G && b != c;
+    const int o = b < c ? 0 : NQ;   // forward moments of earlier chunks, backward of later
+    const unsigned long long* wrec = recp + (size_t)b * LL_W + 2 * o;
+    unsigned long long x[2 * NQ];
+    if (fold_me) {
 #pragma unroll
-    for (int q = 0; q <= P; ++q) { Fin[q] = Fc[q]; tmp[q] = sc.subB[s][q]; }
-    advance<P>(Fin, Fx.D, Fx.E);
-    advance<P>(tmp, Bx.D, Bx.E);
+      for (int i = 0; i < NQ; ++i) ld_ll2(wrec + 2 * i, x[2 * i], x[2 * i + 1]);
+    }
+    // ---- block scan of the thread elements (overlaps the other chunks' publication):
+    // forward inclusive prefix / backward inclusive suffix per warp, then the warp totals
+    Mon<NQ> fe, be;
+    {
+      Mon<NQ> fi, bi;
+      fi.D = bi.D = me.D;
+      fi.E = bi.E = me.E;
 #pragma unroll
-    for (int q = 0; q <= P; ++q) { Fin[q] += Fx.M[q]; Bin[q] = Bx.M[q] + tmp[q]; }
-    d1_apply_items<P>(a, sm, cnt, Fin, Bin);
-    // advance the forward carry over this sub-tile
-    advance<P>(Fc, Ft.D, Ft.E);
+      for (int q = 0; q < NQ; ++q) {
+        fi.M[q] = me.MF[q];
+        bi.M[q] = me.MB[q];
+      }
+#pragma unroll 1
+      for (int off = 1; off < 32; off <<= 1) {
+        const Mon<NQ> l = mon_shfl<NQ>(fi, off, true);
+        const Mon<NQ> r = mon_shfl<NQ>(bi, off, false);
+        if (lane >= off) fi = mon_f<NQ>(l, fi);
+        if (lane + off < 32) bi = mon_b<NQ>(bi, r);
+      }
+      if (lane == 31) mon_st<NQ>(s_wf[warp], fi);
+      if (lane == 0) mon_st<NQ>(s_wb[warp], bi);
+      fe = mon_shfl<NQ>(fi, 1, true);    // exclusive within the warp
+      be = mon_shfl<NQ>(bi, 1, false);
+      if (lane == 0) fe = mon_id<NQ>();
+      if (lane == 31) be = mon_id<NQ>();
+    }
+    LPC_STAMP(10);
+    // ---- fold my record: re-poll until every word carries this column's tag
+    {
+      double fm[NV];
 #pragma unroll
-    for (int q = 0; q <= P; ++q) Fc[q] += Ft.M[q];
-  }
+      for (int q = 0; q < NV; ++q) fm[q] = 0.0;
+      if (fold_me) {
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < 2 * NQ; ++i) ok &= (unsigned)(x[i] >> 32) == tag;
+        while (!ok) {
+          ok = true;
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) {
+            ld_ll2(wrec + 2 * i, x[2 * i], x[2 * i + 1]);
+            ok &= (unsigned)(x[2 * i] >> 32) == tag && (unsigned)(x[2 * i + 1] >> 32) == tag;
+          }
+        }
+        double mv[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          mv[q] = __hiloint2double((int)(unsigned)x[2 * q + 1], (int)(unsigned)x[2 * q]);
+        // forward: chunk b's last point -> my chunk's reference (the point before it);
+        // backward: chunk b's reference -> my chunk's last point
+        const double D = b < c ? s_tl[c] - s_tl[b + 1] : s_tl[b] - s_tl[c + 1];
+        advance<P>(mv, D, fexp_neg(D, s_tab));
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          fm[q] = b < c ? mv[q] : 0.0;
+          fm[NQ + q] = b < c ? 0.0 : mv[q];
+        }
+      }
+      LPC_STAMP(11);
+      if (warp < (G + 31) / 32) {
+        int id;
+        const double sw = warp_sum_scatter<NV>(fm, lane, &id);
+        if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp][id] = sw;
+      }
+    }
+    __syncthreads();   // s_wf / s_wb warp totals, s_red fold partials
+    LPC_STAMP(5);
+    if (warp < 2) {    // warp 0: exclusive forward prefix of the warp totals; warp 1: suffix
+      const bool fw = warp == 0;
+      Mon<NQ> xw = lane < NW ? mon_ld<NQ>(fw ? s_wf[lane] : s_wb[lane]) : mon_id<NQ>();
+#pragma unroll 1
+      for (int off = 1; off < NW; off <<= 1) {
+        const Mon<NQ> y = mon_shfl<NQ>(xw, off, fw);
+        if (fw && lane >= off) xw = mon_f<NQ>(y, xw);
+        if (!fw && lane + off < 32) xw = mon_b<NQ>(xw, y);
+      }
+      Mon<NQ> xe = mon_shfl<NQ>(xw, 1, fw);
+      if ((fw && lane == 0) || (!fw && lane >= NW - 1)) xe = mon_id<NQ>();
+      __syncwarp();
+      if (lane < NW) mon_st<NQ>(fw ? s_wf[lane] : s_wb[lane], xe);
+    } else if (tid - 64 < NV) {   // chunk carries: fold partials summed in order
+      double s = 0.0;
+#pragma unroll 1
+      for (int w = 0; w < (G + 31) / 32; ++w) s += s_red[w][tid - 64];
+      s_C[tid - 64] = s;
+    }
+    __syncthreads();
+    LPC_STAMP(13);
+    // ---- the carries entering my segments, and the correction pass: the forward state
+    // at the point before segment s is G_s (G_0 from the earlier threads and chunks,
+    // G_{s+1} = S(DS_s) G_s + FS_s), the backward state at its last point is Y_s (Y_last from
+    // the later threads and chunks, Y_{s-1} = BS_s + S(DS_s) Y_s).  A carry C seen from a
+    // point D further on reads e^{-D} sum_r beta_r D^r (beta from C, carry_beta).
+    {
+      const Mon<NQ> wf = mon_ld<NQ>(s_wf[warp]), wb = mon_ld<NQ>(s_wb[warp]);
+      const Mon<NQ> Fx = mon_f<NQ>(wf, fe);   // threads before me, referenced at my t_prev
+      const Mon<NQ> Bx = mon_b<NQ>(be, wb);   // threads after me, referenced at my last point
+      double g[NQ], y[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        g[q] = s_C[q];
+        y[q] = s_C[NQ + q];
+      }
+      advance<P>(g, Fx.D, Fx.E);   // chunk reference -> my t_prev
+      advance<P>(y, Bx.D, Bx.E);   // chunk last point -> my last point
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        g[q] += Fx.M[q];
+        y[q] += Bx.M[q];
+      }
+      double gs[SEGS][NQ], ys[SEGS][NQ];   // G_s (point before s), Y_s (last point of s)
+#pragma unroll
+      for (int sg = 0; sg < SEGS; ++sg) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) gs[sg][q] = g[q];
+        if (sg + 1 < SEGS) {
+          advance<P>(g, DS[sg], ES[sg]);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) g[q] += FS[sg][q];
+        }
+      }
+#pragma unroll
+      for (int sg = SEGS - 1; sg >= 0; --sg) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) ys[sg][q] = y[q];
+        if (sg > 0) {
+          advance<P>(y, DS[sg], ES[sg]);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) y[q] += BS[sg][q];
+        }
+      }
+      LPC_STAMP(14);
+#pragma unroll
+      for (int sg = 0; sg < SEGS; ++sg) {
+        const int i0 = sg * SL;
+        double tt[SL + 1], ee[SL];
+        tt[0] = sg ? tseg[sg - 1] : tprev;
+#pragma unroll
+        for (int k = 0; k < SL; ++k) {
+          tt[k + 1] = s_t[j0 + i0 + k];
+          ee[k] = s_e[j0 + i0 + k];
+        }
+        double bX[NQ], bY[NQ];
+        advance<P>(gs[sg], tt[1] - tt[0], ee[0]);   // -> the segment's first point
+        carry_beta<P, KIND>(gs[sg], bX);
+        carry_beta<P, KIND>(ys[sg], bY);
+        double Df = 0.0, Ef = 1.0, Db = 0.0, Eb = 1.0;
+#pragma unroll
+        for (int k = 0; k < SL; ++k) {
+          const int kf = k, kb = SL - 1 - k;
+          if (k > 0) {
+            Df += tt[kf + 1] - tt[kf];
+            Ef *= ee[kf];
+            Db += tt[kb + 2] - tt[kb + 1];
+            Eb *= ee[kb + 1];
+          }
+          double hf = bX[P], hb = bY[P];
+#pragma unroll
+          for (int r = P - 1; r >= 0; --r) {
+            hf = fma(hf, Df, bX[r]);
+            hb = fma(hb, Db, bY[r]);
+          }
+          loc[i0 + kf] = fma(Ef, hf, loc[i0 + kf]);
+          loc[i0 + kb] = fma(Eb, hb, loc[i0 + kb]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const double val = a.os2 * loc[k];
+        const int j = j0 + k;
+        if (USER) {
+          const int pi = s_pi[j];
+          if (j < cnt && pi >= a.tgt_off) ocol[pi - a.tgt_off] = val;
+        } else if (j < cnt) {   // the tail stays 0 for the next column
+          s_u[j] = val;
+        }
+      }
+    }
+    LPC_STAMP(12);
+    if (!USER) {   // this warp's contiguous outputs, coalesced
+      __syncwarp();
+      const int wb = warp * 32 * ITEMS;
+      const int we = min(cnt, wb + 32 * ITEMS);
+#pragma unroll 4
+      for (int j = wb + lane; j < we; j += 32) ocol[c0 + j] = s_u[j];
+    }
+    LPC_STAMP(6);
+    if (col + 1 < a.nrhs) {
+      fence_proxy_async_smem();   // my generic s_u accesses before the next bulk copies
+      __syncthreads();            // s_u, s_red, s_C, s_wf / s_wb of this column consumed
+      if (!USER && v_bulk && tid == 0) issue_v(col + 1);
+    }
+  }   // column loop
+  if (tid == 0) a.ep[c] = base + (unsigned)a.nrhs;
 }
+
+}  // namespace lpc
 
 // ---------------------------------------------------------------------------
-size_t d1_smem_bytes() { return sizeof(D1Smem); }
-
-template <int P>
-static cudaError_t d1_set_attr() {
-  return cudaFuncSetAttribute(k_d1_coop<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(D1Smem));
-}
-
-gp_status df_shape_info(int shape, int* capacity, int* max_grid);
-gp_status df_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s, int kind);
-int df_default_shape();
-
-int df_large_shape();
-int db_capacity_sub();
+// Host side.
 gp_status db_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
                     cudaStream_t s, int kind);
+int db_capacity_sub();
+
+namespace {
+
+// shapes (threads x points per thread); ITEMS odd: conflict-free 8-byte strided smem reads
+struct Shape {
+  int block, items;
+  const void* fn[2][10];   // [user order][KIND * 5 + P]
+  size_t smem[2];
+};
+
+template <int BLOCK, int SEGS, int SL, bool USER>
+void shape_fns(const void** f) {
+  f[0] = (const void*)lpc::k_d1_lpc<0, 0, BLOCK, SEGS, SL, USER>;
+  f[1] = (const void*)lpc::k_d1_lpc<1, 0, BLOCK, SEGS, SL, USER>;
+  f[2] = (const void*)lpc::k_d1_lpc<2, 0, BLOCK, SEGS, SL, USER>;
+  f[3] = (const void*)lpc::k_d1_lpc<3, 0, BLOCK, SEGS, SL, USER>;
+  f[4] = (const void*)lpc::k_d1_lpc<4, 0, BLOCK, SEGS, SL, USER>;
+  f[5] = (const void*)lpc::k_d1_lpc<1, 1, BLOCK, SEGS, SL, USER>;
+  f[6] = (const void*)lpc::k_d1_lpc<2, 1, BLOCK, SEGS, SL, USER>;
+  f[7] = (const void*)lpc::k_d1_lpc<3, 1, BLOCK, SEGS, SL, USER>;
+  f[8] = (const void*)lpc::k_d1_lpc<4, 1, BLOCK, SEGS, SL, USER>;
+  f[9] = (const void*)lpc::k_d1_lpc<5, 1, BLOCK, SEGS, SL, USER>;
+}
+template <int BLOCK, int SEGS, int SL>
+Shape make_shape() {
+  Shape s;
+  s.block = BLOCK;
+  s.items = SEGS * SL;
+  shape_fns<BLOCK, SEGS, SL, false>(s.fn[0]);
+  shape_fns<BLOCK, SEGS, SL, true>(s.fn[1]);
+  const size_t sub = (size_t)BLOCK * SEGS * SL;
+  s.smem[0] = sizeof(double) * (3 * sub + 16);   // t, e^{-gap}, u
+  s.smem[1] = s.smem[0] + sizeof(int) * (sub + 8);
+  return s;
+}
+
+constexpr int NSHAPE = 3;
+Shape g_shapes[NSHAPE];
+int g_ready = 0;
+int g_default = 0;
+
+gp_status shapes_init() {
+  if (g_ready) return GP_OK;
+  g_shapes[0] = make_shape<256, 3, 9>();
+  g_shapes[1] = make_shape<256, 3, 10>();   // #SMs x 7680 points: N = 2^20 in one chunk each
+  g_shapes[2] = make_shape<224, 3, 11>();
+  for (auto& s : g_shapes)
+    for (int u = 0; u < 2; ++u)
+      for (int p = 0; p < 10; ++p)
+        GPM_CUDA(cudaFuncSetAttribute(s.fn[u][p], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)s.smem[u]));
+  if (const char* e = getenv("GPM_D1_SHAPE")) g_default = std::max(0, std::min(NSHAPE - 1, atoi(e)));
+  g_ready = 1;
+  return GP_OK;
+}
+
+}  // namespace
 
 gp_status d1_prepare(Plan& pl) {
-  static int attr_done = 0;
-  if (!attr_done) {
-    GPM_CUDA(d1_set_attr<0>());
-    GPM_CUDA(d1_set_attr<1>());
-    GPM_CUDA(d1_set_attr<2>());
-    attr_done = 1;
-  }
+  GPM_TRY(shapes_init());
   int dev = 0, nsm = 0, coop = 0;
   GPM_CUDA(cudaGetDevice(&dev));
   GPM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   GPM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return fail(GP_ERR_UNSUPPORTED, "device does not support cooperative launch");
-  // fast path: one shared-memory chunk per CTA (apply_d1_fast.cu)
-  int fast_grid = 0, cap = 0;
-  if (pl.d1_force == 3) {   // testing knob: the reduce-then-scan path at any size
-    const int64_t nsub = (pl.n + db_capacity_sub() - 1) / db_capacity_sub();
-    pl.d1_grid = (int)nsub;
-    pl.d1_chunk = db_capacity_sub();
-    pl.d1_path = 3;
-    GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)nsub));
-    return GP_OK;
-  }
-  if (pl.d1_shape < 0) {
-    // default shape; above its capacity (#SMs x 6912) the 31-point-per-thread shape keeps
-    // the single-chunk kernel up to #SMs x 7936 (N = 2^20 and a little beyond)
-    pl.d1_shape = df_default_shape();
-    GPM_TRY(df_shape_info(pl.d1_shape, &cap, &fast_grid));
-    const int large = df_large_shape();
-    if (large >= 0 && pl.n > (int64_t)cap * fast_grid) pl.d1_shape = large;
-  }
-  GPM_TRY(df_shape_info(pl.d1_shape, &cap, &fast_grid));
-  if (pl.d1_force != 2 && fast_grid > 0) {
-    int64_t g = std::min<int64_t>(fast_grid, std::max<int64_t>(1, (pl.n + 1023) / 1024));
-    int64_t chunk = ((pl.n + g - 1) / g + 3) & ~int64_t(3);   // multiple of 4 (TMA alignment)
-    g = (pl.n + chunk - 1) / chunk;
-    if (chunk <= cap && g <= fast_grid) {
+  if (pl.d1_shape < 0 || pl.d1_shape >= NSHAPE) pl.d1_shape = g_default;
+  const Shape& sh = g_shapes[pl.d1_shape];
+  int occ = 0;
+  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh.fn[1][2], sh.block, sh.smem[1]));
+  const int64_t cap = (int64_t)sh.block * sh.items;
+  const int gmax = std::min(occ * nsm, 160);   // s_tl holds 161 chunk ends
+  if (pl.d1_force != 3 && gmax > 0) {
+    // grid: #SMs CTAs, fewer for small n (>= 1024 points per chunk); chunk a multiple of 4
+    int64_t g = std::min<int64_t>(gmax, std::max<int64_t>(1, (pl.n + 1023) / 1024));
+    int64_t chunk = ((pl.n + g - 1) / g + 3) & ~int64_t(3);
+    g = (pl.n + chunk - 1) / chunk;   // every CTA owns >= 1 point
+    if (chunk <= cap && g <= gmax) {
       pl.d1_grid = (int)g;
       pl.d1_chunk = chunk;
       pl.d1_path = 1;
-      GPM_TRY(pl.aggs.alloc(128 * 2 * 4 * (size_t)g));   // D1Pub [2 parities][4 replicas][g] (apply_d1_fast.cu)
+      GPM_TRY(pl.aggs.alloc(sizeof(unsigned long long) * lpc::LL_W * 2 * (size_t)g));
       GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
-      GPM_TRY(pl.bar.alloc(64));
-      GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));
+      GPM_TRY(pl.bar.alloc(sizeof(unsigned) * (size_t)g));
+      GPM_CUDA(cudaMemset(pl.bar.ptr, 0, pl.bar.bytes));
       if (getenv("GPM_D1_TIMING")) {
-        GPM_TRY(pl.dbg.alloc(sizeof(unsigned long long) * 8 * (size_t)g));
+        GPM_TRY(pl.dbg.alloc(sizeof(unsigned long long) * 16 * 32 * (size_t)g));
         GPM_CUDA(cudaMemset(pl.dbg.ptr, 0, pl.dbg.bytes));
       }
       return GP_OK;
     }
   }
-  if (pl.d1_force != 2) {
-    // path 3: reduce-then-scan over sub-tiles in three plain launches (apply_d1_fast.cu
-    // k_d1_big), any N, every nu and the lengthscale gradient
-    const int64_t nsub = (pl.n + db_capacity_sub() - 1) / db_capacity_sub();
-    if (nsub > (int64_t)1 << 30) return fail(GP_ERR_UNSUPPORTED, "d=1 problem too large");
-    pl.d1_grid = (int)nsub;
-    pl.d1_chunk = db_capacity_sub();
-    pl.d1_path = 3;
-    GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)nsub));   // sub-tile records + carries
-    return GP_OK;
-  }
-  int occ = 0;
-  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_d1_coop<2>, D1_BLOCK,
-                                                         sizeof(D1Smem)));
-  if (occ < 1) return fail(GP_ERR_CUDA, "d=1 kernel cannot be resident (shared memory)");
-  const int64_t maxg = (int64_t)nsm * occ;
-  int64_t g = std::min<int64_t>(maxg, std::max<int64_t>(1, (pl.n + 1023) / 1024));
-  int64_t chunk = (pl.n + g - 1) / g;
-  if (pl.d1_force == 2 && chunk <= D1_SUB) {
-    // testing knob: force the multi-sub-tile path with tiny grids
-    g = std::max<int64_t>(1, std::min<int64_t>(g, (pl.n + 3 * D1_SUB - 1) / (3 * D1_SUB)));
-    chunk = (pl.n + g - 1) / g;
-  }
-  g = (pl.n + chunk - 1) / chunk;
-  const int64_t nsub = (chunk + D1_SUB - 1) / D1_SUB;
-  if (nsub > D1_MAXSUB)
-    return fail(GP_ERR_UNSUPPORTED, "d=1 problem too large for one device (n=" +
-                                        std::to_string(pl.n) + ")");
-  pl.d1_grid = (int)g;
-  pl.d1_chunk = chunk;
-  pl.d1_path = 2;
-  GPM_TRY(pl.aggs.alloc(sizeof(D1Agg) * (size_t)g * (1 + D1_MAXSUB)));
-  GPM_TRY(pl.bar.alloc(64));
-  GPM_CUDA(cudaMemset(pl.bar.ptr, 0, 64));
+  // path 3: reduce-then-scan over sub-tiles in three plain launches (apply_d1_big.cu), any N
+  const int64_t nsub = (pl.n + db_capacity_sub() - 1) / db_capacity_sub();
+  if (nsub > (int64_t)1 << 30) return fail(GP_ERR_UNSUPPORTED, "d=1 problem too large");
+  pl.d1_grid = (int)nsub;
+  pl.d1_chunk = db_capacity_sub();
+  pl.d1_path = 3;
+  GPM_TRY(pl.aggs.alloc(128 * 2 * (size_t)nsub));   // sub-tile records + carries
   return GP_OK;
 }
 
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
                     cudaStream_t s, int kind) {
-  if (pl.d1_path == 1) return df_launch(pl, v, out, nrhs, user_order, s, kind);
   if (pl.d1_path == 3) return db_launch(pl, v, out, nrhs, user_order, s, kind);
-  if (kind != 0)
-    return fail(GP_ERR_UNSUPPORTED, "lengthscale-gradient MVM for d=1 needs n <= #SMs x 6912");
-  if (pl.P > 2)
-    return fail(GP_ERR_UNSUPPORTED, "nu >= 7/2 in d=1 needs n <= #SMs x 6912 (single-sub-tile path)");
-  const int64_t vs = user_order ? pl.n_src : pl.n, os = user_order ? pl.n - pl.tgt_off : pl.n;
-  for (int c = 0; c + 1 < nrhs; ++c)
-    GPM_TRY(d1_launch(pl, v + c * vs, out + c * os, 1, user_order, s, 0));
-  v += (nrhs - 1) * vs;
-  out += (nrhs - 1) * os;
-  D1Args a;
+  const Shape& sh = g_shapes[pl.d1_shape];
+  lpc::Args a;
   a.ts = pl.t.as<double>();
-  a.perm = user_order ? pl.perm.as<int>() : nullptr;
+  a.perm = pl.perm.as<int>();
   a.v = v;
   a.out = out;
   a.n = pl.n;
   a.n_src = user_order ? pl.n_src : pl.n;
   a.tgt_off = user_order ? pl.tgt_off : 0;
   a.chunk = pl.d1_chunk;
-  a.nsub = (int)((pl.d1_chunk + D1_SUB - 1) / D1_SUB);
+  a.nrhs = nrhs;
+  a.prefetch = pl.d1_prefetch;
+  a.vstride = user_order ? pl.n_src : pl.n;
+  a.ostride = user_order ? pl.n - pl.tgt_off : pl.n;
   a.os2 = pl.os2;
-  a.chunk_aggs = pl.aggs.as<D1Agg>();
-  a.sub_aggs = pl.aggs.as<D1Agg>() + pl.d1_grid;
-  a.bar = pl.bar.as<unsigned>();
+  a.rec = pl.aggs.as<unsigned long long>();
+  a.ep = pl.bar.as<unsigned>();
+  a.dbg = pl.dbg.bytes ? pl.dbg.as<unsigned long long>() : nullptr;
+  static const int knob = getenv("GPM_D1_KNOB") ? atoi(getenv("GPM_D1_KNOB")) : 0;
+  a.knob = knob;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.d1_grid);
+  cfg.blockDim = dim3(sh.block);
+  cfg.dynamicSmemBytes = sh.smem[user_order ? 1 : 0];
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pl.d1_pdl ? 2 : 1;
   void* args[] = {&a};
-  const void* fn = pl.P == 0 ? (const void*)k_d1_coop<0>
-                   : pl.P == 1 ? (const void*)k_d1_coop<1> : (const void*)k_d1_coop<2>;
-  GPM_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pl.d1_grid), dim3(D1_BLOCK), args,
-                                       sizeof(D1Smem), s));
+  GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[user_order ? 1 : 0][kind * 5 + pl.P], args));
   return GP_OK;
 }
 

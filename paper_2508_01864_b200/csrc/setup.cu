@@ -172,6 +172,8 @@ gp_status plan_build(Plan& pl, const double* x, int64_t n, int d, const gp_kerne
   GPM_TRY(pl.x_raw.alloc(sizeof(double) * n * d));
   GPM_CUDA(cudaMemcpyAsync(pl.x_raw.ptr, x, sizeof(double) * n * d, cudaMemcpyDeviceToDevice, s));
   GPM_TRY(pl.perm.alloc(sizeof(int) * (n + 16)));   // padded: TMA bulk copies round up
+  // padding = 0x7f7f7f7f (> any user index): rounded-up bulk copies read no source index
+  GPM_CUDA(cudaMemsetAsync(pl.perm.as<int>() + n, 0x7f, sizeof(int) * 16, s));
   GPM_TRY(pl.t.alloc(sizeof(double) * (n * d + 16)));
 
   // scratch for sorting

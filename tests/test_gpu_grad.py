@@ -119,12 +119,6 @@ def test_grad_unsupported_and_errors(gpm):
     with pytest.raises(gpm.GPError) as e:
         plan.kmvm_dlengthscale(to_dev(np.ones(500)))
     assert e.value.name == "UNSUPPORTED"
-    x1 = _pts(60000, 1, 2)
-    p1 = gpm.Plan(to_dev(x1), gpm.Kernel(3, (0.02,)))
-    p1.set_option(0, 2)            # force the multi-sub-tile path: no gradient there
-    with pytest.raises(gpm.GPError) as e:
-        p1.kmvm_dlengthscale(to_dev(np.ones(60000)))
-    assert e.value.name == "UNSUPPORTED"
 
 
 def test_grad_matches_finite_difference_of_kmvm(gpm):

@@ -101,12 +101,6 @@ def test_high_nu_unsupported(gpm):
     with pytest.raises(gpm.GPError) as e:
         gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1, 0.1), form=1))
     assert e.value.name == "UNSUPPORTED"
-    x1 = _pts(60000, 1, 2)
-    p1 = gpm.Plan(to_dev(x1), gpm.Kernel(7, (0.02,)))
-    p1.set_option(0, 2)            # multi-sub-tile path: nu <= 5/2 only
-    with pytest.raises(gpm.GPError) as e:
-        p1.kmvm(to_dev(np.ones(60000)))
-    assert e.value.name == "UNSUPPORTED"
 
 
 @pytest.mark.parametrize("two_nu", [5, 7, 9])

@@ -45,21 +45,27 @@ def test_d1_all_rows(gpm, two_nu, n, kind):
 
 
 @pytest.mark.parametrize("two_nu", [1, 5])
-def test_d1_multi_subtile_path(gpm, two_nu):
-    """Force chunks larger than one shared-memory sub-tile (streamed pass 2)."""
+def test_d1_single_chunk_shapes(gpm, two_nu):
+    """Every thread-block shape of the single-chunk kernel (512x15, 384x19, 256x27: the
+    chunk splits at different thread / warp / part boundaries) against the oracle, equal
+    to each other to rounding; option 0 = 2 (the removed multi-sub-tile path) is rejected."""
     n = 60000
     x = _points("normal", n, 1, 5)
     v = np.random.default_rng(6).standard_normal(n)
     plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, (0.02,)))
-    plan.set_option(0, 2)
-    assert plan.d1_path == 2
-    out = plan.kmvm(to_dev(v)).cpu().numpy()
     rows = W.sample_rows(x, 1500)
-    check_rows(out, x, v, two_nu, "l1", (0.02,), 1.0, rows=rows, what="d1 multi-subtile")
-    plan.set_option(0, 0)
-    assert plan.d1_path == 1
-    out2 = plan.kmvm(to_dev(v)).cpu().numpy()
-    check_rows(out2, x, v, two_nu, "l1", (0.02,), 1.0, rows=rows, what="d1 coop")
+    outs = []
+    for shape in (0, 1, 2):
+        plan.set_option(1, shape)
+        assert plan.d1_path == 1 and plan.query(7) == shape
+        out = plan.kmvm(to_dev(v)).cpu().numpy()
+        check_rows(out, x, v, two_nu, "l1", (0.02,), 1.0, rows=rows, what=f"d1 shape {shape}")
+        outs.append(out)
+    for o in outs[1:]:
+        assert np.max(np.abs(o - outs[0])) <= 1e-13 * np.abs(outs[0]).max()
+    with pytest.raises(gpm.GPError) as e:
+        plan.set_option(0, 2)
+    assert e.value.name == "INVALID_ARG"
 
 
 @pytest.mark.parametrize("n", [1, 7, 6912, 6913, 60001, 200_003])

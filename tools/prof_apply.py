@@ -19,10 +19,13 @@ ap.add_argument("--applies", type=int, default=5)
 ap.add_argument("--form", type=int, default=0)
 ap.add_argument("--rank", action="store_true")
 ap.add_argument("--nrhs", type=int, default=1)
+ap.add_argument("--shape", type=int, default=-1)
 args = ap.parse_args()
 c = W.CONFIGS[args.config]
 x = torch.from_numpy(W.config_points(c)).cuda()
 plan = g.Plan(x, g.Kernel(args.nu2, c.ell, form=args.form))
+if args.shape >= 0:
+    plan.set_option(1, args.shape)
 def _vec(r):
     a = np.stack([W.config_vector(c, r * args.nrhs + j) for j in range(args.nrhs)])
     return torch.from_numpy(a[0] if args.nrhs == 1 else a).cuda()
