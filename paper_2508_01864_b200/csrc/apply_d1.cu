@@ -49,6 +49,7 @@ constexpr int LL_W = 32;    // 8-byte words per record slot (<= 2 x 2 x 6 moment
 
 struct Args {
   const double* ts;    // sorted scaled coordinates (plan)
+  const double* e1;    // e^{-gap} per rank (plan, padded with 1)
   const int* perm;     // rank -> user index (plan, padded)
   const double* v;     // input columns: user order or rank order
   double* out;         // output columns: user order (targets only) or rank order
@@ -221,6 +222,10 @@ struct Run {
   double D, E, MF[NQ], MB[NQ];
 };
 
+// u buffers: two in rank order (the next column's v lands while this one computes) when
+// t, e^{-gap} and 2 u fit the 227 KB carve-out, else one
+constexpr int lpc_nub(bool user, int sub) { return (!user && (4 * sub + 16) * 8 <= 221 * 1024) ? 2 : 1; }
+
 // P: moment order (KIND 0: nu = P + 1/2; KIND 1: the lengthscale gradient of nu = P - 1/2)
 template <int P, int KIND, int BLOCK, int SEGS, int SL, bool USER>
 __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
@@ -231,20 +236,19 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   constexpr int PT = BLOCK / NPART;   // threads per load part
   constexpr int PSZ = PT * ITEMS;     // points per load part
   constexpr int NV = 2 * NQ;          // record values: forward + backward moments
-  constexpr double SELF = KIND == 0 ? 1.0 : 0.0;   // k(0) = 1; g(0) = 0
+  constexpr int NUB = lpc_nub(USER, SUB);   // rank order: u double-buffered across columns
   static_assert(PSZ % 4 == 0, "load parts must stay 16-byte aligned");
   static_assert(2 * NV <= LL_W, "record slot too small");
-  static_assert(NW <= 32, "one warp scans the warp totals");
+  static_assert(NW <= 32 && BLOCK >= 64 + 160, "warp roles: 2 totals warps, fold threads for G <= 160");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* s_t = reinterpret_cast<double*>(smem_raw);   // SUB + 8: t (clamped past the end)
-  double* s_e = s_t + SUB + 8;                         // SUB: e^{-gap}
-  double* s_u = s_e + SUB;                             // SUB: u, then out (rank order)
-  int* s_pi = reinterpret_cast<int*>(s_u + SUB);       // SUB + 8 (user order)
-  __shared__ uint64_t mbar[NPART], mbar_v[NPART], mbar_tab;
+  double* s_e = s_t + SUB + 8;                         // SUB + 8: e^{-gap} (plan; 1 past the end)
+  double* s_ub = s_e + SUB + 8;                        // NUB x SUB: u, then out (rank order)
+  int* s_pi = reinterpret_cast<int*>(s_ub + NUB * SUB);   // SUB + 8 (user order)
+  __shared__ uint64_t mbar[NPART], mbar_v[NUB][NPART], mbar_tab;
   __shared__ __align__(16) double s_tab[64];
   __shared__ double s_wf[NW][NQ + 2], s_wb[NW][NQ + 2];   // warp totals of the block scan
-  __shared__ double s_red[NW][NV];                        // warp sums (chunk sum / fold)
-  __shared__ double s_C[NV];                              // folded chunk carries
+  __shared__ double s_red[NW][NV];                        // warp partials of the chunk sum
   __shared__ double s_tl[160 + 1];                        // chunk-end t: s_tl[b + 1], s_tl[0] = t_0
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -256,15 +260,19 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   const bool part_live = mypart * PSZ < cnt;
   const bool v_bulk = !USER && ((reinterpret_cast<uintptr_t>(a.v + c0) & 15) == 0) &&
                       (a.vstride % 2 == 0 || a.nrhs == 1);
-  // rank order: a column of v by bulk copies (thread 0 owns the barriers)
+  const bool o_bulk = !USER && ((reinterpret_cast<uintptr_t>(a.out + c0) & 15) == 0) &&
+                      (a.ostride % 2 == 0 || a.nrhs == 1);
+  // rank order: a column of v by bulk copies into u buffer col % NUB (thread 0 owns the
+  // barriers)
   auto issue_v = [&](int col) {
+    double* dst = s_ub + (col % NUB) * SUB;
 #pragma unroll 1
     for (int p = 0; p < NPART; ++p) {
       const int lo = p * PSZ, hi = min(cnt, lo + PSZ);
       if (lo < hi) {
         const unsigned nu = (unsigned)((hi - lo) & ~1);   // never over-read v
-        mbar_expect_tx(&mbar_v[p], nu * 8);
-        if (nu) tma_load_1d(s_u + lo, a.v + col * a.vstride + c0 + lo, nu * 8, &mbar_v[p]);
+        mbar_expect_tx(&mbar_v[col % NUB][p], nu * 8);
+        if (nu) tma_load_1d(dst + lo, a.v + col * a.vstride + c0 + lo, nu * 8, &mbar_v[col % NUB][p]);
       }
     }
   };
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   if (tid == 0) {
     for (int p = 0; p < NPART; ++p) {
       mbar_init(&mbar[p], 1);
-      mbar_init(&mbar_v[p], 1);
+      for (int ub = 0; ub < NUB; ++ub) mbar_init(&mbar_v[ub][p], 1);
     }
     mbar_init(&mbar_tab, 1);
     mbar_fence_init();
@@ -294,8 +302,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       if (lo < hi) {
         const unsigned nt = (unsigned)(((hi - lo) + 1) & ~1);   // padded plan arrays
         const unsigned np = (unsigned)(((hi - lo) + 3) & ~3);
-        mbar_expect_tx(&mbar[p], nt * 8 + (USER ? np * 4 : 0));
+        mbar_expect_tx(&mbar[p], 2 * nt * 8 + (USER ? np * 4 : 0));
         tma_load_1d(s_t + lo, a.ts + c0 + lo, nt * 8, &mbar[p]);
+        tma_load_1d(s_e + lo, a.e1 + c0 + lo, nt * 8, &mbar[p]);
         if (USER) tma_load_1d(s_pi + lo, a.perm + c0 + lo, np * 4, &mbar[p]);
       }
     }
@@ -319,65 +328,64 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   asm volatile("griddepcontrol.launch_dependents;");
   LPC_STAMP(8);
   const unsigned base = *(volatile const unsigned*)(a.ep + c);   // columns published so far
-  if (tid == 0 && v_bulk) issue_v(0);
+  if (tid == 0 && v_bulk) {
+    issue_v(0);
+    if (NUB > 1 && a.nrhs > 1) issue_v(1);
+  }
   if (USER && a.prefetch && tid == 32) prefetch_v(0);
   mbar_wait(&mbar_tab, 0);
   LPC_STAMP(7);
   if (part_live) mbar_wait(&mbar[mypart], 0);
   LPC_STAMP(9);
-  // ---- my points' e^{-gap} (while v is in flight), neutral tails: t clamped to the last
-  // point (gap 0), u = 0, no source index
-  {
-    double tp = tprev;
+  // ---- neutral tails (once per launch): t clamped to the last point (gap 0), weight 1,
+  // u = 0 (rank order: the bulk copies stop at cnt), no source index (user order)
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const int j = j0 + k;
-      double tk = tlast;
-      if (j < cnt) tk = s_t[j];
-      else s_t[j] = tlast;
-      s_e[j] = fexp_neg(tk - tp, s_tab);
-      tp = tk;
-      if (j >= cnt) s_u[j] = 0.0;
-      if (USER && j >= ((cnt + 3) & ~3)) s_pi[j] = INT_MAX;
-    }
-  }
-  double uu[USER ? ITEMS : 1];
-  if (USER) {   // the first column's gathers
+  for (int k = 0; k < ITEMS; ++k) {
+    const int j = j0 + k;
+    if (j >= cnt) {
+      s_t[j] = tlast;
+      s_e[j] = 1.0;
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const int pi = s_pi[j0 + k];
-      uu[k] = pi < a.n_src ? __ldg(a.v + pi) : 0.0;
+      for (int ub = 0; ub < NUB; ++ub) s_ub[ub * SUB + j] = 0.0;
     }
+    if (USER && j >= ((cnt + 3) & ~3)) s_pi[j] = INT_MAX;
   }
-  // segment spans (the point before a segment -> its last point) for the scan elements
+  // segment spans (the point before a segment -> its last point) for the scan elements,
+  // and the spans from my t_prev to the point before each segment / from each segment's
+  // last point to my last point (the carries)
   double DS[SEGS], ES[SEGS];
 #pragma unroll
   for (int sg = 0; sg < SEGS; ++sg) {
     DS[sg] = tseg[sg] - (sg ? tseg[sg - 1] : tprev);
     ES[sg] = fexp_neg(DS[sg], s_tab);
   }
+  // v-independent shifts, once per launch: my element's span, the chunk-sum shifts (my
+  // last point -> chunk last point, chunk reference -> my t_prev)
+  const double Dme = tmye - tprev, Eme = fexp_neg(Dme, s_tab);
+  const double dF = tlast - tmye, eF = fexp_neg(dF, s_tab);
+  const double dB = tprev - tref0, eB = fexp_neg(dB, s_tab);
   LPC_STAMP(1);
 
 #pragma unroll 1
   for (int col = 0; col < a.nrhs; ++col) {
     const double* vcol = a.v + col * a.vstride;
     double* ocol = a.out + col * a.ostride;
+    double* s_u = s_ub + (col % NUB) * SUB;
     const unsigned tag = base + (unsigned)col + 1u;
     unsigned long long* recp = a.rec + (size_t)(col & 1) * G * LL_W;
     // ---- u of my points into s_u (own items only: no block barrier needed)
     if (USER) {
-      if (col > 0) {
+      double uu[ITEMS];
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-          const int pi = s_pi[j0 + k];
-          uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
-        }
+      for (int k = 0; k < ITEMS; ++k) {
+        const int pi = s_pi[j0 + k];
+        uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
       }
       if (a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = uu[k];
     } else if (v_bulk) {
-      if (part_live) mbar_wait(&mbar_v[mypart], (unsigned)(col & 1));
+      if (part_live) mbar_wait(&mbar_v[col % NUB][mypart], (unsigned)((col / NUB) & 1));
       const int lo = mypart * PSZ, hi = min(cnt, lo + PSZ);
       if (lo < hi && ((hi - lo) & 1) && tid == (hi - 1) / ITEMS)   // odd tail element
         s_u[hi - 1] = __ldg(vcol + c0 + hi - 1);
@@ -388,20 +396,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
     LPC_STAMP(2);
     // ---- local pass from zero state, segment by segment: the forward and backward
     // recurrences over the segment's points interleaved (two chains), the segment's t, u
-    // and e^{-gap} loaded once into registers; loc_j = self u_j + read_F + read_B
+    // and e^{-gap} loaded once into registers; loc_j = u_j (self term) + read_F + read_B,
+    // all scaled by os2 through the injected weights (u' = os2 u)
     double loc[ITEMS];
     double FS[SEGS][NQ], BS[SEGS][NQ];   // segment aggregates (F at its last point, B at
                                          // the point before its first point)
 #pragma unroll
     for (int sg = 0; sg < SEGS; ++sg) {
       const int i0 = sg * SL;
-      double tt[SL + 1], ee[SL], uu2[SL];
+      double tt[SL + 1], ee[SL], uw[SL];
       tt[0] = sg ? tseg[sg - 1] : tprev;
 #pragma unroll
       for (int k = 0; k < SL; ++k) {
         tt[k + 1] = s_t[j0 + i0 + k];
         ee[k] = s_e[j0 + i0 + k];
-        uu2[k] = s_u[j0 + i0 + k];
+        uw[k] = a.os2 * s_u[j0 + i0 + k];
       }
       double F[NQ], B[NQ];
 #pragma unroll
@@ -410,11 +419,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       for (int k = 0; k < SL; ++k) {
         const int kf = k, kb = SL - 1 - k;   // forward point kf, backward point kb
         if (k > 0) advance<P>(F, tt[kf + 1] - tt[kf], ee[kf]);
-        const double rf = fma(SELF, uu2[kf], k > 0 ? readc0<P, KIND>(F) : 0.0);
-        F[0] += uu2[kf];
+        const double rf = KIND == 0 ? (k > 0 ? uw[kf] + readc0<P, KIND>(F) : uw[kf])
+                                    : (k > 0 ? readc0<P, KIND>(F) : 0.0);
+        F[0] += uw[kf];
         if (k > 0) advance<P>(B, tt[kb + 2] - tt[kb + 1], ee[kb + 1]);
         const double rb = k > 0 ? readc0<P, KIND>(B) : 0.0;
-        B[0] += uu2[kb];
+        B[0] += uw[kb];
         // first touch assigns (the middle point is touched by both chains in one step)
         if (kf <= kb) loc[i0 + kf] = rf; else loc[i0 + kf] += rf;
         if (kb > kf) loc[i0 + kb] = rb; else loc[i0 + kb] += rb;
@@ -426,28 +436,40 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         BS[sg][q] = B[q];
       }
     }
-    // my scan element = the segments in order
+    // within-thread carry prefixes (v-dependent but known before the exchange):
+    //   HF_s = forward state at the point before segment s from my earlier segments,
+    //   HB_s = backward state at the last point of segment s from my later segments;
+    // my scan element is (span t_prev -> my last point, HF_SEGS, HB_{-1})
+    double HF[SEGS][NQ], HB[SEGS][NQ];
     Run<NQ> me;
-    me.D = DS[0];
-    me.E = ES[0];
+    {
+      double h[NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      me.MF[q] = FS[0][q];
-      me.MB[q] = BS[SEGS - 1][q];
-    }
+      for (int q = 0; q < NQ; ++q) h[q] = 0.0;
 #pragma unroll
-    for (int sg = 1; sg < SEGS; ++sg) {
-      advance<P>(me.MF, DS[sg], ES[sg]);
+      for (int sg = 0; sg < SEGS; ++sg) {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) me.MF[q] += FS[sg][q];
-      me.D += DS[sg];
-      me.E *= ES[sg];
-    }
+        for (int q = 0; q < NQ; ++q) HF[sg][q] = h[q];
+        if (sg) advance<P>(h, DS[sg], ES[sg]);
 #pragma unroll
-    for (int sg = SEGS - 2; sg >= 0; --sg) {
-      advance<P>(me.MB, DS[sg], ES[sg]);
+        for (int q = 0; q < NQ; ++q) h[q] += FS[sg][q];
+      }
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) me.MB[q] += BS[sg][q];
+      for (int q = 0; q < NQ; ++q) me.MF[q] = h[q];   // at my last point
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) h[q] = 0.0;
+#pragma unroll
+      for (int sg = SEGS - 1; sg >= 0; --sg) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) HB[sg][q] = h[q];
+        advance<P>(h, DS[sg], ES[sg]);   // -> the point before segment sg
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) h[q] += BS[sg][q];
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) me.MB[q] = h[q];   // at my t_prev
+      me.D = Dme;
+      me.E = Eme;
     }
     LPC_STAMP(3);
     // ---- chunk aggregate = fixed-order sum of the shifted thread aggregates -> record
@@ -458,17 +480,15 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         m[q] = me.MF[q];
         m[NQ + q] = me.MB[q];
       }
-      const double dF = tlast - tmye;    // my last point -> chunk last point
-      const double dB = tprev - tref0;   // chunk reference -> my t_prev
-      advance<P>(m, dF, fexp_neg(dF, s_tab));
-      advance<P>(m + NQ, dB, fexp_neg(dB, s_tab));
+      advance<P>(m, dF, eF);
+      advance<P>(m + NQ, dB, eB);
       if (col == 0 && tid <= G) s_tl[tid] = my_tl;   // read after the barrier below
       int id;
       const double sw = warp_sum_scatter<NV>(m, lane, &id);
       if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp][id] = sw;
     }
-    __syncthreads();
-    if (tid < NV) {   // one value per thread, warps summed in order, published as 2 words
+    __syncthreads();   // #1: chunk-sum partials
+    if (tid < NV) {    // one value per thread, warps summed in order, published as 2 words
       double s = 0.0;
 #pragma unroll 1
       for (int w = 0; w < NW; ++w) s += s_red[w][tid];
@@ -476,18 +496,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
              ll_word(tag, (unsigned)__double2hiint(s)));
     }
     LPC_STAMP(4);
-    // ---- the record this thread folds: loads issued now, checked after the block scan
-    const int b = tid;
-    const bool fold_me = b < G && b != c;
-    const int o = b < c ? 0 : NQ;   // forward moments of earlier chunks, backward of later
-    const unsigned long long* wrec = recp + (size_t)b * LL_W + 2 * o;
-    unsigned long long x[2 * NQ];
-    if (fold_me) {
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) ld_ll2(wrec + 2 * i, x[2 * i], x[2 * i + 1]);
-    }
     // ---- block scan of the thread elements (overlaps the other chunks' publication):
-    // forward inclusive prefix / backward inclusive suffix per warp, then the warp totals
+    // forward inclusive prefix / backward inclusive suffix per warp -> the warp totals
     Mon<NQ> fe, be;
     {
       Mon<NQ> fi, bi;
@@ -513,45 +523,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       if (lane == 31) be = mon_id<NQ>();
     }
     LPC_STAMP(10);
-    // ---- fold my record: re-poll until every word carries this column's tag
-    {
-      double fm[NV];
-#pragma unroll
-      for (int q = 0; q < NV; ++q) fm[q] = 0.0;
-      if (fold_me) {
-        bool ok = true;
-#pragma unroll
-        for (int i = 0; i < 2 * NQ; ++i) ok &= (unsigned)(x[i] >> 32) == tag;
-        while (!ok) {
-          ok = true;
-#pragma unroll
-          for (int i = 0; i < NQ; ++i) {
-            ld_ll2(wrec + 2 * i, x[2 * i], x[2 * i + 1]);
-            ok &= (unsigned)(x[2 * i] >> 32) == tag && (unsigned)(x[2 * i + 1] >> 32) == tag;
-          }
-        }
-        double mv[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          mv[q] = __hiloint2double((int)(unsigned)x[2 * q + 1], (int)(unsigned)x[2 * q]);
-        // forward: chunk b's last point -> my chunk's reference (the point before it);
-        // backward: chunk b's reference -> my chunk's last point
-        const double D = b < c ? s_tl[c] - s_tl[b + 1] : s_tl[b] - s_tl[c + 1];
-        advance<P>(mv, D, fexp_neg(D, s_tab));
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          fm[q] = b < c ? mv[q] : 0.0;
-          fm[NQ + q] = b < c ? 0.0 : mv[q];
-        }
-      }
-      LPC_STAMP(11);
-      if (warp < (G + 31) / 32) {
-        int id;
-        const double sw = warp_sum_scatter<NV>(fm, lane, &id);
-        if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp][id] = sw;
-      }
-    }
-    __syncthreads();   // s_wf / s_wb warp totals, s_red fold partials
+    __syncthreads();   // #2: warp totals
     LPC_STAMP(5);
     if (warp < 2) {    // warp 0: exclusive forward prefix of the warp totals; warp 1: suffix
       const bool fw = warp == 0;
@@ -566,28 +538,66 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       if ((fw && lane == 0) || (!fw && lane >= NW - 1)) xe = mon_id<NQ>();
       __syncwarp();
       if (lane < NW) mon_st<NQ>(fw ? s_wf[lane] : s_wb[lane], xe);
-    } else if (tid - 64 < NV) {   // chunk carries: fold partials summed in order
-      double s = 0.0;
-#pragma unroll 1
-      for (int w = 0; w < (G + 31) / 32; ++w) s += s_red[w][tid - 64];
-      s_C[tid - 64] = s;
+    } else if (tid >= 64 && tid < 64 + 32 * ((G + 31) / 32)) {
+      // ---- fold the other chunks' records, one per thread (threads 64 .. 64 + G - 1): poll
+      // until every word carries this column's tag; forward moments of earlier chunks
+      // shifted from their last point to my chunk's reference, backward moments of later
+      // chunks from their reference to my chunk's last point; warp sums in fixed order
+      double fm[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) fm[q] = 0.0;
+      const int b = tid - 64;
+      if (b < G && b != c) {
+        const int o = b < c ? 0 : NQ;
+        const unsigned long long* w = recp + (size_t)b * LL_W + 2 * o;
+        unsigned long long x[2 * NQ];
+        bool ok;
+        do {
+          ok = true;
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) {
+            ld_ll2(w + 2 * i, x[2 * i], x[2 * i + 1]);
+            ok &= (unsigned)(x[2 * i] >> 32) == tag && (unsigned)(x[2 * i + 1] >> 32) == tag;
+          }
+        } while (!ok);
+        double mv[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          mv[q] = __hiloint2double((int)(unsigned)x[2 * q + 1], (int)(unsigned)x[2 * q]);
+        const double D = b < c ? s_tl[c] - s_tl[b + 1] : s_tl[b] - s_tl[c + 1];
+        advance<P>(mv, D, fexp_neg(D, s_tab));
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          fm[q] = b < c ? mv[q] : 0.0;
+          fm[NQ + q] = b < c ? 0.0 : mv[q];
+        }
+      }
+      LPC_STAMP(11);
+      int id;
+      const double sw = warp_sum_scatter<NV>(fm, lane, &id);
+      if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp - 2][id] = sw;
     }
-    __syncthreads();
+    __syncthreads();   // #3: exclusive warp totals, fold partials
     LPC_STAMP(13);
-    // ---- the carries entering my segments, and the correction pass: the forward state
-    // at the point before segment s is G_s (G_0 from the earlier threads and chunks,
-    // G_{s+1} = S(DS_s) G_s + FS_s), the backward state at its last point is Y_s (Y_last from
-    // the later threads and chunks, Y_{s-1} = BS_s + S(DS_s) Y_s).  A carry C seen from a
-    // point D further on reads e^{-D} sum_r beta_r D^r (beta from C, carry_beta).
+    // ---- the carries entering my segments: G_0 = forward state at my t_prev (earlier
+    // threads and chunks), G_s = S(t_prev -> point before s) G_0 + HF_s, X_s = S(first gap
+    // of s) G_s; Y = backward state at my last point, Y_s = S(last of s -> my last) Y + HB_s.
+    // A carry C seen from a point D further on reads e^{-D} sum_r beta_r D^r (carry_beta).
+    double bX[SEGS][NQ], bY[SEGS][NQ];
     {
       const Mon<NQ> wf = mon_ld<NQ>(s_wf[warp]), wb = mon_ld<NQ>(s_wb[warp]);
       const Mon<NQ> Fx = mon_f<NQ>(wf, fe);   // threads before me, referenced at my t_prev
       const Mon<NQ> Bx = mon_b<NQ>(be, wb);   // threads after me, referenced at my last point
-      double g[NQ], y[NQ];
+      double g[NQ], y[NQ];   // the chunk carries: fold partials summed in order
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        g[q] = s_C[q];
-        y[q] = s_C[NQ + q];
+      for (int q = 0; q < NQ; ++q) g[q] = y[q] = 0.0;
+#pragma unroll 1
+      for (int w = 0; w < (G + 31) / 32; ++w) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          g[q] += s_red[w][q];
+          y[q] += s_red[w][NQ + q];
+        }
       }
       advance<P>(g, Fx.D, Fx.E);   // chunk reference -> my t_prev
       advance<P>(y, Bx.D, Bx.E);   // chunk last point -> my last point
@@ -596,90 +606,120 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         g[q] += Fx.M[q];
         y[q] += Bx.M[q];
       }
-      double gs[SEGS][NQ], ys[SEGS][NQ];   // G_s (point before s), Y_s (last point of s)
+      double d1 = 0.0, e1 = 1.0;   // my t_prev -> the point before segment sg
 #pragma unroll
       for (int sg = 0; sg < SEGS; ++sg) {
+        double gs[NQ], ys[NQ];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) gs[sg][q] = g[q];
-        if (sg + 1 < SEGS) {
-          advance<P>(g, DS[sg], ES[sg]);
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) g[q] += FS[sg][q];
+        for (int q = 0; q < NQ; ++q) {
+          gs[q] = g[q];
+          ys[q] = y[q];
         }
-      }
+        const double tb = sg ? tseg[sg - 1] : tprev;   // the point before segment sg
+        double d2 = 0.0, e2 = 1.0;   // the last point of segment sg -> my last point
 #pragma unroll
-      for (int sg = SEGS - 1; sg >= 0; --sg) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) ys[sg][q] = y[q];
-        if (sg > 0) {
-          advance<P>(y, DS[sg], ES[sg]);
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) y[q] += BS[sg][q];
+        for (int s2 = sg + 1; s2 < SEGS; ++s2) {
+          d2 += DS[s2];
+          e2 *= ES[s2];
         }
-      }
-      LPC_STAMP(14);
+        advance<P>(gs, d1, e1);
+        advance<P>(ys, d2, e2);
+        d1 += DS[sg];
+        e1 *= ES[sg];
 #pragma unroll
-      for (int sg = 0; sg < SEGS; ++sg) {
-        const int i0 = sg * SL;
-        double tt[SL + 1], ee[SL];
-        tt[0] = sg ? tseg[sg - 1] : tprev;
-#pragma unroll
-        for (int k = 0; k < SL; ++k) {
-          tt[k + 1] = s_t[j0 + i0 + k];
-          ee[k] = s_e[j0 + i0 + k];
+        for (int q = 0; q < NQ; ++q) {
+          gs[q] += HF[sg][q];
+          ys[q] += HB[sg][q];
         }
-        double bX[NQ], bY[NQ];
-        advance<P>(gs[sg], tt[1] - tt[0], ee[0]);   // -> the segment's first point
-        carry_beta<P, KIND>(gs[sg], bX);
-        carry_beta<P, KIND>(ys[sg], bY);
-        double Df = 0.0, Ef = 1.0, Db = 0.0, Eb = 1.0;
-#pragma unroll
-        for (int k = 0; k < SL; ++k) {
-          const int kf = k, kb = SL - 1 - k;
-          if (k > 0) {
-            Df += tt[kf + 1] - tt[kf];
-            Ef *= ee[kf];
-            Db += tt[kb + 2] - tt[kb + 1];
-            Eb *= ee[kb + 1];
-          }
-          double hf = bX[P], hb = bY[P];
-#pragma unroll
-          for (int r = P - 1; r >= 0; --r) {
-            hf = fma(hf, Df, bX[r]);
-            hb = fma(hb, Db, bY[r]);
-          }
-          loc[i0 + kf] = fma(Ef, hf, loc[i0 + kf]);
-          loc[i0 + kb] = fma(Eb, hb, loc[i0 + kb]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const double val = a.os2 * loc[k];
-        const int j = j0 + k;
-        if (USER) {
-          const int pi = s_pi[j];
-          if (j < cnt && pi >= a.tgt_off) ocol[pi - a.tgt_off] = val;
-        } else if (j < cnt) {   // the tail stays 0 for the next column
-          s_u[j] = val;
-        }
+        const double t1 = s_t[j0 + sg * SL];           // -> the segment's first point
+        advance<P>(gs, t1 - tb, s_e[j0 + sg * SL]);
+        carry_beta<P, KIND>(gs, bX[sg]);
+        carry_beta<P, KIND>(ys, bY[sg]);
       }
     }
+    LPC_STAMP(14);
+    // ---- correction pass (forward and backward chains per segment), then the output
+#pragma unroll
+    for (int sg = 0; sg < SEGS; ++sg) {
+      const int i0 = sg * SL;
+      double tt[SL], ee[SL];
+#pragma unroll
+      for (int k = 0; k < SL; ++k) {
+        tt[k] = s_t[j0 + i0 + k];
+        ee[k] = s_e[j0 + i0 + k];
+      }
+      double Ef = 1.0, Eb = 1.0;
+#pragma unroll
+      for (int k = 0; k < SL; ++k) {
+        const int kf = k, kb = SL - 1 - k;
+        if (k > 0) {
+          Ef *= ee[kf];
+          Eb *= ee[kb + 1];
+        }
+        const double Df = tt[kf] - tt[0], Db = tt[SL - 1] - tt[kb];
+        double hf = bX[sg][P], hb = bY[sg][P];
+#pragma unroll
+        for (int r = P - 1; r >= 0; --r) {
+          hf = fma(hf, Df, bX[sg][r]);
+          hb = fma(hb, Db, bY[sg][r]);
+        }
+        loc[i0 + kf] = fma(Ef, hf, loc[i0 + kf]);
+        loc[i0 + kb] = fma(Eb, hb, loc[i0 + kb]);
+      }
+    }
+    if (USER) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int j = j0 + k;
+        const int pi = s_pi[j];
+        if (j < cnt && pi >= a.tgt_off) ocol[pi - a.tgt_off] = loc[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k)
+        if (j0 + k < cnt) s_u[j0 + k] = loc[k];   // the tail stays 0 for a later column
+    }
     LPC_STAMP(12);
-    if (!USER) {   // this warp's contiguous outputs, coalesced
-      __syncwarp();
+    if (!USER) {   // this warp's contiguous outputs: one bulk store (+ an odd tail element)
       const int wb = warp * 32 * ITEMS;
       const int we = min(cnt, wb + 32 * ITEMS);
+      if (o_bulk) {
+        fence_proxy_async_smem();   // my generic writes of s_u before the bulk store
+        __syncwarp();
+        if (lane == 0 && we > wb) {
+          const int nb = (we - wb) & ~1;
+          if (nb) {
+            bulk_store_1d(ocol + c0 + wb, s_u + wb, (unsigned)nb * 8);
+            bulk_commit();
+          }
+          if ((we - wb) & 1) ocol[c0 + we - 1] = s_u[we - 1];
+        }
+      } else {
+        __syncwarp();
 #pragma unroll 4
-      for (int j = wb + lane; j < we; j += 32) ocol[c0 + j] = s_u[j];
+        for (int j = wb + lane; j < we; j += 32) ocol[c0 + j] = s_u[j];
+      }
     }
     LPC_STAMP(6);
     if (col + 1 < a.nrhs) {
-      fence_proxy_async_smem();   // my generic s_u accesses before the next bulk copies
-      __syncthreads();            // s_u, s_red, s_C, s_wf / s_wb of this column consumed
-      if (!USER && v_bulk && tid == 0) issue_v(col + 1);
+      // the u buffer of this column is the v destination of column col + NUB: the bulk
+      // store must have read it and every thread's generic accesses precede the copy
+      if (!USER && o_bulk && lane == 0) bulk_wait_read0();
+      fence_proxy_async_smem();
+      __syncthreads();   // s_u, s_red, s_C, s_wf / s_wb of this column consumed
+      if (!USER && v_bulk && tid == 0 && col + NUB < a.nrhs) issue_v(col + NUB);
     }
   }   // column loop
+  if (!USER && o_bulk && lane == 0) bulk_wait_read0();   // smem stays valid until read
   if (tid == 0) a.ep[c] = base + (unsigned)a.nrhs;
+}
+
+// e1[r] = e^{-(t_r - t_{r-1})} (e1[0] = 1; padding 1): the v-independent exponentials of
+// the scan, precomputed once per plan (plan data, read by bulk copies beside t)
+__global__ void k_d1_e_build(const double* __restrict__ t, int64_t n, double* __restrict__ e1) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n + 16;
+       r += (int64_t)gridDim.x * blockDim.x)
+    e1[r] = (r > 0 && r < n) ? exp(-(t[r] - t[r - 1])) : 1.0;
 }
 
 }  // namespace lpc
@@ -720,8 +760,8 @@ Shape make_shape() {
   shape_fns<BLOCK, SEGS, SL, false>(s.fn[0]);
   shape_fns<BLOCK, SEGS, SL, true>(s.fn[1]);
   const size_t sub = (size_t)BLOCK * SEGS * SL;
-  s.smem[0] = sizeof(double) * (3 * sub + 16);   // t, e^{-gap}, u
-  s.smem[1] = s.smem[0] + sizeof(int) * (sub + 8);
+  s.smem[0] = sizeof(double) * ((2 + lpc::lpc_nub(false, (int)sub)) * sub + 16);   // t, e, u buffers
+  s.smem[1] = sizeof(double) * (3 * sub + 16) + sizeof(int) * (sub + 8);   // t, e, u, perm
   return s;
 }
 
@@ -773,6 +813,12 @@ gp_status d1_prepare(Plan& pl) {
       GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
       GPM_TRY(pl.bar.alloc(sizeof(unsigned) * (size_t)g));
       GPM_CUDA(cudaMemset(pl.bar.ptr, 0, pl.bar.bytes));
+      if (!pl.d1e.bytes) {
+        GPM_TRY(pl.d1e.alloc(sizeof(double) * (size_t)(pl.n + 16)));
+        lpc::k_d1_e_build<<<148 * 4, 256>>>(pl.t.as<double>(), pl.n, pl.d1e.as<double>());
+        GPM_CUDA(cudaGetLastError());
+        GPM_CUDA(cudaDeviceSynchronize());
+      }
       if (getenv("GPM_D1_TIMING")) {
         GPM_TRY(pl.dbg.alloc(sizeof(unsigned long long) * 16 * 32 * (size_t)g));
         GPM_CUDA(cudaMemset(pl.dbg.ptr, 0, pl.dbg.bytes));
@@ -796,6 +842,7 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   const Shape& sh = g_shapes[pl.d1_shape];
   lpc::Args a;
   a.ts = pl.t.as<double>();
+  a.e1 = pl.d1e.as<double>();
   a.perm = pl.perm.as<int>();
   a.v = v;
   a.out = out;

@@ -113,6 +113,7 @@ struct Plan {
   DevBuf bar;                       // grid barrier words (d = 1 cooperative kernel)
   DevBuf stage_in, stage_out;       // gp_kmvm_host staging
   DevBuf dbg;                       // d=1 phase timestamps (env GPM_D1_TIMING)
+  DevBuf d1e;                       // d=1: e^{-gap} per rank (plan data, padded with 1)
   DevBuf pts;                       // d>=2: packed (t1, t2, t3, u) per rank, rebuilt per apply
   DevBuf hpbuf;                     // d>=2: staged structure of the carried passes (setup)
   DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)

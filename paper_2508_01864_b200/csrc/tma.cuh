@@ -57,3 +57,18 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 }  // namespace gpm
+
+namespace gpm {
+// 1-D bulk store shared -> global (bytes: multiple of 16; both addresses 16-byte aligned),
+// tracked by the issuing thread's bulk groups
+__device__ __forceinline__ void bulk_store_1d(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until this thread's committed bulk stores have read their shared-memory source
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+}  // namespace gpm
