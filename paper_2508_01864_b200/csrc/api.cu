@@ -450,7 +450,7 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
     case 7: *value = pl.d == 1 ? pl.d1_shape : -1; break;
     default: {
       // debug (GPM_D1_TIMING, d = 1 single-chunk path, last launch): what = 100 + slot:
-      // mean over CTAs of stamp[slot] - min stamp[0] (ns); 200 + slot: the max over CTAs
+      // mean over warps of stamp[slot] - stamp[0] (SM cycles); 200 + slot: the max
       if (what < 100 || what >= 216 || (what >= 116 && what < 200))
         return fail(GP_ERR_INVALID_ARG, "unknown query");
       if (!pl.dbg.bytes) return fail(GP_ERR_INVALID_ARG, "GPM_D1_TIMING not enabled");
@@ -458,15 +458,14 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
       if (cudaMemcpy(h.data(), pl.dbg.ptr, pl.dbg.bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         return fail(GP_ERR_CUDA, "dbg copy failed");
       const int slot = what % 100;
-      // per-warp stamps [cta][32 warps][16]; warps that never wrote slot 0 are unused
-      unsigned long long t0 = ~0ull, mx = 0;
+      // per-warp cycle stamps [cta][32 warps][16] (SM clock64): slot minus the same
+      // warp's slot 0; warps that never wrote slot 0 are unused
+      unsigned long long mx = 0;
       double acc = 0;
       int cntw = 0;
-      for (int b = 0; b < pl.d1_grid * 32; ++b)
-        if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
       for (int b = 0; b < pl.d1_grid * 32; ++b) {
         if (!h[b * 16] || !h[b * 16 + slot]) continue;
-        const unsigned long long dt = h[b * 16 + slot] > t0 ? h[b * 16 + slot] - t0 : 0;
+        const unsigned long long dt = h[b * 16 + slot] > h[b * 16] ? h[b * 16 + slot] - h[b * 16] : 0;
         acc += (double)dt;
         mx = std::max(mx, dt);
         ++cntw;

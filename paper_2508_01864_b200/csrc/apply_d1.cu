@@ -49,6 +49,7 @@ constexpr int LL_W = 32;    // 8-byte words per record slot (<= 2 x 2 x 6 moment
 
 struct Args {
   const double* ts;    // sorted scaled coordinates (plan)
+  const double* ends;  // chunk ends: t_0, t[min(b chunk, n) - 1] for b = 1..G (plan, padded)
   const double* e1;    // e^{-gap} per rank (plan, padded with 1)
   const int* perm;     // rank -> user index (plan, padded)
   const double* v;     // input columns: user order or rank order
@@ -64,9 +65,10 @@ struct Args {
   int knob;                  // debug: skip phases (GPM_D1_KNOB; timing experiments only)
 };
 
+// SM cycle counter (per SM; phase stamps are compared within a warp)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
   return t;
 }
 // per-warp phase timestamps (lane 0 of every warp): dbg[(cta * 32 + warp) * 16 + slot]
@@ -224,7 +226,7 @@ struct Run {
 
 // u buffers: two in rank order (the next column's v lands while this one computes) when
 // t, e^{-gap} and 2 u fit the 227 KB carve-out, else one
-constexpr int lpc_nub(bool user, int sub) { return (!user && (4 * sub + 16) * 8 <= 221 * 1024) ? 2 : 1; }
+constexpr int lpc_nub(bool user, int sub) { return (!user && (4 * sub + 18) * 8 <= 221 * 1024) ? 2 : 1; }
 
 // P: moment order (KIND 0: nu = P + 1/2; KIND 1: the lengthscale gradient of nu = P - 1/2)
 template <int P, int KIND, int BLOCK, int SEGS, int SL, bool USER>
@@ -241,15 +243,16 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   static_assert(2 * NV <= LL_W, "record slot too small");
   static_assert(NW <= 32 && BLOCK >= 64 + 160, "warp roles: 2 totals warps, fold threads for G <= 160");
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* s_t = reinterpret_cast<double*>(smem_raw);   // SUB + 8: t (clamped past the end)
-  double* s_e = s_t + SUB + 8;                         // SUB + 8: e^{-gap} (plan; 1 past the end)
+  double* s_t = reinterpret_cast<double*>(smem_raw) + 2;   // [-2, SUB + 8): t (clamped past
+                                                           // the end; s_t[-1] = t[c0 - 1])
+  double* s_e = s_t + SUB + 8;                         // SUB + 8: e^{-gap} (1 past the end)
   double* s_ub = s_e + SUB + 8;                        // NUB x SUB: u, then out (rank order)
   int* s_pi = reinterpret_cast<int*>(s_ub + NUB * SUB);   // SUB + 8 (user order)
   __shared__ uint64_t mbar[NPART], mbar_v[NUB][NPART], mbar_tab;
   __shared__ __align__(16) double s_tab[64];
   __shared__ double s_wf[NW][NQ + 2], s_wb[NW][NQ + 2];   // warp totals of the block scan
   __shared__ double s_red[NW][NV];                        // warp partials of the chunk sum
-  __shared__ double s_tl[160 + 1];                        // chunk-end t: s_tl[b + 1], s_tl[0] = t_0
+  __shared__ __align__(16) double s_tl[160 + 2];         // chunk-end t: s_tl[b + 1], s_tl[0] = t_0
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, c = blockIdx.x;
@@ -284,9 +287,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   };
 
   LPC_STAMP(0);
-  // ---- prologue: the bulk copies go out first (thread 0 initialises and arms the
-  // barriers; the others meet them after the first __syncthreads); every global scalar
-  // goes to a register and is consumed late, so no load latency sits before the copies
+  // ---- prologue.  Thread 0 initialises the barriers; after one __syncthreads it issues
+  // the plan-data bulk copies while the others go on.  Boundary coordinates come from the
+  // copied t (scalar global loads would queue behind the bulk traffic at the L2).
   if (tid == 0) {
     for (int p = 0; p < NPART; ++p) {
       mbar_init(&mbar[p], 1);
@@ -294,49 +297,60 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
     }
     mbar_init(&mbar_tab, 1);
     mbar_fence_init();
-    mbar_expect_tx(&mbar_tab, 64 * 8);
+  }
+  __syncthreads();   // barrier initialisation visible
+  if (tid == 0) {   // plan data: before griddepcontrol.wait
+    const unsigned nend = (unsigned)((G + 2) & ~1);   // chunk ends (padded plan array)
+    mbar_expect_tx(&mbar_tab, 64 * 8 + nend * 8);
     tma_load_1d(s_tab, g_fexp_tab, 64 * 8, &mbar_tab);
+    tma_load_1d(s_tl, a.ends, nend * 8, &mbar_tab);
 #pragma unroll 1
-    for (int p = 0; p < NPART; ++p) {   // plan data: before griddepcontrol.wait
+    for (int p = 0; p < NPART; ++p) {
       const int lo = p * PSZ, hi = min(cnt, lo + PSZ);
       if (lo < hi) {
-        const unsigned nt = (unsigned)(((hi - lo) + 1) & ~1);   // padded plan arrays
+        // part 0 of chunks c > 0 starts two points early (16-byte aligned): s_t[-1] is
+        // the chunk's reference point
+        const int lo2 = (p == 0 && c > 0) ? lo - 2 : lo;
+        const unsigned nt = (unsigned)(((hi - lo2) + 1) & ~1);   // padded plan arrays
         const unsigned np = (unsigned)(((hi - lo) + 3) & ~3);
-        mbar_expect_tx(&mbar[p], 2 * nt * 8 + (USER ? np * 4 : 0));
-        tma_load_1d(s_t + lo, a.ts + c0 + lo, nt * 8, &mbar[p]);
-        tma_load_1d(s_e + lo, a.e1 + c0 + lo, nt * 8, &mbar[p]);
+        const unsigned ne = (unsigned)(((hi - lo) + 1) & ~1);
+        mbar_expect_tx(&mbar[p], nt * 8 + ne * 8 + (USER ? np * 4 : 0));
+        tma_load_1d(s_t + lo2, a.ts + c0 + lo2, nt * 8, &mbar[p]);
+        tma_load_1d(s_e + lo, a.e1 + c0 + lo, ne * 8, &mbar[p]);
         if (USER) tma_load_1d(s_pi + lo, a.perm + c0 + lo, np * 4, &mbar[p]);
       }
     }
   }
-  // boundary coordinates (clamped to the chunk): the point before my first point, the
-  // last points of my segments, this chunk's reference (the point before its first point;
-  // t_0 for chunk 0: its first gap is 0) and last point, and one chunk end per thread
-  // for the fold's shift distances (-> s_tl)
-  const int64_t cl = c0 + cnt - 1;
-  const double tprev = __ldg(a.ts + (j0 < cnt ? (c0 + j0 > 0 ? c0 + j0 - 1 : 0) : cl));
-  double tseg[SEGS];   // the last point of each of my segments
-#pragma unroll
-  for (int sg = 0; sg < SEGS; ++sg) tseg[sg] = __ldg(a.ts + min(c0 + j0 + (sg + 1) * SL - 1, cl));
-  const double tmye = tseg[SEGS - 1];
-  const double tref0 = __ldg(a.ts + (c0 > 0 ? c0 - 1 : 0));
-  const double tlast = __ldg(a.ts + cl);
-  const double my_tl = tid <= G ? __ldg(a.ts + (tid == 0 ? 0 : min((int64_t)tid * a.chunk, a.n) - 1))
-                                : 0.0;
-  __syncthreads();   // barrier initialisation visible
   asm volatile("griddepcontrol.wait;" ::: "memory");   // v, records and ep of earlier launches
   asm volatile("griddepcontrol.launch_dependents;");
   LPC_STAMP(8);
-  const unsigned base = *(volatile const unsigned*)(a.ep + c);   // columns published so far
   if (tid == 0 && v_bulk) {
     issue_v(0);
     if (NUB > 1 && a.nrhs > 1) issue_v(1);
   }
   if (USER && a.prefetch && tid == 32) prefetch_v(0);
+  const unsigned base = __ldcg(a.ep + c);   // columns published so far (L2: the previous grid)
   mbar_wait(&mbar_tab, 0);
   LPC_STAMP(7);
-  if (part_live) mbar_wait(&mbar[mypart], 0);
+#pragma unroll 1
+  for (int p = 0; p < NPART; ++p)   // every live part: boundary points may lie in any
+    if (p * PSZ < cnt) mbar_wait(&mbar[p], 0);
   LPC_STAMP(9);
+  // boundary coordinates (clamped to the chunk): the chunk's reference point (the point
+  // before its first point; t_0 for chunk 0: its first gap is 0), the point before my
+  // first point, the last points of my segments, the chunk's last point
+  const double tref0 = c > 0 ? s_t[-1] : s_t[0];
+  const double tlast = s_t[cnt - 1];
+  const double tprev = j0 == 0 ? tref0 : (j0 - 1 < cnt ? s_t[j0 - 1] : tlast);
+  double tseg[SEGS];   // the last point of each of my segments
+#pragma unroll
+  for (int sg = 0; sg < SEGS; ++sg) tseg[sg] = s_t[min(j0 + (sg + 1) * SL, cnt) - 1];
+  if (j0 >= cnt) {
+#pragma unroll
+    for (int sg = 0; sg < SEGS; ++sg) tseg[sg] = tlast;
+  }
+  const double tmye = tseg[SEGS - 1];
+  __syncthreads();   // every thread's boundary reads before the tails are clamped
   // ---- neutral tails (once per launch): t clamped to the last point (gap 0), weight 1,
   // u = 0 (rank order: the bulk copies stop at cnt), no source index (user order)
 #pragma unroll
@@ -482,7 +496,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       }
       advance<P>(m, dF, eF);
       advance<P>(m + NQ, dB, eB);
-      if (col == 0 && tid <= G) s_tl[tid] = my_tl;   // read after the barrier below
       int id;
       const double sw = warp_sum_scatter<NV>(m, lane, &id);
       if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp][id] = sw;
@@ -680,46 +693,49 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         if (j0 + k < cnt) s_u[j0 + k] = loc[k];   // the tail stays 0 for a later column
     }
     LPC_STAMP(12);
-    if (!USER) {   // this warp's contiguous outputs: one bulk store (+ an odd tail element)
+    if (!USER) {   // this warp's contiguous outputs, coalesced 16-byte stores (+ an odd tail)
+      __syncwarp();
       const int wb = warp * 32 * ITEMS;
       const int we = min(cnt, wb + 32 * ITEMS);
       if (o_bulk) {
-        fence_proxy_async_smem();   // my generic writes of s_u before the bulk store
-        __syncwarp();
-        if (lane == 0 && we > wb) {
-          const int nb = (we - wb) & ~1;
-          if (nb) {
-            bulk_store_1d(ocol + c0 + wb, s_u + wb, (unsigned)nb * 8);
-            bulk_commit();
-          }
-          if ((we - wb) & 1) ocol[c0 + we - 1] = s_u[we - 1];
-        }
+        const int np2 = (we - wb) >> 1;
+        const double2* src = reinterpret_cast<const double2*>(s_u + wb);
+        double2* dst = reinterpret_cast<double2*>(ocol + c0 + wb);
+#pragma unroll 4
+        for (int k = lane; k < np2; k += 32) dst[k] = src[k];
+        if (((we - wb) & 1) && lane == 0) ocol[c0 + we - 1] = s_u[we - 1];
       } else {
-        __syncwarp();
 #pragma unroll 4
         for (int j = wb + lane; j < we; j += 32) ocol[c0 + j] = s_u[j];
       }
     }
     LPC_STAMP(6);
     if (col + 1 < a.nrhs) {
-      // the u buffer of this column is the v destination of column col + NUB: the bulk
-      // store must have read it and every thread's generic accesses precede the copy
-      if (!USER && o_bulk && lane == 0) bulk_wait_read0();
+      // the u buffer of this column is the v destination of column col + NUB: every
+      // thread's generic accesses precede the copy
       fence_proxy_async_smem();
       __syncthreads();   // s_u, s_red, s_C, s_wf / s_wb of this column consumed
       if (!USER && v_bulk && tid == 0 && col + NUB < a.nrhs) issue_v(col + NUB);
     }
   }   // column loop
-  if (!USER && o_bulk && lane == 0) bulk_wait_read0();   // smem stays valid until read
   if (tid == 0) a.ep[c] = base + (unsigned)a.nrhs;
 }
 
 // e1[r] = e^{-(t_r - t_{r-1})} (e1[0] = 1; padding 1): the v-independent exponentials of
-// the scan, precomputed once per plan (plan data, read by bulk copies beside t)
+// the scan, precomputed once per plan (plan data, read by bulk copies beside t: one
+// e^{-x} per point per apply saved for 8 bytes per point of L2-resident plan traffic)
 __global__ void k_d1_e_build(const double* __restrict__ t, int64_t n, double* __restrict__ e1) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n + 16;
        r += (int64_t)gridDim.x * blockDim.x)
     e1[r] = (r > 0 && r < n) ? exp(-(t[r] - t[r - 1])) : 1.0;
+}
+
+// chunk ends of a chunking (plan data for the fold's shift distances): ends[0] = t_0,
+// ends[b] = t[min(b chunk, n) - 1] for b = 1..G (ends[G + 1] padding)
+__global__ void k_d1_ends(const double* __restrict__ t, int64_t n, int64_t chunk, int G,
+                          double* __restrict__ ends) {
+  for (int b = threadIdx.x; b <= G + 1; b += blockDim.x)
+    ends[b] = b == 0 ? t[0] : t[min((int64_t)min(b, G) * chunk, n) - 1];
 }
 
 }  // namespace lpc
@@ -760,8 +776,8 @@ Shape make_shape() {
   shape_fns<BLOCK, SEGS, SL, false>(s.fn[0]);
   shape_fns<BLOCK, SEGS, SL, true>(s.fn[1]);
   const size_t sub = (size_t)BLOCK * SEGS * SL;
-  s.smem[0] = sizeof(double) * ((2 + lpc::lpc_nub(false, (int)sub)) * sub + 16);   // t, e, u buffers
-  s.smem[1] = sizeof(double) * (3 * sub + 16) + sizeof(int) * (sub + 8);   // t, e, u, perm
+  s.smem[0] = sizeof(double) * ((2 + lpc::lpc_nub(false, (int)sub)) * sub + 18);   // t, e, u buffers
+  s.smem[1] = sizeof(double) * (3 * sub + 18) + sizeof(int) * (sub + 8);   // t, e, u, perm
   return s;
 }
 
@@ -813,12 +829,15 @@ gp_status d1_prepare(Plan& pl) {
       GPM_CUDA(cudaMemset(pl.aggs.ptr, 0, pl.aggs.bytes));
       GPM_TRY(pl.bar.alloc(sizeof(unsigned) * (size_t)g));
       GPM_CUDA(cudaMemset(pl.bar.ptr, 0, pl.bar.bytes));
-      if (!pl.d1e.bytes) {
+      // plan data of the d = 1 path: e^{-gap} per rank (once) and the chunk ends
+      if (pl.d1e.bytes < sizeof(double) * (size_t)(pl.n + 16)) {
         GPM_TRY(pl.d1e.alloc(sizeof(double) * (size_t)(pl.n + 16)));
         lpc::k_d1_e_build<<<148 * 4, 256>>>(pl.t.as<double>(), pl.n, pl.d1e.as<double>());
-        GPM_CUDA(cudaGetLastError());
-        GPM_CUDA(cudaDeviceSynchronize());
       }
+      GPM_TRY(pl.d1ends.alloc(sizeof(double) * (size_t)(g + 2)));
+      lpc::k_d1_ends<<<1, 256>>>(pl.t.as<double>(), pl.n, chunk, (int)g, pl.d1ends.as<double>());
+      GPM_CUDA(cudaGetLastError());
+      GPM_CUDA(cudaDeviceSynchronize());
       if (getenv("GPM_D1_TIMING")) {
         GPM_TRY(pl.dbg.alloc(sizeof(unsigned long long) * 16 * 32 * (size_t)g));
         GPM_CUDA(cudaMemset(pl.dbg.ptr, 0, pl.dbg.bytes));
@@ -842,6 +861,7 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   const Shape& sh = g_shapes[pl.d1_shape];
   lpc::Args a;
   a.ts = pl.t.as<double>();
+  a.ends = pl.d1ends.as<double>();
   a.e1 = pl.d1e.as<double>();
   a.perm = pl.perm.as<int>();
   a.v = v;
@@ -870,8 +890,9 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   at[0].val.cooperative = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pl.d1_pdl ? 2 : 1;
+  static const int nocoop = getenv("GPM_D1_NOCOOP") ? atoi(getenv("GPM_D1_NOCOOP")) : 0;   // timing experiment
+  cfg.attrs = nocoop ? at + 1 : at;
+  cfg.numAttrs = nocoop ? (pl.d1_pdl ? 1 : 0) : (pl.d1_pdl ? 2 : 1);
   void* args[] = {&a};
   GPM_CUDA(cudaLaunchKernelExC(&cfg, sh.fn[user_order ? 1 : 0][kind * 5 + pl.P], args));
   return GP_OK;

@@ -114,6 +114,7 @@ struct Plan {
   DevBuf stage_in, stage_out;       // gp_kmvm_host staging
   DevBuf dbg;                       // d=1 phase timestamps (env GPM_D1_TIMING)
   DevBuf d1e;                       // d=1: e^{-gap} per rank (plan data, padded with 1)
+  DevBuf d1ends;                    // d=1: chunk-end coordinates of the chunking (plan data)
   DevBuf pts;                       // d>=2: packed (t1, t2, t3, u) per rank, rebuilt per apply
   DevBuf hpbuf;                     // d>=2: staged structure of the carried passes (setup)
   DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)

@@ -37,8 +37,8 @@ for n in (10000, 1000000):
             with torch.cuda.stream(cs):
                 graph.replay()
             torch.cuda.synchronize()
-            mean = [plan.query(100 + s) / 1e3 for s, _ in SLOTS]
-            mx = [plan.query(200 + s) / 1e3 for s, _ in SLOTS]
+            mean = [plan.query(100 + s) / 1965.0 for s, _ in SLOTS]   # cycles -> us at 1965 MHz
+            mx = [plan.query(200 + s) / 1965.0 for s, _ in SLOTS]
             print(f"n={n} shape={shape} rank={rank} end-of-phase us (mean/max):  " +
                   "  ".join(f"{nm}={m:.2f}/{M:.2f}" for (_, nm), m, M in zip(SLOTS, mean, mx)),
                   flush=True)

@@ -32,6 +32,8 @@ def _vec(r):
 
 
 V = [_vec(r) for r in range(min(args.applies, 8))]
+if os.environ.get('GPM_PROF_TIMING'):
+    pass
 out = torch.empty_like(V[0])
 for k in range(args.applies):
     if args.rank:
