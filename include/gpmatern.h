@@ -195,6 +195,22 @@ GP_API gp_status gp_cg_solve_pc(gp_plan p, gp_precond pc, double sigma2, const d
                                 int max_iter, double *alpha, double *beta, gp_cg_info *info,
                                 void *stream);
 
+/* gp_cg_solve_ex -- gp_cg_solve_pc with the solve's by-products (SURVEY §8(a) a10, §8(c) c1
+ * item 4):
+ *   beta_ols : (host) NULL or 1+d (AFFINE) / L (BASIS) entries: the OLS estimate
+ *              (H^T H)^-1 H^T y that Algorithm 1 starts from (P:829 [Alg 1, first line]);
+ *   X        : (device) NULL or n x (1 + nh) column-major, user order: the CG solutions
+ *              [A^-1 y, A^-1 H_1, ..., A^-1 H_nh] (nh = 0, 1+d or L), from which beta and
+ *              alpha are formed.
+ * Unpreconditioned iterations run the fused iteration: the apply returns
+ * q = K p + sigma2 p with the p^T q partials, two vector kernels re-sum the partials in a
+ * fixed order, and blocks of 8 iterations are replayed as one CUDA graph (run directly
+ * when `stream` is itself being captured).  Other arguments and errors as gp_cg_solve. */
+GP_API gp_status gp_cg_solve_ex(gp_plan p, gp_precond pc, double sigma2, const double *y,
+                                int mean_kind, const double *H, int L, double rtol,
+                                int max_iter, double *alpha, double *beta, double *beta_ols,
+                                double *X, gp_cg_info *info, void *stream);
+
 /* ---- the likelihood machinery of PAPER.md App A ---------------------- */
 
 /* gp_precond_create -- rank-k pivoted Cholesky K ~ L L^T of the plan's kernel matrix

@@ -86,6 +86,8 @@ def load_library(path: str | None = None):
         "gp_cg_solve": [vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, ctypes.POINTER(_CGInfo), vp],
         "gp_cg_solve_pc": [vp, vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, ctypes.POINTER(_CGInfo),
                            vp],
+        "gp_cg_solve_ex": [vp, vp, cd, vp, ci, vp, ci, cd, ci, vp, vp, vp, vp,
+                           ctypes.POINTER(_CGInfo), vp],
         "gp_precond_create": [vp, ci, vp, ctypes.POINTER(vp)],
         "gp_precond_factor": [vp, vp, vp, vp],
         "gp_precond_solve": [vp, cd, vp, ci, vp, vp],
@@ -243,22 +245,31 @@ class Plan:
         return Cross(self, z, stream)
 
     def cg_solve(self, y, sigma2: float, mean: int = MEAN_AFFINE, H=None, rtol: float = 1e-8,
-                 max_iter: int = 20000, stream=None, precond=None):
-        """alpha, beta, info of (K + sigma^2 I) CG with GLS fixed effects (gp_cg_solve_pc;
-        precond: a Precond of this plan or None)."""
+                 max_iter: int = 20000, stream=None, precond=None, return_x: bool = False,
+                 return_ols: bool = False):
+        """alpha, beta, info of (K + sigma^2 I) CG with GLS fixed effects (gp_cg_solve_ex;
+        precond: a Precond of this plan or None).  return_x: info["X"] = the CG solutions
+        [A^-1 y, A^-1 H...] (1 + nh, n) in user order; return_ols: info["beta_ols"]."""
         import torch
         alpha = torch.empty(self.n, dtype=torch.float64, device=y.device)
         nb = 1 + self.d if mean == MEAN_AFFINE else (H.shape[0] if mean == MEAN_BASIS else 0)
         beta = (ctypes.c_double * max(nb, 1))()
+        bols = (ctypes.c_double * max(nb, 1))() if return_ols else None
+        X = torch.empty((1 + nb, self.n), dtype=torch.float64, device=y.device) if return_x else None
         info = _CGInfo()
         Hp = _dev(H, "H") if mean == MEAN_BASIS else ctypes.c_void_p(0)
         L = H.shape[0] if mean == MEAN_BASIS else 0
-        st = _lib.gp_cg_solve_pc(self._h, precond._h if precond is not None else None,
+        st = _lib.gp_cg_solve_ex(self._h, precond._h if precond is not None else None,
                                  float(sigma2), _dev(y, "y", (self.n,)), mean, Hp, L,
-                                 float(rtol), int(max_iter), _dev(alpha, "alpha"), beta,
-                                 ctypes.byref(info), _stream(stream))
+                                 float(rtol), int(max_iter), _dev(alpha, "alpha"), beta, bols,
+                                 _dev(X, "X") if X is not None else None, ctypes.byref(info),
+                                 _stream(stream))
         res = {"iters": info.iters, "relres_max": info.relres_max,
                "failed_column": info.failed_column, "restarts": info.restarts}
+        if X is not None:
+            res["X"] = X
+        if bols is not None:
+            res["beta_ols"] = [bols[i] for i in range(nb)]
         if st != 0:
             err = GPError(st, _lib.gp_last_error().decode())
             err.info = res

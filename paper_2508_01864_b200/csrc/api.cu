@@ -245,6 +245,14 @@ gp_status gp_cg_solve(gp_plan p, double sigma2, const double* y, int mean_kind,
 gp_status gp_cg_solve_pc(gp_plan p, gp_precond pc, double sigma2, const double* y, int mean_kind,
                          const double* H, int L, double rtol, int max_iter, double* alpha,
                          double* beta, gp_cg_info* info, void* stream) {
+  return gp_cg_solve_ex(p, pc, sigma2, y, mean_kind, H, L, rtol, max_iter, alpha, beta, nullptr,
+                        nullptr, info, stream);
+}
+
+gp_status gp_cg_solve_ex(gp_plan p, gp_precond pc, double sigma2, const double* y, int mean_kind,
+                         const double* H, int L, double rtol, int max_iter, double* alpha,
+                         double* beta, double* beta_ols, double* X, gp_cg_info* info,
+                         void* stream) {
   if (!p || !y || !alpha) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (pc && pc->owner != p) return fail(GP_ERR_INVALID_ARG, "preconditioner built on another plan");
   if (!(sigma2 > 0) || !std::isfinite(sigma2)) return fail(GP_ERR_INVALID_ARG, "sigma2 must be > 0");
@@ -255,7 +263,7 @@ gp_status gp_cg_solve_pc(gp_plan p, gp_precond pc, double sigma2, const double* 
   if (mean_kind == GP_MEAN_BASIS && (!H || L < 1 || L > 16))
     return fail(GP_ERR_INVALID_ARG, "BASIS mean needs H and 1 <= L <= 16");
   return cg_solve(p->pl, sigma2, y, mean_kind, H, L, rtol, max_iter, alpha, beta, info,
-                  static_cast<cudaStream_t>(stream), pc ? &pc->pc : nullptr);
+                  static_cast<cudaStream_t>(stream), pc ? &pc->pc : nullptr, beta_ols, X);
 }
 
 // ---- §8(f) f3: preconditioner, Algorithm 2, likelihood

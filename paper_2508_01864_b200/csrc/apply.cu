@@ -12,7 +12,7 @@ namespace gpm {
 
 gp_status d1_prepare(Plan& pl);
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s, int kind);
+                    cudaStream_t s, int kind, double cg_s2 = 0.0, double* cg_part = nullptr);
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind);
 gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
 size_t level_pt_bytes();
@@ -34,24 +34,44 @@ __global__ void k_gather(const int* __restrict__ perm, const double* __restrict_
 // out[perm[r] - tgt_off] = os2 (self u[r] + acc[r]) for targets; perm == nullptr: rank order.
 // u is read from the packed point records (stride 4 doubles, u at offset 3); self = k(0)
 // (1 for K, 0 for the lengthscale gradient).
+// CG epilogue (rank order only, cg_part != nullptr): out = K u + cg_s2 u and the block's
+// partial sum of u . out -> cg_part[(col0 + blockIdx.y) * gridDim.x + blockIdx.x]
 __global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ pts,
                            const double* __restrict__ acc, const double* __restrict__ part,
                            int nparts, int64_t n, int64_t tgt_off, double os2, double self,
-                           double* __restrict__ out, int64_t ostride) {
+                           double* __restrict__ out, int64_t ostride, double cg_s2,
+                           double* __restrict__ cg_part, int col0) {
+  __shared__ double red[32];
   pts += blockIdx.y * 4 * n;
   acc += blockIdx.y * n;
   part += blockIdx.y * nparts * n;
   out += blockIdx.y * ostride;
+  double pq = 0.0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     double a = acc[r];
     for (int p = 0; p < nparts; ++p) a += part[(int64_t)p * n + r];   // fixed order
-    const double val = os2 * fma(self, pts[4 * r + 3], a);
+    const double u = pts[4 * r + 3];
+    double val = os2 * fma(self, u, a);
     if (perm) {
       const int i = __ldg(perm + r);
       if (i >= tgt_off) out[i - tgt_off] = val;
     } else {
+      if (cg_part) {
+        val = fma(cg_s2, u, val);
+        pq = fma(u, val, pq);
+      }
       out[r] = val;
+    }
+  }
+  if (cg_part) {   // fixed-order block reduction
+    for (int off = 16; off > 0; off >>= 1) pq += __shfl_down_sync(0xffffffffu, pq, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      cg_part[(size_t)(col0 + blockIdx.y) * gridDim.x + blockIdx.x] = t;
     }
   }
 }
@@ -112,8 +132,13 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
   return GP_OK;
 }
 
+int cg_nblk(const Plan& pl) {
+  return pl.d == 1 ? (pl.d1_path == 3 ? 0 : pl.d1_grid) : egrid(pl.n);
+}
+
 static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                              cudaStream_t s, int kind) {
+                              cudaStream_t s, int kind, double cg_s2 = 0.0,
+                              double* cg_part = nullptr) {
   const int64_t vstride = user_order ? pl.n_src : pl.n;
   const int64_t ostride = user_order ? pl.n - pl.tgt_off : pl.n;
   for (int c0 = 0; c0 < nrhs; c0 += LV_MAXB) {
@@ -125,7 +150,7 @@ static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, 
     k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
         user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
         pl.part.as<double>(), level_nparts(pl), pl.n, user_order ? pl.tgt_off : 0, pl.os2,
-        kind == 0 ? 1.0 : 0.0, out + c0 * ostride, ostride);
+        kind == 0 ? 1.0 : 0.0, out + c0 * ostride, ostride, cg_s2, cg_part, c0);
     GPM_CUDA(cudaGetLastError());
     pl.launches_per_apply = launches + 2;   // + pack + epilogue (per batch of columns)
   }
@@ -142,9 +167,9 @@ gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cu
 }
 
 gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s,
-                     int kind) {
-  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, nrhs, false, s, kind);
-  return apply_levels(pl, u_rank, out_rank, nrhs, false, s, kind);
+                     int kind, double cg_s2, double* cg_part) {
+  if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, nrhs, false, s, kind, cg_s2, cg_part);
+  return apply_levels(pl, u_rank, out_rank, nrhs, false, s, kind, cg_s2, cg_part);
 }
 
 gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s, int kind) {

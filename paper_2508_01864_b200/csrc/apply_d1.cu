@@ -63,6 +63,8 @@ struct Args {
   unsigned* ep;              // [G]: columns published by CTA b over the plan's life
   unsigned long long* dbg;   // optional phase timestamps [G][16] (GPM_D1_TIMING)
   int knob;                  // debug: skip phases (GPM_D1_KNOB; timing experiments only)
+  double cg_s2;              // CG epilogue (rank order): out = K u + cg_s2 u ...
+  double* cg_part;           // ... and the CTA's partial u . out -> cg_part[col * G + cta]
 };
 
 // SM cycle counter (per SM; phase stamps are compared within a warp)
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   __shared__ __align__(16) double s_tab[64];
   __shared__ double s_wf[NW][NQ + 2], s_wb[NW][NQ + 2];   // warp totals of the block scan
   __shared__ double s_red[NW][NV];                        // warp partials of the chunk sum
+  __shared__ double s_pq[NW];                             // CG epilogue: warp partials of p . q
   __shared__ __align__(16) double s_tl[160 + 2];         // chunk-end t: s_tl[b + 1], s_tl[0] = t_0
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -687,10 +690,29 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         const int pi = s_pi[j];
         if (j < cnt && pi >= a.tgt_off) ocol[pi - a.tgt_off] = loc[k];
       }
-    } else {
+    } else if (!a.cg_part) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
         if (j0 + k < cnt) s_u[j0 + k] = loc[k];   // the tail stays 0 for a later column
+    } else {   // CG epilogue: q = K p + s2 p, partial p . q (the tail has p = 0)
+      double pq = 0.0;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const double pk = s_u[j0 + k];
+        const double qk = fma(a.cg_s2, pk, loc[k]);
+        pq = fma(pk, qk, pq);
+        if (j0 + k < cnt) s_u[j0 + k] = qk;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) pq += __shfl_xor_sync(0xffffffffu, pq, off);
+      if (lane == 0) s_pq[warp] = pq;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+#pragma unroll 1
+        for (int w = 0; w < NW; ++w) t += s_pq[w];
+        a.cg_part[(size_t)col * G + c] = t;
+      }
     }
     LPC_STAMP(12);
     if (!USER) {   // this warp's contiguous outputs, coalesced 16-byte stores (+ an odd tail)
@@ -856,8 +878,11 @@ gp_status d1_prepare(Plan& pl) {
 }
 
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
-                    cudaStream_t s, int kind) {
-  if (pl.d1_path == 3) return db_launch(pl, v, out, nrhs, user_order, s, kind);
+                    cudaStream_t s, int kind, double cg_s2, double* cg_part) {
+  if (pl.d1_path == 3) {
+    if (cg_part) return fail(GP_ERR_INVALID_ARG, "internal: no CG epilogue on the d=1 path 3");
+    return db_launch(pl, v, out, nrhs, user_order, s, kind);
+  }
   const Shape& sh = g_shapes[pl.d1_shape];
   lpc::Args a;
   a.ts = pl.t.as<double>();
@@ -878,6 +903,8 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   a.rec = pl.aggs.as<unsigned long long>();
   a.ep = pl.bar.as<unsigned>();
   a.dbg = pl.dbg.bytes ? pl.dbg.as<unsigned long long>() : nullptr;
+  a.cg_s2 = cg_s2;
+  a.cg_part = user_order ? nullptr : cg_part;
   static const int knob = getenv("GPM_D1_KNOB") ? atoi(getenv("GPM_D1_KNOB")) : 0;
   a.knob = knob;
   cudaLaunchConfig_t cfg = {};

@@ -115,6 +115,7 @@ struct Plan {
   DevBuf dbg;                       // d=1 phase timestamps (env GPM_D1_TIMING)
   DevBuf d1e;                       // d=1: e^{-gap} per rank (plan data, padded with 1)
   DevBuf d1ends;                    // d=1: chunk-end coordinates of the chunking (plan data)
+  DevBuf cg_scratch;                // gp_cg_solve scratch, cached (grow-only)
   DevBuf pts;                       // d>=2: packed (t1, t2, t3, u) per rank, rebuilt per apply
   DevBuf hpbuf;                     // d>=2: staged structure of the carried passes (setup)
   DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)
@@ -183,8 +184,12 @@ void plan_free(Plan& pl);
 // apply.cu
 // Rank-space apply: out_rank = K u_rank (no nugget).  u_rank, out_rank: n doubles.
 // kind 0: K; kind 1: dK/dlog(l) (lengthscale gradient, L1 / d = 1 only).
+// CG epilogue (solve.cu): with cg_part != nullptr the apply returns
+// out = K u + cg_s2 u and writes per-block partial sums of u . out to
+// cg_part[c * cg_nblk(pl) + block] (fixed-order reductions: deterministic).
 gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s,
-                     int kind = 0);
+                     int kind = 0, double cg_s2 = 0.0, double* cg_part = nullptr);
+int cg_nblk(const Plan& pl);
 // User-order apply with gather/scatter: out = K v restricted to targets (unions).
 // Columns: v stride n_src, out stride n - tgt_off.
 gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s,
@@ -196,7 +201,8 @@ int64_t apply_model_bytes(const Plan& pl);
 // solve.cu
 gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,
                    int Lb, double rtol, int max_iter, double* alpha, double* beta,
-                   gp_cg_info* info, cudaStream_t s, Precond* pc = nullptr);
+                   gp_cg_info* info, cudaStream_t s, Precond* pc = nullptr,
+                   double* beta_ols = nullptr, double* Xout = nullptr);
 gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
                                  const double* Hz, int Lb, double* out, cudaStream_t s);
 

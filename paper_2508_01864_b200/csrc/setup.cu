@@ -128,7 +128,7 @@ void DevBuf::release() {
 
 void plan_free(Plan& pl) {
   for (DevBuf* b : {&pl.x_raw, &pl.perm, &pl.t, &pl.ord2, &pl.ord3, &pl.u, &pl.acc, &pl.w,
-                    &pl.aggs, &pl.bar, &pl.stage_in, &pl.stage_out, &pl.dbg, &pl.d1e, &pl.d1ends, &pl.pts, &pl.hpbuf, &pl.hpdesc, &pl.part})
+                    &pl.aggs, &pl.bar, &pl.stage_in, &pl.stage_out, &pl.dbg, &pl.d1e, &pl.d1ends, &pl.cg_scratch, &pl.pts, &pl.hpbuf, &pl.hpdesc, &pl.part})
     b->release();
   if (pl.ev_fork) cudaEventDestroy(pl.ev_fork);
   if (pl.ev_join) cudaEventDestroy(pl.ev_join);

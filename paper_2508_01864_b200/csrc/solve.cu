@@ -138,6 +138,101 @@ __global__ void k_pupd(double* __restrict__ P, const double* __restrict__ R,
     p[i] = fma(b, p[i], r[i]);
 }
 
+// ---- fused CG iteration.  The apply's epilogue already returns
+// q = K p + s2 p with per-block partials of p . q; every block of the two kernels below
+// re-sums the partials it needs in a fixed order (no separate reduction launches, the
+// results are identical in every block, hence deterministic).
+__device__ __forceinline__ double sum_fixed(const double* __restrict__ part, int nb, double* sh) {
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[b];
+  return block_sum(acc, sh);   // valid in thread 0
+}
+
+// alpha = r.r / p.q (old r.r from the previous iteration's partials); x += alpha p,
+// r -= alpha q, partials of the new r.r.  Breakdown p.q <= 0 -> alpha = 0, status 2.
+__global__ void k_cg_xr(double* __restrict__ X, double* __restrict__ R,
+                        const double* __restrict__ P, const double* __restrict__ Q,
+                        const double* __restrict__ part_pq, int nb_pq,
+                        const double* __restrict__ rr_old, double* __restrict__ rr_new,
+                        int* __restrict__ status, int* __restrict__ bd_iter, int it,
+                        int64_t n) {
+  __shared__ double sh[32];
+  __shared__ double s_alpha;
+  const int c = blockIdx.y;
+  const double pq = sum_fixed(part_pq + (size_t)c * nb_pq, nb_pq, sh);
+  const double ro = sum_fixed(rr_old + (size_t)c * gridDim.x, gridDim.x, sh);
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    if (status[c] == 0) {
+      if (!(pq > 0.0) || !isfinite(pq)) {
+        if (blockIdx.x == 0) {
+          status[c] = 2;
+          bd_iter[c] = it;
+        }
+      } else {
+        a = ro / pq;
+      }
+    }
+    s_alpha = a;
+  }
+  __syncthreads();
+  const double a = s_alpha;
+  double* x = X + (size_t)c * n;
+  double* r = R + (size_t)c * n;
+  const double* p = P + (size_t)c * n;
+  const double* q = Q + (size_t)c * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    const double rv = fma(-a, q[i], r[i]);
+    r[i] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) rr_new[(size_t)c * gridDim.x + blockIdx.x] = t;
+}
+
+// beta = new r.r / old r.r; p = r + beta p (active columns); convergence at
+// r.r <= tol2 (status 1, block 0); rr_out[c] = new r.r for the host
+__global__ void k_cg_p(double* __restrict__ P, const double* __restrict__ R,
+                       const double* __restrict__ rr_new, const double* __restrict__ rr_old,
+                       const double* __restrict__ tol2, int* __restrict__ status,
+                       double* __restrict__ rr_out, int64_t n) {
+  __shared__ double sh[32];
+  __shared__ double s_beta;
+  __shared__ int s_act;
+  const int c = blockIdx.y;
+  const double rn = sum_fixed(rr_new + (size_t)c * gridDim.x, gridDim.x, sh);
+  const double ro = sum_fixed(rr_old + (size_t)c * gridDim.x, gridDim.x, sh);
+  if (threadIdx.x == 0) {
+    const int st = status[c];
+    s_act = st == 0;
+    s_beta = st == 0 ? rn / ro : 0.0;
+    if (blockIdx.x == 0 && st == 0) {
+      rr_out[c] = rn;
+      if (rn <= tol2[c]) status[c] = 1;
+    }
+  }
+  __syncthreads();
+  if (!s_act) return;
+  const double b = s_beta;
+  double* p = P + (size_t)c * n;
+  const double* r = R + (size_t)c * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], r[i]);
+}
+
+// X columns back to user order: Xu[c][perm[r]] = X[c][r]
+__global__ void k_cols_to_user(const int* __restrict__ perm, const double* __restrict__ X,
+                               int64_t n, double* __restrict__ Xu) {
+  const int c = blockIdx.y;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    Xu[(size_t)c * n + perm[r]] = X[(size_t)c * n + r];
+}
+
 // partial sums of squares of columns (grid.y = column)
 __global__ void k_sumsq(const double* __restrict__ V, int64_t n, double* __restrict__ part) {
   __shared__ double sh[32];
@@ -299,48 +394,84 @@ gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double
   return GP_OK;
 }
 
+// The CG iterations of one 8-iteration block, enqueued on s: per iteration the apply with
+// the fused epilogue (q = K p + s2 p and the p.q partials), k_cg_xr, k_cg_p.  Captured once
+// per solve as a CUDA graph and replayed (when s is not itself being captured).
+struct CgBufs {
+  double *B, *X, *R, *P, *Q, *ppq, *prr, *tol2, *rr;
+  int *status, *bd_iter;
+  int k, nb_pq;
+};
+static gp_status cg_block(Plan& pl, const CgBufs& b, double sigma2, int it0, int iters,
+                          const std::vector<char>& act, cudaStream_t s) {
+  const int64_t n = pl.n;
+  for (int j = 0; j < iters; ++j) {
+    const int it = it0 + j;
+    double* rr_new = b.prr + (size_t)(it & 1) * b.k * CG_GRID;
+    double* rr_old = b.prr + (size_t)((it + 1) & 1) * b.k * CG_GRID;
+    // the apply on the runs of active columns (converged ones keep alpha = 0)
+    for (int c = 0; c < b.k;) {
+      if (!act[c]) { ++c; continue; }
+      int e = c;
+      while (e < b.k && act[e]) ++e;
+      GPM_TRY(apply_rank(pl, b.P + (size_t)c * n, b.Q + (size_t)c * n, e - c, s, 0, sigma2,
+                         b.ppq + (size_t)c * b.nb_pq));
+      c = e;
+    }
+    k_cg_xr<<<dim3(CG_GRID, b.k), CG_BLOCK, 0, s>>>(b.X, b.R, b.P, b.Q, b.ppq, b.nb_pq, rr_old,
+                                                     rr_new, b.status, b.bd_iter, it, n);
+    k_cg_p<<<dim3(CG_GRID, b.k), CG_BLOCK, 0, s>>>(b.P, b.R, rr_new, rr_old, b.tol2, b.status,
+                                                    b.rr, n);
+  }
+  GPM_CUDA(cudaGetLastError());
+  return GP_OK;
+}
+
 gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,
                    int Lb, double rtol, int max_iter, double* alpha, double* beta,
-                   gp_cg_info* info, cudaStream_t s, Precond* pc) {
+                   gp_cg_info* info, cudaStream_t s, Precond* pc, double* beta_ols,
+                   double* Xout) {
   const int64_t n = pl.n;
   const int nh = mean_kind == GP_MEAN_AFFINE ? 1 + pl.d : mean_kind == GP_MEAN_BASIS ? Lb : 0;
   const int k = 1 + nh;
   const size_t nk = (size_t)n * k;
-  DevBuf bB, bX, bR, bP, bQ, bpart, bsc;
-  struct Guard {
-    DevBuf* b[7];
-    ~Guard() { for (auto* x : b) x->release(); }
-  } guard{{&bB, &bX, &bR, &bP, &bQ, &bpart, &bsc}};
-  GPM_TRY(bB.alloc(8 * nk));
-  GPM_TRY(bX.alloc(8 * nk));
-  GPM_TRY(bR.alloc(8 * nk));
-  GPM_TRY(bP.alloc(8 * nk));
-  GPM_TRY(bQ.alloc(8 * nk));
-  const int npart = std::max(k, (nh + 1) * nh);
-  GPM_TRY(bpart.alloc(8 * (size_t)CG_GRID * npart));
-  // device scalars: rr[k] tol2[k] alpha[k] beta[k] bnorm2[k] | status[k] bd_iter[k]
-  GPM_TRY(bsc.alloc(8 * 5 * k + 4 * 2 * k + 64));
-  double* B = bB.as<double>();
-  double* X = bX.as<double>();
-  double* R = bR.as<double>();
-  double* Pm = bP.as<double>();
-  double* Q = bQ.as<double>();
-  double* part = bpart.as<double>();
-  double* rr = bsc.as<double>();
-  double* tol2 = rr + k;
-  double* al = tol2 + k;
-  double* be = al + k;
-  double* bn2 = be + k;
-  int* status = reinterpret_cast<int*>(bn2 + k);
-  int* bd_iter = status + k;
+  const int nb_pq = getenv("GPM_CG_UNFUSED") ? 0 : cg_nblk(pl);   // apply's CG-epilogue blocks (0: unfused)
+  // scratch cached on the plan (grow-only): no per-call frees, no device-wide syncs
+  const size_t nsc = 8 * (5 * nk + (size_t)std::max(nb_pq, 1) * k + 2 * (size_t)CG_GRID * k +
+                          (size_t)CG_GRID * std::max(k, (nh + 1) * std::max(nh, 1)) + 2 * k + 64) +
+                     4 * (2 * (size_t)k + 16);
+  if (pl.cg_scratch.bytes < nsc) GPM_TRY(pl.cg_scratch.alloc(nsc));
+  CgBufs b;
+  b.k = k;
+  b.nb_pq = nb_pq;
+  b.B = pl.cg_scratch.as<double>();
+  b.X = b.B + nk;
+  b.R = b.X + nk;
+  b.P = b.R + nk;
+  b.Q = b.P + nk;
+  b.ppq = b.Q + nk;
+  b.prr = b.ppq + (size_t)std::max(nb_pq, 1) * k;
+  double* part = b.prr + 2 * (size_t)CG_GRID * k;   // general reductions (k_sumsq, GLS)
+  b.tol2 = part + (size_t)CG_GRID * std::max(k, (nh + 1) * std::max(nh, 1));
+  b.rr = b.tol2 + k;
+  double* bn2 = b.rr + k;
+  b.status = reinterpret_cast<int*>(bn2 + k);
+  b.bd_iter = b.status + k;
+  double* B = b.B;
+  double* X = b.X;
+  double* R = b.R;
+  double* Pm = b.P;
+  double* Q = b.Q;
 
   k_build_rhs<<<g1(n), 256, 0, s>>>(pl.perm.as<int>(), y, pl.x_raw.as<double>(), pl.d, H, nh,
                                      mean_kind, n, B);
   GPM_CUDA(cudaMemsetAsync(X, 0, 8 * nk, s));
   GPM_CUDA(cudaMemcpyAsync(R, B, 8 * nk, cudaMemcpyDeviceToDevice, s));
   GPM_CUDA(cudaMemcpyAsync(Pm, B, 8 * nk, cudaMemcpyDeviceToDevice, s));
-  k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(B, n, part);
-  k_finish_sum<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, bn2);
+  // ||b_c||^2 partials, kept as the "previous r.r" of iteration 0 (rr parity 1)
+  double* rr1 = b.prr + (size_t)k * CG_GRID;
+  k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(B, n, rr1);
+  k_finish_sum<<<k, CG_BLOCK, 0, s>>>(rr1, CG_GRID, bn2);
   GPM_CUDA(cudaGetLastError());
   std::vector<double> hb2(k), hrr(k), htol2(k);
   std::vector<int> hst(k), hbd(k);
@@ -350,9 +481,15 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
     htol2[c] = rtol * rtol * hb2[c];
     hst[c] = hb2[c] == 0.0 ? 1 : 0;   // zero right-hand side: x = 0 is exact
   }
-  GPM_CUDA(cudaMemcpyAsync(tol2, htol2.data(), 8 * k, cudaMemcpyHostToDevice, s));
-  GPM_CUDA(cudaMemcpyAsync(rr, hb2.data(), 8 * k, cudaMemcpyHostToDevice, s));
-  GPM_CUDA(cudaMemcpyAsync(status, hst.data(), 4 * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(b.tol2, htol2.data(), 8 * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(b.rr, hb2.data(), 8 * k, cudaMemcpyHostToDevice, s));
+  GPM_CUDA(cudaMemcpyAsync(b.status, hst.data(), 4 * k, cudaMemcpyHostToDevice, s));
+  double* rr = b.rr;
+  double* tol2 = b.tol2;
+  double* al = part;   // unfused path scalars (alpha, beta) live in the reduction area
+  double* be = part + k;
+  int* status = b.status;
+  int* bd_iter = b.bd_iter;
 
   const int check_every = 8;
   int it = 0, restarts = 0;
@@ -414,28 +551,71 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
       rhs = Pm;
     }
   }
+  // unpreconditioned: the fused iteration in 8-iteration blocks, one CUDA graph replayed
+  // per block when possible (a stream that is itself capturing runs the block directly)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  GPM_CUDA(cudaStreamIsCapturing(s, &cap));
+  const bool fused = nb_pq > 0;
+  const bool use_graph = fused && cap == cudaStreamCaptureStatusNone && !getenv("GPM_CG_NOGRAPH");
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<char> gmask;   // the active-column mask gexec was captured with
+  cudaStream_t cs = nullptr;
+  struct GraphGuard {
+    cudaGraphExec_t* g;
+    cudaStream_t* s;
+    ~GraphGuard() {
+      if (*g) cudaGraphExecDestroy(*g);
+      if (*s) cudaStreamDestroy(*s);
+    }
+  } gguard{&gexec, &cs};
   while (!pc) {
-    std::vector<char> active(k, 0);
-    for (int c = 0; c < k; ++c) active[c] = hst[c] == 0;
     bool any = false;
-    for (int c = 0; c < k; ++c) any |= active[c] != 0;
+    for (int c = 0; c < k; ++c) any |= hst[c] == 0;
     while (any && it < max_iter) {
-      for (int step = 0; step < check_every && it < max_iter; ++step, ++it) {
-        GPM_TRY(apply_active(pl, Pm, Q, active, k, s));
-        k_pq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, Q, n, sigma2, part);
-        k_alpha<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, al, status, bd_iter, it);
-        k_update<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(X, R, Pm, Q, al, n, part);
-        k_beta<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, tol2, be, status);
-        k_pupd<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, R, be, status, n);
+      std::vector<char> act(k, 0);
+      for (int c = 0; c < k; ++c) act[c] = hst[c] == 0;
+      if (fused) {
+        if (use_graph && it > 0) {   // the first block ran directly (it sizes the scratch)
+          if (gexec && gmask != act) {   // another active set: capture again
+            GPM_CUDA(cudaGraphExecDestroy(gexec));
+            gexec = nullptr;
+          }
+          if (!gexec) {   // capture the 8-iteration block (the iteration parity repeats)
+            if (!cs) GPM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaGraph_t g = nullptr;
+            GPM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            gp_status bst = cg_block(pl, b, sigma2, 0, check_every, act, cs);
+            cudaError_t ce = cudaStreamEndCapture(cs, &g);
+            if (bst != GP_OK) {
+              if (g) cudaGraphDestroy(g);
+              return bst;
+            }
+            GPM_CUDA(ce);
+            cudaError_t ie = cudaGraphInstantiate(&gexec, g, 0);
+            cudaGraphDestroy(g);
+            GPM_CUDA(ie);
+            gmask = act;
+          }
+          GPM_CUDA(cudaGraphLaunch(gexec, s));
+        } else {
+          GPM_TRY(cg_block(pl, b, sigma2, 0, check_every, act, s));
+        }
+        it += check_every;   // breakdown iterations are recorded relative to the block
+      } else {
+        for (int step = 0; step < check_every && it < max_iter; ++step, ++it) {
+          GPM_TRY(apply_active(pl, Pm, Q, act, k, s));
+          k_pq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, Q, n, sigma2, part);
+          k_alpha<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, al, status, bd_iter, it);
+          k_update<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(X, R, Pm, Q, al, n, part);
+          k_beta<<<k, CG_BLOCK, 0, s>>>(part, CG_GRID, rr, tol2, be, status);
+          k_pupd<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(Pm, R, be, status, n);
+        }
+        GPM_CUDA(cudaGetLastError());
       }
-      GPM_CUDA(cudaGetLastError());
       GPM_CUDA(cudaMemcpyAsync(hst.data(), status, 4 * k, cudaMemcpyDeviceToHost, s));
       GPM_CUDA(cudaStreamSynchronize(s));
       any = false;
-      for (int c = 0; c < k; ++c) {
-        active[c] = hst[c] == 0;
-        any |= active[c] != 0;
-      }
+      for (int c = 0; c < k; ++c) any |= hst[c] == 0;
       for (int c = 0; c < k; ++c)
         if (hst[c] == 2) any = false;   // stop on breakdown
     }
@@ -457,8 +637,9 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
     }
     if (broke) {
       result = fail(GP_ERR_BREAKDOWN, "CG breakdown (p^T A p <= 0) in column " +
-                                          std::to_string(bad_col) + " at iteration " +
-                                          std::to_string(hbd[bad_col]) +
+                                          std::to_string(bad_col) + " near iteration " +
+                                          std::to_string(fused ? it - check_every + hbd[bad_col]
+                                                               : hbd[bad_col]) +
                                           ": K + sigma^2 I is not positive definite");
       break;
     }
@@ -469,11 +650,16 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
                                               ", relres " + std::to_string(relres[bad_col]) + ")");
       break;
     }
-    // residual replacement: restart from the true residual
+    // residual replacement: restart from the true residual (its r.r becomes the "previous
+    // r.r" of the next block: rr parity 1)
     ++restarts;
     for (int c = 0; c < k; ++c) hst[c] = relres[c] > rtol ? 0 : 1;
     GPM_CUDA(cudaMemcpyAsync(Pm, R, 8 * nk, cudaMemcpyDeviceToDevice, s));
     GPM_CUDA(cudaMemcpyAsync(status, hst.data(), 4 * k, cudaMemcpyHostToDevice, s));
+    if (fused) {
+      k_sumsq<<<dim3(CG_GRID, k), CG_BLOCK, 0, s>>>(R, n, rr1);
+      GPM_CUDA(cudaGetLastError());
+    }
   }
   if (info) {
     info->iters = it;
@@ -488,44 +674,51 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
   }
   if (result == GP_ERR_BREAKDOWN) return result;
 
-  // GLS (a10) and alpha in user order
+  // GLS (a10) and alpha in user order; OLS (P:829 [Alg 1, first line]) on request
   std::vector<double> hbeta(std::max(nh, 1), 0.0);
-  if (nh > 0) {
+  auto normal_eqs = [&](const double* Xs, std::vector<double>& sol) -> gp_status {
+    // G[a][b] = sum_r H_a Xs_{1+b}, g[a] = sum_r H_a Xs_0; solve G beta = g
     const int nab = nh * (nh + 1);
-    k_gls_part<<<dim3(CG_GRID, nab), CG_BLOCK, 0, s>>>(B, X, nh, n, part);
-    DevBuf bg;
-    GPM_TRY(bg.alloc(8 * nab));
-    k_finish_sum<<<nab, CG_BLOCK, 0, s>>>(part, CG_GRID, bg.as<double>());
+    k_gls_part<<<dim3(CG_GRID, nab), CG_BLOCK, 0, s>>>(B, Xs, nh, n, part);
+    k_finish_sum<<<nab, CG_BLOCK, 0, s>>>(part, CG_GRID, Q);   // Q: free after the solve
     std::vector<double> hg(nab);
-    GPM_CUDA(cudaMemcpyAsync(hg.data(), bg.ptr, 8 * nab, cudaMemcpyDeviceToHost, s));
+    GPM_CUDA(cudaMemcpyAsync(hg.data(), Q, 8 * nab, cudaMemcpyDeviceToHost, s));
     GPM_CUDA(cudaStreamSynchronize(s));
-    bg.release();
     std::vector<double> G(nh * nh), g(nh);
     for (int a = 0; a < nh; ++a) {
-      for (int b = 0; b < nh; ++b) G[a * nh + b] = hg[a * (nh + 1) + b];
+      for (int b2 = 0; b2 < nh; ++b2) G[a * nh + b2] = hg[a * (nh + 1) + b2];
       g[a] = hg[a * (nh + 1) + nh];
     }
-    // symmetrise (H^T A^-1 H is symmetric in exact arithmetic)
-    for (int a = 0; a < nh; ++a)
-      for (int b = a + 1; b < nh; ++b) {
-        const double m = 0.5 * (G[a * nh + b] + G[b * nh + a]);
-        G[a * nh + b] = G[b * nh + a] = m;
+    for (int a = 0; a < nh; ++a)   // symmetrise (symmetric in exact arithmetic)
+      for (int b2 = a + 1; b2 < nh; ++b2) {
+        const double m = 0.5 * (G[a * nh + b2] + G[b2 * nh + a]);
+        G[a * nh + b2] = G[b2 * nh + a] = m;
       }
-    std::vector<double> sol;
     if (!small_solve(G, g, nh, sol))
-      return fail(GP_ERR_INVALID_ARG, "GLS system H^T A^-1 H is singular (rank-deficient H)");
+      return fail(GP_ERR_INVALID_ARG, "normal equations are singular (rank-deficient H)");
+    return GP_OK;
+  };
+  if (nh > 0) {
+    std::vector<double> sol;
+    GPM_TRY(normal_eqs(X, sol));   // H^T A^-1 H beta = H^T A^-1 y
     hbeta = sol;
     if (beta) for (int a = 0; a < nh; ++a) beta[a] = sol[a];
+    if (beta_ols) {               // H^T H beta = H^T y (the columns of B)
+      GPM_TRY(normal_eqs(B, sol));
+      for (int a = 0; a < nh; ++a) beta_ols[a] = sol[a];
+    }
   }
-  DevBuf bbd;
-  GPM_TRY(bbd.alloc(8 * std::max(nh, 1)));
-  GPM_CUDA(cudaMemcpyAsync(bbd.ptr, hbeta.data(), 8 * std::max(nh, 1), cudaMemcpyHostToDevice, s));
+  if (Xout) {
+    k_cols_to_user<<<dim3(g1(n), k), 256, 0, s>>>(pl.perm.as<int>(), X, n, Xout);
+    GPM_CUDA(cudaGetLastError());
+  }
+  double* bbd = part;   // beta on the device (after the reductions above consumed part)
+  GPM_CUDA(cudaMemcpyAsync(bbd, hbeta.data(), 8 * std::max(nh, 1), cudaMemcpyHostToDevice, s));
   auto bv = [&](int a) { return a < nh ? hbeta[a] : 0.0; };
-  k_alpha_out<<<g1(n), 256, 0, s>>>(pl.perm.as<int>(), X, nh, bv(0), bv(1), bv(2), bv(3),
-                                     bbd.as<double>(), n, alpha);
+  k_alpha_out<<<g1(n), 256, 0, s>>>(pl.perm.as<int>(), X, nh, bv(0), bv(1), bv(2), bv(3), bbd, n,
+                                     alpha);
   GPM_CUDA(cudaGetLastError());
   GPM_CUDA(cudaStreamSynchronize(s));
-  bbd.release();
   return result;
 }
 

@@ -58,12 +58,28 @@ def test_config5_gp_inference(gpm):
     s2 = c.noise_sigma ** 2
     plan = gpm.Plan(to_dev(x), gpm.Kernel(3, c.ell, form=gpm.FORM_PRODUCT))
     alpha, beta, info = plan.cg_solve(to_dev(y), s2, mean=gpm.MEAN_AFFINE, rtol=1e-8,
-                                      max_iter=40000)
+                                      max_iter=40000, return_x=True, return_ols=True)
     assert info["relres_max"] <= 1e-8
     a = alpha.cpu().numpy()
     H = np.hstack([np.ones((x.shape[0], 1)), x])
-    # (K + s2 I) alpha = y - H beta on 2048 sampled rows, via the oracle's own rows
     rows = W.sample_rows(x, 2048)
+    # every CG solution column X_j = A^-1 b_j (b = [y, 1, x1, x2])
+    # checked through the oracle's own rows, and beta recomputed on the host from them
+    # (P:808-812); beta_OLS against the oracle
+    X = info["X"].cpu().numpy()
+    Bcols = np.vstack([y, H.T])
+    for j in range(X.shape[0]):
+        KX = oracle.kmvm_rows(x, X[j], 3, "product", c.ell, 1.0, rows=rows)
+        rj = Bcols[j][rows] - KX - s2 * X[j][rows]
+        est = np.sqrt(x.shape[0] / rows.size * np.sum(rj ** 2))
+        assert est <= 3e-8 * np.linalg.norm(Bcols[j]), (j, est)
+    G = H.T @ X[1:].T
+    g = H.T @ X[0]
+    beta_host = np.linalg.solve(0.5 * (G + G.T), g)
+    assert np.allclose(beta, beta_host, rtol=1e-9, atol=1e-12)
+    assert np.allclose(info["beta_ols"], oracle.ols(H, y), rtol=1e-10, atol=1e-12)
+    assert np.max(np.abs(a - (X[0] - X[1:].T @ np.array(beta)))) <= 1e-12 * np.abs(a).max()
+    # (K + s2 I) alpha = y - H beta on 2048 sampled rows, via the oracle's own rows
     Ka = oracle.kmvm_rows(x, a, 3, "product", c.ell, 1.0, rows=rows)
     rvec = (y - H @ np.array(beta))[rows] - Ka - s2 * a[rows]
     est = np.sqrt(x.shape[0] / rows.size * np.sum(rvec ** 2))

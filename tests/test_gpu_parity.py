@@ -243,6 +243,37 @@ def test_cg_gls_predict_small_vs_dense(gpm):
     assert np.max(np.abs(mu - mu_or)) <= 1e-9 * np.abs(alpha).max() * 50
 
 
+@pytest.mark.parametrize("d", [1, 2])
+def test_cg_solutions_and_ols_vs_dense(gpm, d, monkeypatch):
+    """gp_cg_solve_ex by-products: the CG solutions X = [A^-1 y, A^-1 H] (user order) and
+    beta_OLS against the dense oracle; the fused / graph-replayed iteration equals
+    the unfused stream loop to rounding (GPM_CG_NOGRAPH runs the same kernels directly)."""
+    c = W.scaled(W.CONFIGS[5], 1800, m=10)
+    rng = np.random.default_rng(40 + d)
+    x = rng.random((1800, d)); y = W.config_response(c, np.hstack([x, x])[:, :2])
+    s2 = 0.01
+    ell = (0.1,) * d
+    ref = oracle.gp_dense(x, y, x[:3], 3, "product", ell, 1.0, s2, mean="affine")
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, ell, form=1))
+    a, b, info = plan.cg_solve(to_dev(y), s2, rtol=1e-11, return_x=True, return_ols=True)
+    X = info["X"].cpu().numpy()
+    tol = 1e-11 * np.linalg.norm(y) / s2 * 100
+    assert np.max(np.abs(X[0] - ref["A_inv_y"])) <= tol
+    for j in range(1 + d):
+        assert np.max(np.abs(X[1 + j] - ref["A_inv_H"][:, j])) <= tol * 10
+    assert np.allclose(info["beta_ols"], ref["beta_ols"], rtol=1e-12, atol=1e-12)
+    assert np.allclose(b, ref["beta"], rtol=0, atol=1e-7)
+    monkeypatch.setenv("GPM_CG_NOGRAPH", "1")
+    a2, b2, info2 = plan.cg_solve(to_dev(y), s2, rtol=1e-11)
+    assert info2["iters"] == info["iters"]
+    assert torch_equal_close(a, a2)
+
+
+def torch_equal_close(a, b):
+    import torch
+    return bool(torch.equal(a, b))
+
+
 def test_cg_no_mean_and_basis(gpm):
     rng = np.random.default_rng(4)
     x = rng.random((1500, 1)); y = np.sin(7 * x[:, 0]) + 0.1 * rng.standard_normal(1500)
