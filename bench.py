@@ -576,7 +576,36 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
                              "relres_max": info["relres_max"], "rhs": 4, "beta": beta,
                              "ms_per_iter": cg_s / max(info["iters"], 1) * 1e3,
                              "preconditioner": "none (Alg 2 with s_P = I)",
+                             "iteration": ("fused (apply epilogue q = Kp + s2 p with p.q partials, "
+                                           "2 vector kernels), 8-iteration CUDA graphs"),
                              "clocks": cg_clock.summary()}
+        # per-iteration split: the 4-column rank-order apply alone (CUDA graph of 20) vs
+        # the whole iteration
+        P4 = torch.randn((4, c5.n), dtype=torch.float64, device=dev)
+        Q4 = torch.empty_like(P4)
+        lib5 = g.load_library()
+        cs5 = torch.cuda.Stream()
+        def ap5(k, st=cs5):
+            assert lib5.gp_kmvm_rank(plan._h, ctypes.c_void_p(P4.data_ptr()), 4,
+                                     ctypes.c_void_p(Q4.data_ptr()), ctypes.c_void_p(st.cuda_stream)) == 0
+        r5 = time_graph(lambda st: (lambda k: ap5(k, st)), 20, 3, 1, reps=3)
+        # the same 4 columns through 400 CG iterations (all active: stopped by max_iter)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        try:
+            plan.cg_solve(yt, c5.noise_sigma ** 2, mean=g.MEAN_AFFINE, rtol=1e-8, max_iter=400)
+        except g.GPError:
+            pass
+        torch.cuda.synchronize()
+        it4_ms = (time.perf_counter() - t0) / 400 * 1e3
+        if r5:
+            apply_ms = r5[0] / 20 * 1e3
+            out["config5_cg"]["split_4_active_columns"] = {
+                "iteration_ms": it4_ms, "apply_ms": apply_ms,
+                "vector_ops_frac": max(0.0, (it4_ms - apply_ms) / it4_ms),
+                "note": ("400 iterations with all 4 columns active (max_iter stop; includes "
+                         "setup and the final true-residual apply) vs the 4-column rank-order "
+                         "apply alone in a CUDA graph")}
         flop, peak = ncu_fp64("config5_d2_prod32_nrhs4")
         if flop:   # one 4-column apply per iteration dominates (vector updates are O(N))
             tf = flop * info["iters"] / cg_s / 1e12
@@ -620,7 +649,8 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
             ts.append(time.perf_counter() - t0)
         out["config5_predict"] = {"predict_s": ts[0], "predict_s_repeat": min(ts[1:]),
                                   "m": int(z5.shape[0]),
-                                  "note": "gp_predict builds the union x u z structure per call"}
+                                  "note": ("the first gp_predict builds the union x u z structure; "
+                                           "repeats with the same z reuse it (bitwise check)")}
         pc.close()
         plan.close()
     return out

@@ -317,8 +317,10 @@ GP_API gp_status gp_fit(const double *x, int64_t n, int d, const gp_kernel *k0, 
  *            out = K_zx alpha exactly;
  *   Hz     : for a basis mean, the m x L column-major basis at z (device) and
  *            beta of length L; pass NULL and L = 0 for the affine mean.
- *   out    : m (device).  Builds and frees a union structure internally (for repeated
- *            predictions at the same z, gp_kzx_setup once + gp_kzx reuse it). */
+ *   out    : m (device).  The union structure x U z is built on the first call and cached
+ *            on the plan: a later call with the same z pointer, the same m and bitwise-equal
+ *            contents (compared on the device, one pass over z) reuses it (SURVEY §8(b)
+ *            convention 4); any other z replaces the cache.  Synchronises `stream`. */
 GP_API gp_status gp_predict(gp_plan p, const double *z, int64_t m, const double *alpha,
                      const double *beta, const double *Hz, int L, double *out, void *stream);
 

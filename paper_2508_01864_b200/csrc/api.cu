@@ -335,8 +335,8 @@ void gp_precond_destroy(gp_precond pc) {
   delete pc;
   // a plan whose gp_destroy came first is freed with its last preconditioner
   if (owner && --owner->live_preconds == 0 && owner->destroy_pending) {
-    plan_free(owner->pl);
-    delete owner;
+    owner->destroy_pending = false;
+    gp_destroy(owner);
   }
 }
 
@@ -430,18 +430,34 @@ gp_status gp_predict(gp_plan p, const double* z, int64_t m, const double* alpha,
                      const double* beta, const double* Hz, int L, double* out, void* stream) {
   if (!p || !z || !alpha || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (Hz && (L < 1 || !beta)) return fail(GP_ERR_INVALID_ARG, "basis mean needs beta and L >= 1");
-  gp_cross c = nullptr;
-  GPM_TRY(gp_kzx_setup(p, z, m, stream, &c));
-  gp_status st = gp_kzx(c, alpha, 1, out, stream);
-  if (st == GP_OK && beta)
-    st = launch_affine_epilogue(z, m, p->pl.d, beta, Hz, L, out,
-                                static_cast<cudaStream_t>(stream));
-  if (st == GP_OK) {
-    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) st = fail(GP_ERR_CUDA, cudaGetErrorString(e));
+  if (m < 1) return fail(GP_ERR_INVALID_ARG, "m must be >= 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t zn = (size_t)m * p->pl.d;
+  bool reuse = false;
+  if (p->pred_cross && p->pred_z == z && p->pred_m == m) {   // same query set?
+    bool differs = true;
+    GPM_TRY(device_differs(z, p->pred_zcopy.as<double>(), (int64_t)zn, p->pred_flag.as<int>(), s,
+                           &differs));
+    reuse = !differs;
   }
-  gp_kzx_destroy(c);
-  return st;
+  if (!reuse) {
+    if (p->pred_cross) {
+      gp_kzx_destroy(p->pred_cross);
+      p->pred_cross = nullptr;
+    }
+    gp_cross c = nullptr;
+    GPM_TRY(gp_kzx_setup(p, z, m, stream, &c));
+    p->pred_cross = c;
+    p->pred_z = z;
+    p->pred_m = m;
+    if (p->pred_zcopy.bytes < sizeof(double) * zn) GPM_TRY(p->pred_zcopy.alloc(sizeof(double) * zn));
+    if (!p->pred_flag.bytes) GPM_TRY(p->pred_flag.alloc(16));
+    GPM_CUDA(cudaMemcpyAsync(p->pred_zcopy.ptr, z, sizeof(double) * zn, cudaMemcpyDeviceToDevice, s));
+  }
+  GPM_TRY(gp_kzx(p->pred_cross, alpha, 1, out, stream));
+  if (beta) GPM_TRY(launch_affine_epilogue(z, m, p->pl.d, beta, Hz, L, out, s, p->pred_beta));
+  GPM_CUDA(cudaStreamSynchronize(s));
+  return GP_OK;
 }
 
 gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
@@ -512,6 +528,10 @@ void gp_destroy(gp_plan p) {
     p->destroy_pending = true;
     return;
   }
+  if (p->pred_cross) gp_kzx_destroy(p->pred_cross);
+  p->pred_zcopy.release();
+  p->pred_flag.release();
+  p->pred_beta.release();
   plan_free(p->pl);
   delete p;
 }

@@ -204,12 +204,22 @@ gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, cons
                    gp_cg_info* info, cudaStream_t s, Precond* pc = nullptr,
                    double* beta_ols = nullptr, double* Xout = nullptr);
 gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
-                                 const double* Hz, int Lb, double* out, cudaStream_t s);
+                                 const double* Hz, int Lb, double* out, cudaStream_t s,
+                                 DevBuf& beta_dev);
+gp_status device_differs(const double* a, const double* b, int64_t m, int* flag, cudaStream_t s,
+                         bool* out);
 
 }  // namespace gpm
 
+struct gp_cross_s;
 struct gp_plan_s {
   gpm::Plan pl;
+  // gp_predict cache: the union structure x U z of the last query set, reused while the
+  // same z pointer and m come back with bitwise-equal contents (checked on the device)
+  gp_cross_s* pred_cross = nullptr;
+  const double* pred_z = nullptr;
+  int64_t pred_m = 0;
+  gpm::DevBuf pred_zcopy, pred_flag, pred_beta;
   int live_preconds = 0;     // preconditioners built on this plan (they point into pl)
   bool destroy_pending = false;   // gp_destroy called while preconditioners were alive
 };

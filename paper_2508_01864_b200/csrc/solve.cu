@@ -382,15 +382,35 @@ static gp_status apply_active(Plan& pl, const double* P, double* Q, const std::v
 }
 
 gp_status launch_affine_epilogue(const double* z, int64_t m, int d, const double* beta_host,
-                                 const double* Hz, int Lb, double* out, cudaStream_t s) {
+                                 const double* Hz, int Lb, double* out, cudaStream_t s,
+                                 DevBuf& bd) {
   const int nb = Hz ? Lb : 1 + d;
-  DevBuf bd;
-  GPM_TRY(bd.alloc(sizeof(double) * nb));
+  if (bd.bytes < sizeof(double) * nb) GPM_TRY(bd.alloc(sizeof(double) * 16));
   GPM_CUDA(cudaMemcpyAsync(bd.ptr, beta_host, sizeof(double) * nb, cudaMemcpyHostToDevice, s));
   k_mean_epi<<<g1(m), 256, 0, s>>>(z, m, d, Hz, Lb, bd.as<double>(), out);
   GPM_CUDA(cudaGetLastError());
+  return GP_OK;   // the host beta is copied: the caller synchronises before returning
+}
+
+namespace {
+__global__ void k_differs(const double* __restrict__ a, const double* __restrict__ b, int64_t m,
+                          int* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (__double_as_longlong(a[i]) != __double_as_longlong(b[i])) *flag = 1;
+}
+}  // namespace
+
+// 1 when the m doubles at a and b differ bitwise (synchronises s; flag: 4 device bytes)
+gp_status device_differs(const double* a, const double* b, int64_t m, int* flag, cudaStream_t s,
+                         bool* out) {
+  GPM_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  k_differs<<<g1(m), 256, 0, s>>>(a, b, m, flag);
+  GPM_CUDA(cudaGetLastError());
+  int h = 0;
+  GPM_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   GPM_CUDA(cudaStreamSynchronize(s));
-  bd.release();
+  *out = h != 0;
   return GP_OK;
 }
 

@@ -407,3 +407,26 @@ def test_torch_allocator_hook(gpm):
         plan.close()
     finally:
         gpm.use_torch_allocator(False)
+
+
+def test_predict_union_cache(gpm):
+    """gp_predict caches the x U z structure (SURVEY §8(b) convention 4): a repeat call with
+    the same z is bitwise equal to the first; z changed in place (same pointer, same m) is
+    detected and gives the oracle's answer for the new points; a new m rebuilds."""
+    import torch
+    rng = np.random.default_rng(11)
+    x = rng.random((3000, 2)); a = rng.standard_normal(3000)
+    z = torch.from_numpy(rng.random((400, 2))).cuda()
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.2), form=1))
+    ad = to_dev(a)
+    m1 = plan.predict(z, ad, [0.5, 1.0, -1.0])
+    m2 = plan.predict(z, ad, [0.5, 1.0, -1.0])
+    assert torch.equal(m1, m2)
+    z.mul_(0.5)   # in place: same pointer and m, new contents
+    m3 = plan.predict(z, ad, None).cpu().numpy()
+    zh = z.cpu().numpy()
+    ref, ab = oracle.kzx_rows(x, a, zh, 3, "product", (0.1, 0.2), 1.0, return_abs=True)
+    assert np.max(np.abs(m3 - ref)) <= 1e-9 * ab.max() * np.abs(a).max()
+    m4 = plan.predict(z[:100].contiguous(), ad, None).cpu().numpy()
+    assert np.max(np.abs(m4 - ref[:100])) <= 1e-9 * ab.max() * np.abs(a).max()
+    plan.close()
