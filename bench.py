@@ -50,11 +50,12 @@ def peaks():
         return FALLBACK_HBM, "fallback"
 
 
-def d1_kernel_name(shape):
-    """Name of the d = 1 kernel (nu = 5/2, user order) of a plan's thread-block shape
-    (gp_plan_set_option option 1)."""
-    shapes = {0: "k_d1_lpc<2,0,512,15,user>", 1: "k_d1_lpc<2,0,384,19,user>",
-              2: "k_d1_lpc<2,0,256,27,user>"}
+def d1_kernel_name(shape, user=True):
+    """Name of the d = 1 kernel (nu = 5/2) of a plan's thread-block shape (gp_plan_set_option
+    option 1): k_d1_lpc<P, KIND, threads, segments, points per segment, user order>."""
+    u = "user" if user else "rank"
+    shapes = {0: f"k_d1_lpc<2,0,256,3,9,{u}>", 1: f"k_d1_lpc<2,0,256,3,10,{u}>",
+              2: f"k_d1_lpc<2,0,224,3,11,{u}>"}
     return shapes.get(shape, f"d1 shape {shape}")
 
 
@@ -423,21 +424,23 @@ def run_ours(args, ws, rank, local):
     if not args.no_extras:
         # nu = 3/2 on the same config
         sx = min(args.steps, 1000)
-        p3, _, smax3, _, m3, _, _, _ = measure(3, sx, 3)
+        p3, _, smax3, s3, m3, _, _, t3 = measure(3, sx, 3)
+        l3 = s3 / sx if t3["graph"] else m3
         extras["config2_d1_nu32"] = {"api": "gp_kmvm", "mvm_per_s": sum_over_ranks(sx, ws) / smax3,
-                                     "launch_ms_mean": m3 * 1e3,
-                                     "hbm_gbs": p3.model_bytes / m3 / 1e9,
-                                     "frac_hbm": p3.model_bytes / m3 / 1e9 / hbm}
+                                     "launch_ms_mean": l3 * 1e3,
+                                     "hbm_gbs": p3.model_bytes / l3 / 1e9,
+                                     "frac_hbm": p3.model_bytes / l3 / 1e9 / hbm}
         p3.close()
         # the same apply in the plan's stored order (the operator inside CG: no gather/scatter)
         for nu2 in (5, 3):
             to_rank = lambda pl: torch.stack([pl.to_rank(V[i]) for i in range(nv)])
-            pr, _, smr, _, mr, _, _, _ = measure(nu2, sx, 3, vin=to_rank, rank_order=True)
+            pr, _, smr, sr, mr, _, _, tr = measure(nu2, sx, 3, vin=to_rank, rank_order=True)
             rb = n * 24   # t + v + out, all coalesced
+            lr = sr / sx if tr["graph"] else mr   # per launch over the graph replay
             extras[f"config2_d1_nu{nu2}2_rank_order"] = {
                 "api": "gp_kmvm_rank", "mvm_per_s": sum_over_ranks(sx, ws) / smr,
-                "launch_ms_mean": mr * 1e3, "model_bytes": rb, "hbm_gbs": rb / mr / 1e9,
-                "frac_hbm": rb / mr / 1e9 / hbm}
+                "launch_ms_mean": lr * 1e3, "launch_ms_isolated_mean": mr * 1e3,
+                "model_bytes": rb, "hbm_gbs": rb / lr / 1e9, "frac_hbm": rb / lr / 1e9 / hbm}
             pr.close()
         # f1: batched multi-RHS applies (one gp_kmvm call with nb fresh vectors)
         for nb, rank_order in ((16, False), (16, True)):
@@ -466,13 +469,67 @@ def run_ours(args, ws, rank, local):
                            "us_per_mvm": per * 1e6, "hbm_gbs": bpm / per / 1e9,
                            "frac_hbm": bpm / per / 1e9 / hbm}
             pb.close()
+        extras["permutation_floor"] = permutation_floor(n, dev)
         extras.update(extra_configs(g, dev, stream, ws, rank, hbm, args))
     if extras:
         line["extra"] = extras
+        rk = extras.get("config2_d1_nu52_rank_order")
+        if rk:   # the CG operator: same kernel, vectors in the stored order (24 B/pt)
+            line["roofline_rank_order"] = {
+                "bound": "hbm", "kernel": d1_kernel_name(0, user=False), "achieved": rk["hbm_gbs"],
+                "peak": hbm, "unit": "GB/s", "frac": rk["frac_hbm"],
+                "algorithmic_bytes_per_launch": rk["model_bytes"], "launch_ms_mean": rk["launch_ms_mean"]}
+        bt = extras.get("config2_d1_nu52_batched16_rank_order")
+        if bt:
+            line["roofline_batched16_rank_order"] = {
+                "bound": "hbm", "achieved": bt["hbm_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": bt["frac_hbm"], "us_per_mvm": bt["us_per_mvm"], "nrhs_per_call": 16}
+        pf = extras.get("permutation_floor")
+        if pf:
+            line["user_order_floor"] = pf
 
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, two_nu, args.cpu_rows)
     return line
+
+
+def permutation_floor(n, dev):
+    """What the user-order permutations alone cost (profiles/r02_user_order_floor.md): a
+    random gather v[p] and scatter o[p] = u of n doubles with PyTorch's own kernels (no
+    arithmetic), back to back in one CUDA graph, against the 50 % budget of the whole
+    apply (28 B/pt / (0.5 x peak))."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(7)
+    p = torch.randperm(n, generator=g).to(dev)
+    v = torch.randn(n, dtype=torch.float64, device=dev)
+    o = torch.empty_like(v)
+    u = torch.empty_like(v)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            torch.index_select(v, 0, p, out=u)
+            o.index_copy_(0, p, u)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    R = 50
+    with torch.cuda.graph(graph, stream=s):
+        for _ in range(R):
+            torch.index_select(v, 0, p, out=u)
+            o.index_copy_(0, p, u)
+    with torch.cuda.stream(s):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        graph.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / R * 1e3
+    hbm, _ = peaks()
+    return {"gather_plus_scatter_us": us, "budget_50pct_us": 28 * n / (0.5 * hbm * 1e9) * 1e6,
+            "how": "torch index_select + index_copy_ of 1e6 doubles through a random permutation, CUDA graph of 50",
+            "evidence": "profiles/r02_user_order_floor.md (tools/micro/perm_floor.cu: 9.25 us L2-resident, ncu L2 requests)"}
 
 
 def ncu_fp64(key):

@@ -471,7 +471,7 @@ gp_status gp_plan_query(gp_plan p, int what, int64_t* value) {
     case 4: *value = pl.launches_per_apply; break;
     case 5: *value = apply_model_bytes(pl); break;
     case 6: *value = pl.d == 1 ? pl.d1_path : 0; break;
-    case 7: *value = pl.d == 1 ? pl.d1_shape : -1; break;
+    case 7: *value = pl.d == 1 ? pl.d1_shape_used : -1; break;
     default: {
       // debug (GPM_D1_TIMING, d = 1 single-chunk path, last launch): what = 100 + slot:
       // mean over warps of stamp[slot] - stamp[0] (SM cycles); 200 + slot: the max

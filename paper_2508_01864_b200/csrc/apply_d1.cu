@@ -832,18 +832,24 @@ gp_status d1_prepare(Plan& pl) {
   GPM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   GPM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return fail(GP_ERR_UNSUPPORTED, "device does not support cooperative launch");
-  if (pl.d1_shape < 0 || pl.d1_shape >= NSHAPE) pl.d1_shape = g_default;
-  const Shape& sh = g_shapes[pl.d1_shape];
-  int occ = 0;
-  GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh.fn[1][2], sh.block, sh.smem[1]));
-  const int64_t cap = (int64_t)sh.block * sh.items;
-  const int gmax = std::min(occ * nsm, 160);   // s_tl holds 161 chunk ends
-  if (pl.d1_force != 3 && gmax > 0) {
+  // shape: the requested one, or (auto) the default and, above its capacity, the larger
+  // ones (shape 1: #SMs x 7680 points, N = 2^20 in one chunk per CTA)
+  const int first = pl.d1_shape >= 0 && pl.d1_shape < NSHAPE ? pl.d1_shape : g_default;
+  const int last = pl.d1_shape >= 0 && pl.d1_shape < NSHAPE ? pl.d1_shape : NSHAPE - 1;
+  for (int shp = first; shp <= last && pl.d1_force != 3; ++shp) {
+    if (pl.d1_shape < 0 && shp != first && shp == 2) break;   // auto: shapes 0 and 1 only
+    const Shape& sh = g_shapes[shp];
+    int occ = 0;
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sh.fn[1][2], sh.block, sh.smem[1]));
+    const int64_t cap = (int64_t)sh.block * sh.items;
+    const int gmax = std::min(occ * nsm, 160);   // s_tl holds 161 chunk ends
+    if (gmax <= 0) continue;
     // grid: #SMs CTAs, fewer for small n (>= 1024 points per chunk); chunk a multiple of 4
     int64_t g = std::min<int64_t>(gmax, std::max<int64_t>(1, (pl.n + 1023) / 1024));
     int64_t chunk = ((pl.n + g - 1) / g + 3) & ~int64_t(3);
     g = (pl.n + chunk - 1) / chunk;   // every CTA owns >= 1 point
     if (chunk <= cap && g <= gmax) {
+      pl.d1_shape_used = shp;
       pl.d1_grid = (int)g;
       pl.d1_chunk = chunk;
       pl.d1_path = 1;
@@ -883,7 +889,7 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
     if (cg_part) return fail(GP_ERR_INVALID_ARG, "internal: no CG epilogue on the d=1 path 3");
     return db_launch(pl, v, out, nrhs, user_order, s, kind);
   }
-  const Shape& sh = g_shapes[pl.d1_shape];
+  const Shape& sh = g_shapes[pl.d1_shape_used];
   lpc::Args a;
   a.ts = pl.t.as<double>();
   a.ends = pl.d1ends.as<double>();

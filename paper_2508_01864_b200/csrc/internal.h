@@ -131,7 +131,8 @@ struct Plan {
   DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
   int near_lb2 = 4, near_lb3 = 8, near_lb3m = 5;   // near-field block log2 sizes (tuned)
   // d = 1 launch geometry
-  int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;
+  int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;   // d1_shape: requested (-1 auto)
+  int d1_shape_used = 0;            // the shape of the single-chunk kernel in use
   int d1_pdl = 1;                   // programmatic dependent launch for back-to-back applies
   int d1_prefetch = 1;    // d = 1 user order: L2 prefetch of v before the gathers (option 3)
   int64_t d1_chunk = 0;

@@ -24,3 +24,19 @@ def test_large_n_sampled_rows(gpm, d, n, two_nu):
     rows = W.sample_rows(x, 96)
     check_rows(out, x, v, two_nu, "l1", ell, 1.0, rows=rows, what=f"large d={d} n={n}")
     plan.close()
+
+
+def test_d1_two_pow_20_single_chunk(gpm):
+    """N = 2^20 is above the default shape's capacity (#SMs x 6912): the automatic choice
+    takes the 256 x 30 shape (#SMs x 7680) and keeps the single-launch kernel."""
+    n = 1 << 20
+    rng = np.random.default_rng(20)
+    x = rng.random((n, 1)); v = rng.standard_normal(n)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(5, (0.1,)))
+    assert plan.d1_path == 1 and plan.query(7) == 1
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, 5, "l1", (0.1,), 1.0, rows=W.sample_rows(x, 256), what="d1 2^20")
+    vr = plan.to_rank(to_dev(v))
+    o2 = plan.from_rank(plan.kmvm_rank(vr)).cpu().numpy()
+    assert np.max(np.abs(o2 - out)) <= 1e-13 * np.abs(out).max()
+    plan.close()
