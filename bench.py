@@ -55,7 +55,7 @@ def d1_kernel_name(shape, user=True):
     option 1): k_d1_lpc<P, KIND, threads, segments, points per segment, user order>."""
     u = "user" if user else "rank"
     shapes = {0: f"k_d1_lpc<2,0,256,3,9,{u}>", 1: f"k_d1_lpc<2,0,256,3,10,{u}>",
-              2: f"k_d1_lpc<2,0,224,3,11,{u}>"}
+              2: f"k_d1_lpc<2,0,256,4,7,{u}>"}
     return shapes.get(shape, f"d1 shape {shape}")
 
 

@@ -812,7 +812,7 @@ gp_status shapes_init() {
   if (g_ready) return GP_OK;
   g_shapes[0] = make_shape<256, 3, 9>();
   g_shapes[1] = make_shape<256, 3, 10>();   // #SMs x 7680 points: N = 2^20 in one chunk each
-  g_shapes[2] = make_shape<224, 3, 11>();
+  g_shapes[2] = make_shape<256, 4, 7>();
   for (auto& s : g_shapes)
     for (int u = 0; u < 2; ++u)
       for (int p = 0; p < 10; ++p)
