@@ -367,15 +367,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
     }
     if (USER && j >= ((cnt + 3) & ~3)) s_pi[j] = INT_MAX;
   }
-  // segment spans (the point before a segment -> its last point) for the scan elements,
-  // and the spans from my t_prev to the point before each segment / from each segment's
-  // last point to my last point (the carries)
-  double DS[SEGS], ES[SEGS];
-#pragma unroll
-  for (int sg = 0; sg < SEGS; ++sg) {
-    DS[sg] = tseg[sg] - (sg ? tseg[sg - 1] : tprev);
-    ES[sg] = fexp_neg(DS[sg], s_tab);
-  }
   // v-independent shifts, once per launch: my element's span, the chunk-sum shifts (my
   // last point -> chunk last point, chunk reference -> my t_prev)
   const double Dme = tmye - tprev, Eme = fexp_neg(Dme, s_tab);
@@ -411,82 +402,63 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = j0 + k < cnt ? __ldg(vcol + c0 + j0 + k) : 0.0;
     }
     LPC_STAMP(2);
-    // ---- local pass from zero state, segment by segment: the forward and backward
-    // recurrences over the segment's points interleaved (two chains), the segment's t, u
-    // and e^{-gap} loaded once into registers; loc_j = u_j (self term) + read_F + read_B,
-    // all scaled by os2 through the injected weights (u' = os2 u)
+    // ---- local pass from zero state: the forward recurrence over all my points and the
+    // backward one, interleaved (two chains), continuous across my segments; a phase
+    // stages the forward chain's segment and the backward chain's segment (t, e^{-gap},
+    // u, once each from shared memory); loc_j = u_j (self term) + read_F + read_B, all
+    // scaled by os2 through the injected weights (u' = os2 u)
     double loc[ITEMS];
-    double FS[SEGS][NQ], BS[SEGS][NQ];   // segment aggregates (F at its last point, B at
-                                         // the point before its first point)
+    double F[NQ], B[NQ];
 #pragma unroll
-    for (int sg = 0; sg < SEGS; ++sg) {
-      const int i0 = sg * SL;
-      double tt[SL + 1], ee[SL], uw[SL];
-      tt[0] = sg ? tseg[sg - 1] : tprev;
+    for (int q = 0; q < NQ; ++q) F[q] = B[q] = 0.0;
 #pragma unroll
-      for (int k = 0; k < SL; ++k) {
-        tt[k + 1] = s_t[j0 + i0 + k];
-        ee[k] = s_e[j0 + i0 + k];
-        uw[k] = a.os2 * s_u[j0 + i0 + k];
-      }
-      double F[NQ], B[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) F[q] = B[q] = 0.0;
+    for (int ph = 0; ph < SEGS; ++ph) {
+      const int sf = ph, sb = SEGS - 1 - ph;       // forward / backward segment
+      const int f0 = sf * SL, b0 = sb * SL;
+      double tf[SL + 1], ef[SL], uf[SL], tb[SL + 1], eb[SL + 1], ub[SL];
+      tf[0] = sf ? s_t[j0 + f0 - 1] : tprev;
 #pragma unroll
       for (int k = 0; k < SL; ++k) {
-        const int kf = k, kb = SL - 1 - k;   // forward point kf, backward point kb
-        if (k > 0) advance<P>(F, tt[kf + 1] - tt[kf], ee[kf]);
-        const double rf = KIND == 0 ? (k > 0 ? uw[kf] + readc0<P, KIND>(F) : uw[kf])
-                                    : (k > 0 ? readc0<P, KIND>(F) : 0.0);
-        F[0] += uw[kf];
-        if (k > 0) advance<P>(B, tt[kb + 2] - tt[kb + 1], ee[kb + 1]);
-        const double rb = k > 0 ? readc0<P, KIND>(B) : 0.0;
-        B[0] += uw[kb];
-        // first touch assigns (the middle point is touched by both chains in one step)
-        if (kf <= kb) loc[i0 + kf] = rf; else loc[i0 + kf] += rf;
-        if (kb > kf) loc[i0 + kb] = rb; else loc[i0 + kb] += rb;
+        tf[k + 1] = s_t[j0 + f0 + k];
+        ef[k] = s_e[j0 + f0 + k];
+        uf[k] = a.os2 * s_u[j0 + f0 + k];
       }
-      advance<P>(B, tt[1] - tt[0], ee[0]);   // -> the point before the segment
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        FS[sg][q] = F[q];
-        BS[sg][q] = B[q];
+      for (int k = 0; k < SL; ++k) {   // the backward segment's t, e^{-gap} of the next point
+        tb[k] = sf == sb ? tf[k + 1] : s_t[j0 + b0 + k];
+        ub[k] = sf == sb ? uf[k] : a.os2 * s_u[j0 + b0 + k];
+        eb[k] = k == 0 ? 0.0 : (sf == sb ? ef[k] : s_e[j0 + b0 + k]);
+      }
+      tb[SL] = sb + 1 < SEGS ? s_t[j0 + b0 + SL] : 0.0;
+      eb[SL] = sb + 1 < SEGS ? s_e[j0 + b0 + SL] : 1.0;
+#pragma unroll
+      for (int k = 0; k < SL; ++k) {
+        const int i = f0 + k;              // forward point
+        if (i > 0) advance<P>(F, tf[k + 1] - tf[k], ef[k]);
+        const double rf = KIND == 0 ? (i > 0 ? uf[k] + readc0<P, KIND>(F) : uf[k])
+                                    : (i > 0 ? readc0<P, KIND>(F) : 0.0);
+        F[0] += uf[k];
+        const int kb = SL - 1 - k, ib = b0 + kb;   // backward point
+        if (ib < ITEMS - 1) advance<P>(B, tb[kb + 1] - tb[kb], eb[kb + 1]);
+        const double rb = ib < ITEMS - 1 ? readc0<P, KIND>(B) : 0.0;
+        B[0] += ub[kb];
+        // first touch assigns: point i meets the forward chain at step i and the backward
+        // chain at step ITEMS-1-i (the middle point: both in one step, forward first)
+        if (i <= ITEMS - 1 - i) loc[i] = rf; else loc[i] += rf;
+        if (ITEMS - 1 - ib < ib) loc[ib] = rb; else loc[ib] += rb;
       }
     }
-    // within-thread carry prefixes (v-dependent but known before the exchange):
-    //   HF_s = forward state at the point before segment s from my earlier segments,
-    //   HB_s = backward state at the last point of segment s from my later segments;
-    // my scan element is (span t_prev -> my last point, HF_SEGS, HB_{-1})
-    double HF[SEGS][NQ], HB[SEGS][NQ];
-    Run<NQ> me;
-    {
-      double h[NQ];
+    {   // backward aggregate -> my t_prev
+      const double t0 = s_t[j0];
+      advance<P>(B, t0 - tprev, s_e[j0]);
+    }
+    Run<NQ> me;   // my scan element: span t_prev -> my last point
+    me.D = Dme;
+    me.E = Eme;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) h[q] = 0.0;
-#pragma unroll
-      for (int sg = 0; sg < SEGS; ++sg) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) HF[sg][q] = h[q];
-        if (sg) advance<P>(h, DS[sg], ES[sg]);
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) h[q] += FS[sg][q];
-      }
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) me.MF[q] = h[q];   // at my last point
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) h[q] = 0.0;
-#pragma unroll
-      for (int sg = SEGS - 1; sg >= 0; --sg) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) HB[sg][q] = h[q];
-        advance<P>(h, DS[sg], ES[sg]);   // -> the point before segment sg
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) h[q] += BS[sg][q];
-      }
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) me.MB[q] = h[q];   // at my t_prev
-      me.D = Dme;
-      me.E = Eme;
+    for (int q = 0; q < NQ; ++q) {
+      me.MF[q] = F[q];
+      me.MB[q] = B[q];
     }
     LPC_STAMP(3);
     // ---- chunk aggregate = fixed-order sum of the shifted thread aggregates -> record
@@ -595,11 +567,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
     }
     __syncthreads();   // #3: exclusive warp totals, fold partials
     LPC_STAMP(13);
-    // ---- the carries entering my segments: G_0 = forward state at my t_prev (earlier
-    // threads and chunks), G_s = S(t_prev -> point before s) G_0 + HF_s, X_s = S(first gap
-    // of s) G_s; Y = backward state at my last point, Y_s = S(last of s -> my last) Y + HB_s.
-    // A carry C seen from a point D further on reads e^{-D} sum_r beta_r D^r (carry_beta).
-    double bX[SEGS][NQ], bY[SEGS][NQ];
+    // ---- my carries: X = forward state entering my first point (earlier threads and
+    // chunks), Y = backward state entering my last point; a carry C seen from a point D
+    // further on reads e^{-D} sum_r beta_r D^r (carry_beta)
+    double bX[NQ], bY[NQ];
     {
       const Mon<NQ> wf = mon_ld<NQ>(s_wf[warp]), wb = mon_ld<NQ>(s_wb[warp]);
       const Mon<NQ> Fx = mon_f<NQ>(wf, fe);   // threads before me, referenced at my t_prev
@@ -622,65 +593,43 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         g[q] += Fx.M[q];
         y[q] += Bx.M[q];
       }
-      double d1 = 0.0, e1 = 1.0;   // my t_prev -> the point before segment sg
-#pragma unroll
-      for (int sg = 0; sg < SEGS; ++sg) {
-        double gs[NQ], ys[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          gs[q] = g[q];
-          ys[q] = y[q];
-        }
-        const double tb = sg ? tseg[sg - 1] : tprev;   // the point before segment sg
-        double d2 = 0.0, e2 = 1.0;   // the last point of segment sg -> my last point
-#pragma unroll
-        for (int s2 = sg + 1; s2 < SEGS; ++s2) {
-          d2 += DS[s2];
-          e2 *= ES[s2];
-        }
-        advance<P>(gs, d1, e1);
-        advance<P>(ys, d2, e2);
-        d1 += DS[sg];
-        e1 *= ES[sg];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          gs[q] += HF[sg][q];
-          ys[q] += HB[sg][q];
-        }
-        const double t1 = s_t[j0 + sg * SL];           // -> the segment's first point
-        advance<P>(gs, t1 - tb, s_e[j0 + sg * SL]);
-        carry_beta<P, KIND>(gs, bX[sg]);
-        carry_beta<P, KIND>(ys, bY[sg]);
-      }
+      advance<P>(g, s_t[j0] - tprev, s_e[j0]);   // -> my first point
+      carry_beta<P, KIND>(g, bX);
+      carry_beta<P, KIND>(y, bY);
     }
     LPC_STAMP(14);
-    // ---- correction pass (forward and backward chains per segment), then the output
-#pragma unroll
-    for (int sg = 0; sg < SEGS; ++sg) {
-      const int i0 = sg * SL;
-      double tt[SL], ee[SL];
-#pragma unroll
-      for (int k = 0; k < SL; ++k) {
-        tt[k] = s_t[j0 + i0 + k];
-        ee[k] = s_e[j0 + i0 + k];
-      }
+    // ---- correction pass (forward and backward chains interleaved, staged per phase as
+    // the local pass), then the output
+    {
       double Ef = 1.0, Eb = 1.0;
+      const double tfirst = s_t[j0], tmyl = s_t[j0 + ITEMS - 1];
 #pragma unroll
-      for (int k = 0; k < SL; ++k) {
-        const int kf = k, kb = SL - 1 - k;
-        if (k > 0) {
-          Ef *= ee[kf];
-          Eb *= ee[kb + 1];
-        }
-        const double Df = tt[kf] - tt[0], Db = tt[SL - 1] - tt[kb];
-        double hf = bX[sg][P], hb = bY[sg][P];
+      for (int ph = 0; ph < SEGS; ++ph) {
+        const int f0 = ph * SL, b0 = (SEGS - 1 - ph) * SL;
+        double tf[SL], ef[SL], tb[SL], eb[SL + 1];
 #pragma unroll
-        for (int r = P - 1; r >= 0; --r) {
-          hf = fma(hf, Df, bX[sg][r]);
-          hb = fma(hb, Db, bY[sg][r]);
+        for (int k = 0; k < SL; ++k) {
+          tf[k] = s_t[j0 + f0 + k];
+          ef[k] = s_e[j0 + f0 + k];
+          tb[k] = f0 == b0 ? tf[k] : s_t[j0 + b0 + k];
+          eb[k] = k == 0 ? 0.0 : (f0 == b0 ? ef[k] : s_e[j0 + b0 + k]);
         }
-        loc[i0 + kf] = fma(Ef, hf, loc[i0 + kf]);
-        loc[i0 + kb] = fma(Eb, hb, loc[i0 + kb]);
+        eb[SL] = b0 + SL < ITEMS ? s_e[j0 + b0 + SL] : 1.0;
+#pragma unroll
+        for (int k = 0; k < SL; ++k) {
+          const int i = f0 + k, kb = SL - 1 - k, ib = b0 + kb;
+          if (i > 0) Ef *= ef[k];
+          if (ib < ITEMS - 1) Eb *= eb[kb + 1];
+          const double Df = tf[k] - tfirst, Db = tmyl - tb[kb];
+          double hf = bX[P], hb = bY[P];
+#pragma unroll
+          for (int r = P - 1; r >= 0; --r) {
+            hf = fma(hf, Df, bX[r]);
+            hb = fma(hb, Db, bY[r]);
+          }
+          loc[i] = fma(Ef, hf, loc[i]);
+          loc[ib] = fma(Eb, hb, loc[ib]);
+        }
       }
     }
     if (USER) {
