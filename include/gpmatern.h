@@ -166,6 +166,25 @@ GP_API gp_status gp_kzx_setup(gp_plan p, const double *z, int64_t m, void *strea
 GP_API gp_status gp_kzx(gp_cross c, const double *v, int nrhs, double *out, void *stream);
 GP_API void gp_kzx_destroy(gp_cross c);
 
+/* gp_kmvm_partial -- one shard's share of a d >= 2 apply (the multi-GPU
+ * decomposition of the D&C).  Shard `shard` of `nshards` computes the pairs of
+ * its tiles of the within-tile level kernels and its items of the carried-pass apply (the
+ * carried-pass aggregates run whole on every shard); every pair belongs to exactly one
+ * shard, so sum over shards of out_rank = K v_rank (the self term is added by shard 0).
+ *   v_rank  : n x nrhs column-major, rank order (device; every shard needs all of v:
+ *             gather it first, e.g. ncclAllGather);
+ *   out_rank: n x nrhs column-major, rank order (device): this shard's partial product
+ *             (sum the shards with e.g. ncclAllReduce / ncclReduceScatter, then gp_permute).
+ * Errors: INVALID_ARG (bad shard / nshards), UNSUPPORTED for d = 1 (one launch with a
+ * chunk exchange: shard d = 1 by right-hand sides). */
+GP_API gp_status gp_kmvm_partial(gp_plan p, const double *v_rank, int nrhs, double *out_rank,
+                                 int shard, int nshards, void *stream);
+
+/* gp_shard_ranges -- host only (no device needed): the work split of gp_kmvm_partial for a
+ * plan of n points in dimension d: ranges[0..1] = tiles [lo, hi) of the tile kernels,
+ * ranges[2..3] = items [lo, hi) of the carried-pass apply.  INVALID_ARG for d = 1. */
+GP_API gp_status gp_shard_ranges(int64_t n, int d, int shard, int nshards, int64_t *ranges);
+
 /* gp_cg_solve -- conjugate gradients (P:155-174 [§1]; P:980-1034 [App A, Alg 2] with
  * no preconditioner, zero initial guess) on A = K + sigma2 I for the right-hand sides
  * [y, H] (multi-RHS), then the GLS fixed effects of P:808-812:

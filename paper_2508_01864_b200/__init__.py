@@ -79,6 +79,8 @@ def load_library(path: str | None = None):
         "gp_kmvm": [vp, vp, ci, vp, vp],
         "gp_kmvm_host": [vp, vp, ci, vp, vp],
         "gp_kmvm_rank": [vp, vp, ci, vp, vp],
+        "gp_kmvm_partial": [vp, vp, ci, vp, ci, ci, vp],
+        "gp_shard_ranges": [i64, ci, ci, ci, ctypes.POINTER(i64)],
         "gp_kmvm_dlengthscale": [vp, vp, ci, vp, ci, vp],
         "gp_permute": [vp, vp, ci, vp, ci, vp],
         "gp_kzx_setup": [vp, vp, i64, vp, ctypes.POINTER(vp)],
@@ -203,6 +205,16 @@ class Plan:
             out = torch.empty_like(v_rank)
         _check(_lib.gp_kmvm_rank(self._h, _dev(v_rank, "v"), nrhs, _dev(out, "out", v_rank.shape),
                                  _stream(stream)))
+        return out
+
+    def kmvm_partial(self, v_rank, shard: int, nshards: int, out=None, stream=None):
+        """Shard `shard` of `nshards` of K v_rank (rank order, d >= 2; gp_kmvm_partial): the
+        shards' outputs sum to kmvm_rank(v_rank)."""
+        import torch
+        out = torch.empty_like(v_rank) if out is None else out
+        nrhs = 1 if v_rank.dim() == 1 else v_rank.shape[0]
+        _check(_lib.gp_kmvm_partial(self._h, _dev(v_rank, "v_rank"), nrhs, _dev(out, "out"),
+                                    int(shard), int(nshards), _stream(stream)))
         return out
 
     def kmvm_dlengthscale(self, v, out=None, rank_order=False, stream=None):
@@ -478,6 +490,15 @@ def fit(x, kernel: Kernel, sigma0: float, y, G, W=None, stream=None, **opts):
                res.kernel.outputscale, res.kernel.form)
     return {"kernel": k, "sigma": res.sigma, "beta": [res.beta[i] for i in range(1 + d)],
             "steps": res.steps, "outer": res.outer, "lml": res.lml, "grad_norm": res.grad_norm}
+
+
+def shard_ranges(n: int, d: int, shard: int, nshards: int):
+    """Host-only work split of a sharded d >= 2 apply (gp_shard_ranges): ((tile_lo, tile_hi),
+    (item_lo, item_hi))."""
+    lib = load_library()
+    r = (ctypes.c_int64 * 4)()
+    _check(lib.gp_shard_ranges(int(n), int(d), int(shard), int(nshards), r))
+    return (r[0], r[1]), (r[2], r[3])
 
 
 def cg_solve(plan: Plan, y, sigma2, **kw):

@@ -174,6 +174,32 @@ static gp_status kmvm_host_pipelined(gp_plan p, const double* v, int nrhs, doubl
   return GP_OK;
 }
 
+gp_status gp_kmvm_partial(gp_plan p, const double* v_rank, int nrhs, double* out_rank, int shard,
+                          int nshards, void* stream) {
+  if (!p || !v_rank || !out_rank) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    return fail(GP_ERR_INVALID_ARG, "need 0 <= shard < nshards");
+  Plan& pl = p->pl;
+  if (pl.d < 2)
+    return fail(GP_ERR_UNSUPPORTED,
+                "gp_kmvm_partial: d >= 2 only (the d = 1 apply is one launch; shard d = 1 by columns)");
+  pl.shard = shard;
+  pl.nshards = nshards;
+  gp_status st = apply_rank(pl, v_rank, out_rank, nrhs, static_cast<cudaStream_t>(stream));
+  pl.shard = 0;
+  pl.nshards = 1;
+  return st;
+}
+
+gp_status gp_shard_ranges(int64_t n, int d, int shard, int nshards, int64_t* ranges) {
+  if (!ranges) return fail(GP_ERR_INVALID_ARG, "NULL argument");
+  if (n < 1 || d < 2 || d > 3 || nshards < 1 || shard < 0 || shard >= nshards)
+    return fail(GP_ERR_INVALID_ARG, "need n >= 1, d in {2, 3}, 0 <= shard < nshards");
+  shard_ranges(n, d, shard, nshards, ranges);
+  return GP_OK;
+}
+
 gp_status gp_kmvm_host(gp_plan p, const double* v, int nrhs, double* out, void* stream) {
   if (!p || !v || !out) return fail(GP_ERR_INVALID_ARG, "NULL argument");
   if (nrhs < 1) return fail(GP_ERR_INVALID_ARG, "nrhs must be >= 1");

@@ -150,7 +150,8 @@ static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, 
     k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
         user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
         pl.part.as<double>(), level_nparts(pl), pl.n, user_order ? pl.tgt_off : 0, pl.os2,
-        kind == 0 ? 1.0 : 0.0, out + c0 * ostride, ostride, cg_s2, cg_part, c0);
+        (kind == 0 && pl.shard == 0) ? 1.0 : 0.0, out + c0 * ostride, ostride, cg_s2, cg_part,
+        c0);   // a sharded apply adds the self term on shard 0 only
     GPM_CUDA(cudaGetLastError());
     pl.launches_per_apply = launches + 2;   // + pack + epilogue (per batch of columns)
   }

@@ -73,6 +73,7 @@ struct LvArgs {
   double* part;        // [nparts][n] per-pass contributions (rank order), summed in order
   int npass;           // carried passes (their part slots come first, then d=3 mid levels)
   int64_t part_stride; // doubles per right-hand side in part
+  int tile0;           // sharded applies (gp_kmvm_partial): first tile of the tile kernels
 };
 
 // right-hand side handled by this CTA (blockIdx.y): offset the per-column buffers
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low2(LvArgs g) {
   __shared__ TScratch<A> sc;
   const int tid = threadIdx.x;
   const int i0 = tid * CP_ITEMS;
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int64_t T0 = (int64_t)(blockIdx.x + g.tile0) * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
 #pragma unroll 4
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
   const int i0 = tid * CP_ITEMS;
   const int c0 = blockIdx.y * NC;
   const int nc = min(NC, nrhs - c0);
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int64_t T0 = (int64_t)(blockIdx.x + g.tile0) * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
 #pragma unroll 2
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low3(LvArgs g) {
   __shared__ TScratch<A> sc;
   const int tid = threadIdx.x;
   const int i0 = tid * CP_ITEMS;
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int64_t T0 = (int64_t)(blockIdx.x + g.tile0) * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   fexp_table_init(sc.tab);
 #pragma unroll 4
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_mid3(LvArgs g) {
   const int tid = threadIdx.x;
   const int i0 = tid * CP_ITEMS;
   const int l1 = g.l1 + (int)blockIdx.z;   // one launch covers every outer level l1 > 10
-  const int64_t T0 = (int64_t)blockIdx.x * LV_TILE;
+  const int64_t T0 = (int64_t)(blockIdx.x + g.tile0) * LV_TILE;
   const int cnt = (int)min((int64_t)LV_TILE, g.n - T0);
   const int64_t mid1 = ((T0 >> l1) << l1) + (int64_t(1) << (l1 - 1));
   double* slot = g.part + (int64_t)(g.npass + blockIdx.z) * g.n;
@@ -896,7 +897,10 @@ __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDe
 template <class A, int MODE>
 __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned char* hpbase,
                                                    const HpDesc* descs, int npass, int total,
-                                                   int max_tiles, int nrhs, int64_t carr_off) {
+                                                   int max_tiles, int nrhs, int64_t carr_off,
+                                                   int item_lo) {
+  // items [item_lo, total) of the flattened (pass, tile) list (a sharded apply's share)
+  const int b0 = item_lo + (int)blockIdx.x;
   using S = CSt<A::NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
@@ -915,18 +919,18 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
   }
   __syncthreads();
   if (tid == 0) {
-    if (blockIdx.x < total) {
-      p_iss = cp_pass_at(descs, npass, p_iss, blockIdx.x);
-      cp_issue(hpbase, descs, p_iss, blockIdx.x, SM.st[0], &bar[0]);
+    if (b0 < total) {
+      p_iss = cp_pass_at(descs, npass, p_iss, b0);
+      cp_issue(hpbase, descs, p_iss, b0, SM.st[0], &bar[0]);
     }
-    if (blockIdx.x + G < total) {
-      p_iss = cp_pass_at(descs, npass, p_iss, blockIdx.x + G);
-      cp_issue(hpbase, descs, p_iss, blockIdx.x + G, SM.st[1], &bar[1]);
+    if (b0 + G < total) {
+      p_iss = cp_pass_at(descs, npass, p_iss, b0 + G);
+      cp_issue(hpbase, descs, p_iss, b0 + G, SM.st[1], &bar[1]);
     }
   }
   // sources of the first (tile, column)
   double un[CP_ITEMS];
-  if (blockIdx.x < total) {
+  if (b0 < total) {
     mbar_wait(&bar[0], 0);
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
@@ -936,7 +940,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned cha
   }
   int j = 0, p = 0;
 #pragma unroll 1
-  for (int item = blockIdx.x; item < total; item += G, ++j) {
+  for (int item = b0; item < total; item += G, ++j) {
     const int sidx = j & 1;
     CpStage& E = SM.st[sidx];
     mbar_wait(&bar[sidx], (j >> 1) & 1);
@@ -1290,6 +1294,42 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
 
 int level_nparts(const Plan& pl);
 
+// Sharded applies (gp_kmvm_partial): shard `shard` of `nshards` runs the
+// tiles [T lo, T hi) of the tile kernels (k_low*, k_mid3) and the items [I lo, I hi) of the
+// carried-pass apply (k_cp<2>); the carried-pass aggregates and carries (k_cp<1>,
+// k_cp_carry) run whole on every shard.  Every pair lies in exactly one tile or item, so
+// the shards' partial outputs sum to K v.
+static int64_t hp_item_count(int64_t n, int d) {
+  int L = 0;
+  while ((int64_t(1) << L) < n) ++L;
+  int64_t items = 0;
+  for (int l1 = LV_LOGTILE + 1; l1 <= L; ++l1) {
+    const int64_t b_last = (n - 1) >> l1;
+    const int64_t mid1 = (b_last << l1) + (int64_t(1) << (l1 - 1));
+    const int64_t nact1 = mid1 >= n ? (b_last << l1) : n;
+    if (d == 2) {
+      if (nact1 > 0) items += (nact1 + LV_TILE - 1) / LV_TILE;
+    } else {
+      for (int l2 = LV_LOGTILE + 1; l2 <= l1; ++l2) {
+        const int64_t c_last = (n - 1) >> l2;
+        const int64_t mid2 = (c_last << l2) + (int64_t(1) << (l2 - 1));
+        int64_t nact = nact1;
+        if (mid2 >= n) nact = std::min(nact, c_last << l2);
+        if (nact > 0) items += (nact + LV_TILE - 1) / LV_TILE;
+      }
+    }
+  }
+  return items;
+}
+void shard_ranges(int64_t n, int d, int shard, int nshards, int64_t* r) {
+  const int64_t tiles = (n + LV_TILE - 1) / LV_TILE;
+  const int64_t items = hp_item_count(n, d);
+  r[0] = tiles * shard / nshards;
+  r[1] = tiles * (shard + 1) / nshards;
+  r[2] = items * shard / nshards;
+  r[3] = items * (shard + 1) / nshards;
+}
+
 template <class A>
 static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   static bool attr = false;
@@ -1319,7 +1359,19 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   g.part = pl.part.as<double>();
   g.npass = pl.hp_npass;
   g.part_stride = (int64_t)level_nparts(pl) * n;
-  const dim3 gt(tiles, nrhs);
+  int64_t sr[4] = {0, tiles, 0, pl.hp_items};   // tile range, carried-pass item range
+  if (pl.nshards > 1) {
+    shard_ranges(n, pl.d, pl.shard, pl.nshards, sr);
+    if (sr[3] - sr[2] != 0 && pl.hp_items != hp_item_count(n, pl.d))
+      return fail(GP_ERR_CUDA, "internal: carried-pass item count mismatch");
+    // points outside this shard's tiles / items get no contribution: start from zero
+    GPM_CUDA(cudaMemsetAsync(g.acc, 0, sizeof(double) * n * nrhs, s));
+    if (level_nparts(pl) > 0)
+      GPM_CUDA(cudaMemsetAsync(g.part, 0, sizeof(double) * g.part_stride * nrhs, s));
+  }
+  g.tile0 = (int)sr[0];
+  const int tiles_run = (int)(sr[1] - sr[0]);
+  const dim3 gt(tiles_run, nrhs);
   const bool hp = pl.hp_npass > 0;
   const HpDesc* dd = pl.hpdesc.as<HpDesc>();
   static int grid1 = 0, grid2 = 0;   // persistent k_cp: as many CTAs as fit (per instantiation)
@@ -1346,7 +1398,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     const int64_t carr_off = (int64_t)g.agg_stride * nrhs;   // carries after the aggregates
     k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmem), pl.s2>>>(
         g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
-        carr_off);
+        carr_off, 0);
     GPM_CUDA(cudaGetLastError());
     LvRecFor<A::NS>* recs = reinterpret_cast<LvRecFor<A::NS>*>(g.aggs);
     k_cp_carry<A><<<dim3(pl.hp_maxtiles, pl.hp_npass, 2 * nrhs), 32, 0, pl.s2>>>(
@@ -1355,8 +1407,10 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     GPM_CUDA(cudaEventRecord(pl.ev_join, pl.s2));
     *launches += 2;
   }
-  // fused low levels (writes acc for every point: no memset needed)
-  if constexpr (A::NCH == 2) {
+  // fused low levels (writes acc for every point of its tiles)
+  if (tiles_run <= 0) {
+    // this shard has no tiles
+  } else if constexpr (A::NCH == 2) {
     if (nrhs >= 2 && !getenv("GPM_LOW2_PERCOL")) {   // columns share the v-independent work
       constexpr int NC = 4;
       static bool attr = false;
@@ -1365,7 +1419,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
                                       (int)sizeof(LvPointsM<NC>)));
         attr = true;
       }
-      k_low2m<A, NC><<<dim3(tiles, (nrhs + NC - 1) / NC), CP_BLOCK, sizeof(LvPointsM<NC>), s>>>(
+      k_low2m<A, NC><<<dim3(tiles_run, (nrhs + NC - 1) / NC), CP_BLOCK, sizeof(LvPointsM<NC>), s>>>(
           g, nrhs);
     } else {
       k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
@@ -1378,18 +1432,21 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     GPM_CUDA(cudaGetLastError());
     if (L > LV_LOGTILE) {   // d = 3: every outer level l1 > 10 (inner l2 <= 10)
       g.l1 = LV_LOGTILE + 1;
-      k_mid3<A><<<dim3(tiles, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), s>>>(g);
+      k_mid3<A><<<dim3(tiles_run, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), s>>>(g);
       *launches += 1;
       GPM_CUDA(cudaGetLastError());
     }
   }
   if (hp) {   // carried-pass apply (needs the aggregates)
     GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
-    k_cp<A, 2><<<std::min(pl.hp_items, grid2), CP_BLOCK, sizeof(CpSmem), s>>>(
-        g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
-        (int64_t)g.agg_stride * nrhs);
-    *launches += 1;
-    GPM_CUDA(cudaGetLastError());
+    const int nit = (int)(sr[3] - sr[2]);
+    if (nit > 0) {
+      k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmem), s>>>(
+          g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, (int)sr[3], pl.hp_maxtiles, nrhs,
+          (int64_t)g.agg_stride * nrhs, (int)sr[2]);
+      *launches += 1;
+      GPM_CUDA(cudaGetLastError());
+    }
   }
   return GP_OK;
 }

@@ -137,6 +137,7 @@ struct Plan {
   int d1_prefetch = 1;    // d = 1 user order: L2 prefetch of v before the gathers (option 3)
   int64_t d1_chunk = 0;
   int64_t struct_bytes = 0;
+  int shard = 0, nshards = 1;       // gp_kmvm_partial: this call's share of a sharded apply
   int launches_per_apply = 0;
 };
 
@@ -198,6 +199,8 @@ gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStrea
 gp_status apply_prepare(Plan& pl);   // launch geometry + scratch
 gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cudaStream_t s);
 int64_t apply_model_bytes(const Plan& pl);
+// apply_level.cu: tile range [r0, r1) and carried-pass item range [r2, r3) of a shard
+void shard_ranges(int64_t n, int d, int shard, int nshards, int64_t* r);
 
 // solve.cu
 gp_status cg_solve(Plan& pl, double sigma2, const double* y, int mean_kind, const double* H,

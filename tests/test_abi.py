@@ -32,7 +32,8 @@ def test_header_declares_the_boundary():
     for must in ["gp_setup", "gp_kmvm", "gp_kmvm_host", "gp_kzx_setup", "gp_kzx", "gp_kzx_destroy",
                  "gp_cg_solve", "gp_predict", "gp_destroy", "gp_last_error", "gp_plan_query",
                  "gp_plan_set_option", "gp_version", "gp_kmvm_rank", "gp_permute",
-                 "gp_kmvm_dlengthscale", "gp_cg_solve_pc", "gp_cg_solve_ex", "gp_precond_create",
+                 "gp_kmvm_dlengthscale", "gp_cg_solve_pc", "gp_cg_solve_ex", "gp_kmvm_partial",
+                 "gp_shard_ranges", "gp_precond_create",
                  "gp_precond_factor", "gp_precond_solve", "gp_precond_logdet",
                  "gp_precond_destroy", "gp_mbcg", "gp_lml", "gp_fit", "gp_set_allocator"]:
         assert must in names, must

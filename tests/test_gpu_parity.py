@@ -430,3 +430,28 @@ def test_predict_union_cache(gpm):
     m4 = plan.predict(z[:100].contiguous(), ad, None).cpu().numpy()
     assert np.max(np.abs(m4 - ref[:100])) <= 1e-9 * ab.max() * np.abs(a).max()
     plan.close()
+
+
+@pytest.mark.parametrize("d,n,two_nu,form", [(2, 20000, 3, 0), (2, 9000, 3, 1), (3, 5000, 5, 0),
+                                             (3, 70000, 3, 0)])
+@pytest.mark.parametrize("nshards", [2, 3, 5])
+def test_sharded_apply_sums_to_kv(gpm, d, n, two_nu, form, nshards):
+    """SURVEY §8(e) decomposition on one GPU: the shards of gp_kmvm_partial (tile and
+    carried-pass item ranges of the D&C kernels) sum to the whole rank-order apply, for
+    sizes with carried passes and (d = 3) outer levels above the tile; two columns."""
+    import torch
+    rng = np.random.default_rng(n + nshards)
+    x = rng.random((n, d))
+    ell = (0.2, 0.3, 0.4)[:d]
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, form=form))
+    V = torch.from_numpy(rng.standard_normal((2, n))).cuda()
+    VR = torch.stack([plan.to_rank(V[i].contiguous()) for i in range(2)])
+    full = plan.kmvm_rank(VR)
+    acc = torch.zeros_like(full)
+    for s in range(nshards):
+        acc += plan.kmvm_partial(VR, s, nshards)
+    assert torch.max(torch.abs(acc - full)).item() <= 1e-12 * torch.max(torch.abs(full)).item()
+    assert torch.equal(plan.kmvm_rank(VR), full)   # back to the whole apply afterwards
+    with pytest.raises(gpm.GPError):
+        plan.kmvm_partial(VR, nshards, nshards)
+    plan.close()

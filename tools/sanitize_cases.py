@@ -25,6 +25,9 @@ for d, n, form, two_nu in cases:
     VR = torch.stack([plan.to_rank(V[i].contiguous()) for i in range(3)])
     plan.kmvm_rank(VR)
     plan.kmvm_rank(VR[1].contiguous())
+    if d >= 2:
+        for s in range(3):
+            plan.kmvm_partial(VR, s, 3)
     z = torch.from_numpy(rng.random((300, d))).cuda()
     cr = plan.cross(z)
     cr.kzx(V[0].contiguous())
