@@ -68,7 +68,7 @@ def load_library(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("GPM_LIB") or LIB_PATH   # GPM_LIB: an experiment build (build.py)
     if not os.path.exists(path):
         raise FileNotFoundError(f"{path} missing: run `python -m paper_2508_01864_b200.build` "
                                 f"(no CPU fallback exists)")

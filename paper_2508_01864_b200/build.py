@@ -11,14 +11,18 @@ import concurrent.futures as cf
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libgpmatern.so")
-OBJDIR = os.path.join(HERE, "build")
+# experiment builds: GPM_LIB_SUFFIX=_x GPM_EXTRA_FLAGS="-DFOO=1" -> libgpmatern_x.so (load it with
+# GPM_LIB=<path>); the product build uses neither
+SUFFIX = os.environ.get("GPM_LIB_SUFFIX", "")
+LIB = os.path.join(HERE, f"libgpmatern{SUFFIX}.so")
+OBJDIR = os.path.join(HERE, "build" + SUFFIX)
 SOURCES = ["api.cu", "setup.cu", "apply.cu", "apply_d1.cu", "apply_d1_big.cu", "apply_level.cu",
            "solve.cu", "lml.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v" if os.environ.get("GPM_PTXAS_V") else "-O3"]
+         "-Xptxas", "-v" if os.environ.get("GPM_PTXAS_V") else "-O3",
+         *os.environ.get("GPM_EXTRA_FLAGS", "").split()]
 
 
 def _newer(target: str, deps) -> bool:

@@ -38,13 +38,13 @@ __global__ void k_gather(const int* __restrict__ perm, const double* __restrict_
 // partial sum of u . out -> cg_part[(col0 + blockIdx.y) * gridDim.x + blockIdx.x]
 __global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ pts,
                            const double* __restrict__ acc, const double* __restrict__ part,
-                           int nparts, int64_t n, int64_t tgt_off, double os2, double self,
+                           int nparts, int64_t pstride, int64_t n, int64_t tgt_off, double os2, double self,
                            double* __restrict__ out, int64_t ostride, double cg_s2,
                            double* __restrict__ cg_part, int col0) {
   __shared__ double red[32];
   pts += blockIdx.y * 4 * n;
   acc += blockIdx.y * n;
-  part += blockIdx.y * nparts * n;
+  part += blockIdx.y * pstride;
   out += blockIdx.y * ostride;
   double pq = 0.0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
@@ -97,16 +97,16 @@ gp_status apply_prepare(Plan& pl) {
     GPM_TRY(d1_prepare(pl));
     pl.launches_per_apply = 1;
   } else {
+    if (const char* e = getenv("GPM_NEAR_LB")) {   // tuning knob: "lb2,lb3,lb3m"
+      int a = pl.near_lb2, b = pl.near_lb3, c = pl.near_lb3m;
+      if (sscanf(e, "%d,%d,%d", &a, &b, &c) >= 1) { pl.near_lb2 = a; pl.near_lb3 = b; pl.near_lb3m = c; }
+    }
     GPM_TRY(level_buffers(pl, 1));
     // stage the carried passes' structure (lv_elem reads t through the packed records)
     if (!pl.hpbuf.bytes) {
       GPM_TRY(level_pack(pl, pl.t.as<double>(), 1, false, nullptr));   // u := t1 (unused)
       GPM_TRY(level_setup(pl, nullptr));
       GPM_CUDA(cudaDeviceSynchronize());
-    }
-    if (const char* e = getenv("GPM_NEAR_LB")) {   // tuning knob: "lb2,lb3,lb3m"
-      int a = pl.near_lb2, b = pl.near_lb3, c = pl.near_lb3m;
-      if (sscanf(e, "%d,%d,%d", &a, &b, &c) >= 1) { pl.near_lb2 = a; pl.near_lb3 = b; pl.near_lb3m = c; }
     }
   }
   GPM_TRY(pl.w.alloc(sizeof(double) * n));
@@ -149,7 +149,8 @@ static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, 
     GPM_TRY(level_passes(pl, nb, s, &launches, kind));   // first level launch initialises acc
     k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
         user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
-        pl.part.as<double>(), level_nparts(pl), pl.n, user_order ? pl.tgt_off : 0, pl.os2,
+        pl.part.as<double>(), level_nparts(pl) - pl.low_unused, (int64_t)level_nparts(pl) * pl.n,
+        pl.n, user_order ? pl.tgt_off : 0, pl.os2,
         (kind == 0 && pl.shard == 0) ? 1.0 : 0.0, out + c0 * ostride, ostride, cg_s2, cg_part,
         c0);   // a sharded apply adds the self term on shard 0 only
     GPM_CUDA(cudaGetLastError());

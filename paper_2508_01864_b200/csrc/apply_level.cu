@@ -74,6 +74,7 @@ struct LvArgs {
   int npass;           // carried passes (their part slots come first, then d=3 mid levels)
   int64_t part_stride; // doubles per right-hand side in part
   int tile0;           // sharded applies (gp_kmvm_partial): first tile of the tile kernels
+  int low_slot0;       // part slot of the fused low kernels' part 1 (part 0 writes acc)
 };
 
 // right-hand side handled by this CTA (blockIdx.y): offset the per-column buffers
@@ -127,6 +128,12 @@ __device__ __forceinline__ double kval(double d1, double d2, double d3, const do
   }
 }
 
+#ifndef GPM_CP_MINB    // resident CTAs per SM the kernels are compiled for (register caps)
+#define GPM_CP_MINB 3
+#endif
+#ifndef GPM_LOW_MINB
+#define GPM_LOW_MINB 3
+#endif
 constexpr int CP_BLOCK = 128;
 constexpr int CP_ITEMS = 8;
 constexpr int CP_WARPS = CP_BLOCK / 32;
@@ -230,9 +237,10 @@ struct CpScratch {
 // levels <= lb; position blocks of ord2[l1] with opposite x1 sides (l1side > 0): exactly
 // the pairs split at (l1, l2 <= lb)).  IND: position p holds point Pt.o2[p] (k_low3's inner
 // blocks), else point p.  Pt.acc[point] += sum_j K(i,j) u_j.
+// (zz, znf): this CTA's slice of the partners (the block's partners in znf equal ranges).
 template <class A, int D, bool IND>
 __device__ __forceinline__ void near_field(LvPoints& Pt, int cnt, int lb, int l1side,
-                                           const double* tab) {
+                                           const double* tab, int zz = 0, int znf = 1) {
   const int i0 = threadIdx.x * CP_ITEMS;
   if (i0 >= cnt) return;
   double ti1[CP_ITEMS], ti2[CP_ITEMS], ti3[CP_ITEMS], acc[CP_ITEMS];
@@ -247,8 +255,9 @@ __device__ __forceinline__ void near_field(LvPoints& Pt, int cnt, int lb, int l1
     hi[k] = l1side ? ((IND ? pi : Pt.o2[i]) >> (l1side - 1)) & 1 : 0;
     acc[k] = 0.0;
   }
-  const int bs = (i0 >> lb) << lb;
-  const int be = min(bs + (1 << lb), cnt);
+  const int sub = (1 << lb) / znf;
+  const int bs = ((i0 >> lb) << lb) + zz * sub;
+  const int be = min(bs + sub, cnt);
 #pragma unroll 1
   for (int j = bs; j < be; ++j) {
     const int pj = IND ? Pt.o2[j] : j;
@@ -399,11 +408,32 @@ __device__ __forceinline__ void load_ord8(const int* ord, int i0, int cnt, int b
   }
 }
 
-__device__ __forceinline__ int lv_clamp_lb(int lb, int lmax) { return min(max(lb, 3), lmax); }
+__host__ __device__ __forceinline__ int lv_clamp_lb(int lb, int lmax) {
+  return lb < 3 ? (3 < lmax ? 3 : lmax) : (lb < lmax ? lb : lmax);
+}
+// The fused low kernels run in parts (blockIdx.z), each with its own output slot (summed in
+// a fixed order by the epilogue): the near field in low_znf partner slices (a 256-rank block
+// costs as much as four engine levels), then the engine levels -- d = 2: two levels per part,
+// d = 3: one outer level l1 per part.  More, shorter CTAs: small n fills the SMs and the last
+// wave of a large grid is short.
+__host__ __device__ __forceinline__ int low_lb(int lb_opt, int L) {
+  const int lmax = L < LV_LOGTILE ? L : LV_LOGTILE;
+  const int lb = lv_clamp_lb(lb_opt, LV_LOGTILE);
+  return lb < lmax ? lb : lmax;
+}
+__host__ __device__ __forceinline__ int low_znf(int lb) { return lb >= 8 ? 4 : (lb == 7 ? 2 : 1); }
+__host__ __device__ __forceinline__ int low_lpart(int d, int lb, int l) {   // part of level l > lb
+  return low_znf(lb) + (d == 2 ? (l - lb - 1) / 2 : l - lb - 1);
+}
+__host__ __device__ __forceinline__ int low_parts(int d, int lb_opt, int L) {
+  const int lmax = L < LV_LOGTILE ? L : LV_LOGTILE;
+  const int lb = low_lb(lb_opt, L);
+  return lmax > lb ? low_lpart(d, lb, lmax) + 1 : low_znf(lb);
+}
 
 // ---- fused low levels, d = 2: every level l <= min(10, L) of one 1024-rank tile
 template <class A>
-__global__ void __launch_bounds__(CP_BLOCK, 3) k_low2(LvArgs g) {
+__global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low2(LvArgs g) {
   lv_col(g);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw);
@@ -423,11 +453,13 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low2(LvArgs g) {
   }
   __syncthreads();
   const int lmax = min(LV_LOGTILE, g.L);
-  const int lb = min(lv_clamp_lb(g.lb, LV_LOGTILE), lmax);
-  if (lb > 0) near_field<A, 2, false>(Pt, cnt, lb, 0, sc.tab);
+  const int lb = low_lb(g.lb, g.L);
+  const int z = blockIdx.z, znf = low_znf(lb);
+  if (lb > 0 && z < znf) near_field<A, 2, false>(Pt, cnt, lb, 0, sc.tab, z, znf);
   __syncthreads();
 #pragma unroll 1
   for (int l = lb + 1; l <= lmax; ++l) {
+    if (low_lpart(2, lb, l) != z) continue;
     const int* ord = g.ord2 + (size_t)(l - 1) * g.n + T0;
     TItems it;
     double y[CP_ITEMS];
@@ -452,8 +484,9 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low2(LvArgs g) {
     for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
   }
   __syncthreads();
+  double* dst = z == 0 ? g.acc : g.part + (int64_t)(g.low_slot0 + z - 1) * g.n;
 #pragma unroll 4
-  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) dst[T0 + i] = Pt.acc[i];
 }
 
 // ---- fused low levels, d = 2, NC right-hand sides per CTA (nrhs >= 2, e.g. config 5's CG
@@ -490,8 +523,10 @@ __global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
   }
   __syncthreads();
   const int lmax = min(LV_LOGTILE, g.L);
-  const int lb = min(lv_clamp_lb(g.lb, LV_LOGTILE), lmax);
-  if (lb > 0 && i0 < cnt) {   // near field: one kernel value per pair, NC columns
+  const int lb = low_lb(g.lb, g.L);
+  const bool split = gridDim.z > 1;   // large grids run every part in one CTA (one staging)
+  const int z = blockIdx.z, znf = split ? low_znf(lb) : 1;
+  if (lb > 0 && i0 < cnt && z < znf) {   // near field: one kernel value per pair, NC columns
     double ti1[CP_ITEMS], ti2[CP_ITEMS], acc[CP_ITEMS][NC];
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
@@ -501,8 +536,9 @@ __global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) acc[k][c] = 0.0;
     }
-    const int bs = (i0 >> lb) << lb;
-    const int be = min(bs + (1 << lb), cnt);
+    const int sub = (1 << lb) / znf;
+    const int bs = ((i0 >> lb) << lb) + z * sub;
+    const int be = min(bs + sub, cnt);
 #pragma unroll 1
     for (int j = bs; j < be; ++j) {
       const double tj1 = Pt.t1[j], tj2 = Pt.t2[j];
@@ -526,6 +562,7 @@ __global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
   __syncthreads();
 #pragma unroll 1
   for (int l = lb + 1; l <= lmax; ++l) {
+    if (split && low_lpart(2, lb, l) != z) continue;
     const int* ord = g.ord2 + (size_t)(l - 1) * g.n + T0;
     TItems it;
     double y[CP_ITEMS];
@@ -555,15 +592,19 @@ __global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
   }
   __syncthreads();
 #pragma unroll 1
-  for (int c = 0; c < nc; ++c)
+  for (int c = 0; c < nc; ++c) {
+    double* dst = z == 0 ? g.acc + (int64_t)(c0 + c) * g.n
+                         : g.part + (int64_t)(c0 + c) * g.part_stride +
+                               (int64_t)(g.low_slot0 + z - 1) * g.n;
 #pragma unroll 4
     for (int i = tid; i < LV_TILE; i += CP_BLOCK)
-      if (i < cnt) g.acc[(int64_t)(c0 + c) * g.n + T0 + i] = Pt.acc[c][i];
+      if (i < cnt) dst[T0 + i] = Pt.acc[c][i];
+  }
 }
 
 // ---- fused low levels, d = 3: every (l1 <= min(10, L), l2 <= l1) of one tile
 template <class A>
-__global__ void __launch_bounds__(CP_BLOCK, 3) k_low3(LvArgs g) {
+__global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low3(LvArgs g) {
   lv_col(g);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw);
@@ -584,10 +625,12 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low3(LvArgs g) {
   }
   __syncthreads();
   const int lmax = min(LV_LOGTILE, g.L);
-  const int lb = min(lv_clamp_lb(g.lb, LV_LOGTILE), lmax);
-  if (lb > 0) near_field<A, 3, false>(Pt, cnt, lb, 0, sc.tab);
+  const int lb = low_lb(g.lb, g.L);
+  const int z = blockIdx.z, znf = low_znf(lb);
+  if (lb > 0 && z < znf) near_field<A, 3, false>(Pt, cnt, lb, 0, sc.tab, z, znf);
 #pragma unroll 1
   for (int l1 = lb + 1; l1 <= lmax; ++l1) {
+    if (low_lpart(3, lb, l1) != z) continue;
     __syncthreads();
 #pragma unroll 4
     for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt)
@@ -628,14 +671,15 @@ __global__ void __launch_bounds__(CP_BLOCK, 3) k_low3(LvArgs g) {
     }
   }
   __syncthreads();
+  double* dst = z == 0 ? g.acc : g.part + (int64_t)(g.low_slot0 + z - 1) * g.n;
 #pragma unroll 4
-  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) g.acc[T0 + i] = Pt.acc[i];
+  for (int i = tid; i < LV_TILE; i += CP_BLOCK) if (i < cnt) dst[T0 + i] = Pt.acc[i];
 }
 
 // ---- d = 3, one outer level l1 > 10, all inner levels l2 <= 10 (tile = 1024 positions of
 // ord2[l1], i.e. one slice of one outer node; its points are gathered once)
 template <class A>
-__global__ void __launch_bounds__(CP_BLOCK, 3) k_mid3(LvArgs g) {
+__global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_mid3(LvArgs g) {
   lv_col(g);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LvPoints& Pt = *reinterpret_cast<LvPoints*>(smem_raw);
@@ -825,52 +869,76 @@ constexpr unsigned CP_STAGE_BYTES = 20u * LV_TILE;
 // tile aggregates of k_cp<1> (forward: tiles in order; backward: reversed), one warp per
 // node, 32 tiles per step (Kogge-Stone with the same combine as the tile scans).  k_cp<2>
 // then loads one record per direction instead of folding up to #tiles aggregates per column.
+constexpr int CC_WARPS = 8;   // k_cp_carry: 8 warps x 32 tiles per step
 template <class A>
-__global__ void __launch_bounds__(32) k_cp_carry(LvRecFor<A::NS>* aggs, LvRecFor<A::NS>* carr,
-                                                 const HpDesc* descs, int npass, int max_tiles) {
+__global__ void __launch_bounds__(32 * CC_WARPS) k_cp_carry(LvRecFor<A::NS>* aggs,
+                                                            LvRecFor<A::NS>* carr,
+                                                            const HpDesc* descs, int npass,
+                                                            int max_tiles) {
   using S = CSt<A::NS>;
   using Rec = LvRecFor<A::NS>;
+  __shared__ S wtot[CC_WARPS];
   const int p = blockIdx.y;
   const int c = blockIdx.z >> 1, dir = blockIdx.z & 1;
   const HpDesc hd = descs[p];
   const int tps = 1 << (hd.lseg - LV_LOGTILE);
-  const int first = blockIdx.x * tps;
-  if (first >= hd.ntiles) return;
-  const int last = min(first + tps, hd.ntiles) - 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t base = ((int64_t)c * npass + p) * 2 * max_tiles;
   const Rec* ag = aggs + base;
   Rec* cr = carr + base;
-  const int lane = threadIdx.x;
-  S cin = cs_id<A>();
-  if (dir == 0) {
+  if (tps <= 32) {   // short nodes: one warp per node, one step, no block barrier
+    const int first = (blockIdx.x * CC_WARPS + warp) * tps;
+    if (first >= hd.ntiles) return;
+    const int last = min(first + tps, hd.ntiles) - 1;
+    const int t = dir == 0 ? first + lane : last - lane;
+    const bool in = lane <= last - first;
+    S x = in ? cs_get<A::NS>(ag + 2 * t + dir) : cs_id<A>();
 #pragma unroll 1
-    for (int b0 = first; b0 <= last; b0 += 32) {
-      const int t = b0 + lane;
-      S x = t <= last ? cs_get<A::NS>(ag + 2 * t) : cs_id<A>();
-#pragma unroll 1
-      for (int off = 1; off < 32; off <<= 1) {
-        const S y = cs_shfl<A::NS>(x, off, true);
-        if (lane >= off) x = cs_fw<A>(y, x);
-      }
-      S ex = cs_shfl<A::NS>(x, 1, true);
-      if (lane == 0) ex = cs_id<A>();
-      if (t <= last) cs_put<A::NS>(cr + 2 * t, cs_fw<A>(cin, ex));
-      cin = cs_fw<A>(cin, cs_bcast<A::NS>(x, 31));   // + lane 31's inclusive
+    for (int off = 1; off < tps; off <<= 1) {
+      const S y = cs_shfl<A::NS>(x, off, true);
+      if (lane >= off) x = dir == 0 ? cs_fw<A>(y, x) : cs_bw<A>(x, y);
     }
-  } else {
+    S ex = cs_shfl<A::NS>(x, 1, true);
+    if (lane == 0) ex = cs_id<A>();
+    if (in) cs_put<A::NS>(cr + 2 * t + dir, ex);
+    return;
+  }
+  const int first = blockIdx.x * tps;   // long nodes: one CTA per node
+  if (first >= hd.ntiles) return;
+  const int last = min(first + tps, hd.ntiles) - 1;
+  const int cnt = last - first + 1;
+  S cin = cs_id<A>();   // fold of the tiles before this step (same value in every thread)
+  // step: 256 tiles, tile index j (0 = first tile in scan order); forward scans first..last,
+  // backward scans last..first with the mirrored combine
 #pragma unroll 1
-    for (int b0 = last; b0 >= first; b0 -= 32) {
-      const int t = b0 - lane;
-      S x = t >= first ? cs_get<A::NS>(ag + 2 * t + 1) : cs_id<A>();
+  for (int j0 = 0; j0 < cnt; j0 += 32 * CC_WARPS) {
+    const int j = j0 + threadIdx.x;
+    const int t = dir == 0 ? first + j : last - j;
+    const bool in = j < cnt;
+    const bool wact = j0 + 32 * warp < cnt;   // this warp has tiles (uniform per warp)
+    S ex = cs_id<A>();
+    if (wact) {
+      S x = in ? cs_get<A::NS>(ag + 2 * t + dir) : cs_id<A>();
 #pragma unroll 1
       for (int off = 1; off < 32; off <<= 1) {
         const S y = cs_shfl<A::NS>(x, off, true);
-        if (lane >= off) x = cs_bw<A>(x, y);
+        if (lane >= off) x = dir == 0 ? cs_fw<A>(y, x) : cs_bw<A>(x, y);
       }
-      S ex = cs_shfl<A::NS>(x, 1, true);
+      if (lane == 31) wtot[warp] = x;
+      ex = cs_shfl<A::NS>(x, 1, true);
       if (lane == 0) ex = cs_id<A>();
-      if (t >= first) cs_put<A::NS>(cr + 2 * t + 1, cs_bw<A>(ex, cin));
-      cin = cs_bw<A>(cs_bcast<A::NS>(x, 31), cin);
+    }
+    __syncthreads();
+    if (wact) {
+      S pre = cin;
+#pragma unroll 1
+      for (int w = 0; w < warp; ++w) pre = dir == 0 ? cs_fw<A>(pre, wtot[w]) : cs_bw<A>(wtot[w], pre);
+      if (in) cs_put<A::NS>(cr + 2 * t + dir, dir == 0 ? cs_fw<A>(pre, ex) : cs_bw<A>(ex, pre));
+    }
+    if (j0 + 32 * CC_WARPS < cnt) {   // another step: carry the whole step's fold
+#pragma unroll 1
+      for (int w = 0; w < CC_WARPS; ++w) cin = dir == 0 ? cs_fw<A>(cin, wtot[w]) : cs_bw<A>(wtot[w], cin);
+      __syncthreads();
     }
   }
 }
@@ -895,7 +963,7 @@ __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDe
 }
 
 template <class A, int MODE>
-__global__ void __launch_bounds__(CP_BLOCK, 3) k_cp(LvArgs g, const unsigned char* hpbase,
+__global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const unsigned char* hpbase,
                                                    const HpDesc* descs, int npass, int total,
                                                    int max_tiles, int nrhs, int64_t carr_off,
                                                    int item_lo) {
@@ -1371,7 +1439,10 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   }
   g.tile0 = (int)sr[0];
   const int tiles_run = (int)(sr[1] - sr[0]);
-  const dim3 gt(tiles_run, nrhs);
+  const int nlow = low_parts(pl.d, g.lb, L);
+  pl.low_unused = 0;   // trailing part slots this apply leaves unwritten (the epilogue skips them)
+  g.low_slot0 = pl.hp_npass + (pl.d == 3 ? std::max(0, L - LV_LOGTILE) : 0);
+  const dim3 gt(tiles_run, nrhs, nlow);
   const bool hp = pl.hp_npass > 0;
   const HpDesc* dd = pl.hpdesc.as<HpDesc>();
   static int grid1 = 0, grid2 = 0;   // persistent k_cp: as many CTAs as fit (per instantiation)
@@ -1401,7 +1472,9 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
         carr_off, 0);
     GPM_CUDA(cudaGetLastError());
     LvRecFor<A::NS>* recs = reinterpret_cast<LvRecFor<A::NS>*>(g.aggs);
-    k_cp_carry<A><<<dim3(pl.hp_maxtiles, pl.hp_npass, 2 * nrhs), 32, 0, pl.s2>>>(
+    // grid.x covers the level-11 nodes (two tiles each, CC_WARPS nodes per CTA)
+    k_cp_carry<A><<<dim3((pl.hp_maxtiles + 2 * CC_WARPS - 1) / (2 * CC_WARPS), pl.hp_npass, 2 * nrhs),
+                    32 * CC_WARPS, 0, pl.s2>>>(
         recs, recs + carr_off, dd, pl.hp_npass, pl.hp_maxtiles);
     GPM_CUDA(cudaGetLastError());
     GPM_CUDA(cudaEventRecord(pl.ev_join, pl.s2));
@@ -1419,7 +1492,12 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
                                       (int)sizeof(LvPointsM<NC>)));
         attr = true;
       }
-      k_low2m<A, NC><<<dim3(tiles_run, (nrhs + NC - 1) / NC), CP_BLOCK, sizeof(LvPointsM<NC>), s>>>(
+      // two CTAs per SM (80 KB of staged columns each): the parts only pay while the grid
+      // leaves SMs empty
+      const int groups = (nrhs + NC - 1) / NC;
+      const bool msplit = (int64_t)tiles_run * groups < 148;
+      if (!msplit) pl.low_unused = nlow - 1;
+      k_low2m<A, NC><<<dim3(tiles_run, groups, msplit ? nlow : 1), CP_BLOCK, sizeof(LvPointsM<NC>), s>>>(
           g, nrhs);
     } else {
       k_low2<A><<<gt, CP_BLOCK, lv_smem_fused(), s>>>(g);
@@ -1451,9 +1529,11 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   return GP_OK;
 }
 
-// per-pass contribution slots: carried passes, then (d = 3) one per outer level l1 > 10
+// per-pass contribution slots: carried passes, then (d = 3) one per outer level l1 > 10, then
+// the parts 1.. of the fused low kernels
 int level_nparts(const Plan& pl) {
-  return pl.hp_npass + (pl.d == 3 ? std::max(0, pl.L - LV_LOGTILE) : 0);
+  return pl.hp_npass + (pl.d == 3 ? std::max(0, pl.L - LV_LOGTILE) : 0) +
+         low_parts(pl.d, pl.d == 2 ? pl.near_lb2 : pl.near_lb3, pl.L) - 1;
 }
 
 // pack the rank-order point records (t1, t2, t3, u) used by every level kernel
@@ -1493,6 +1573,12 @@ size_t level_pt_bytes() { return sizeof(Pt4); }
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
   const int P = pl.P;
+#ifdef GPM_FEW   // experiment builds (build.py GPM_EXTRA_FLAGS): the three bench algebras only
+  if (kind == 0 && pl.d == 2 && P == 1 && !prod) return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
+  if (kind == 0 && pl.d == 2 && P == 1 && prod) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
+  if (kind == 0 && pl.d == 3 && P == 2 && !prod) return lv_run<Alg<2, 4, false>>(pl, nrhs, s, launches);
+  return fail(GP_ERR_UNSUPPORTED, "GPM_FEW experiment build");
+#else
   if (kind != 0) {   // lengthscale gradient: moment order p + 1
     if (prod) {        // d = 2 product form, nu <= 7/2 ((p+2)^2 moments per channel)
       if (pl.d != 2 || P > 3)
@@ -1543,6 +1629,7 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
     case 3: return lv_run<Alg<3, 4, false>>(pl, nrhs, s, launches);
     default: return lv_run<Alg<4, 4, false>>(pl, nrhs, s, launches);
   }
+#endif
 }
 
 int64_t level_tiles(int64_t n) { return (n + LV_TILE - 1) / LV_TILE; }

@@ -123,13 +123,14 @@ struct Plan {
   // d >= 2: side stream for the carried-pass aggregates (independent of the low levels)
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int low_unused = 0;       // trailing low-kernel part slots the last apply left unwritten
   int part_zero_cols = 0;   // columns of `part` whose never-written tail slots are zeroed
   // gp_kmvm_host pipelining: copy streams and per-slot events (in, compute, out) x 3
   cudaStream_t hs_in = nullptr, hs_out = nullptr;
   cudaEvent_t hev[9] = {};
   std::vector<char> hp_tail;        // carried pass has an inactive tail (slot must be zeroed)
   DevBuf part;                      // d>=2: per-pass contribution slots [nrhs][nparts][n]
-  int near_lb2 = 4, near_lb3 = 8, near_lb3m = 5;   // near-field block log2 sizes (tuned)
+  int near_lb2 = 4, near_lb3 = 7, near_lb3m = 5;   // near-field block log2 sizes (tuned)
   // d = 1 launch geometry
   int d1_grid = 0, d1_path = 1, d1_force = 0, d1_shape = -1;   // d1_shape: requested (-1 auto)
   int d1_shape_used = 0;            // the shape of the single-chunk kernel in use
