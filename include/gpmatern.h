@@ -53,8 +53,10 @@ enum { GP_MEAN_NONE = 0, GP_MEAN_AFFINE = 1, GP_MEAN_BASIS = 2 }; /* P:73-82 [eq
  *   L1:      K(x,x') = s^2 k_nu( sum_k |x_k - x'_k| / l_k )        (§2.3)
  *   product: K(x,x') = s^2 prod_k k_nu( |x_k - x'_k| / l_k )
  * with k_nu the half-integer closed forms of P:1273-1275.  Supported:
- *   two_nu in {1,3,5,7,9} (nu = 7/2, 9/2: P:1276-1277); d in {1,2,3}; form L1 for every d and nu; form PRODUCT for
- *   d <= 2 and every nu ((p+1)^2 mixed moments per channel; d = 3 only for two_nu = 1)
+ *   two_nu in {1,3,5,7,9} (nu = 7/2, 9/2: P:1276-1277); d in {1,2,3}; forms L1 and
+ *   PRODUCT for every d and nu (PRODUCT, d = 2: (p+1)^2 mixed moments per channel; d = 3:
+ *   (p+1)^2 re-weighted passes of the (p+1)-moment scan per level, P:487-509 [Prop 2] with both
+ *   split factors separated -- exact, about (p+1)^2 times the cost of the L1 apply)
  *   (for d == 1 or two_nu == 1 the two forms coincide, and form is ignored).
  * Per-dimension lengthscales are reading R2 (the paper uses one l). */
 typedef struct {

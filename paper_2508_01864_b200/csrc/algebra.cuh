@@ -178,18 +178,43 @@ __device__ __forceinline__ double readc_poly(const double* R, double beta) {
   }
 }
 
+// x^e, small runtime e >= 0 (x^0 = 1 also at x = 0)
+__device__ __forceinline__ double powi(double x, int e) {
+  double r = 1.0;
+  for (int i = 0; i < e; ++i) r *= x;
+  return r;
+}
+// target factor of the separated split kernel: sum_{q=a..P} a_q C(q,a) beta^{q-a} (runtime a)
+template <int P>
+__device__ __forceinline__ double tpoly(int a, double beta) {
+  double acc = 0.0;
+#pragma unroll
+  for (int q = P; q >= 0; --q)
+    if (q >= a) acc = fma(acc, beta, mcoef(P, q) * binom(q, a));
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // Multi-channel algebra for the d >= 2 level passes.
 //   NCH channels (2 for d = 2: side of the x1 split; 4 for d = 3: sides of the x1 and
 //   inner x2 splits).  A source on channel c feeds targets on channel NCH-1-c.
 //   NM moments per channel: P+1 (L1) or (P+1)^2 (product, d = 2).
-template <int P_, int NCH_, bool PROD_, int KIND_ = 0>
+//
+// Product form, d = 3 (P3; P:414-416, P:487-509 [Prop 2]): each split factor separates,
+//   k(a_s + a_t) = sum_{a<=P} [a_s^a e^{-a_s}] [e^{-a_t} sum_{q>=a} a_q C(q,a) a_t^{q-a}],
+// so the pair sum over a node is sum_{a,b} T_a(alpha1_t) T_b(alpha2_t) times a scan along the
+// last coordinate with source weights u alpha1^a alpha2^b e^{-alpha1-alpha2} and NO split
+// offset: the L1 engine (P+1 moments per channel) run NAB = (P+1)^2 times per level with
+// re-weighted sources and a target multiplier (tpoly), instead of a (P+1)^3-moment state.
+template <int P_, int NCH_, bool PROD_, int KIND_ = 0, bool P3_ = false>
 struct Alg {
   static constexpr int P = P_;          // moment order (gradient: nu - 1/2 + 1)
   static constexpr int NCH = NCH_;
   static constexpr bool PROD = PROD_;   // product form
   static constexpr int KIND = KIND_;
+  static constexpr bool P3 = P3_;       // d = 3 product form by (a, b) passes of the L1 engine
   static constexpr int NQ = P + 1;
+  static constexpr int NAB = P3 ? NQ * NQ : 1;
   static constexpr int NM = PROD ? NQ * NQ : NQ;
   static constexpr int NS = NCH * NM;
 

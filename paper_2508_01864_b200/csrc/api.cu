@@ -28,15 +28,12 @@ static gp_status check_kernel(const gp_kernel* k, int d) {
     if (!(k->lengthscale[j] > 0) || !std::isfinite(k->lengthscale[j]))
       return fail(GP_ERR_INVALID_ARG, "lengthscale[" + std::to_string(j) + "] must be > 0");
   static const char* kSupp =
-      "supported: two_nu in {1,3,5,7,9} with the L1 form (d<=3) and with the PRODUCT form "
-      "(d<=2); PRODUCT with d=3 only for two_nu=1 (where it equals L1)";
+      "supported: two_nu in {1,3,5,7,9}, d in {1,2,3}, forms L1 and PRODUCT";
   if (k->two_nu != 1 && k->two_nu != 3 && k->two_nu != 5 && k->two_nu != 7 && k->two_nu != 9)
     return fail(GP_ERR_UNSUPPORTED,
                 "two_nu=" + std::to_string(k->two_nu) + " unsupported; " + kSupp);
   if (k->form != GP_FORM_L1 && k->form != GP_FORM_PRODUCT)
     return fail(GP_ERR_INVALID_ARG, "form must be GP_FORM_L1 or GP_FORM_PRODUCT");
-  if (k->form == GP_FORM_PRODUCT && d == 3 && k->two_nu != 1)
-    return fail(GP_ERR_UNSUPPORTED, std::string("this PRODUCT-form kernel is not implemented; ") + kSupp);
   return GP_OK;
 }
 

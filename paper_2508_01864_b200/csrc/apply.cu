@@ -17,6 +17,7 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
 gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
 size_t level_pt_bytes();
 int level_nparts(const Plan& pl);
+int level_nab(const Plan& pl);
 gp_status level_setup(Plan& pl, cudaStream_t s);
 int64_t level_tiles(int64_t n);
 
@@ -121,7 +122,7 @@ static gp_status level_buffers(Plan& pl, int nrhs) {
   if (pl.pts.bytes < level_pt_bytes() * need) GPM_TRY(pl.pts.alloc(level_pt_bytes() * need));
   // tile aggregates and (k_cp_carry) tile carries, same layout
   const size_t ag = 2 * level_rec_bytes(pl.d, pl.form == GP_FORM_PRODUCT, pl.P) * 2 *
-                   (size_t)level_tiles(pl.n) * nrhs *
+                   (size_t)level_tiles(pl.n) * nrhs * level_nab(pl) *
                    std::max(1, pl.hp_npass);
   if (pl.aggs.bytes < ag) GPM_TRY(pl.aggs.alloc(ag));
   const size_t pb = sizeof(double) * (size_t)std::max(1, level_nparts(pl)) * pl.n * nrhs;

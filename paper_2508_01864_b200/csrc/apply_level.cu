@@ -102,7 +102,10 @@ __device__ __forceinline__ double kpoly(double s) {
 template <class A, int D>
 __device__ __forceinline__ double kval(double d1, double d2, double d3, const double* tab) {
   constexpr int P = A::P;
-  if constexpr (!A::PROD) {
+  if constexpr (A::P3) {   // product form, d = 3 (P:416 [eq product_kernel])
+    const double e = fexp_neg((d1 + d2) + d3, tab);
+    return e * (kpoly<P, 0>(d1) * kpoly<P, 0>(d2) * kpoly<P, 0>(d3));
+  } else if constexpr (!A::PROD) {
     // L1: sum_q c_q s^q e^{-s} with the read coefficients of the algebra (Matern a_q for
     // KIND 0, gradient b_q = a_{q-1} - q a_q for KIND 1), Horner in s
     const double s = D == 3 ? (d1 + d2) + d3 : d1 + d2;
@@ -382,6 +385,38 @@ __device__ __forceinline__ void seg_engine(const TItems& it, int ls, double* of,
   __syncthreads();   // scratch reuse
 }
 
+// One level of a tile kernel: the engine once, or (P3, d = 3 product form) once per (a, b)
+// with sources re-weighted by alpha1^a alpha2^b and the target factors T_a(alpha1) T_b(alpha2)
+// (algebra.cuh); it.ea = e^{-(alpha1+alpha2)} as for L1, the split offset of the scan is 0.
+template <class A>
+__device__ __forceinline__ void level_apply(TItems& it, const double* a1, const double* a2, int ls,
+                                            double* of, TScratch<A>& sc) {
+  if constexpr (!A::P3) {
+    seg_engine<A>(it, ls, of, sc);
+  } else {
+    double ub[CP_ITEMS], tot[CP_ITEMS];
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      ub[k] = it.u[k];
+      tot[k] = 0.0;
+      it.a[k] = 0.0;
+    }
+#pragma unroll 1
+    for (int ab = 0; ab < A::NAB; ++ab) {
+      const int a = ab / A::NQ, b = ab - a * A::NQ;
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k) it.u[k] = ub[k] * (powi(a1[k], a) * powi(a2[k], b));
+      double o[CP_ITEMS];
+      seg_engine<A>(it, ls, o, sc);
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k)
+        tot[k] = fma(o[k], tpoly<A::P>(a, a1[k]) * tpoly<A::P>(b, a2[k]), tot[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) of[k] = tot[k];
+  }
+}
+
 // Gaps from the scan coordinates y[k] (ypre: y of the position before the thread's first,
 // ignored at a node start); padding items (o < 0) repeat the last y (gap 0).
 __device__ __forceinline__ void titems_gaps(TItems& it, const double* y, double ypre,
@@ -643,7 +678,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low3(LvArgs g) {
     for (int l2 = 4; l2 <= l1; ++l2) {
       const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
       TItems it;
-      double y[CP_ITEMS];
+      double y[CP_ITEMS], a1k[CP_ITEMS], a2k[CP_ITEMS];
       int qq[CP_ITEMS];
       load_ord8(ord, i0, cnt, (int)T0, qq);
 #pragma unroll
@@ -657,7 +692,9 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low3(LvArgs g) {
         it.o[k] = r;
         y[k] = r >= 0 ? Pt.t3[r] : (k > 0 ? y[k - 1] : 0.0);
         it.u[k] = r >= 0 ? Pt.u[r] : 0.0;
-        it.a[k] = act ? fabs(Pt.t1[r] - Pt.t1[mid1]) + fabs(Pt.t2[r] - Pt.t2[Pt.o2[mid2]]) : 0.0;
+        a1k[k] = act ? fabs(Pt.t1[r] - Pt.t1[mid1]) : 0.0;
+        a2k[k] = act ? fabs(Pt.t2[r] - Pt.t2[Pt.o2[mid2]]) : 0.0;
+        it.a[k] = a1k[k] + a2k[k];
         it.ch[k] = act ? 2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1) : -1;
       }
       const bool nstart = (i0 & ((1 << l2) - 1)) == 0;
@@ -665,7 +702,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low3(LvArgs g) {
           (!nstart && i0 <= cnt) ? Pt.t3[Pt.o2[__ldg(ord + i0 - 1) - (int)T0]] : 0.0;
       titems_gaps(it, y, ypre, nstart, sc.tab);
       double of[CP_ITEMS];
-      seg_engine<A>(it, l2, of, sc);
+      level_apply<A>(it, a1k, a2k, l2, of, sc);
 #pragma unroll
       for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
     }
@@ -718,7 +755,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_mid3(LvArgs g) {
   for (int l2 = lb2 + 1; l2 <= LV_LOGTILE; ++l2) {
     const int* ord = g.ord3 + (size_t)ord3_index(l1, l2) * g.n + T0;
     TItems it;
-    double y[CP_ITEMS];
+    double y[CP_ITEMS], a1k[CP_ITEMS], a2k[CP_ITEMS];
     load_ord8(ord, i0, cnt, (int)T0, it.o);          // tile-local position = point index
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
@@ -728,14 +765,16 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_mid3(LvArgs g) {
       const bool act = q >= 0 && T0 + mid2 < g.n;
       y[k] = q >= 0 ? Pt.t3[q] : (k > 0 ? y[k - 1] : 0.0);
       it.u[k] = q >= 0 ? Pt.u[q] : 0.0;
-      it.a[k] = act ? fabs(Pt.t1[q] - m1) + fabs(Pt.t2[q] - Pt.t2[mid2]) : 0.0;
+      a1k[k] = act ? fabs(Pt.t1[q] - m1) : 0.0;
+      a2k[k] = act ? fabs(Pt.t2[q] - Pt.t2[mid2]) : 0.0;
+      it.a[k] = a1k[k] + a2k[k];
       it.ch[k] = act ? 2 * ((Pt.o2[q] >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1) : -1;
     }
     const bool nstart = (i0 & ((1 << l2) - 1)) == 0;
     const double ypre = (!nstart && i0 <= cnt) ? Pt.t3[__ldg(ord + i0 - 1) - (int)T0] : 0.0;
     titems_gaps(it, y, ypre, nstart, sc.tab);
     double of[CP_ITEMS];
-    seg_engine<A>(it, l2, of, sc);
+    level_apply<A>(it, a1k, a2k, l2, of, sc);
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
   }
@@ -746,7 +785,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_mid3(LvArgs g) {
 
 // ---- one pass whose segments span several tiles (mode 1: aggregates, 2: apply)
 struct Elem {
-  double y, u, a;
+  double y, u, a, a2;   // a: the x1 split offset (d = 2: the only one), a2: the x2 split offset
   int r, ch;
 };
 
@@ -758,6 +797,7 @@ __device__ __forceinline__ Elem lv_elem(const LvArgs& g, int64_t pos) {
     const int64_t mid = ((pos >> l) << l) + (int64_t(1) << (l - 1));
     const Pt4 p = g.pts[r];
     el.a = fabs(p.t1 - __ldg(g.t1 + mid));
+    el.a2 = 0.0;
     el.ch = (r >> (l - 1)) & 1;
     el.y = p.t2;
     el.u = p.u;
@@ -769,7 +809,8 @@ __device__ __forceinline__ Elem lv_elem(const LvArgs& g, int64_t pos) {
     const int64_t mid1 = ((int64_t)(q >> l1) << l1) + (int64_t(1) << (l1 - 1));
     const int64_t mid2 = ((pos >> l2) << l2) + (int64_t(1) << (l2 - 1));
     const Pt4 p = g.pts[r];
-    el.a = fabs(p.t1 - __ldg(g.t1 + mid1)) + fabs(p.t2 - __ldg(g.t2 + __ldg(g.ord2l1 + mid2)));
+    el.a = fabs(p.t1 - __ldg(g.t1 + mid1));
+    el.a2 = fabs(p.t2 - __ldg(g.t2 + __ldg(g.ord2l1 + mid2)));
     el.ch = 2 * ((r >> (l1 - 1)) & 1) + ((q >> (l2 - 1)) & 1);
     el.y = p.t3;
     el.u = p.u;
@@ -791,7 +832,8 @@ __device__ __forceinline__ double lv_y(const LvArgs& g, int64_t pos) {
 // staged structure per apply at 36 B per position).
 struct HpView {
   const double* d;
-  const double* a;
+  const double* a;      // split offset (d = 3 L1: alpha1 + alpha2; P3: alpha1)
+  const double* a2;     // P3 (d = 3 product form) only: alpha2, 28 B per position
   const unsigned* rc;   // rank | channel << 30; CP_NONE: padding
 };
 constexpr unsigned CP_RMASK = 0x3FFFFFFFu;
@@ -801,22 +843,24 @@ constexpr unsigned CP_NONE = 0xFFFFFFFFu;   // rank field CP_RMASK: no point (n 
 __host__ __device__ inline int64_t hp_padded(int64_t nact) {
   return (nact + LV_TILE - 1) / LV_TILE * LV_TILE;
 }
-__host__ __device__ inline size_t hp_bytes(int64_t nact) {
-  return ((size_t)hp_padded(nact) * 20 + 255) & ~size_t(255);
+__host__ __device__ inline size_t hp_bytes(int64_t nact, bool p3) {
+  return ((size_t)hp_padded(nact) * (p3 ? 28 : 20) + 255) & ~size_t(255);
 }
-__host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nact) {
+__host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nact, bool p3) {
   const int64_t np = hp_padded(nact);
   HpView v;
   v.d = reinterpret_cast<const double*>(base);
   v.a = v.d + np;
-  v.rc = reinterpret_cast<const unsigned*>(v.a + np);
+  v.a2 = p3 ? v.a + np : nullptr;
+  v.rc = reinterpret_cast<const unsigned*>(v.a + (p3 ? 2 : 1) * np);
   return v;
 }
 
-__global__ void k_hp_prep(LvArgs g, unsigned char* base) {
-  HpView v = hp_view(base, g.n_act);
+__global__ void k_hp_prep(LvArgs g, unsigned char* base, bool p3) {
+  HpView v = hp_view(base, g.n_act, p3);
   double* d = const_cast<double*>(v.d);
   double* a = const_cast<double*>(v.a);
+  double* a2 = const_cast<double*>(v.a2);
   unsigned* rc = const_cast<unsigned*>(v.rc);
   const int64_t smask = (int64_t(1) << g.lseg) - 1;
   const int64_t np = hp_padded(g.n_act);
@@ -827,10 +871,12 @@ __global__ void k_hp_prep(LvArgs g, unsigned char* base) {
       const Elem el = lv_elem(g, pos);
       const double dl = (pos & smask) == 0 ? 0.0 : el.y - lv_y(g, pos - 1);
       d[w] = dl;
-      a[w] = el.a;
+      a[w] = p3 ? el.a : el.a + el.a2;
+      if (p3) a2[w] = el.a2;
       rc[w] = (unsigned)el.r | ((unsigned)el.ch << 30);
     } else {   // identity: no gap; alpha = 800 makes e^{-alpha} exactly 0 (fexp_neg: d >= 708)
       d[w] = 0.0; a[w] = 800.0; rc[w] = CP_NONE;
+      if (p3) a2[w] = 0.0;
     }
   }
 }
@@ -856,14 +902,20 @@ struct HpDesc {
 // (Alg::inject_at), warp scans, block carry, apply loops.
 //   MODE 1: tile aggregates (forward, backward) -> aggs;
 //   MODE 2: apply, with the tile carries folded from MODE 1's aggregates of the node.
-struct CpStage {
+template <bool P3>
+struct CpStageT {
   double d[LV_TILE], a[LV_TILE];
   unsigned rc[LV_TILE];   // rank | channel << 30
 };
-struct CpSmem {
-  CpStage st[2];
+template <>
+struct CpStageT<true> {   // d = 3 product form: both split offsets
+  double d[LV_TILE], a[LV_TILE], a2[LV_TILE];
+  unsigned rc[LV_TILE];
 };
-constexpr unsigned CP_STAGE_BYTES = 20u * LV_TILE;
+template <bool P3>
+struct CpSmemT {
+  CpStageT<P3> st[2];
+};
 
 // Tile carries of every node, once per (column, pass, direction): an exclusive scan of the
 // tile aggregates of k_cp<1> (forward: tiles in order; backward: reversed), one warp per
@@ -950,16 +1002,41 @@ __device__ __forceinline__ int cp_pass_at(const HpDesc* descs, int npass, int p,
   return p;
 }
 
-// thread 0: bulk-copy tile `item` of pass p into stage buffer st (expects 36 KB on bar)
+// thread 0: bulk-copy tile `item` of pass p into stage buffer st (20 / 28 KB on bar)
+template <bool P3>
 __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDesc* descs, int p,
-                                         int item, CpStage& st, uint64_t* bar) {
+                                         int item, CpStageT<P3>& st, uint64_t* bar) {
   const HpDesc hd = descs[p];
   const int64_t T0 = (int64_t)(item - hd.item0) * LV_TILE;
-  const HpView v = hp_view(hpbase + hd.off, hd.nact);
-  mbar_expect_tx(bar, CP_STAGE_BYTES);
+  const HpView v = hp_view(hpbase + hd.off, hd.nact, P3);
+  mbar_expect_tx(bar, (P3 ? 28u : 20u) * LV_TILE);
   tma_load_1d(st.d, v.d + T0, 8 * LV_TILE, bar);
   tma_load_1d(st.a, v.a + T0, 8 * LV_TILE, bar);
+  if constexpr (P3) tma_load_1d(st.a2, v.a2 + T0, 8 * LV_TILE, bar);
   tma_load_1d(st.rc, v.rc + T0, 4 * LV_TILE, bar);
+}
+
+// staged split offsets as the engine sees them: L1 / d = 2: the offset alpha and e^{-alpha};
+// P3: offset 0 (the split factors sit in the source weight and the target factor), e^{-(a1+a2)}
+template <bool P3>
+__device__ __forceinline__ double cp_aoff(const CpStageT<P3>& E, int z) {
+  if constexpr (P3) return 0.0;
+  else return E.a[z];
+}
+template <bool P3>
+__device__ __forceinline__ double cp_asum(const CpStageT<P3>& E, int z) {
+  if constexpr (P3) return E.a[z] + E.a2[z];
+  else return E.a[z];
+}
+template <bool P3>
+__device__ __forceinline__ double cp_srcw(const CpStageT<P3>& E, int z, int pa, int pb) {
+  if constexpr (P3) return powi(E.a[z], pa) * powi(E.a2[z], pb);
+  else return 1.0;
+}
+template <int P, bool P3>
+__device__ __forceinline__ double cp_tgtw(const CpStageT<P3>& E, int z, int pa, int pb) {
+  if constexpr (P3) return tpoly<P>(pa, E.a[z]) * tpoly<P>(pb, E.a2[z]);
+  else return 1.0;
 }
 
 template <class A, int MODE>
@@ -971,7 +1048,8 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
   const int b0 = item_lo + (int)blockIdx.x;
   using S = CSt<A::NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  CpSmem& SM = *reinterpret_cast<CpSmem*>(smem_raw);
+  using Stage = CpStageT<A::P3>;
+  CpSmemT<A::P3>& SM = *reinterpret_cast<CpSmemT<A::P3>*>(smem_raw);
   __shared__ CpScratch<A> sc;
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ double s_tab[64];
@@ -1010,7 +1088,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll 1
   for (int item = b0; item < total; item += G, ++j) {
     const int sidx = j & 1;
-    CpStage& E = SM.st[sidx];
+    Stage& E = SM.st[sidx];
     mbar_wait(&bar[sidx], (j >> 1) & 1);
     p = cp_pass_at(descs, npass, p, item);
     const HpDesc hd = descs[p];
@@ -1024,15 +1102,22 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
     for (int k = 0; k < CP_ITEMS; ++k) {
       const int z = cpz(i0 + k);
       ek[k] = fexp_neg(E.d[z], s_tab);
-      eak[k] = fexp_neg(E.a[z], s_tab);
+      eak[k] = fexp_neg(cp_asum(E, z), s_tab);
     }
+    // P3 (d = 3 product form): every column runs NAB = (P+1)^2 sub-passes (a, b) with sources
+    // re-weighted by alpha1^a alpha2^b and the target factor T_a(alpha1) T_b(alpha2); each
+    // sub-pass has its own tile aggregates / carries (index cc), the outputs are summed
+    double ur[CP_ITEMS], tot[CP_ITEMS];
 #pragma unroll 1
-    for (int c = 0; c < nrhs; ++c) {
+    for (int cc = 0; cc < nrhs * A::NAB; ++cc) {
+      const int c = cc / A::NAB, ab = cc - c * A::NAB;
+      const int pa = ab / A::NQ, pb = ab - pa * A::NQ;
       LvRecFor<A::NS>* aggs =
-          reinterpret_cast<LvRecFor<A::NS>*>(g.aggs) + ((int64_t)c * npass + p) * 2 * max_tiles;
+          reinterpret_cast<LvRecFor<A::NS>*>(g.aggs) + ((int64_t)cc * npass + p) * 2 * max_tiles;
       double uc[CP_ITEMS], of[CP_ITEMS];
+      if (ab == 0) {
 #pragma unroll
-      for (int k = 0; k < CP_ITEMS; ++k) uc[k] = un[k];
+      for (int k = 0; k < CP_ITEMS; ++k) { ur[k] = un[k]; tot[k] = 0.0; }
       // prefetch the sources of the next (tile, column)
       if (c + 1 < nrhs) {
         const Pt4* pn = g.pts + (int64_t)(c + 1) * g.n;
@@ -1042,13 +1127,19 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
           un[k] = r != CP_RMASK ? pn[r].u : 0.0;
         }
       } else if (item + G < total) {
-        CpStage& En = SM.st[sidx ^ 1];
+        Stage& En = SM.st[sidx ^ 1];
         mbar_wait(&bar[sidx ^ 1], ((j + 1) >> 1) & 1);
 #pragma unroll
         for (int k = 0; k < CP_ITEMS; ++k) {
           const unsigned r = En.rc[cpz(i0 + k)] & CP_RMASK;
           un[k] = r != CP_RMASK ? g.pts[r].u : 0.0;
         }
+      }
+      }
+#pragma unroll
+      for (int k = 0; k < CP_ITEMS; ++k) {
+        if constexpr (A::P3) uc[k] = ur[k] * cp_srcw(E, cpz(i0 + k), pa, pb);
+        else uc[k] = ur[k];
       }
       if (MODE == 2) {   // tile carries (k_cp_carry); read after the next barrier
         const double* cr = reinterpret_cast<const double*>(aggs + carr_off + 2 * t);
@@ -1067,7 +1158,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
         for (int k = CP_ITEMS - 1; k >= 0; --k) {    // forward: reference at item 7
           const int z = cpz(i0 + k);
-          A::inject_at(XF.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], D, Ee);
+          A::inject_at(XF.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], D, Ee);
           D += E.d[z];
           Ee *= ek[k];
         }
@@ -1076,7 +1167,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
           const int z = cpz(i0 + k);
           Db += E.d[z];
           Eb *= ek[k];
-          A::inject_at(XB.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], Db, Eb);
+          A::inject_at(XB.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], Db, Eb);
         }
         // spans after my last position / before my first one within the tile
         double incl = D;   // inclusive prefix sum of the thread spans (warp)
@@ -1134,7 +1225,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
         for (int k = CP_ITEMS - 1; k >= 0; --k) {    // reference at item 7
           const int z = cpz(i0 + k);
-          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], D, Ee);
           D += E.d[z];
           Ee *= ek[k];
         }
@@ -1168,7 +1259,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
             const int z = cpz(i0 + k);
             A::advance_all(M, E.d[z], ek[k]);
             const int ch = E.rc[z] >> 30;
-            const double a = E.a[z], ea = eak[k];
+            const double a = cp_aoff(E, z), ea = eak[k];
             of[k] = A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
           }
@@ -1185,7 +1276,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
           const int z = cpz(i0 + k);
           D += E.d[z];
           Ee *= ek[k];
-          A::inject_at(X.M, E.rc[z] >> 30, uc[k], E.a[z], eak[k], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], D, Ee);
         }
         X.D = D; X.E = Ee;
 #pragma unroll 1
@@ -1218,12 +1309,17 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
             const int z = cpz(i0 + k);
             const unsigned rcz = E.rc[z];
             const int ch = rcz >> 30;
-            const double a = E.a[z], ea = eak[k];
+            const double a = cp_aoff(E, z), ea = eak[k];
             const double val = of[k] + A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
             A::advance_all(M, E.d[z], ek[k]);
             const unsigned r = rcz & CP_RMASK;
-            if (r != CP_RMASK) slot[r] = val;
+            if constexpr (A::P3) {
+              tot[k] = fma(val, cp_tgtw<A::P>(E, z, pa, pb), tot[k]);
+              if (ab == A::NAB - 1 && r != CP_RMASK) slot[r] = tot[k];
+            } else {
+              if (r != CP_RMASK) slot[r] = val;
+            }
           }
         }
       }
@@ -1257,10 +1353,10 @@ static cudaError_t lv_set_attrs() {
       return e;
   }
   if ((e = cudaFuncSetAttribute(k_cp<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(CpSmem))))
+                                (int)sizeof(CpSmemT<A::P3>))))
     return e;
   return cudaFuncSetAttribute(k_cp<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(CpSmem));
+                              (int)sizeof(CpSmemT<A::P3>));
 }
 
 // The carried passes of a plan, in apply order: (ord, ord2l1, lseg, l1, n_act).
@@ -1294,6 +1390,10 @@ static std::vector<HPass> high_passes(const Plan& pl) {
   return v;
 }
 
+// d = 3 product form with nu >= 3/2: the (a, b) sub-passes of algebra.cuh (P3)
+bool level_p3(const Plan& pl) { return pl.d == 3 && pl.form == GP_FORM_PRODUCT && pl.P > 0; }
+int level_nab(const Plan& pl) { return level_p3(pl) ? (pl.P + 1) * (pl.P + 1) : 1; }
+
 static LvArgs lv_base_args(const Plan& pl) {
   LvArgs g{};
   const int64_t n = pl.n;
@@ -1318,8 +1418,9 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     GPM_CUDA(cudaEventCreateWithFlags(&pl.ev_join, cudaEventDisableTiming));
   }
   const std::vector<HPass> hp = high_passes(pl);
+  const bool p3 = level_p3(pl);
   size_t total = 0;
-  for (const HPass& h : hp) total += hp_bytes(h.nact);
+  for (const HPass& h : hp) total += hp_bytes(h.nact, p3);
   if (total == 0) return GP_OK;
   GPM_TRY(pl.hpbuf.alloc(total));
   {
@@ -1330,7 +1431,7 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     for (const HPass& h : hp) {
       const int nt = (int)((h.nact + LV_TILE - 1) / LV_TILE);
       dv.push_back({(int64_t)o, h.nact, h.lseg, nt, items, 0});
-      o += hp_bytes(h.nact);
+      o += hp_bytes(h.nact, p3);
       mt = std::max(mt, nt);
       items += nt;
     }
@@ -1352,9 +1453,9 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     g.l1 = h.l1;
     g.n_act = h.nact;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hp_padded(h.nact) + 255) / 256, 148 * 8));
-    k_hp_prep<<<grid, 256, 0, s>>>(g, pl.hpbuf.as<unsigned char>() + off);
+    k_hp_prep<<<grid, 256, 0, s>>>(g, pl.hpbuf.as<unsigned char>() + off, p3);
     GPM_CUDA(cudaGetLastError());
-    off += hp_bytes(h.nact);
+    off += hp_bytes(h.nact, p3);
   }
   pl.struct_bytes += (int64_t)total;
   return GP_OK;
@@ -1450,8 +1551,8 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     int dev = 0, sms = 0, o1 = 0, o2 = 0;
     GPM_CUDA(cudaGetDevice(&dev));
     GPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmem)));
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmem)));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmemT<A::P3>)));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmemT<A::P3>)));
     grid1 = std::max(1, o1) * sms;
     grid2 = std::max(1, o2) * sms;
   }
@@ -1466,14 +1567,15 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     // the carried-pass tile aggregates do not depend on the low levels: side stream
     GPM_CUDA(cudaEventRecord(pl.ev_fork, s));
     GPM_CUDA(cudaStreamWaitEvent(pl.s2, pl.ev_fork, 0));
-    const int64_t carr_off = (int64_t)g.agg_stride * nrhs;   // carries after the aggregates
-    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmem), pl.s2>>>(
+    const int64_t carr_off = (int64_t)g.agg_stride * nrhs * A::NAB;   // carries after the aggregates
+    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmemT<A::P3>), pl.s2>>>(
         g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
         carr_off, 0);
     GPM_CUDA(cudaGetLastError());
     LvRecFor<A::NS>* recs = reinterpret_cast<LvRecFor<A::NS>*>(g.aggs);
     // grid.x covers the level-11 nodes (two tiles each, CC_WARPS nodes per CTA)
-    k_cp_carry<A><<<dim3((pl.hp_maxtiles + 2 * CC_WARPS - 1) / (2 * CC_WARPS), pl.hp_npass, 2 * nrhs),
+    k_cp_carry<A><<<dim3((pl.hp_maxtiles + 2 * CC_WARPS - 1) / (2 * CC_WARPS), pl.hp_npass,
+                         2 * nrhs * A::NAB),
                     32 * CC_WARPS, 0, pl.s2>>>(
         recs, recs + carr_off, dd, pl.hp_npass, pl.hp_maxtiles);
     GPM_CUDA(cudaGetLastError());
@@ -1519,9 +1621,9 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     const int nit = (int)(sr[3] - sr[2]);
     if (nit > 0) {
-      k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmem), s>>>(
+      k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmemT<A::P3>), s>>>(
           g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, (int)sr[3], pl.hp_maxtiles, nrhs,
-          (int64_t)g.agg_stride * nrhs, (int)sr[2]);
+          (int64_t)g.agg_stride * nrhs * A::NAB, (int)sr[2]);
       *launches += 1;
       GPM_CUDA(cudaGetLastError());
     }
@@ -1621,6 +1723,14 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
     if (P == 2) return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
     if (P == 3) return lv_run<Alg<3, 2, true>>(pl, nrhs, s, launches);
     return lv_run<Alg<4, 2, true>>(pl, nrhs, s, launches);
+  }
+  if (level_p3(pl)) {   // d = 3 product form (nu = 1/2 is the L1 kernel)
+    switch (P) {
+      case 1: return lv_run<Alg<1, 4, false, 0, true>>(pl, nrhs, s, launches);
+      case 2: return lv_run<Alg<2, 4, false, 0, true>>(pl, nrhs, s, launches);
+      case 3: return lv_run<Alg<3, 4, false, 0, true>>(pl, nrhs, s, launches);
+      default: return lv_run<Alg<4, 4, false, 0, true>>(pl, nrhs, s, launches);
+    }
   }
   switch (P) {
     case 0: return lv_run<Alg<0, 4, false>>(pl, nrhs, s, launches);

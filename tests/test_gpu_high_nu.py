@@ -97,9 +97,11 @@ def test_high_nu_product_d2_multilevel_multirhs(gpm, two_nu):
 
 
 def test_high_nu_unsupported(gpm):
+    """The d = 3 product form has no lengthscale-gradient MVM (include/gpmatern.h)."""
     x = _pts(300, 3, 1)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1, 0.1), form=1))
     with pytest.raises(gpm.GPError) as e:
-        gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1, 0.1), form=1))
+        plan.kmvm_dlengthscale(to_dev(np.ones(300)))
     assert e.value.name == "UNSUPPORTED"
 
 

@@ -135,7 +135,40 @@ def test_d3_all_rows(gpm, two_nu, n):
     check_rows(out, x, v, two_nu, "l1", ell, 1.1, what=f"d3 nu={two_nu}/2 n={n}")
 
 
-@pytest.mark.parametrize("d,form", [(1, 0), (2, 0), (2, 1), (3, 0)])
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
+@pytest.mark.parametrize("n", [1, 2, 5, 64, 1000, 2049, 5000])
+def test_d3_product_all_rows(gpm, two_nu, n):
+    """Product form at d = 3 (P:416 [eq product_kernel], P:487-509 [Prop 2]): the
+    (p+1)^2 re-weighted passes per level against the dense definition, every row, ties."""
+    x = _points("ties" if n % 2 else "uniform", n, 3, 9 * n + two_nu)
+    v = np.random.default_rng(n + 4).standard_normal(n)
+    ell = (0.2, 0.3, 0.5)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.1, form=1))
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "product", ell, 1.1, what=f"d3 product nu={two_nu}/2 n={n}")
+
+
+@pytest.mark.parametrize("two_nu,n,nrhs", [(3, 70_001, 2), (5, 33_000, 1), (3, 200_003, 1)])
+def test_d3_product_multilevel_rows(gpm, two_nu, n, nrhs):
+    """d = 3 product form with carried passes and outer levels > 10 (k_mid3, k_cp sub-passes),
+    several right-hand sides, sampled rows; K_zx on a union plan."""
+    rng = np.random.default_rng(n + two_nu)
+    x = rng.random((n, 3))
+    V = rng.standard_normal((nrhs, n))
+    ell = (0.15, 0.25, 0.4)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 0.8, form=1))
+    out = plan.kmvm(to_dev(V if nrhs > 1 else V[0])).cpu().numpy().reshape(nrhs, n)
+    rows = W.sample_rows(x, 256)
+    for c in range(nrhs):
+        check_rows(out[c], x, V[c], two_nu, "product", ell, 0.8, rows=rows,
+                   what=f"d3 product nu={two_nu}/2 n={n} col {c}")
+    if n == 70_001:
+        z = rng.random((500, 3))
+        got = plan.predict(to_dev(z), to_dev(V[0])).cpu().numpy()
+        check_rows(got, x, V[0], two_nu, "product", ell, 0.8, z=z, what="d3 product predict")
+
+
+@pytest.mark.parametrize("d,form", [(1, 0), (2, 0), (2, 1), (3, 0), (3, 1)])
 def test_kzx_all_rows(gpm, d, form):
     n, m = 3000, 700
     x = _points("uniform", n, d, 3 + d)
@@ -217,7 +250,7 @@ def test_errors(gpm):
         gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1, 0.1)))
     assert e.value.name == "NONFINITE" and "row 37" in str(e.value)
     with pytest.raises(gpm.GPError) as e:
-        gpm.Plan(to_dev(np.zeros((10, 3))), gpm.Kernel(3, (0.1,) * 3, form=1))
+        gpm.Plan(to_dev(np.zeros((10, 3))), gpm.Kernel(4, (0.1,) * 3, form=1))
     assert e.value.name == "UNSUPPORTED"
 
 
@@ -241,6 +274,26 @@ def test_cg_gls_predict_small_vs_dense(gpm):
     mu_or = oracle.kzx_rows(x, alpha, z, 3, "product", c.ell, 1.0) + \
         np.hstack([np.ones((z.shape[0], 1)), z]) @ np.array(beta)
     assert np.max(np.abs(mu - mu_or)) <= 1e-9 * np.abs(alpha).max() * 50
+
+
+@pytest.mark.parametrize("two_nu", [3, 5])
+def test_cg_gls_predict_d3_product_vs_dense(gpm, two_nu):
+    """Full GP inference on the d = 3 product form (PD, App B): CG + GLS with
+    H = [1, x] + posterior mean against the dense oracle."""
+    rng = np.random.default_rng(60 + two_nu)
+    n, m = 2200, 300
+    x = rng.random((n, 3)); z = rng.random((m, 3))
+    y = 1 + 0.5 * x[:, 0] - 0.3 * x[:, 1] + 0.2 * x[:, 2] + np.sin(5 * x[:, 0]) * np.cos(3 * x[:, 2]) \
+        + 0.1 * rng.standard_normal(n)
+    ell = (0.2, 0.3, 0.25); s2 = 0.01
+    ref = oracle.gp_dense(x, y, z, two_nu, "product", ell, 1.0, s2, mean="affine")
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, form=1))
+    alpha, beta, info = plan.cg_solve(to_dev(y), s2, mean=gpm.MEAN_AFFINE, rtol=1e-10)
+    assert info["relres_max"] <= 1e-10
+    assert np.allclose(beta, ref["beta"], rtol=0, atol=1e-6)
+    assert np.max(np.abs(alpha.cpu().numpy() - ref["alpha"])) <= 1e-10 * np.linalg.norm(y) / s2 * 10
+    mu = plan.predict(to_dev(z), alpha, beta).cpu().numpy()
+    assert np.max(np.abs(mu - ref["mu"])) <= 1e-6
 
 
 @pytest.mark.parametrize("d", [1, 2])
@@ -433,7 +486,7 @@ def test_predict_union_cache(gpm):
 
 
 @pytest.mark.parametrize("d,n,two_nu,form", [(2, 20000, 3, 0), (2, 9000, 3, 1), (3, 5000, 5, 0),
-                                             (3, 70000, 3, 0)])
+                                             (3, 70000, 3, 0), (3, 9000, 3, 1)])
 @pytest.mark.parametrize("nshards", [2, 3, 5])
 def test_sharded_apply_sums_to_kv(gpm, d, n, two_nu, form, nshards):
     """SURVEY §8(e) decomposition on one GPU: the shards of gp_kmvm_partial (tile and
