@@ -65,10 +65,8 @@ def test_argument_validation_without_device(lib):
     assert b"supported" in lib.gp_last_error()
     k = g.Kernel(3, (-0.1,)).c()
     assert lib.gp_setup(dummy, 10, 1, ctypes.byref(k), None, ctypes.byref(h)) == 1     # l <= 0
-    k = g.Kernel(5, (0.1, 0.1, 0.1), form=g.FORM_PRODUCT).c()
-    assert lib.gp_setup(dummy, 10, 3, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product d=3
-    k = g.Kernel(7, (0.1, 0.1, 0.1), form=g.FORM_PRODUCT).c()
-    assert lib.gp_setup(dummy, 10, 3, ctypes.byref(k), None, ctypes.byref(h)) == 2     # product d=3 7/2
+    k = g.Kernel(5, (0.1, 0.1, 0.1), form=2).c()
+    assert lib.gp_setup(dummy, 10, 3, ctypes.byref(k), None, ctypes.byref(h)) == 1     # form
 
 
 def test_no_cpu_fallback(lib):
