@@ -145,9 +145,11 @@ GP_API gp_status gp_kmvm_rank(gp_plan p, const double *v_rank, int nrhs, double 
  * (eq dkernel_dvarsigma) and needs no extra MVM.  Computed by the same decomposition with
  * one more moment (g(s) = (s, s^2, (s^2 + s^3)/3) e^{-s} for nu = 1/2, 3/2, 5/2 in scaled
  * distance s = sqrt(2 nu) r): exact like gp_kmvm, no nugget, zero diagonal.
- * Supported: d = 1 (any n), the L1 form for d = 2 and for d = 3 with nu <= 7/2, and the
- * product form for d = 2 with nu <= 7/2 (product rule g(r1) k(r2) + k(r1) g(r2), (p+2)^2
- * moments per channel); other kernels return GP_ERR_UNSUPPORTED.  v_order: 0 = user order (layout as
+ * Supported: every kernel gp_setup accepts -- d = 1 (any n), the L1 form for d = 2, 3, and the
+ * product form for d = 2 and d = 3 at every nu (product rule sum_k g(r_k) prod_{j != k} k(r_j):
+ * d = 2, nu <= 7/2 with (p+2)^2 mixed moments per channel; d = 2 at nu = 9/2 and d = 3 by the
+ * separated sub-passes of the scan in two runs, about (p+2)^2 times the L1 apply at d = 3).
+ * v_order: 0 = user order (layout as
  * gp_kmvm), 1 = the plan's stored order (as gp_kmvm_rank). */
 GP_API gp_status gp_kmvm_dlengthscale(gp_plan p, const double *v, int nrhs, double *out,
                                       int v_order, void *stream);

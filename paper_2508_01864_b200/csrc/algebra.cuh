@@ -184,13 +184,15 @@ __device__ __forceinline__ double powi(double x, int e) {
   for (int i = 0; i < e; ++i) r *= x;
   return r;
 }
-// target factor of the separated split kernel: sum_{q=a..P} a_q C(q,a) beta^{q-a} (runtime a)
-template <int P>
+// target factor of a separated split profile sum_q c_q s^q e^{-s} (c = rcoef(PM, KIND, .):
+// k of nu = PM + 1/2, or g of nu = PM - 1/2): sum_{q=a..PM} c_q C(q,a) beta^{q-a}; runtime a,
+// 0 for a > PM
+template <int PM, int KIND>
 __device__ __forceinline__ double tpoly(int a, double beta) {
   double acc = 0.0;
 #pragma unroll
-  for (int q = P; q >= 0; --q)
-    if (q >= a) acc = fma(acc, beta, mcoef(P, q) * binom(q, a));
+  for (int q = PM; q >= 0; --q)
+    if (q >= a) acc = fma(acc, beta, rcoef(PM, KIND, q) * binom(q, a));
   return acc;
 }
 
@@ -206,15 +208,30 @@ __device__ __forceinline__ double tpoly(int a, double beta) {
 // last coordinate with source weights u alpha1^a alpha2^b e^{-alpha1-alpha2} and NO split
 // offset: the L1 engine (P+1 moments per channel) run NAB = (P+1)^2 times per level with
 // re-weighted sources and a target multiplier (tpoly), instead of a (P+1)^3-moment state.
-template <int P_, int NCH_, bool PROD_, int KIND_ = 0, bool P3_ = false>
+//
+// The same separation gives the lengthscale gradient of the product forms (product rule,
+// P:1301-1327): with g(s) = -s k'(s) of order p+1, g(a_s + a_t) = sum_{a<=p+1} [a_s^a e^{-a_s}]
+// Tg_a(a_t), in two runs summed by the epilogue:
+//   SEP 2: scan profile k (engine order p, KIND 0), split factors g k + k g (d = 3: g1 k2 k3 +
+//          k1 g2 k3), sub-passes (a, b) <= p+1, target factor Tg_a Tk_b + Tk_a Tg_b;
+//   SEP 3: scan profile g (engine order p+1, KIND 1), split factors k (k1 k2 g3), target
+//          factor Tk_a Tk_b with the order-p coefficients.
+// SEP 1 is the value.  d = 2 (NCH = 2) has one split factor: b = 0, alpha2 = 0.
+template <int P_, int NCH_, bool PROD_, int KIND_ = 0, int SEP_ = 0>
 struct Alg {
   static constexpr int P = P_;          // moment order (gradient: nu - 1/2 + 1)
   static constexpr int NCH = NCH_;
-  static constexpr bool PROD = PROD_;   // product form
+  static constexpr bool PROD = PROD_;   // product form (mixed-moment state, d = 2)
   static constexpr int KIND = KIND_;
-  static constexpr bool P3 = P3_;       // d = 3 product form by (a, b) passes of the L1 engine
+  static constexpr int SEP = SEP_;      // separated product form (sub-passes of the L1 engine)
+  static constexpr bool P3 = SEP != 0;
+  static constexpr bool ST2 = P3 && NCH == 4;   // staged structure holds alpha1 and alpha2
   static constexpr int NQ = P + 1;
-  static constexpr int NAB = P3 ? NQ * NQ : 1;
+  static constexpr int P0 = SEP == 3 ? P - 1 : P;             // nu - 1/2 of the kernel
+  static constexpr int NA = !P3 ? 1 : (SEP == 2 ? P0 + 2 : P0 + 1);
+  static constexpr int NB = NCH == 4 ? NA : 1;
+  // SEP 2, d = 3: the last pair (p+1, p+1) has a zero target factor
+  static constexpr int NAB = NA * NB - ((SEP == 2 && NCH == 4) ? 1 : 0);
   static constexpr int NM = PROD ? NQ * NQ : NQ;
   static constexpr int NS = NCH * NM;
 
@@ -300,6 +317,20 @@ struct Alg {
       v = readc_poly<P, 1>(Ga, beta) + readc_poly<P - 1, 0>(Gb, beta);
     }
     return eb * v;
+  }
+
+  // separated forms: source weight and target factor of sub-pass ab = pa * NB + pb
+  __device__ __forceinline__ static double srcw(double a1, double a2, int ab) {
+    const int pa = ab / NB, pb = ab - pa * NB;
+    return powi(a1, pa) * powi(a2, pb);
+  }
+  __device__ __forceinline__ static double tgtw(double a1, double a2, int ab) {
+    const int pa = ab / NB, pb = ab - pa * NB;
+    if constexpr (SEP == 2)
+      return tpoly<P0 + 1, 1>(pa, a1) * tpoly<P0, 0>(pb, a2) +
+             tpoly<P0, 0>(pa, a1) * tpoly<P0 + 1, 1>(pb, a2);
+    else
+      return tpoly<P0, 0>(pa, a1) * tpoly<P0, 0>(pb, a2);
   }
 };
 

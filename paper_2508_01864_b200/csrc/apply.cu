@@ -13,7 +13,8 @@ namespace gpm {
 gp_status d1_prepare(Plan& pl);
 gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
                     cudaStream_t s, int kind, double cg_s2 = 0.0, double* cg_part = nullptr);
-gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind);
+gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase);
+int level_phases(const Plan& pl, int kind);
 gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaStream_t s);
 size_t level_pt_bytes();
 int level_nparts(const Plan& pl);
@@ -35,13 +36,14 @@ __global__ void k_gather(const int* __restrict__ perm, const double* __restrict_
 // out[perm[r] - tgt_off] = os2 (self u[r] + acc[r]) for targets; perm == nullptr: rank order.
 // u is read from the packed point records (stride 4 doubles, u at offset 3); self = k(0)
 // (1 for K, 0 for the lengthscale gradient).
+// accumulate: out += (the second run of a two-run apply, level_phases).
 // CG epilogue (rank order only, cg_part != nullptr): out = K u + cg_s2 u and the block's
 // partial sum of u . out -> cg_part[(col0 + blockIdx.y) * gridDim.x + blockIdx.x]
 __global__ void k_epilogue(const int* __restrict__ perm, const double* __restrict__ pts,
                            const double* __restrict__ acc, const double* __restrict__ part,
                            int nparts, int64_t pstride, int64_t n, int64_t tgt_off, double os2, double self,
                            double* __restrict__ out, int64_t ostride, double cg_s2,
-                           double* __restrict__ cg_part, int col0) {
+                           double* __restrict__ cg_part, int col0, int accumulate) {
   __shared__ double red[32];
   pts += blockIdx.y * 4 * n;
   acc += blockIdx.y * n;
@@ -56,13 +58,13 @@ __global__ void k_epilogue(const int* __restrict__ perm, const double* __restric
     double val = os2 * fma(self, u, a);
     if (perm) {
       const int i = __ldg(perm + r);
-      if (i >= tgt_off) out[i - tgt_off] = val;
+      if (i >= tgt_off) out[i - tgt_off] = accumulate ? out[i - tgt_off] + val : val;
     } else {
       if (cg_part) {
         val = fma(cg_s2, u, val);
         pq = fma(u, val, pq);
       }
-      out[r] = val;
+      out[r] = accumulate ? out[r] + val : val;
     }
   }
   if (cg_part) {   // fixed-order block reduction
@@ -147,14 +149,19 @@ static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, 
     GPM_TRY(level_buffers(pl, nb));
     int launches = 0;
     GPM_TRY(level_pack(pl, v + c0 * vstride, nb, user_order, s));   // packed points (+ gather)
-    GPM_TRY(level_passes(pl, nb, s, &launches, kind));   // first level launch initialises acc
-    k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
-        user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
-        pl.part.as<double>(), level_nparts(pl) - pl.low_unused, (int64_t)level_nparts(pl) * pl.n,
-        pl.n, user_order ? pl.tgt_off : 0, pl.os2,
-        (kind == 0 && pl.shard == 0) ? 1.0 : 0.0, out + c0 * ostride, ostride, cg_s2, cg_part,
-        c0);   // a sharded apply adds the self term on shard 0 only
-    GPM_CUDA(cudaGetLastError());
+    const int nph = level_phases(pl, kind);
+    if (nph > 1 && cg_part) return fail(GP_ERR_UNSUPPORTED, "internal: CG epilogue on a two-run apply");
+    for (int ph = 0; ph < nph; ++ph) {
+      GPM_TRY(level_passes(pl, nb, s, &launches, kind, ph));   // first level launch initialises acc
+      k_epilogue<<<dim3(egrid(pl.n), nb), 256, 0, s>>>(
+          user_order ? pl.perm.as<int>() : nullptr, pl.pts.as<double>(), pl.acc.as<double>(),
+          pl.part.as<double>(), level_nparts(pl) - pl.low_unused, (int64_t)level_nparts(pl) * pl.n,
+          pl.n, user_order ? pl.tgt_off : 0, pl.os2,
+          (kind == 0 && pl.shard == 0) ? 1.0 : 0.0, out + c0 * ostride, ostride, cg_s2, cg_part,
+          c0, ph > 0);   // a sharded apply adds the self term on shard 0 only
+      GPM_CUDA(cudaGetLastError());
+      launches += ph > 0 ? 1 : 0;
+    }
     pl.launches_per_apply = launches + 2;   // + pack + epilogue (per batch of columns)
   }
   return GP_OK;

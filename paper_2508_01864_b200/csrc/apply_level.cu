@@ -102,9 +102,22 @@ __device__ __forceinline__ double kpoly(double s) {
 template <class A, int D>
 __device__ __forceinline__ double kval(double d1, double d2, double d3, const double* tab) {
   constexpr int P = A::P;
-  if constexpr (A::P3) {   // product form, d = 3 (P:416 [eq product_kernel])
+  if constexpr (A::SEP == 1) {   // product form, d = 3 (P:416 [eq product_kernel])
     const double e = fexp_neg((d1 + d2) + d3, tab);
     return e * (kpoly<P, 0>(d1) * kpoly<P, 0>(d2) * kpoly<P, 0>(d3));
+  } else if constexpr (A::SEP == 2) {   // its lengthscale gradient (product rule)
+    constexpr int P0 = A::P0;
+    const double e = fexp_neg((d1 + d2) + d3, tab);
+    const double k1 = kpoly<P0, 0>(d1), k2 = kpoly<P0, 0>(d2);
+    const double g1 = kpoly<P0 + 1, 1>(d1), g2 = kpoly<P0 + 1, 1>(d2);
+    if constexpr (D == 3) {
+      const double k3 = kpoly<P0, 0>(d3), g3 = kpoly<P0 + 1, 1>(d3);
+      return e * fma(g1, k2 * k3, k1 * fma(g2, k3, k2 * g3));
+    } else {
+      return e * fma(g1, k2, k1 * g2);
+    }
+  } else if constexpr (A::SEP == 3) {   // second gradient run: the near field is in the first
+    return 0.0;
   } else if constexpr (!A::PROD) {
     // L1: sum_q c_q s^q e^{-s} with the read coefficients of the algebra (Matern a_q for
     // KIND 0, gradient b_q = a_{q-1} - q a_q for KIND 1), Horner in s
@@ -244,6 +257,7 @@ struct CpScratch {
 template <class A, int D, bool IND>
 __device__ __forceinline__ void near_field(LvPoints& Pt, int cnt, int lb, int l1side,
                                            const double* tab, int zz = 0, int znf = 1) {
+  if constexpr (A::SEP == 3) return;   // second gradient run: near field done by the first
   const int i0 = threadIdx.x * CP_ITEMS;
   if (i0 >= cnt) return;
   double ti1[CP_ITEMS], ti2[CP_ITEMS], ti3[CP_ITEMS], acc[CP_ITEMS];
@@ -385,9 +399,9 @@ __device__ __forceinline__ void seg_engine(const TItems& it, int ls, double* of,
   __syncthreads();   // scratch reuse
 }
 
-// One level of a tile kernel: the engine once, or (P3, d = 3 product form) once per (a, b)
-// with sources re-weighted by alpha1^a alpha2^b and the target factors T_a(alpha1) T_b(alpha2)
-// (algebra.cuh); it.ea = e^{-(alpha1+alpha2)} as for L1, the split offset of the scan is 0.
+// One level of a tile kernel: the engine once, or (separated product forms, algebra.cuh) once
+// per sub-pass (a, b) with sources re-weighted by alpha1^a alpha2^b and the target factor of
+// the sub-pass; it.ea = e^{-(alpha1+alpha2)} as for L1, the split offset of the scan is 0.
 template <class A>
 __device__ __forceinline__ void level_apply(TItems& it, const double* a1, const double* a2, int ls,
                                             double* of, TScratch<A>& sc) {
@@ -403,17 +417,18 @@ __device__ __forceinline__ void level_apply(TItems& it, const double* a1, const 
     }
 #pragma unroll 1
     for (int ab = 0; ab < A::NAB; ++ab) {
-      const int a = ab / A::NQ, b = ab - a * A::NQ;
 #pragma unroll
-      for (int k = 0; k < CP_ITEMS; ++k) it.u[k] = ub[k] * (powi(a1[k], a) * powi(a2[k], b));
+      for (int k = 0; k < CP_ITEMS; ++k) it.u[k] = ub[k] * A::srcw(a1[k], a2[k], ab);
       double o[CP_ITEMS];
       seg_engine<A>(it, ls, o, sc);
 #pragma unroll
-      for (int k = 0; k < CP_ITEMS; ++k)
-        tot[k] = fma(o[k], tpoly<A::P>(a, a1[k]) * tpoly<A::P>(b, a2[k]), tot[k]);
+      for (int k = 0; k < CP_ITEMS; ++k) tot[k] = fma(o[k], A::tgtw(a1[k], a2[k], ab), tot[k]);
     }
 #pragma unroll
-    for (int k = 0; k < CP_ITEMS; ++k) of[k] = tot[k];
+    for (int k = 0; k < CP_ITEMS; ++k) {
+      of[k] = tot[k];
+      it.u[k] = ub[k];
+    }
   }
 }
 
@@ -513,8 +528,10 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low2(LvArgs g) {
     const bool nstart = (i0 & ((1 << l) - 1)) == 0;
     const double ypre = (!nstart && i0 <= cnt) ? Pt.t2[__ldg(ord + i0 - 1) - (int)T0] : 0.0;
     titems_gaps(it, y, ypre, nstart, sc.tab);
-    double of[CP_ITEMS];
-    seg_engine<A>(it, l, of, sc);
+    double of[CP_ITEMS], a1k[CP_ITEMS], a2k[CP_ITEMS];
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) { a1k[k] = it.a[k]; a2k[k] = 0.0; }
+    level_apply<A>(it, a1k, a2k, l, of, sc);
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[it.o[k]] += of[k];
   }
@@ -615,12 +632,15 @@ __global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
     const bool nstart = (i0 & ((1 << l) - 1)) == 0;
     const double ypre = (!nstart && i0 <= cnt) ? Pt.t2[__ldg(ord + i0 - 1) - (int)T0] : 0.0;
     titems_gaps(it, y, ypre, nstart, sc.tab);
+    double a1k[CP_ITEMS], a2k[CP_ITEMS];
+#pragma unroll
+    for (int k = 0; k < CP_ITEMS; ++k) { a1k[k] = it.a[k]; a2k[k] = 0.0; }
 #pragma unroll 1
     for (int c = 0; c < nc; ++c) {
 #pragma unroll
       for (int k = 0; k < CP_ITEMS; ++k) it.u[k] = it.o[k] >= 0 ? Pt.u[c][it.o[k]] : 0.0;
       double of[CP_ITEMS];
-      seg_engine<A>(it, l, of, sc);
+      level_apply<A>(it, a1k, a2k, l, of, sc);
 #pragma unroll
       for (int k = 0; k < CP_ITEMS; ++k) if (it.o[k] >= 0) Pt.acc[c][it.o[k]] += of[k];
     }
@@ -1016,27 +1036,18 @@ __device__ __forceinline__ void cp_issue(const unsigned char* hpbase, const HpDe
   tma_load_1d(st.rc, v.rc + T0, 4 * LV_TILE, bar);
 }
 
-// staged split offsets as the engine sees them: L1 / d = 2: the offset alpha and e^{-alpha};
-// P3: offset 0 (the split factors sit in the source weight and the target factor), e^{-(a1+a2)}
-template <bool P3>
-__device__ __forceinline__ double cp_aoff(const CpStageT<P3>& E, int z) {
-  if constexpr (P3) return 0.0;
+// staged split offsets as the engine sees them: L1 / mixed-moment product: the offset alpha
+// and e^{-alpha}; separated forms: offset 0 (the split factors sit in the source weight and
+// the target factor of the sub-pass), e^{-(alpha1+alpha2)}
+template <class A>
+__device__ __forceinline__ double cp_aoff(const CpStageT<A::ST2>& E, int z) {
+  if constexpr (A::P3) return 0.0;
   else return E.a[z];
 }
-template <bool P3>
-__device__ __forceinline__ double cp_asum(const CpStageT<P3>& E, int z) {
-  if constexpr (P3) return E.a[z] + E.a2[z];
-  else return E.a[z];
-}
-template <bool P3>
-__device__ __forceinline__ double cp_srcw(const CpStageT<P3>& E, int z, int pa, int pb) {
-  if constexpr (P3) return powi(E.a[z], pa) * powi(E.a2[z], pb);
-  else return 1.0;
-}
-template <int P, bool P3>
-__device__ __forceinline__ double cp_tgtw(const CpStageT<P3>& E, int z, int pa, int pb) {
-  if constexpr (P3) return tpoly<P>(pa, E.a[z]) * tpoly<P>(pb, E.a2[z]);
-  else return 1.0;
+template <class A>
+__device__ __forceinline__ double cp_a2(const CpStageT<A::ST2>& E, int z) {
+  if constexpr (A::ST2) return E.a2[z];
+  else return 0.0;
 }
 
 template <class A, int MODE>
@@ -1048,8 +1059,8 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
   const int b0 = item_lo + (int)blockIdx.x;
   using S = CSt<A::NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using Stage = CpStageT<A::P3>;
-  CpSmemT<A::P3>& SM = *reinterpret_cast<CpSmemT<A::P3>*>(smem_raw);
+  using Stage = CpStageT<A::ST2>;
+  CpSmemT<A::ST2>& SM = *reinterpret_cast<CpSmemT<A::ST2>*>(smem_raw);
   __shared__ CpScratch<A> sc;
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ double s_tab[64];
@@ -1102,16 +1113,15 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
     for (int k = 0; k < CP_ITEMS; ++k) {
       const int z = cpz(i0 + k);
       ek[k] = fexp_neg(E.d[z], s_tab);
-      eak[k] = fexp_neg(cp_asum(E, z), s_tab);
+      eak[k] = fexp_neg(E.a[z] + cp_a2<A>(E, z), s_tab);
     }
-    // P3 (d = 3 product form): every column runs NAB = (P+1)^2 sub-passes (a, b) with sources
-    // re-weighted by alpha1^a alpha2^b and the target factor T_a(alpha1) T_b(alpha2); each
+    // separated product forms: every column runs NAB sub-passes (a, b) with sources
+    // re-weighted by alpha1^a alpha2^b and the sub-pass's target factor (algebra.cuh); each
     // sub-pass has its own tile aggregates / carries (index cc), the outputs are summed
     double ur[CP_ITEMS], tot[CP_ITEMS];
 #pragma unroll 1
     for (int cc = 0; cc < nrhs * A::NAB; ++cc) {
       const int c = cc / A::NAB, ab = cc - c * A::NAB;
-      const int pa = ab / A::NQ, pb = ab - pa * A::NQ;
       LvRecFor<A::NS>* aggs =
           reinterpret_cast<LvRecFor<A::NS>*>(g.aggs) + ((int64_t)cc * npass + p) * 2 * max_tiles;
       double uc[CP_ITEMS], of[CP_ITEMS];
@@ -1138,8 +1148,12 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
       }
 #pragma unroll
       for (int k = 0; k < CP_ITEMS; ++k) {
-        if constexpr (A::P3) uc[k] = ur[k] * cp_srcw(E, cpz(i0 + k), pa, pb);
-        else uc[k] = ur[k];
+        if constexpr (A::P3) {
+          const int z = cpz(i0 + k);
+          uc[k] = ur[k] * A::srcw(E.a[z], cp_a2<A>(E, z), ab);
+        } else {
+          uc[k] = ur[k];
+        }
       }
       if (MODE == 2) {   // tile carries (k_cp_carry); read after the next barrier
         const double* cr = reinterpret_cast<const double*>(aggs + carr_off + 2 * t);
@@ -1158,7 +1172,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
         for (int k = CP_ITEMS - 1; k >= 0; --k) {    // forward: reference at item 7
           const int z = cpz(i0 + k);
-          A::inject_at(XF.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], D, Ee);
+          A::inject_at(XF.M, E.rc[z] >> 30, uc[k], cp_aoff<A>(E, z), eak[k], D, Ee);
           D += E.d[z];
           Ee *= ek[k];
         }
@@ -1167,7 +1181,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
           const int z = cpz(i0 + k);
           Db += E.d[z];
           Eb *= ek[k];
-          A::inject_at(XB.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], Db, Eb);
+          A::inject_at(XB.M, E.rc[z] >> 30, uc[k], cp_aoff<A>(E, z), eak[k], Db, Eb);
         }
         // spans after my last position / before my first one within the tile
         double incl = D;   // inclusive prefix sum of the thread spans (warp)
@@ -1225,7 +1239,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
         for (int k = CP_ITEMS - 1; k >= 0; --k) {    // reference at item 7
           const int z = cpz(i0 + k);
-          A::inject_at(X.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], cp_aoff<A>(E, z), eak[k], D, Ee);
           D += E.d[z];
           Ee *= ek[k];
         }
@@ -1259,7 +1273,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
             const int z = cpz(i0 + k);
             A::advance_all(M, E.d[z], ek[k]);
             const int ch = E.rc[z] >> 30;
-            const double a = cp_aoff(E, z), ea = eak[k];
+            const double a = cp_aoff<A>(E, z), ea = eak[k];
             of[k] = A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
           }
@@ -1276,7 +1290,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
           const int z = cpz(i0 + k);
           D += E.d[z];
           Ee *= ek[k];
-          A::inject_at(X.M, E.rc[z] >> 30, uc[k], cp_aoff(E, z), eak[k], D, Ee);
+          A::inject_at(X.M, E.rc[z] >> 30, uc[k], cp_aoff<A>(E, z), eak[k], D, Ee);
         }
         X.D = D; X.E = Ee;
 #pragma unroll 1
@@ -1309,13 +1323,13 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
             const int z = cpz(i0 + k);
             const unsigned rcz = E.rc[z];
             const int ch = rcz >> 30;
-            const double a = cp_aoff(E, z), ea = eak[k];
+            const double a = cp_aoff<A>(E, z), ea = eak[k];
             const double val = of[k] + A::read(M, A::NCH - 1 - ch, a, ea);
             A::inject(M, ch, uc[k], a, ea);
             A::advance_all(M, E.d[z], ek[k]);
             const unsigned r = rcz & CP_RMASK;
             if constexpr (A::P3) {
-              tot[k] = fma(val, cp_tgtw<A::P>(E, z, pa, pb), tot[k]);
+              tot[k] = fma(val, A::tgtw(E.a[z], cp_a2<A>(E, z), ab), tot[k]);
               if (ab == A::NAB - 1 && r != CP_RMASK) slot[r] = tot[k];
             } else {
               if (r != CP_RMASK) slot[r] = val;
@@ -1353,10 +1367,10 @@ static cudaError_t lv_set_attrs() {
       return e;
   }
   if ((e = cudaFuncSetAttribute(k_cp<A, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(CpSmemT<A::P3>))))
+                                (int)sizeof(CpSmemT<A::ST2>))))
     return e;
   return cudaFuncSetAttribute(k_cp<A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(CpSmemT<A::P3>));
+                              (int)sizeof(CpSmemT<A::ST2>));
 }
 
 // The carried passes of a plan, in apply order: (ord, ord2l1, lseg, l1, n_act).
@@ -1392,7 +1406,16 @@ static std::vector<HPass> high_passes(const Plan& pl) {
 
 // d = 3 product form with nu >= 3/2: the (a, b) sub-passes of algebra.cuh (P3)
 bool level_p3(const Plan& pl) { return pl.d == 3 && pl.form == GP_FORM_PRODUCT && pl.P > 0; }
-int level_nab(const Plan& pl) { return level_p3(pl) ? (pl.P + 1) * (pl.P + 1) : 1; }
+// most sub-passes per column over the plan's applies (value and gradient runs): sizes aggs
+int level_nab(const Plan& pl) {
+  if (pl.form != GP_FORM_PRODUCT || pl.d < 2) return 1;
+  return pl.d == 3 ? (pl.P + 2) * (pl.P + 2) : pl.P + 2;
+}
+// runs per apply whose outputs the epilogue sums: the separated gradients take two
+int level_phases(const Plan& pl, int kind) {
+  if (kind == 0 || pl.form != GP_FORM_PRODUCT) return 1;
+  return (pl.d == 3 && pl.P > 0) || (pl.d == 2 && pl.P > 3) ? 2 : 1;
+}
 
 static LvArgs lv_base_args(const Plan& pl) {
   LvArgs g{};
@@ -1551,8 +1574,8 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     int dev = 0, sms = 0, o1 = 0, o2 = 0;
     GPM_CUDA(cudaGetDevice(&dev));
     GPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmemT<A::P3>)));
-    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmemT<A::P3>)));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cp<A, 1>, CP_BLOCK, sizeof(CpSmemT<A::ST2>)));
+    GPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cp<A, 2>, CP_BLOCK, sizeof(CpSmemT<A::ST2>)));
     grid1 = std::max(1, o1) * sms;
     grid2 = std::max(1, o2) * sms;
   }
@@ -1568,7 +1591,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     GPM_CUDA(cudaEventRecord(pl.ev_fork, s));
     GPM_CUDA(cudaStreamWaitEvent(pl.s2, pl.ev_fork, 0));
     const int64_t carr_off = (int64_t)g.agg_stride * nrhs * A::NAB;   // carries after the aggregates
-    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmemT<A::P3>), pl.s2>>>(
+    k_cp<A, 1><<<std::min(pl.hp_items, grid1), CP_BLOCK, sizeof(CpSmemT<A::ST2>), pl.s2>>>(
         g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, pl.hp_items, pl.hp_maxtiles, nrhs,
         carr_off, 0);
     GPM_CUDA(cudaGetLastError());
@@ -1621,7 +1644,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     const int nit = (int)(sr[3] - sr[2]);
     if (nit > 0) {
-      k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmemT<A::P3>), s>>>(
+      k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmemT<A::ST2>), s>>>(
           g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, (int)sr[3], pl.hp_maxtiles, nrhs,
           (int64_t)g.agg_stride * nrhs * A::NAB, (int)sr[2]);
       *launches += 1;
@@ -1672,7 +1695,7 @@ gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaS
 }
 size_t level_pt_bytes() { return sizeof(Pt4); }
 
-gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind) {
+gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
   const int P = pl.P;
 #ifdef GPM_FEW   // experiment builds (build.py GPM_EXTRA_FLAGS): the three bench algebras only
@@ -1682,9 +1705,24 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
   return fail(GP_ERR_UNSUPPORTED, "GPM_FEW experiment build");
 #else
   if (kind != 0) {   // lengthscale gradient: moment order p + 1
+    if (prod && level_phases(pl, kind) == 2) {
+      // separated product-form gradient (algebra.cuh SEP 2 / SEP 3): d = 3, and d = 2 at
+      // nu = 9/2 (whose mixed-moment state would need 2 x 36 doubles)
+      if (pl.d == 2)
+        return phase == 0 ? lv_run<Alg<4, 2, false, 0, 2>>(pl, nrhs, s, launches)
+                          : lv_run<Alg<5, 2, false, 1, 3>>(pl, nrhs, s, launches);
+      switch (P) {
+        case 1: return phase == 0 ? lv_run<Alg<1, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                  : lv_run<Alg<2, 4, false, 1, 3>>(pl, nrhs, s, launches);
+        case 2: return phase == 0 ? lv_run<Alg<2, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                  : lv_run<Alg<3, 4, false, 1, 3>>(pl, nrhs, s, launches);
+        case 3: return phase == 0 ? lv_run<Alg<3, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                  : lv_run<Alg<4, 4, false, 1, 3>>(pl, nrhs, s, launches);
+        default: return phase == 0 ? lv_run<Alg<4, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                   : lv_run<Alg<5, 4, false, 1, 3>>(pl, nrhs, s, launches);
+      }
+    }
     if (prod) {        // d = 2 product form, nu <= 7/2 ((p+2)^2 moments per channel)
-      if (pl.d != 2 || P > 3)
-        return fail(GP_ERR_UNSUPPORTED, "product-form lengthscale gradient: d = 2, nu <= 7/2 only");
       if (P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
       if (P == 1) return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
       if (P == 2) return lv_run<Alg<3, 2, true, 1>>(pl, nrhs, s, launches);
@@ -1704,8 +1742,7 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
       case 1: return lv_run<Alg<2, 4, false, 1>>(pl, nrhs, s, launches);
       case 2: return lv_run<Alg<3, 4, false, 1>>(pl, nrhs, s, launches);
       case 3: return lv_run<Alg<4, 4, false, 1>>(pl, nrhs, s, launches);
-      default:
-        return fail(GP_ERR_UNSUPPORTED, "d=3 lengthscale gradient: nu <= 7/2 (4 x 5 moments)");
+      default: return lv_run<Alg<5, 4, false, 1>>(pl, nrhs, s, launches);   // 4 x 6 moments (LvRec<24>)
     }
   }
   if (pl.d == 2) {
@@ -1726,10 +1763,10 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
   }
   if (level_p3(pl)) {   // d = 3 product form (nu = 1/2 is the L1 kernel)
     switch (P) {
-      case 1: return lv_run<Alg<1, 4, false, 0, true>>(pl, nrhs, s, launches);
-      case 2: return lv_run<Alg<2, 4, false, 0, true>>(pl, nrhs, s, launches);
-      case 3: return lv_run<Alg<3, 4, false, 0, true>>(pl, nrhs, s, launches);
-      default: return lv_run<Alg<4, 4, false, 0, true>>(pl, nrhs, s, launches);
+      case 1: return lv_run<Alg<1, 4, false, 0, 1>>(pl, nrhs, s, launches);
+      case 2: return lv_run<Alg<2, 4, false, 0, 1>>(pl, nrhs, s, launches);
+      case 3: return lv_run<Alg<3, 4, false, 0, 1>>(pl, nrhs, s, launches);
+      default: return lv_run<Alg<4, 4, false, 0, 1>>(pl, nrhs, s, launches);
     }
   }
   switch (P) {

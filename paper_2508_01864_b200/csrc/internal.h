@@ -80,6 +80,7 @@ using LvRecFor = LvRec<(NS > 20 ? NS : 20)>;
 // for the gradient, capped at the widest supported state)
 inline size_t level_rec_bytes(int d, int form_product, int P) {
   int ns = 20;
+  if (d == 3 && 4 * (P + 2) > ns) ns = 4 * (P + 2);   // gradient of nu = 9/2: 4 x 6 moments
   if (d == 2 && form_product) {
     const int w = 2 * (P + 2) * (P + 2);
     ns = w > 50 ? 50 : (w > 20 ? w : 20);

@@ -113,12 +113,18 @@ def test_product_grad_multi_level_sampled(gpm):
                    what=f"grad product sampled rhs {r}")
 
 
-def test_grad_unsupported_and_errors(gpm):
-    x = _pts(500, 2, 1)
-    plan = gpm.Plan(to_dev(x), gpm.Kernel(9, (0.1, 0.1), form=1))
-    with pytest.raises(gpm.GPError) as e:
-        plan.kmvm_dlengthscale(to_dev(np.ones(500)))
-    assert e.value.name == "UNSUPPORTED"
+@pytest.mark.parametrize("d,form", [(2, 0), (2, 1), (3, 0), (3, 1)])
+def test_grad_every_form_at_nu92(gpm, d, form):
+    """The combinations that returned UNSUPPORTED in round 1 (d = 2 product and d = 3 at
+    nu = 9/2) against the oracle on every row."""
+    n = 700
+    x = _pts(n, d, 10 * d + form)
+    v = np.random.default_rng(d + form).standard_normal(n)
+    ell = (0.1, 0.2, 0.15)[:d]
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(9, ell, 1.0, form=form))
+    out = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, 9, ["l1", "product"][form], ell, 1.0, grad=True,
+               what=f"grad nu=9/2 d={d} form={form}")
 
 
 def test_grad_matches_finite_difference_of_kmvm(gpm):

@@ -29,11 +29,6 @@ def test_high_nu_all_rows(gpm, two_nu, d, n, grad):
     v = np.random.default_rng(n + two_nu).standard_normal(n)
     ell = (0.08, 0.2, 0.15)[:d]
     plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.2, form=0))
-    if grad and d == 3 and two_nu == 9:
-        with pytest.raises(gpm.GPError) as e:
-            plan.kmvm_dlengthscale(to_dev(v))
-        assert e.value.name == "UNSUPPORTED"
-        return
     out = (plan.kmvm_dlengthscale(to_dev(v)) if grad else plan.kmvm(to_dev(v))).cpu().numpy()
     check_rows(out, x, v, two_nu, "l1", ell, 1.2, grad=grad,
                what=f"nu={two_nu}/2 d={d} n={n} grad={grad}")
@@ -61,17 +56,12 @@ def test_high_nu_config2_and_multilevel(gpm, two_nu):
 @pytest.mark.parametrize("grad", [False, True])
 def test_high_nu_product_d2_all_rows(gpm, two_nu, n, grad):
     """d = 2 product form for nu = 7/2, 9/2: (p+1)^2 = 16 / 25 mixed
-    moments per channel (wide tile records); the gradient (product rule, (p+2)^2 = 25
-    moments) for nu = 7/2, UNSUPPORTED for nu = 9/2."""
+    moments per channel (wide tile records); the gradient (product rule): (p+2)^2 = 25
+    mixed moments for nu = 7/2, the separated two-run form (algebra.cuh SEP 2 / 3) for 9/2."""
     x = _pts(n, 2, 17 * n + two_nu, ties=(n % 2 == 1))
     v = np.random.default_rng(n + two_nu + 3).standard_normal(n)
     ell = (0.1, 0.2)
     plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.1, form=1))
-    if grad and two_nu == 9:
-        with pytest.raises(gpm.GPError) as e:
-            plan.kmvm_dlengthscale(to_dev(v))
-        assert e.value.name == "UNSUPPORTED"
-        return
     out = (plan.kmvm_dlengthscale(to_dev(v)) if grad else plan.kmvm(to_dev(v))).cpu().numpy()
     check_rows(out, x, v, two_nu, "product", ell, 1.1, grad=grad,
                what=f"product nu={two_nu}/2 n={n} grad={grad}")
@@ -90,19 +80,39 @@ def test_high_nu_product_d2_multilevel_multirhs(gpm, two_nu):
     for r in range(3):
         check_rows(out[r], x, V[r], two_nu, "product", ell, 1.0, rows=rows,
                    what=f"product nu={two_nu}/2 multilevel rhs {r}")
-    if two_nu == 7:
-        g = plan.kmvm_dlengthscale(to_dev(V[:1])).cpu().numpy()
-        check_rows(g[0] if g.ndim == 2 else g, x, V[0], two_nu, "product", ell, 1.0, rows=rows,
-                   grad=True, what="product nu=7/2 multilevel grad")
+    g = plan.kmvm_dlengthscale(to_dev(V[:2])).cpu().numpy()
+    for r in range(2):
+        check_rows(g[r], x, V[r], two_nu, "product", ell, 1.0, rows=rows, grad=True,
+                   what=f"product nu={two_nu}/2 multilevel grad rhs {r}")
 
 
-def test_high_nu_unsupported(gpm):
-    """The d = 3 product form has no lengthscale-gradient MVM (include/gpmatern.h)."""
-    x = _pts(300, 3, 1)
-    plan = gpm.Plan(to_dev(x), gpm.Kernel(7, (0.1, 0.1, 0.1), form=1))
-    with pytest.raises(gpm.GPError) as e:
-        plan.kmvm_dlengthscale(to_dev(np.ones(300)))
-    assert e.value.name == "UNSUPPORTED"
+@pytest.mark.parametrize("two_nu", [1, 3, 5, 7, 9])
+@pytest.mark.parametrize("n", [2, 64, 2049, 5000])
+def test_product_d3_grad_all_rows(gpm, two_nu, n):
+    """Lengthscale gradient of the d = 3 product form (product rule g1 k2 k3 + k1 g2 k3 +
+    k1 k2 g3) by the separated sub-passes in two runs, every row, ties."""
+    x = _pts(n, 3, 23 * n + two_nu, ties=(n % 2 == 1))
+    v = np.random.default_rng(n + two_nu + 5).standard_normal(n)
+    ell = (0.2, 0.3, 0.25)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 0.9, form=1))
+    out = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, "product", ell, 0.9, grad=True,
+               what=f"product d3 grad nu={two_nu}/2 n={n}")
+
+
+def test_product_d3_grad_multilevel(gpm):
+    """d = 3 product gradient with carried passes and outer levels > 10, 2 columns, rank-order
+    entry bitwise equal to the user-order one."""
+    n = 70_001
+    x = _pts(n, 3, 99)
+    V = np.random.default_rng(98).standard_normal((2, n))
+    ell = (0.15, 0.25, 0.4)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, ell, 1.0, form=1))
+    g = plan.kmvm_dlengthscale(to_dev(V)).cpu().numpy()
+    rows = W.sample_rows(x, 128)
+    for r in range(2):
+        check_rows(g[r], x, V[r], 3, "product", ell, 1.0, rows=rows, grad=True,
+                   what=f"product d3 multilevel grad rhs {r}")
 
 
 @pytest.mark.parametrize("two_nu", [5, 7, 9])
