@@ -317,6 +317,7 @@ __device__ __forceinline__ void seg_engine(const TItems& it, int ls, double* of,
   const int i0 = tid * CP_ITEMS;
   const int smask = (1 << ls) - 1;
   const int seg = i0 >> ls;
+  const int nthr = min(32, 1 << (ls - 3));   // threads of a node within a warp: scan steps beyond are masked off
   // ---- forward
   {
     S X;
@@ -331,7 +332,7 @@ __device__ __forceinline__ void seg_engine(const TItems& it, int ls, double* of,
     }
     X.D = D; X.E = Ee;
 #pragma unroll 1
-    for (int off = 1; off < 32; off <<= 1) {
+    for (int off = 1; off < nthr; off <<= 1) {
       const S Y = cs_shfl<A::NS>(X, off, true);
       if (lane >= off && ((i0 - CP_ITEMS * off) >> ls) == seg) X = cs_fw<A>(Y, X);
     }
@@ -370,7 +371,7 @@ __device__ __forceinline__ void seg_engine(const TItems& it, int ls, double* of,
     }
     X.D = D; X.E = Ee;
 #pragma unroll 1
-    for (int off = 1; off < 32; off <<= 1) {
+    for (int off = 1; off < nthr; off <<= 1) {
       const S Y = cs_shfl<A::NS>(X, off, false);
       if (lane + off < 32 && ((i0 + CP_ITEMS * off) >> ls) == seg) X = cs_bw<A>(X, Y);
     }
@@ -551,7 +552,7 @@ struct LvPointsM {
 };
 
 template <class A, int NC>
-__global__ void __launch_bounds__(CP_BLOCK, 2) k_low2m(LvArgs g, int nrhs) {
+__global__ void __launch_bounds__(CP_BLOCK, NC <= 2 ? 3 : 2) k_low2m(LvArgs g, int nrhs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LvPointsM<NC>& Pt = *reinterpret_cast<LvPointsM<NC>*>(smem_raw);
   __shared__ TScratch<A> sc;
@@ -1540,6 +1541,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   g.u = nullptr;
   g.pts = reinterpret_cast<const Pt4*>(pl.pts.ptr);
   g.lb = pl.d == 2 ? pl.near_lb2 : pl.near_lb3;
+  const bool multi2 = A::NCH == 2 && nrhs >= 2 && !getenv("GPM_LOW2_PERCOL");
   g.lb2 = pl.near_lb3m;
   g.acc = pl.acc.as<double>();
   g.aggs = pl.aggs.as<LvAgg>();
@@ -1563,8 +1565,10 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   }
   g.tile0 = (int)sr[0];
   const int tiles_run = (int)(sr[1] - sr[0]);
+  const int nlow_alloc = low_parts(pl.d, pl.d == 2 ? pl.near_lb2 : pl.near_lb3, L);   // level_nparts
   const int nlow = low_parts(pl.d, g.lb, L);
-  pl.low_unused = 0;   // trailing part slots this apply leaves unwritten (the epilogue skips them)
+  // trailing part slots this apply leaves unwritten (the epilogue skips them)
+  pl.low_unused = nlow_alloc - nlow;
   g.low_slot0 = pl.hp_npass + (pl.d == 3 ? std::max(0, L - LV_LOGTILE) : 0);
   const dim3 gt(tiles_run, nrhs, nlow);
   const bool hp = pl.hp_npass > 0;
@@ -1609,8 +1613,11 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   if (tiles_run <= 0) {
     // this shard has no tiles
   } else if constexpr (A::NCH == 2) {
-    if (nrhs >= 2 && !getenv("GPM_LOW2_PERCOL")) {   // columns share the v-independent work
-      constexpr int NC = 4;
+    if (multi2) {   // columns share the v-independent work
+#ifndef GPM_LOW2M_NC
+#define GPM_LOW2M_NC 4
+#endif
+      constexpr int NC = GPM_LOW2M_NC;
       static bool attr = false;
       if (!attr) {
         GPM_CUDA(cudaFuncSetAttribute(k_low2m<A, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1621,7 +1628,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
       // leaves SMs empty
       const int groups = (nrhs + NC - 1) / NC;
       const bool msplit = (int64_t)tiles_run * groups < 148;
-      if (!msplit) pl.low_unused = nlow - 1;
+      if (!msplit) pl.low_unused = nlow_alloc - 1;
       k_low2m<A, NC><<<dim3(tiles_run, groups, msplit ? nlow : 1), CP_BLOCK, sizeof(LvPointsM<NC>), s>>>(
           g, nrhs);
     } else {
