@@ -628,6 +628,12 @@ def extra_configs(g, dev, stream, ws, rank, hbm, args):
     for d, reps in [(2, 10), (3, 3)]:
         xn = W.uniform_points(1 << 20, d, 1000 + d)
         out[f"sweep_d{d}_n2^20_nu32_l1"] = apply_stats(xn, g.Kernel(3, (0.1,) * d), reps)
+    # small n at d = 3 (the fused low kernels run in parts: 16 tiles fill the SMs) and the
+    # d = 3 product form ((p+1)^2 re-weighted scan runs per level) on config 4's points
+    out["sweep_d3_n2^14_nu32_l1"] = apply_stats(W.uniform_points(1 << 14, 3, 1014),
+                                               g.Kernel(3, (0.1,) * 3), 20)
+    out["config4_points_product_nu32"] = apply_stats(
+        W.config_points(c4), g.Kernel(3, c4.ell, form=g.FORM_PRODUCT), 3)
     if not args.no_cg:
         c5 = W.CONFIGS[5]
         x = W.config_points(c5); y = W.config_response(c5, x)

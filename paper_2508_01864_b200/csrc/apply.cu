@@ -116,7 +116,6 @@ gp_status apply_prepare(Plan& pl) {
   return GP_OK;
 }
 
-static constexpr int LV_MAXB = 8;   // right-hand sides per level-pass batch
 
 static gp_status level_buffers(Plan& pl, int nrhs) {
   const size_t need = (size_t)nrhs * pl.n;
@@ -141,14 +140,15 @@ int cg_nblk(const Plan& pl) {
 
 static gp_status apply_levels(Plan& pl, const double* v, double* out, int nrhs, bool user_order,
                               cudaStream_t s, int kind, double cg_s2 = 0.0,
-                              double* cg_part = nullptr) {
+                              double* cg_part = nullptr, bool prepacked = false) {
   const int64_t vstride = user_order ? pl.n_src : pl.n;
   const int64_t ostride = user_order ? pl.n - pl.tgt_off : pl.n;
   for (int c0 = 0; c0 < nrhs; c0 += LV_MAXB) {
     const int nb = std::min(LV_MAXB, nrhs - c0);
     GPM_TRY(level_buffers(pl, nb));
     int launches = 0;
-    GPM_TRY(level_pack(pl, v + c0 * vstride, nb, user_order, s));   // packed points (+ gather)
+    if (!(prepacked && !user_order && nrhs <= LV_MAXB))
+      GPM_TRY(level_pack(pl, v + c0 * vstride, nb, user_order, s));   // packed points (+ gather)
     const int nph = level_phases(pl, kind);
     if (nph > 1 && cg_part) return fail(GP_ERR_UNSUPPORTED, "internal: CG epilogue on a two-run apply");
     for (int ph = 0; ph < nph; ++ph) {
@@ -177,9 +177,9 @@ gp_status permute_vec(Plan& pl, const double* src, double* dst, bool to_rank, cu
 }
 
 gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s,
-                     int kind, double cg_s2, double* cg_part) {
+                     int kind, double cg_s2, double* cg_part, bool prepacked) {
   if (pl.d == 1) return d1_launch(pl, u_rank, out_rank, nrhs, false, s, kind, cg_s2, cg_part);
-  return apply_levels(pl, u_rank, out_rank, nrhs, false, s, kind, cg_s2, cg_part);
+  return apply_levels(pl, u_rank, out_rank, nrhs, false, s, kind, cg_s2, cg_part, prepacked);
 }
 
 gp_status apply_user(Plan& pl, const double* v, double* out, int nrhs, cudaStream_t s, int kind) {

@@ -191,8 +191,12 @@ void plan_free(Plan& pl);
 // CG epilogue (solve.cu): with cg_part != nullptr the apply returns
 // out = K u + cg_s2 u and writes per-block partial sums of u . out to
 // cg_part[c * cg_nblk(pl) + block] (fixed-order reductions: deterministic).
+// prepacked (d >= 2, nrhs <= LV_MAXB): the packed point records pl.pts already hold u_rank in
+// their u field (the CG driver's k_cg_p writes p there): the pack launch is skipped.
 gp_status apply_rank(Plan& pl, const double* u_rank, double* out_rank, int nrhs, cudaStream_t s,
-                     int kind = 0, double cg_s2 = 0.0, double* cg_part = nullptr);
+                     int kind = 0, double cg_s2 = 0.0, double* cg_part = nullptr,
+                     bool prepacked = false);
+constexpr int LV_MAXB = 8;   // right-hand sides per level-pass batch (apply.cu)
 int cg_nblk(const Plan& pl);
 // User-order apply with gather/scatter: out = K v restricted to targets (unions).
 // Columns: v stride n_src, out stride n - tgt_off.

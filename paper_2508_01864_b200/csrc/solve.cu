@@ -133,9 +133,13 @@ __global__ void k_pupd(double* __restrict__ P, const double* __restrict__ R,
   const double b = beta[c];
   double* p = P + (size_t)c * n;
   const double* r = R + (size_t)c * n;
+  double* pu = (pts && c >= c0 && c < c1) ? pts + (size_t)(c - c0) * n * 4 + 3 : nullptr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(b, p[i], r[i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double pn = fma(b, p[i], r[i]);
+    p[i] = pn;
+    if (pu) pu[4 * i] = pn;
+  }
 }
 
 // ---- fused CG iteration.  The apply's epilogue already returns
@@ -195,10 +199,14 @@ __global__ void k_cg_xr(double* __restrict__ X, double* __restrict__ R,
 
 // beta = new r.r / old r.r; p = r + beta p (active columns); convergence at
 // r.r <= tol2 (status 1, block 0); rr_out[c] = new r.r for the host
+// pts != nullptr (d >= 2): columns c0 <= c < c1 are the next apply's one run of active columns;
+// the new p also goes into the u field of its packed point records (32 B per point, column
+// c - c0), so that apply needs no pack launch (apply_rank prepacked).
 __global__ void k_cg_p(double* __restrict__ P, const double* __restrict__ R,
                        const double* __restrict__ rr_new, const double* __restrict__ rr_old,
                        const double* __restrict__ tol2, int* __restrict__ status,
-                       double* __restrict__ rr_out, int64_t n) {
+                       double* __restrict__ rr_out, int64_t n, double* __restrict__ pts, int c0,
+                       int c1) {
   __shared__ double sh[32];
   __shared__ double s_beta;
   __shared__ int s_act;
@@ -219,9 +227,13 @@ __global__ void k_cg_p(double* __restrict__ P, const double* __restrict__ R,
   const double b = s_beta;
   double* p = P + (size_t)c * n;
   const double* r = R + (size_t)c * n;
+  double* pu = (pts && c >= c0 && c < c1) ? pts + (size_t)(c - c0) * n * 4 + 3 : nullptr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(b, p[i], r[i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double pn = fma(b, p[i], r[i]);
+    p[i] = pn;
+    if (pu) pu[4 * i] = pn;
+  }
 }
 
 // X columns back to user order: Xu[c][perm[r]] = X[c][r]
@@ -425,6 +437,18 @@ struct CgBufs {
 static gp_status cg_block(Plan& pl, const CgBufs& b, double sigma2, int it0, int iters,
                           const std::vector<char>& act, cudaStream_t s) {
   const int64_t n = pl.n;
+  // d >= 2 with one run of at most LV_MAXB active columns: k_cg_p writes the new p straight
+  // into the packed point records of the next apply (no pack launch after the block's first
+  // iteration, which packs t and p itself)
+  int nruns = 0, r0 = 0, r1 = 0;
+  for (int c = 0; c < b.k;) {
+    if (!act[c]) { ++c; continue; }
+    int e = c;
+    while (e < b.k && act[e]) ++e;
+    if (nruns++ == 0) { r0 = c; r1 = e; }
+    c = e;
+  }
+  const bool fuse_pack = pl.d >= 2 && nruns == 1 && r1 - r0 <= LV_MAXB && !getenv("GPM_CG_NOPACKFUSE");
   for (int j = 0; j < iters; ++j) {
     const int it = it0 + j;
     double* rr_new = b.prr + (size_t)(it & 1) * b.k * CG_GRID;
@@ -435,13 +459,15 @@ static gp_status cg_block(Plan& pl, const CgBufs& b, double sigma2, int it0, int
       int e = c;
       while (e < b.k && act[e]) ++e;
       GPM_TRY(apply_rank(pl, b.P + (size_t)c * n, b.Q + (size_t)c * n, e - c, s, 0, sigma2,
-                         b.ppq + (size_t)c * b.nb_pq));
+                         b.ppq + (size_t)c * b.nb_pq, fuse_pack && j > 0));
       c = e;
     }
     k_cg_xr<<<dim3(CG_GRID, b.k), CG_BLOCK, 0, s>>>(b.X, b.R, b.P, b.Q, b.ppq, b.nb_pq, rr_old,
                                                      rr_new, b.status, b.bd_iter, it, n);
     k_cg_p<<<dim3(CG_GRID, b.k), CG_BLOCK, 0, s>>>(b.P, b.R, rr_new, rr_old, b.tol2, b.status,
-                                                    b.rr, n);
+                                                    b.rr, n,
+                                                    fuse_pack && j + 1 < iters ? pl.pts.as<double>() : nullptr,
+                                                    r0, r1);
   }
   GPM_CUDA(cudaGetLastError());
   return GP_OK;

@@ -4,7 +4,7 @@ import collections
 import csv
 import sys
 
-APPLY = ("k_d1_ov", "k_d1_fast", "k_pack", "k_low2", "k_low3", "k_mid3", "k_cp", "k_epilogue")
+APPLY = ("k_d1_lpc", "k_d1_big", "k_cp_carry", "k_pack", "k_low2", "k_low3", "k_mid3", "k_cp", "k_epilogue")
 
 
 def summary(path, applies):
