@@ -133,13 +133,9 @@ __global__ void k_pupd(double* __restrict__ P, const double* __restrict__ R,
   const double b = beta[c];
   double* p = P + (size_t)c * n;
   const double* r = R + (size_t)c * n;
-  double* pu = (pts && c >= c0 && c < c1) ? pts + (size_t)(c - c0) * n * 4 + 3 : nullptr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double pn = fma(b, p[i], r[i]);
-    p[i] = pn;
-    if (pu) pu[4 * i] = pn;
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], r[i]);
 }
 
 // ---- fused CG iteration.  The apply's epilogue already returns
