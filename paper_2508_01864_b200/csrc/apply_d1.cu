@@ -249,8 +249,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
                                                            // the end; s_t[-1] = t[c0 - 1])
   double* s_e = s_t + SUB + 8;                         // SUB + 8: e^{-gap} (1 past the end)
   double* s_ub = s_e + SUB + 8;                        // NUB x SUB: u, then out (rank order)
-  int* s_pi = reinterpret_cast<int*>(s_ub + NUB * SUB);   // SUB + 8 (user order)
-  __shared__ uint64_t mbar[NPART], mbar_v[NUB][NPART], mbar_tab;
+  // user order: the chunk's perm (SUB + 8 ints) lives in the upper half of the one u buffer
+  // (28 KB less shared memory: the 3x10 shape stays below the largest carve-out, whose small L1
+  // halves the gather rate -- profiles/r02_notes.md).  It is read before u is written (one block barrier) and
+  // bulk-copied again after the local pass, for the scatter.
+  int* s_pi = reinterpret_cast<int*>(s_ub + SUB / 2);
+  __shared__ uint64_t mbar[NPART], mbar_v[NUB][NPART], mbar_tab, mbar_pi;
   __shared__ __align__(16) double s_tab[64];
   __shared__ double s_wf[NW][NQ + 2], s_wb[NW][NQ + 2];   // warp totals of the block scan
   __shared__ double s_red[NW][NV];                        // warp partials of the chunk sum
@@ -299,6 +303,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       for (int ub = 0; ub < NUB; ++ub) mbar_init(&mbar_v[ub][p], 1);
     }
     mbar_init(&mbar_tab, 1);
+    mbar_init(&mbar_pi, 1);
     mbar_fence_init();
   }
   __syncthreads();   // barrier initialisation visible
@@ -362,8 +367,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
     if (j >= cnt) {
       s_t[j] = tlast;
       s_e[j] = 1.0;
+      if (!USER) {   // user order: every thread writes all its u slots per column
 #pragma unroll
-      for (int ub = 0; ub < NUB; ++ub) s_ub[ub * SUB + j] = 0.0;
+        for (int ub = 0; ub < NUB; ++ub) s_ub[ub * SUB + j] = 0.0;
+      }
     }
     if (USER && j >= ((cnt + 3) & ~3)) s_pi[j] = INT_MAX;
   }
@@ -387,9 +394,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const int pi = s_pi[j0 + k];
-        uu[k] = pi < a.n_src ? __ldg(vcol + pi) : 0.0;
+        uu[k] = (j0 + k < cnt && pi < a.n_src) ? __ldg(vcol + pi) : 0.0;
       }
       if (a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
+      __syncthreads();   // perm shares the u buffer: every thread's perm reads precede the u writes
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = uu[k];
     } else if (v_bulk) {
@@ -476,6 +484,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       if ((lane & (32 / pow2_at_least(NV) - 1)) == 0 && id < NV) s_red[warp][id] = sw;
     }
     __syncthreads();   // #1: chunk-sum partials
+    if (USER && tid == 0) {   // u is consumed: perm back into its upper half for the scatter
+      fence_proxy_async_smem();
+      const unsigned np = (unsigned)((cnt + 3) & ~3);
+      mbar_expect_tx(&mbar_pi, np * 4);
+      tma_load_1d(s_pi, a.perm + c0, np * 4, &mbar_pi);
+    }
     if (tid < NV) {    // one value per thread, warps summed in order, published as 2 words
       double s = 0.0;
 #pragma unroll 1
@@ -633,6 +647,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       }
     }
     if (USER) {
+      mbar_wait(&mbar_pi, (unsigned)(col & 1));
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const int j = j0 + k;
@@ -748,7 +763,7 @@ Shape make_shape() {
   shape_fns<BLOCK, SEGS, SL, true>(s.fn[1]);
   const size_t sub = (size_t)BLOCK * SEGS * SL;
   s.smem[0] = sizeof(double) * ((2 + lpc::lpc_nub(false, (int)sub)) * sub + 18);   // t, e, u buffers
-  s.smem[1] = sizeof(double) * (3 * sub + 18) + sizeof(int) * (sub + 8);   // t, e, u, perm
+  s.smem[1] = sizeof(double) * (3 * sub + 18 + 8);   // t, e, u (perm shares u's upper half)
   return s;
 }
 
