@@ -57,6 +57,7 @@ struct Args {
   int64_t n, n_src, tgt_off, chunk;
   int nrhs;
   int prefetch;        // user order: L2 prefetch of a 1/G slice of v per CTA
+  int cap;             // user order: shared-memory array capacity (multiple of 4, >= chunk + items)
   int64_t vstride, ostride;
   double os2;
   unsigned long long* rec;   // [2 parities][G][LL_W] LL words
@@ -247,13 +248,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* s_t = reinterpret_cast<double*>(smem_raw) + 2;   // [-2, SUB + 8): t (clamped past
                                                            // the end; s_t[-1] = t[c0 - 1])
-  double* s_e = s_t + SUB + 8;                         // SUB + 8: e^{-gap} (1 past the end)
-  double* s_ub = s_e + SUB + 8;                        // NUB x SUB: u, then out (rank order)
+  // Array capacity: SUB, or (user order, default shape) a.cap = the chunk's points + one
+  // thread's items, so that a 10^6-point plan stays in the 164 KB shared-memory class (more
+  // L1 for the random gathers).  Threads wholly past the chunk all use the last ITEMS slots
+  // (window base jb), which hold the neutral tail values.
+  constexpr bool RTCAP = USER && ITEMS == 27;   // the default shape only: the larger shapes sit
+                                                // at the register cap and lose more to the
+                                                // run-time strides than the L1 gives them
+  const int CAP = RTCAP ? a.cap : SUB;
+  double* s_e = s_t + CAP + 8;                         // CAP + 8: e^{-gap} (1 past the end)
+  double* s_ub = s_e + CAP + 8;                        // NUB x CAP: u, then out (rank order)
   // user order: the chunk's perm (SUB + 8 ints) lives in the upper half of the one u buffer
   // (28 KB less shared memory: the 3x10 shape stays below the largest carve-out, whose small L1
   // halves the gather rate -- profiles/r02_notes.md).  It is read before u is written (one block barrier) and
   // bulk-copied again after the local pass, for the scatter.
-  int* s_pi = reinterpret_cast<int*>(s_ub + SUB / 2);
+  int* s_pi = reinterpret_cast<int*>(s_ub + CAP / 2);
   __shared__ uint64_t mbar[NPART], mbar_v[NUB][NPART], mbar_tab, mbar_pi;
   __shared__ __align__(16) double s_tab[64];
   __shared__ double s_wf[NW][NQ + 2], s_wb[NW][NQ + 2];   // warp totals of the block scan
@@ -266,6 +275,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   const int64_t c0 = (int64_t)c * a.chunk;
   const int cnt = (int)min(a.chunk, a.n - c0);   // >= 1 (host: every CTA owns points)
   const int j0 = tid * ITEMS;
+  const int jb = (RTCAP && j0 >= cnt) ? a.cap - ITEMS : j0;   // shared-memory window of my items
   const int mypart = tid / PT;
   const bool part_live = mypart * PSZ < cnt;
   const bool v_bulk = !USER && ((reinterpret_cast<uintptr_t>(a.v + c0) & 15) == 0) &&
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   // rank order: a column of v by bulk copies into u buffer col % NUB (thread 0 owns the
   // barriers)
   auto issue_v = [&](int col) {
-    double* dst = s_ub + (col % NUB) * SUB;
+    double* dst = s_ub + (col % NUB) * CAP;
 #pragma unroll 1
     for (int p = 0; p < NPART; ++p) {
       const int lo = p * PSZ, hi = min(cnt, lo + PSZ);
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   // first point, the last points of my segments, the chunk's last point
   const double tref0 = c > 0 ? s_t[-1] : s_t[0];
   const double tlast = s_t[cnt - 1];
-  const double tprev = j0 == 0 ? tref0 : (j0 - 1 < cnt ? s_t[j0 - 1] : tlast);
+  const double tprev = j0 == 0 ? tref0 : (j0 - 1 < cnt ? s_t[jb - 1] : tlast);
   double tseg[SEGS];   // the last point of each of my segments
 #pragma unroll
   for (int sg = 0; sg < SEGS; ++sg) tseg[sg] = s_t[min(j0 + (sg + 1) * SL, cnt) - 1];
@@ -363,16 +373,16 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   // u = 0 (rank order: the bulk copies stop at cnt), no source index (user order)
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
-    const int j = j0 + k;
+    const int j = j0 + k, js = jb + k;
     if (j >= cnt) {
-      s_t[j] = tlast;
-      s_e[j] = 1.0;
+      s_t[js] = tlast;
+      s_e[js] = 1.0;
       if (!USER) {   // user order: every thread writes all its u slots per column
 #pragma unroll
-        for (int ub = 0; ub < NUB; ++ub) s_ub[ub * SUB + j] = 0.0;
+        for (int ub = 0; ub < NUB; ++ub) s_ub[ub * CAP + js] = 0.0;
       }
     }
-    if (USER && j >= ((cnt + 3) & ~3)) s_pi[j] = INT_MAX;
+    if (USER && j >= ((cnt + 3) & ~3)) s_pi[js] = INT_MAX;
   }
   // v-independent shifts, once per launch: my element's span, the chunk-sum shifts (my
   // last point -> chunk last point, chunk reference -> my t_prev)
@@ -385,7 +395,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   for (int col = 0; col < a.nrhs; ++col) {
     const double* vcol = a.v + col * a.vstride;
     double* ocol = a.out + col * a.ostride;
-    double* s_u = s_ub + (col % NUB) * SUB;
+    double* s_u = s_ub + (col % NUB) * CAP;
     const unsigned tag = base + (unsigned)col + 1u;
     unsigned long long* recp = a.rec + (size_t)(col & 1) * G * LL_W;
     // ---- u of my points into s_u (own items only: no block barrier needed)
@@ -393,13 +403,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       double uu[ITEMS];
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const int pi = s_pi[j0 + k];
+        const int pi = s_pi[jb + k];
         uu[k] = (j0 + k < cnt && pi < a.n_src) ? __ldg(vcol + pi) : 0.0;
       }
       if (a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
       __syncthreads();   // perm shares the u buffer: every thread's perm reads precede the u writes
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = uu[k];
+      for (int k = 0; k < ITEMS; ++k) s_u[jb + k] = uu[k];
     } else if (v_bulk) {
       if (part_live) mbar_wait(&mbar_v[col % NUB][mypart], (unsigned)((col / NUB) & 1));
       const int lo = mypart * PSZ, hi = min(cnt, lo + PSZ);
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         s_u[hi - 1] = __ldg(vcol + c0 + hi - 1);
     } else {
 #pragma unroll
-      for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = j0 + k < cnt ? __ldg(vcol + c0 + j0 + k) : 0.0;
+      for (int k = 0; k < ITEMS; ++k) s_u[jb + k] = j0 + k < cnt ? __ldg(vcol + c0 + j0 + k) : 0.0;
     }
     LPC_STAMP(2);
     // ---- local pass from zero state: the forward recurrence over all my points and the
@@ -424,21 +434,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       const int sf = ph, sb = SEGS - 1 - ph;       // forward / backward segment
       const int f0 = sf * SL, b0 = sb * SL;
       double tf[SL + 1], ef[SL], uf[SL], tb[SL + 1], eb[SL + 1], ub[SL];
-      tf[0] = sf ? s_t[j0 + f0 - 1] : tprev;
+      tf[0] = sf ? s_t[jb + f0 - 1] : tprev;
 #pragma unroll
       for (int k = 0; k < SL; ++k) {
-        tf[k + 1] = s_t[j0 + f0 + k];
-        ef[k] = s_e[j0 + f0 + k];
-        uf[k] = a.os2 * s_u[j0 + f0 + k];
+        tf[k + 1] = s_t[jb + f0 + k];
+        ef[k] = s_e[jb + f0 + k];
+        uf[k] = a.os2 * s_u[jb + f0 + k];
       }
 #pragma unroll
       for (int k = 0; k < SL; ++k) {   // the backward segment's t, e^{-gap} of the next point
-        tb[k] = sf == sb ? tf[k + 1] : s_t[j0 + b0 + k];
-        ub[k] = sf == sb ? uf[k] : a.os2 * s_u[j0 + b0 + k];
-        eb[k] = k == 0 ? 0.0 : (sf == sb ? ef[k] : s_e[j0 + b0 + k]);
+        tb[k] = sf == sb ? tf[k + 1] : s_t[jb + b0 + k];
+        ub[k] = sf == sb ? uf[k] : a.os2 * s_u[jb + b0 + k];
+        eb[k] = k == 0 ? 0.0 : (sf == sb ? ef[k] : s_e[jb + b0 + k]);
       }
-      tb[SL] = sb + 1 < SEGS ? s_t[j0 + b0 + SL] : 0.0;
-      eb[SL] = sb + 1 < SEGS ? s_e[j0 + b0 + SL] : 1.0;
+      tb[SL] = sb + 1 < SEGS ? s_t[jb + b0 + SL] : 0.0;
+      eb[SL] = sb + 1 < SEGS ? s_e[jb + b0 + SL] : 1.0;
 #pragma unroll
       for (int k = 0; k < SL; ++k) {
         const int i = f0 + k;              // forward point
@@ -457,8 +467,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
       }
     }
     {   // backward aggregate -> my t_prev
-      const double t0 = s_t[j0];
-      advance<P>(B, t0 - tprev, s_e[j0]);
+      const double t0 = s_t[jb];
+      advance<P>(B, t0 - tprev, s_e[jb]);
     }
     Run<NQ> me;   // my scan element: span t_prev -> my last point
     me.D = Dme;
@@ -607,7 +617,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
         g[q] += Fx.M[q];
         y[q] += Bx.M[q];
       }
-      advance<P>(g, s_t[j0] - tprev, s_e[j0]);   // -> my first point
+      advance<P>(g, s_t[jb] - tprev, s_e[jb]);   // -> my first point
       carry_beta<P, KIND>(g, bX);
       carry_beta<P, KIND>(y, bY);
     }
@@ -616,19 +626,19 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
     // the local pass), then the output
     {
       double Ef = 1.0, Eb = 1.0;
-      const double tfirst = s_t[j0], tmyl = s_t[j0 + ITEMS - 1];
+      const double tfirst = s_t[jb], tmyl = s_t[jb + ITEMS - 1];
 #pragma unroll
       for (int ph = 0; ph < SEGS; ++ph) {
         const int f0 = ph * SL, b0 = (SEGS - 1 - ph) * SL;
         double tf[SL], ef[SL], tb[SL], eb[SL + 1];
 #pragma unroll
         for (int k = 0; k < SL; ++k) {
-          tf[k] = s_t[j0 + f0 + k];
-          ef[k] = s_e[j0 + f0 + k];
-          tb[k] = f0 == b0 ? tf[k] : s_t[j0 + b0 + k];
-          eb[k] = k == 0 ? 0.0 : (f0 == b0 ? ef[k] : s_e[j0 + b0 + k]);
+          tf[k] = s_t[jb + f0 + k];
+          ef[k] = s_e[jb + f0 + k];
+          tb[k] = f0 == b0 ? tf[k] : s_t[jb + b0 + k];
+          eb[k] = k == 0 ? 0.0 : (f0 == b0 ? ef[k] : s_e[jb + b0 + k]);
         }
-        eb[SL] = b0 + SL < ITEMS ? s_e[j0 + b0 + SL] : 1.0;
+        eb[SL] = b0 + SL < ITEMS ? s_e[jb + b0 + SL] : 1.0;
 #pragma unroll
         for (int k = 0; k < SL; ++k) {
           const int i = f0 + k, kb = SL - 1 - k, ib = b0 + kb;
@@ -651,21 +661,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const int j = j0 + k;
-        const int pi = s_pi[j];
+        const int pi = s_pi[jb + k];
         if (j < cnt && pi >= a.tgt_off) ocol[pi - a.tgt_off] = loc[k];
       }
     } else if (!a.cg_part) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k)
-        if (j0 + k < cnt) s_u[j0 + k] = loc[k];   // the tail stays 0 for a later column
+        if (j0 + k < cnt) s_u[jb + k] = loc[k];   // the tail stays 0 for a later column
     } else {   // CG epilogue: q = K p + s2 p, partial p . q (the tail has p = 0)
       double pq = 0.0;
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
-        const double pk = s_u[j0 + k];
+        const double pk = s_u[jb + k];
         const double qk = fma(a.cg_s2, pk, loc[k]);
         pq = fma(pk, qk, pq);
-        if (j0 + k < cnt) s_u[j0 + k] = qk;
+        if (j0 + k < cnt) s_u[jb + k] = qk;
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) pq += __shfl_xor_sync(0xffffffffu, pq, off);
@@ -880,7 +890,11 @@ gp_status d1_launch(Plan& pl, const double* v, double* out, int nrhs, bool user_
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.d1_grid);
   cfg.blockDim = dim3(sh.block);
-  cfg.dynamicSmemBytes = sh.smem[user_order ? 1 : 0];
+  // user order: arrays sized by the chunk (+ one thread's items for the neutral tail window)
+  a.cap = (int)std::min<int64_t>((int64_t)sh.block * sh.items,
+                                 ((pl.d1_chunk + 3) & ~int64_t(3)) + ((sh.items + 3) & ~3));
+  cfg.dynamicSmemBytes = (user_order && sh.items == 27) ? sizeof(double) * (3 * (size_t)a.cap + 18 + 8)
+                                                          : sh.smem[user_order ? 1 : 0];
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
