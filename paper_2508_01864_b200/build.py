@@ -17,7 +17,7 @@ SUFFIX = os.environ.get("GPM_LIB_SUFFIX", "")
 LIB = os.path.join(HERE, f"libgpmatern{SUFFIX}.so")
 OBJDIR = os.path.join(HERE, "build" + SUFFIX)
 SOURCES = ["api.cu", "setup.cu", "apply.cu", "apply_d1.cu", "apply_d1_big.cu", "apply_level.cu",
-           "solve.cu", "lml.cu"]
+           "apply_level_p1.cu", "apply_level_p2.cu", "apply_level_p3.cu", "solve.cu", "lml.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -34,6 +34,7 @@ def _newer(target: str, deps) -> bool:
 
 def _headers():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hs.append(os.path.join(CSRC, "apply_level.cu"))   # included by apply_level_p{1,2,3}.cu
     hs.append(os.path.join(os.path.dirname(HERE), "include", "gpmatern.h"))
     return hs
 

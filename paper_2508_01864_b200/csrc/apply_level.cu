@@ -33,7 +33,24 @@
 #include "internal.h"
 #include "tma.cuh"
 
+// This file is compiled four times (build.py: apply_level.cu and apply_level_p{1,2,3}.cu, which
+// only set GPM_LEVEL_PART and include it) so that the template instantiations build in
+// parallel: part 0 = the non-template host code and the d = 2 value algebras, 1 = the d = 2
+// gradients, 2 = the d = 3 value algebras, 3 = the d = 3 gradients.
+#ifndef GPM_LEVEL_PART
+#define GPM_LEVEL_PART 0
+#endif
+
 namespace gpm {
+
+int level_nparts(const Plan& pl);
+bool level_p3(const Plan& pl);
+int level_nab(const Plan& pl);
+int level_phases(const Plan& pl, int kind);
+int64_t hp_item_count(int64_t n, int d);
+gp_status level_passes_p1(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase);
+gp_status level_passes_p2(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase);
+gp_status level_passes_p3(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase);
 
 constexpr int LV_LOGTILE = 10;
 constexpr int LV_TILE = 1 << LV_LOGTILE;
@@ -877,6 +894,7 @@ __host__ __device__ inline HpView hp_view(const unsigned char* base, int64_t nac
   return v;
 }
 
+#if GPM_LEVEL_PART == 0
 __global__ void k_hp_prep(LvArgs g, unsigned char* base, bool p3) {
   HpView v = hp_view(base, g.n_act, p3);
   double* d = const_cast<double*>(v.d);
@@ -901,6 +919,8 @@ __global__ void k_hp_prep(LvArgs g, unsigned char* base, bool p3) {
     }
   }
 }
+
+#endif   // GPM_LEVEL_PART == 0
 
 // one carried pass (flattened work items item0 .. item0 + ntiles - 1 of k_cp)
 struct HpDesc {
@@ -1374,6 +1394,7 @@ static cudaError_t lv_set_attrs() {
                               (int)sizeof(CpSmemT<A::ST2>));
 }
 
+#if GPM_LEVEL_PART == 0
 // The carried passes of a plan, in apply order: (ord, ord2l1, lseg, l1, n_act).
 struct HPass {
   const int* ord;
@@ -1485,14 +1506,13 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
   return GP_OK;
 }
 
-int level_nparts(const Plan& pl);
 
 // Sharded applies (gp_kmvm_partial): shard `shard` of `nshards` runs the
 // tiles [T lo, T hi) of the tile kernels (k_low*, k_mid3) and the items [I lo, I hi) of the
 // carried-pass apply (k_cp<2>); the carried-pass aggregates and carries (k_cp<1>,
 // k_cp_carry) run whole on every shard.  Every pair lies in exactly one tile or item, so
 // the shards' partial outputs sum to K v.
-static int64_t hp_item_count(int64_t n, int d) {
+int64_t hp_item_count(int64_t n, int d) {
   int L = 0;
   while ((int64_t(1) << L) < n) ++L;
   int64_t items = 0;
@@ -1522,6 +1542,8 @@ void shard_ranges(int64_t n, int d, int shard, int nshards, int64_t* r) {
   r[2] = items * shard / nshards;
   r[3] = items * (shard + 1) / nshards;
 }
+
+#endif   // GPM_LEVEL_PART == 0
 
 template <class A>
 static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
@@ -1661,6 +1683,7 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   return GP_OK;
 }
 
+#if GPM_LEVEL_PART == 0
 // per-pass contribution slots: carried passes, then (d = 3) one per outer level l1 > 10, then
 // the parts 1.. of the fused low kernels
 int level_nparts(const Plan& pl) {
@@ -1702,73 +1725,75 @@ gp_status level_pack(Plan& pl, const double* v, int nrhs, bool user_order, cudaS
 }
 size_t level_pt_bytes() { return sizeof(Pt4); }
 
+#endif   // GPM_LEVEL_PART == 0
+
+// Dispatch on the algebra.  Every part defines its own share of the instantiations.
+#if GPM_LEVEL_PART == 0
 gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase) {
   const bool prod = pl.form == GP_FORM_PRODUCT;
   const int P = pl.P;
 #ifdef GPM_FEW   // experiment builds (build.py GPM_EXTRA_FLAGS): the three bench algebras only
   if (kind == 0 && pl.d == 2 && P == 1 && !prod) return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
   if (kind == 0 && pl.d == 2 && P == 1 && prod) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
-  if (kind == 0 && pl.d == 3 && P == 2 && !prod) return lv_run<Alg<2, 4, false>>(pl, nrhs, s, launches);
+  if (kind == 0 && pl.d == 3 && P == 2 && !prod) return level_passes_p2(pl, nrhs, s, launches, kind, phase);
   return fail(GP_ERR_UNSUPPORTED, "GPM_FEW experiment build");
 #else
-  if (kind != 0) {   // lengthscale gradient: moment order p + 1
-    if (prod && level_phases(pl, kind) == 2) {
-      // separated product-form gradient (algebra.cuh SEP 2 / SEP 3): d = 3, and d = 2 at
-      // nu = 9/2 (whose mixed-moment state would need 2 x 36 doubles)
-      if (pl.d == 2)
-        return phase == 0 ? lv_run<Alg<4, 2, false, 0, 2>>(pl, nrhs, s, launches)
-                          : lv_run<Alg<5, 2, false, 1, 3>>(pl, nrhs, s, launches);
-      switch (P) {
-        case 1: return phase == 0 ? lv_run<Alg<1, 4, false, 0, 2>>(pl, nrhs, s, launches)
-                                  : lv_run<Alg<2, 4, false, 1, 3>>(pl, nrhs, s, launches);
-        case 2: return phase == 0 ? lv_run<Alg<2, 4, false, 0, 2>>(pl, nrhs, s, launches)
-                                  : lv_run<Alg<3, 4, false, 1, 3>>(pl, nrhs, s, launches);
-        case 3: return phase == 0 ? lv_run<Alg<3, 4, false, 0, 2>>(pl, nrhs, s, launches)
-                                  : lv_run<Alg<4, 4, false, 1, 3>>(pl, nrhs, s, launches);
-        default: return phase == 0 ? lv_run<Alg<4, 4, false, 0, 2>>(pl, nrhs, s, launches)
-                                   : lv_run<Alg<5, 4, false, 1, 3>>(pl, nrhs, s, launches);
-      }
-    }
-    if (prod) {        // d = 2 product form, nu <= 7/2 ((p+2)^2 moments per channel)
-      if (P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
-      if (P == 1) return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
-      if (P == 2) return lv_run<Alg<3, 2, true, 1>>(pl, nrhs, s, launches);
-      return lv_run<Alg<4, 2, true, 1>>(pl, nrhs, s, launches);
-    }
-    if (pl.d == 2) {
-      switch (P) {
-        case 0: return lv_run<Alg<1, 2, false, 1>>(pl, nrhs, s, launches);
-        case 1: return lv_run<Alg<2, 2, false, 1>>(pl, nrhs, s, launches);
-        case 2: return lv_run<Alg<3, 2, false, 1>>(pl, nrhs, s, launches);
-        case 3: return lv_run<Alg<4, 2, false, 1>>(pl, nrhs, s, launches);
-        default: return lv_run<Alg<5, 2, false, 1>>(pl, nrhs, s, launches);
-      }
-    }
+  if (pl.d == 3) return kind != 0 ? level_passes_p3(pl, nrhs, s, launches, kind, phase)
+                                  : level_passes_p2(pl, nrhs, s, launches, kind, phase);
+  if (kind != 0) return level_passes_p1(pl, nrhs, s, launches, kind, phase);
+  if (!prod) {
     switch (P) {
-      case 0: return lv_run<Alg<1, 4, false, 1>>(pl, nrhs, s, launches);
-      case 1: return lv_run<Alg<2, 4, false, 1>>(pl, nrhs, s, launches);
-      case 2: return lv_run<Alg<3, 4, false, 1>>(pl, nrhs, s, launches);
-      case 3: return lv_run<Alg<4, 4, false, 1>>(pl, nrhs, s, launches);
-      default: return lv_run<Alg<5, 4, false, 1>>(pl, nrhs, s, launches);   // 4 x 6 moments (LvRec<24>)
+      case 0: return lv_run<Alg<0, 2, false>>(pl, nrhs, s, launches);
+      case 1: return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
+      case 2: return lv_run<Alg<2, 2, false>>(pl, nrhs, s, launches);
+      case 3: return lv_run<Alg<3, 2, false>>(pl, nrhs, s, launches);
+      default: return lv_run<Alg<4, 2, false>>(pl, nrhs, s, launches);
     }
   }
-  if (pl.d == 2) {
-    if (!prod) {
-      switch (P) {
-        case 0: return lv_run<Alg<0, 2, false>>(pl, nrhs, s, launches);
-        case 1: return lv_run<Alg<1, 2, false>>(pl, nrhs, s, launches);
-        case 2: return lv_run<Alg<2, 2, false>>(pl, nrhs, s, launches);
-        case 3: return lv_run<Alg<3, 2, false>>(pl, nrhs, s, launches);
-        default: return lv_run<Alg<4, 2, false>>(pl, nrhs, s, launches);
-      }
-    }
-    if (P == 0) return lv_run<Alg<0, 2, true>>(pl, nrhs, s, launches);
-    if (P == 1) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
-    if (P == 2) return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
-    if (P == 3) return lv_run<Alg<3, 2, true>>(pl, nrhs, s, launches);
-    return lv_run<Alg<4, 2, true>>(pl, nrhs, s, launches);
+  if (P == 0) return lv_run<Alg<0, 2, true>>(pl, nrhs, s, launches);
+  if (P == 1) return lv_run<Alg<1, 2, true>>(pl, nrhs, s, launches);
+  if (P == 2) return lv_run<Alg<2, 2, true>>(pl, nrhs, s, launches);
+  if (P == 3) return lv_run<Alg<3, 2, true>>(pl, nrhs, s, launches);
+  return lv_run<Alg<4, 2, true>>(pl, nrhs, s, launches);
+#endif
+}
+#elif GPM_LEVEL_PART == 1
+// d = 2 lengthscale gradients: moment order p + 1
+gp_status level_passes_p1(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase) {
+#ifdef GPM_FEW
+  return fail(GP_ERR_UNSUPPORTED, "GPM_FEW experiment build");
+#else
+  const bool prod = pl.form == GP_FORM_PRODUCT;
+  const int P = pl.P;
+  if (prod && level_phases(pl, kind) == 2)
+    // separated product-form gradient (algebra.cuh SEP 2 / SEP 3) at nu = 9/2, whose
+    // mixed-moment state would need 2 x 36 doubles
+    return phase == 0 ? lv_run<Alg<4, 2, false, 0, 2>>(pl, nrhs, s, launches)
+                      : lv_run<Alg<5, 2, false, 1, 3>>(pl, nrhs, s, launches);
+  if (prod) {        // product form, nu <= 7/2 ((p+2)^2 moments per channel)
+    if (P == 0) return lv_run<Alg<1, 2, true, 1>>(pl, nrhs, s, launches);
+    if (P == 1) return lv_run<Alg<2, 2, true, 1>>(pl, nrhs, s, launches);
+    if (P == 2) return lv_run<Alg<3, 2, true, 1>>(pl, nrhs, s, launches);
+    return lv_run<Alg<4, 2, true, 1>>(pl, nrhs, s, launches);
   }
-  if (level_p3(pl)) {   // d = 3 product form (nu = 1/2 is the L1 kernel)
+  switch (P) {
+    case 0: return lv_run<Alg<1, 2, false, 1>>(pl, nrhs, s, launches);
+    case 1: return lv_run<Alg<2, 2, false, 1>>(pl, nrhs, s, launches);
+    case 2: return lv_run<Alg<3, 2, false, 1>>(pl, nrhs, s, launches);
+    case 3: return lv_run<Alg<4, 2, false, 1>>(pl, nrhs, s, launches);
+    default: return lv_run<Alg<5, 2, false, 1>>(pl, nrhs, s, launches);
+  }
+#endif
+}
+#elif GPM_LEVEL_PART == 2
+// d = 3 values: the L1 form, and the product form by the separated sub-passes (SEP 1)
+gp_status level_passes_p2(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase) {
+  const int P = pl.P;
+#ifdef GPM_FEW
+  if (P == 2 && !level_p3(pl)) return lv_run<Alg<2, 4, false>>(pl, nrhs, s, launches);
+  return fail(GP_ERR_UNSUPPORTED, "GPM_FEW experiment build");
+#else
+  if (level_p3(pl)) {   // product form (nu = 1/2 is the L1 kernel)
     switch (P) {
       case 1: return lv_run<Alg<1, 4, false, 0, 1>>(pl, nrhs, s, launches);
       case 2: return lv_run<Alg<2, 4, false, 0, 1>>(pl, nrhs, s, launches);
@@ -1785,7 +1810,38 @@ gp_status level_passes(Plan& pl, int nrhs, cudaStream_t s, int* launches, int ki
   }
 #endif
 }
+#else
+// d = 3 lengthscale gradients: L1 with one more moment; product form in two separated runs
+gp_status level_passes_p3(Plan& pl, int nrhs, cudaStream_t s, int* launches, int kind, int phase) {
+#ifdef GPM_FEW
+  return fail(GP_ERR_UNSUPPORTED, "GPM_FEW experiment build");
+#else
+  const int P = pl.P;
+  if (level_phases(pl, kind) == 2) {
+    switch (P) {
+      case 1: return phase == 0 ? lv_run<Alg<1, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                : lv_run<Alg<2, 4, false, 1, 3>>(pl, nrhs, s, launches);
+      case 2: return phase == 0 ? lv_run<Alg<2, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                : lv_run<Alg<3, 4, false, 1, 3>>(pl, nrhs, s, launches);
+      case 3: return phase == 0 ? lv_run<Alg<3, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                : lv_run<Alg<4, 4, false, 1, 3>>(pl, nrhs, s, launches);
+      default: return phase == 0 ? lv_run<Alg<4, 4, false, 0, 2>>(pl, nrhs, s, launches)
+                                 : lv_run<Alg<5, 4, false, 1, 3>>(pl, nrhs, s, launches);
+    }
+  }
+  switch (P) {
+    case 0: return lv_run<Alg<1, 4, false, 1>>(pl, nrhs, s, launches);
+    case 1: return lv_run<Alg<2, 4, false, 1>>(pl, nrhs, s, launches);
+    case 2: return lv_run<Alg<3, 4, false, 1>>(pl, nrhs, s, launches);
+    case 3: return lv_run<Alg<4, 4, false, 1>>(pl, nrhs, s, launches);
+    default: return lv_run<Alg<5, 4, false, 1>>(pl, nrhs, s, launches);   // 4 x 6 moments (LvRec<24>)
+  }
+#endif
+}
+#endif
 
+#if GPM_LEVEL_PART == 0
 int64_t level_tiles(int64_t n) { return (n + LV_TILE - 1) / LV_TILE; }
+#endif   // GPM_LEVEL_PART == 0
 
 }  // namespace gpm
