@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
 #pragma unroll
       for (int k = 0; k < ITEMS; ++k) {
         const int pi = s_pi[jb + k];
-        uu[k] = (j0 + k < cnt && pi < a.n_src) ? __ldg(vcol + pi) : 0.0;
+        uu[k] = (j0 + k < cnt && pi < a.n_src) ? __ldcg(vcol + pi) : 0.0;   // no reuse: L2 only (gs_variants.cu)
       }
       if (a.prefetch && tid == 32 && col + 1 < a.nrhs) prefetch_v(col + 1);
       __syncthreads();   // perm shares the u buffer: every thread's perm reads precede the u writes

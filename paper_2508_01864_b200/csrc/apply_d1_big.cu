@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK >= 256 ? 1 : (ITEMS > 16 ? 2 : 4)
     for (int k = 0; k < ITEMS; ++k) {
       const int j = j0 + k;
       const int pi = j < cnt ? s_pi[j] : INT_MAX;
-      uu[k] = pi < a.n_src ? __ldg(a.v + pi) : 0.0;
+      uu[k] = pi < a.n_src ? __ldcg(a.v + pi) : 0.0;   // no reuse: L2 only
     }
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) s_u[j0 + k] = uu[k];

@@ -1113,7 +1113,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
       const unsigned r = SM.st[0].rc[cpz(i0 + k)] & CP_RMASK;
-      un[k] = r != CP_RMASK ? g.pts[r].u : 0.0;
+      un[k] = r != CP_RMASK ? __ldcg(&g.pts[r].u) : 0.0;
     }
   }
   int j = 0, p = 0;
@@ -1155,7 +1155,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
         for (int k = 0; k < CP_ITEMS; ++k) {
           const unsigned r = E.rc[cpz(i0 + k)] & CP_RMASK;
-          un[k] = r != CP_RMASK ? pn[r].u : 0.0;
+          un[k] = r != CP_RMASK ? __ldcg(&pn[r].u) : 0.0;
         }
       } else if (item + G < total) {
         Stage& En = SM.st[sidx ^ 1];
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
 #pragma unroll
         for (int k = 0; k < CP_ITEMS; ++k) {
           const unsigned r = En.rc[cpz(i0 + k)] & CP_RMASK;
-          un[k] = r != CP_RMASK ? g.pts[r].u : 0.0;
+          un[k] = r != CP_RMASK ? __ldcg(&g.pts[r].u) : 0.0;
         }
       }
       }
@@ -1705,7 +1705,7 @@ __global__ void k_pack(const double* __restrict__ t, int64_t n, int d,
     p.t3 = d == 3 ? t[2 * n + r] : 0.0;
     if (perm) {
       const int i = __ldg(perm + r);
-      p.u = i < n_src ? __ldg(v + i) : 0.0;
+      p.u = i < n_src ? __ldcg(v + i) : 0.0;
     } else {
       p.u = v[r];
     }
