@@ -926,9 +926,7 @@ gp_status lml_eval(Plan& pl, Precond* pc, double s2, const double* r_user, const
   GPM_CUDA(cudaMemcpyAsync(P0, X, 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));   // col 0: a
   // (3) K [a, P^-1 z] and l dK/dl [a, P^-1 z]
   GPM_TRY(apply_rank(pl, P0, KP, nc, s, 0));
-  const bool has_dl = (pl.d == 1 || (pl.d == 2 && pl.form == GP_FORM_L1)) ||
-                      (pl.d == 3 && pl.form == GP_FORM_L1 && pl.P <= 3) ||
-                      (pl.d == 2 && pl.form == GP_FORM_PRODUCT && pl.P <= 3);
+  const bool has_dl = true;   // every (nu, form, d) has a lengthscale-gradient MVM (round 2)
   if (has_dl) GPM_TRY(apply_rank(pl, P0, DP, nc, s, 1));
   // (4) dots: col 0: a.Ka, a.dKa, a.a, r.a ; probe c: x_c.K p_c, x_c.dK p_c, x_c.p_c
   //     (x_c = A^-1 z_c from Lanczos, p_c = P^-1 z_c)

@@ -62,7 +62,8 @@ def test_pivoted_cholesky_factor(gpm, d, form):
 
 
 STABLE = [(1, 3, "l1", [0.01], 0.1), (2, 3, "product", [0.05, 0.05], 0.05),
-          (3, 5, "l1", [0.1, 0.1, 0.1], 0.2), (2, 5, "product", [0.04, 0.05], 0.05)]
+          (3, 5, "l1", [0.1, 0.1, 0.1], 0.2), (2, 5, "product", [0.04, 0.05], 0.05),
+          (3, 3, "product", [0.08, 0.1, 0.09], 0.1), (2, 9, "product", [0.04, 0.05], 0.05)]
 
 
 @pytest.mark.parametrize("case", range(len(STABLE)))
@@ -127,7 +128,7 @@ def test_lml_matches_oracle_estimator(gpm, case, precond):
         ldP = ol.sylvester_logdet(Lo, s2, 600)
         Z = Lo @ Wn.T + math.sqrt(s2) * G[:, ro].T
     got = plan.lml(to_dev(r), s2, to_dev(G), lanczos_iters=m, cg_rtol=1e-12, **kw)
-    has_dl = form == "l1" or d == 1 or (d == 2 and two_nu <= 7)
+    has_dl = True   # every (nu, form, d) has a lengthscale-gradient MVM
     dAs = [2.0 / os_ * (A - s2 * np.eye(600)),
            oracle.dense_dkernel(x[ro], x[ro], two_nu, form, ell, os_) if has_dl
            else np.zeros((600, 600)),
@@ -214,7 +215,7 @@ def test_lml_errors(gpm):
 
 
 @pytest.mark.parametrize("d,two_nu,form", [(1, 3, "l1"), (2, 1, "l1"), (2, 3, "product"),
-                                             (2, 5, "product")])
+                                             (2, 5, "product"), (3, 3, "product")])
 def test_fit_alg1_matches_oracle_trajectory(gpm, d, two_nu, form):
     """Algorithm 1 with the same probes: a few ADAM steps, one GLS round -- the GPU and the
     oracle follow the same trajectory (gradients agree to ~1e-7, ADAM is smooth in them)."""
@@ -222,9 +223,9 @@ def test_fit_alg1_matches_oracle_trajectory(gpm, d, two_nu, form):
     n = 400
     x = rng.random((n, d))
     H = np.hstack([np.ones((n, 1)), x])
-    y = H @ np.array([1.0, 0.5, -0.3][:1 + d]) + np.sin(5 * x[:, 0]) + 0.2 * rng.standard_normal(n)
+    y = H @ np.array([1.0, 0.5, -0.3, 0.2][:1 + d]) + np.sin(5 * x[:, 0]) + 0.2 * rng.standard_normal(n)
     G = rng.standard_normal((8, n))
-    ell0 = [0.02, 0.2][:d] if d == 1 else [0.05, 0.05]
+    ell0 = [0.02, 0.2][:d] if d == 1 else [0.05] * d
     ro = _rank_order(x)
     kw = dict(lr=0.05, max_steps=4, max_outer=1, grad_tol=1e-300, beta_tol=1e-300,
               lanczos_iters=20, cg_rtol=1e-12)
