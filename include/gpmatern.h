@@ -90,8 +90,8 @@ typedef struct {
   double logdet;          /* estimate of log det A (+ log det P when preconditioned) */
   double logdet_precond;  /* log det P, 0 without preconditioner */
   double grad[3];         /* dL/d outputscale, dL/d log(c) (all lengthscales scaled by c;
-                             = l dL/dl for one l; NaN where gp_kmvm_dlengthscale is
-                             unsupported), dL/d sigma */
+                             = l dL/dl for one l; every kernel has gp_kmvm_dlengthscale),
+                             dL/d sigma */
   int cg_iters;           /* iterations of the A^-1 r solve */
   int lanczos_iters;      /* Lanczos steps per probe (max over probes) */
 } gp_lml_result;
