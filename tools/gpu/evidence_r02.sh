@@ -28,6 +28,17 @@ case "${1:-fp64}" in
       python tools/prof_apply.py --config 3 --nu2 3 --applies 3 > gpurun_out/full_d2.log 2>&1
     ncu -i gpurun_out/d2.ncu-rep --page details > gpurun_out/r02_d2_config3_details.txt 2>&1
     rm -f gpurun_out/d2.ncu-rep ;;
+  d1)
+    # the headline kernel: plain run, launch list (time + DRAM bytes), one --set full capture
+    B="--steps 20 --warmup 3 --no-extras --no-cpu --no-cg"
+    python bench.py $B > gpurun_out/d1_plain.log 2>&1 &&
+    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file gpurun_out/r02_launches_bench_d1_final.csv python bench.py $B > gpurun_out/d1_launches.log 2>&1
+    ncu --set full --clock-control none --import-source on -k regex:k_d1_lpc -s 30 -c 1 -o gpurun_out/d1full \
+      python bench.py $B > gpurun_out/d1_full.log 2>&1
+    ncu -i gpurun_out/d1full.ncu-rep --page details > gpurun_out/r02_d1_lpc_user_full_details_final.txt 2>&1
+    python tools/ncu_lines.py gpurun_out/d1full.ncu-rep 100 > gpurun_out/r02_d1_lpc_user_lines_final.txt 2>&1
+    rm -f gpurun_out/d1full.ncu-rep ;;
   launches)
     python bench.py --steps 20 --warmup 3 --no-cg --no-cpu > gpurun_out/launches_plain.log 2>&1 &&
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
