@@ -476,6 +476,12 @@ __device__ __forceinline__ void load_ord8(const int* ord, int i0, int cnt, int b
   }
 }
 
+// L1 prefetch of this thread's 8 entries (32 B) of a later level's order: the level loops
+// are long, and the first use of the order stalls on an L2 round trip otherwise
+__device__ __forceinline__ void prefetch_ord8(const int* ord, int i0, int cnt) {
+  if (i0 < cnt) asm volatile("prefetch.global.L1 [%0];" ::"l"(ord + i0));
+}
+
 __host__ __device__ __forceinline__ int lv_clamp_lb(int lb, int lmax) {
   return lb < 3 ? (3 < lmax ? 3 : lmax) : (lb < lmax ? lb : lmax);
 }
@@ -532,6 +538,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low2(LvArgs g) {
     TItems it;
     double y[CP_ITEMS];
     load_ord8(ord, i0, cnt, (int)T0, it.o);
+    if (l < lmax) prefetch_ord8(ord + g.n, i0, cnt);   // the next level's order
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
       const int i = i0 + k;
@@ -637,6 +644,7 @@ __global__ void __launch_bounds__(CP_BLOCK, NC <= 2 ? 3 : 2) k_low2m(LvArgs g, i
     TItems it;
     double y[CP_ITEMS];
     load_ord8(ord, i0, cnt, (int)T0, it.o);
+    if (l < lmax) prefetch_ord8(ord + g.n, i0, cnt);   // the next level's order
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
       const int i = i0 + k;
@@ -719,6 +727,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_low3(LvArgs g) {
       double y[CP_ITEMS], a1k[CP_ITEMS], a2k[CP_ITEMS];
       int qq[CP_ITEMS];
       load_ord8(ord, i0, cnt, (int)T0, qq);
+      if (l2 < l1) prefetch_ord8(ord + g.n, i0, cnt);   // ord3[(l1, l2 + 1)] follows
 #pragma unroll
       for (int k = 0; k < CP_ITEMS; ++k) {
         const int i = i0 + k;
@@ -795,6 +804,7 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_LOW_MINB) k_mid3(LvArgs g) {
     TItems it;
     double y[CP_ITEMS], a1k[CP_ITEMS], a2k[CP_ITEMS];
     load_ord8(ord, i0, cnt, (int)T0, it.o);          // tile-local position = point index
+    if (l2 < LV_LOGTILE) prefetch_ord8(ord + g.n, i0, cnt);   // ord3[(l1, l2 + 1)] follows
 #pragma unroll
     for (int k = 0; k < CP_ITEMS; ++k) {
       const int i = i0 + k;
