@@ -1048,8 +1048,9 @@ __global__ void __launch_bounds__(32 * CC_WARPS) k_cp_carry(LvRecFor<A::NS>* agg
 
 // flattened work item -> pass: items are visited in increasing order, so each CTA keeps a
 // running pass index
+constexpr int CP_MAXDESC = 64;   // pass descriptors kept in k_cp's shared memory (2 KB)
 __device__ __forceinline__ int cp_pass_at(const HpDesc* descs, int npass, int p, int item) {
-  while (p + 1 < npass && __ldg(&descs[p + 1].item0) <= item) ++p;
+  while (p + 1 < npass && descs[p + 1].item0 <= item) ++p;
   return p;
 }
 
@@ -1083,7 +1084,7 @@ __device__ __forceinline__ double cp_a2(const CpStageT<A::ST2>& E, int z) {
 
 template <class A, int MODE>
 __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const unsigned char* hpbase,
-                                                   const HpDesc* descs, int npass, int total,
+                                                   const HpDesc* descs_g, int npass, int total,
                                                    int max_tiles, int nrhs, int64_t carr_off,
                                                    int item_lo) {
   // items [item_lo, total) of the flattened (pass, tile) list (a sharded apply's share)
@@ -1095,6 +1096,12 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
   __shared__ CpScratch<A> sc;
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ double s_tab[64];
+  // the pass descriptors in shared memory (every item looks its pass up; the global copy
+  // misses L1 behind the streamed tiles): up to CP_MAXDESC passes, else the global array
+  __shared__ HpDesc s_desc[CP_MAXDESC];
+  const HpDesc* descs = npass <= CP_MAXDESC ? s_desc : descs_g;
+  if (npass <= CP_MAXDESC)
+    for (int i = threadIdx.x; i < npass; i += CP_BLOCK) s_desc[i] = descs_g[i];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = tid * CP_ITEMS;
   const int G = gridDim.x;
