@@ -18,13 +18,18 @@
 // per CTA; nodes are aligned power-of-two position blocks, so node boundaries fall between
 // threads and the scans need no per-position flags.  Launch structure per apply:
 //   k_pack: rank-order point records (t1, t2, t3, u);
-//   d = 2: k_low2 -- near field (pairs split at levels <= lb) + levels lb < l <= 10 of each
-//          tile (point data staged once in shared memory);
+//   d = 2: k_low2 / k_low2m -- near field (pairs split at levels <= lb) + levels lb < l <= 10
+//          of each tile (point data staged once in shared memory), run in parts (blockIdx.z:
+//          near-field partner slices, then groups of levels; one output slot per part);
 //   d = 3: k_low3 -- the same for (l1 <= 10, all l2); k_mid3 -- every l1 > 10 with l2 <= 10
 //          (one launch, blockIdx.z = l1);
-//   carried passes (nodes longer than a tile): k_cp<1> tile aggregates + k_cp<2> apply,
-//          persistent over all passes with a bulk-copy pipeline of setup-staged tiles;
+//   carried passes (nodes longer than a tile): k_cp<1> tile aggregates, k_cp_carry (exclusive
+//          scan of a node's tile aggregates), k_cp<2> apply; persistent over all passes with a
+//          bulk-copy pipeline of setup-staged tiles;
 //   k_epilogue (apply.cu): fixed-order sum of the per-pass slots, scale, scatter.
+// Product forms: d = 2 carries (P+1)^2 mixed moments per channel (Alg PROD); d = 3, and the
+// gradients the mixed state cannot hold, run the (P+1)-moment engine once per separated
+// sub-pass (Alg SEP, algebra.cuh): level_apply in the tile kernels, extra columns in k_cp.
 #include <algorithm>
 #include <vector>
 
