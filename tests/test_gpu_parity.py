@@ -63,6 +63,16 @@ def test_d1_single_chunk_shapes(gpm, two_nu):
         outs.append(out)
     for o in outs[1:]:
         assert np.max(np.abs(o - outs[0])) <= 1e-13 * np.abs(outs[0]).max()
+    # user order, several columns per launch (the perm chunk shares the u buffer and is copied
+    # again for every column's scatter): each column bitwise equal to its single-column apply
+    V = np.random.default_rng(7).standard_normal((3, n))
+    for shape in (0, 1, 2):
+        plan.set_option(1, shape)
+        multi = plan.kmvm(to_dev(V)).cpu().numpy()
+        for c in range(3):
+            assert np.array_equal(multi[c], plan.kmvm(to_dev(V[c])).cpu().numpy())
+        check_rows(multi[2], x, V[2], two_nu, "l1", (0.02,), 1.0, rows=rows[:200],
+                   what=f"d1 shape {shape} column 2 of 3")
     with pytest.raises(gpm.GPError) as e:
         plan.set_option(0, 2)
     assert e.value.name == "INVALID_ARG"
