@@ -1198,11 +1198,15 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
           uc[k] = ur[k];
         }
       }
-      if (MODE == 2) {   // tile carries (k_cp_carry); read after the next barrier
+      // tile carries (k_cp_carry): loaded into registers now, stored to shared memory just
+      // before the barrier that precedes their first use (the load's latency hides behind
+      // the thread aggregates and the warp scan)
+      double cvf = 0.0, cvb = 0.0;
+      if (MODE == 2) {
         const double* cr = reinterpret_cast<const double*>(aggs + carr_off + 2 * t);
-        if (tid < A::NS + 2) reinterpret_cast<double*>(&sc.cf)[tid] = __ldcg(cr + tid);
+        if (tid < A::NS + 2) cvf = __ldcg(cr + tid);
         if (tid >= 32 && tid < 32 + A::NS + 2)
-          reinterpret_cast<double*>(&sc.cb)[tid - 32] = __ldcg(cr + sizeof(LvRecFor<A::NS>) / 8 + tid - 32);
+          cvb = __ldcg(cr + sizeof(LvRecFor<A::NS>) / 8 + tid - 32);
       }
       if constexpr (MODE == 1) {
         // ---- tile aggregates only: each thread's aggregates (direct form) shifted to the
@@ -1295,6 +1299,10 @@ __global__ void __launch_bounds__(CP_BLOCK, GPM_CP_MINB) k_cp(LvArgs g, const un
         if (lane == 31) sc.wf[warp] = X;
         S ex = cs_shfl<A::NS>(X, 1, true);
         if (lane == 0) ex = cs_id<A>();
+        if (MODE == 2) {
+          if (tid < A::NS + 2) reinterpret_cast<double*>(&sc.cf)[tid] = cvf;
+          if (tid >= 32 && tid < 32 + A::NS + 2) reinterpret_cast<double*>(&sc.cb)[tid - 32] = cvb;
+        }
         __syncthreads();
         if (MODE == 1) {
           if (tid == 0) {
