@@ -113,6 +113,11 @@ def test_product_d3_grad_multilevel(gpm):
     for r in range(2):
         check_rows(g[r], x, V[r], 3, "product", ell, 1.0, rows=rows, grad=True,
                    what=f"product d3 multilevel grad rhs {r}")
+    vr = plan.to_rank(to_dev(V[0]))
+    gr = plan.from_rank(plan.kmvm_dlengthscale(vr, rank_order=True)).cpu().numpy()
+    assert np.array_equal(gr, g[0])
+    # deterministic: the two-run gradient repeats bitwise
+    assert np.array_equal(plan.kmvm_dlengthscale(to_dev(V)).cpu().numpy(), g)
 
 
 @pytest.mark.parametrize("two_nu", [5, 7, 9])
