@@ -1658,6 +1658,20 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
                     32 * CC_WARPS, 0, pl.s2>>>(
         recs, recs + carr_off, dd, pl.hp_npass, pl.hp_maxtiles);
     GPM_CUDA(cudaGetLastError());
+    // the carried-pass apply follows on the side stream too (it only needs the aggregates
+    // and carries): its tail overlaps the tile kernels' (config 4 2.02 -> 1.99 ms;
+    // GPM_CP2_SIDE=0 puts it back on the main stream after the tile kernels)
+    static const int cp2_side = getenv("GPM_CP2_SIDE") ? atoi(getenv("GPM_CP2_SIDE")) : 1;
+    if (cp2_side) {
+      const int nit = (int)(sr[3] - sr[2]);
+      if (nit > 0) {
+        k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmemT<A::ST2>), pl.s2>>>(
+            g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, (int)sr[3], pl.hp_maxtiles, nrhs,
+            (int64_t)g.agg_stride * nrhs * A::NAB, (int)sr[2]);
+        *launches += 1;
+        GPM_CUDA(cudaGetLastError());
+      }
+    }
     GPM_CUDA(cudaEventRecord(pl.ev_join, pl.s2));
     *launches += 2;
   }
@@ -1701,7 +1715,8 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
   }
   if (hp) {   // carried-pass apply (needs the aggregates)
     GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
-    const int nit = (int)(sr[3] - sr[2]);
+    static const int cp2_side = getenv("GPM_CP2_SIDE") ? atoi(getenv("GPM_CP2_SIDE")) : 1;
+    const int nit = cp2_side ? 0 : (int)(sr[3] - sr[2]);
     if (nit > 0) {
       k_cp<A, 2><<<std::min(nit, grid2), CP_BLOCK, sizeof(CpSmemT<A::ST2>), s>>>(
           g, pl.hpbuf.as<unsigned char>(), dd, pl.hp_npass, (int)sr[3], pl.hp_maxtiles, nrhs,
