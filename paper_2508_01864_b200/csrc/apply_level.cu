@@ -1491,6 +1491,8 @@ gp_status level_setup(Plan& pl, cudaStream_t s) {
     GPM_CUDA(cudaStreamCreateWithFlags(&pl.s2, cudaStreamNonBlocking));
     GPM_CUDA(cudaEventCreateWithFlags(&pl.ev_fork, cudaEventDisableTiming));
     GPM_CUDA(cudaEventCreateWithFlags(&pl.ev_join, cudaEventDisableTiming));
+    GPM_CUDA(cudaStreamCreateWithFlags(&pl.s3, cudaStreamNonBlocking));
+    GPM_CUDA(cudaEventCreateWithFlags(&pl.ev_join3, cudaEventDisableTiming));
   }
   const std::vector<HPass> hp = high_passes(pl);
   const bool p3 = level_p3(pl);
@@ -1708,9 +1710,23 @@ static gp_status lv_run(Plan& pl, int nrhs, cudaStream_t s, int* launches) {
     GPM_CUDA(cudaGetLastError());
     if (L > LV_LOGTILE) {   // d = 3: every outer level l1 > 10 (inner l2 <= 10)
       g.l1 = LV_LOGTILE + 1;
-      k_mid3<A><<<dim3(tiles_run, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), s>>>(g);
+      // k_mid3 does not depend on k_low3: while the grids are small (up to two waves of tiles)
+      // it runs beside it on a stream of its own (d = 3, n = 2^14: 108 -> 67 us; at config 4's
+      // size the kernels fill the GPU either way).  GPM_MID3_SIDE = 0 / 1 forces it off / on.
+      static const int mid_env = getenv("GPM_MID3_SIDE") ? atoi(getenv("GPM_MID3_SIDE")) : -1;
+      const bool mid_side = mid_env >= 0 ? mid_env != 0 : tiles_run <= 296;
+      cudaStream_t sm = s;
+      if (mid_side && hp && pl.s3) {   // (ev_fork is recorded on s whenever hp)
+        GPM_CUDA(cudaStreamWaitEvent(pl.s3, pl.ev_fork, 0));
+        sm = pl.s3;
+      }
+      k_mid3<A><<<dim3(tiles_run, nrhs, L - LV_LOGTILE), CP_BLOCK, lv_smem_fused(), sm>>>(g);
       *launches += 1;
       GPM_CUDA(cudaGetLastError());
+      if (sm != s) {
+        GPM_CUDA(cudaEventRecord(pl.ev_join3, pl.s3));
+        GPM_CUDA(cudaStreamWaitEvent(s, pl.ev_join3, 0));
+      }
     }
   }
   if (hp) {   // carried-pass apply (needs the aggregates)

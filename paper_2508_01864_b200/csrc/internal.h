@@ -122,8 +122,8 @@ struct Plan {
   DevBuf hpdesc;                    // d>=2: per carried pass (offset, n_act, lseg, tiles)
   int hp_npass = 0, hp_maxtiles = 0, hp_items = 0;   // carried passes, max tiles, total tiles
   // d >= 2: side stream for the carried-pass aggregates (independent of the low levels)
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s2 = nullptr, s3 = nullptr;   // s3: d = 3 mid levels (k_mid3) beside the low levels
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join3 = nullptr;
   int low_unused = 0;       // trailing low-kernel part slots the last apply left unwritten
   int part_zero_cols = 0;   // columns of `part` whose never-written tail slots are zeroed
   // gp_kmvm_host pipelining: copy streams and per-slot events (in, compute, out) x 3

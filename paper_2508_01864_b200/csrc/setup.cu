@@ -132,7 +132,11 @@ void plan_free(Plan& pl) {
     b->release();
   if (pl.ev_fork) cudaEventDestroy(pl.ev_fork);
   if (pl.ev_join) cudaEventDestroy(pl.ev_join);
+  if (pl.ev_join3) cudaEventDestroy(pl.ev_join3);
   if (pl.s2) cudaStreamDestroy(pl.s2);
+  if (pl.s3) cudaStreamDestroy(pl.s3);
+  pl.s3 = nullptr;
+  pl.ev_join3 = nullptr;
   for (cudaEvent_t& e : pl.hev)
     if (e) { cudaEventDestroy(e); e = nullptr; }
   if (pl.hs_in) cudaStreamDestroy(pl.hs_in);
