@@ -359,7 +359,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_d1_lpc(Args a) {
   // first point, the last points of my segments, the chunk's last point
   const double tref0 = c > 0 ? s_t[-1] : s_t[0];
   const double tlast = s_t[cnt - 1];
-  const double tprev = j0 == 0 ? tref0 : (j0 - 1 < cnt ? s_t[jb - 1] : tlast);
+  // (true index: the first thread past the chunk, j0 == cnt, still reads the chunk's last point)
+  const double tprev = j0 == 0 ? tref0 : (j0 - 1 < cnt ? s_t[j0 - 1] : tlast);
   double tseg[SEGS];   // the last point of each of my segments
 #pragma unroll
   for (int sg = 0; sg < SEGS; ++sg) tseg[sg] = s_t[min(j0 + (sg + 1) * SL, cnt) - 1];

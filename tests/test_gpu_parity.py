@@ -44,6 +44,25 @@ def test_d1_all_rows(gpm, two_nu, n, kind):
     check_rows(out, x, v, two_nu, "l1", ell, 1.3, what=f"d1 nu={two_nu}/2 n={n} {kind}")
 
 
+@pytest.mark.parametrize("n", [1295, 1296, 1297, 2582, 2916, 4845, 2 * 27 * 4 * 7 + 1])
+def test_d1_chunks_that_are_multiples_of_the_thread_items(gpm, n):
+    """Chunks of 648 / 864 / 972 points are whole multiples of a thread's 27 items: no thread
+    straddles the chunk end, and the first thread past it must still see the chunk's last
+    point (a randomised sweep, tools/fuzz_parity.py, found its t_prev read from the shared
+    tail window instead).  User and rank order, every row, and K_zx on a union."""
+    rng = np.random.default_rng(n)
+    x = rng.random((n, 1)); v = rng.standard_normal(n)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(3, (0.1,), 1.0))
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, 3, "l1", (0.1,), 1.0, what=f"d1 n={n} user order")
+    outr = plan.from_rank(plan.kmvm_rank(plan.to_rank(to_dev(v)))).cpu().numpy()
+    assert np.max(np.abs(outr - out)) <= 1e-13 * np.abs(out).max()
+    z = rng.random((n // 3 + 1, 1))   # union sizes hit other chunk sizes
+    cr = plan.cross(to_dev(z))
+    check_rows(cr.kzx(to_dev(v)).cpu().numpy(), x, v, 3, "l1", (0.1,), 1.0, z=z, what=f"d1 n={n} kzx")
+    cr.close()
+
+
 @pytest.mark.parametrize("two_nu", [1, 5])
 def test_d1_single_chunk_shapes(gpm, two_nu):
     """Every thread-block shape of the single-chunk kernel (512x15, 384x19, 256x27: the
