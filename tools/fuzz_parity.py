@@ -26,6 +26,10 @@ for it in range(cases):
     n = int(rng.integers(1, 40000 if big else 5000))
     if d == 1 and rng.random() < 0.3:
         n = int(rng.integers(5000, 300000))
+    if d == 1 and rng.random() < 0.08:
+        n = int(rng.integers(900_000, 2_400_000))   # the large shapes and the three-launch path
+    if d >= 2 and rng.random() < 0.05:
+        n = int(rng.integers(40_000, 160_000))
     nrhs = int(rng.choice([1, 1, 2, 5]))
     grad = rng.random() < 0.3
     kzx = (not grad) and rng.random() < 0.2
@@ -45,6 +49,7 @@ for it in range(cases):
         m = int(rng.integers(1, 800))
         z = rng.random((m, d))
     rows = rng.choice(n, min(n, 200), replace=False)
+    rng_case = rng.random()
     if only >= 0 and it != only:
         continue
     if only >= 0:
@@ -64,6 +69,16 @@ for it in range(cases):
                 ref, ab = oracle.kzx_rows(x, V[c], z, nu2, fname, ell, os_, rows=zr, return_abs=True)
                 worst = max(worst, np.max(np.abs(out[c][zr] - ref)) / max(ab.max() * np.abs(V[c]).max(), 1e-300))
             cr.close()
+        elif d >= 2 and not grad and rng_case < 0.25:   # sharded partial applies sum to K v
+            G = 2 + int(rng_case * 12)
+            vr = torch.stack([plan.to_rank(Vd[c].contiguous()) for c in range(nrhs)])
+            acc = torch.zeros_like(vr)
+            for sh in range(G):
+                acc += plan.kmvm_partial(vr if nrhs > 1 else vr[0], sh, G).reshape(nrhs, n)
+            out = torch.stack([plan.from_rank(acc[c].contiguous()) for c in range(nrhs)]).cpu().numpy()
+            for c in range(nrhs):
+                ref, ab = oracle.kmvm_rows(x, V[c], nu2, fname, ell, os_, rows=rows, return_abs=True)
+                worst = max(worst, np.max(np.abs(out[c][rows] - ref)) / max(ab.max() * np.abs(V[c]).max(), 1e-300))
         else:
             if rank:
                 vr = torch.stack([plan.to_rank(Vd[c].contiguous()) for c in range(nrhs)])
