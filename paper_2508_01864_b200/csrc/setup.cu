@@ -34,7 +34,9 @@ __global__ void k_check_key0(const double* __restrict__ x, int64_t n, int d, dou
     bool ok = true;
     for (int k = 0; k < d; ++k) ok &= isfinite(x[i * d + k]);
     if (!ok) atomicMin(bad, static_cast<unsigned long long>(i));
-    key[i] = orderable_key(ok ? s0 * x[i * d] : 0.0);
+    // centred on the first point (the kernel depends on differences only; without
+    // it a large common offset costs eps * offset / l in every scaled distance)
+    key[i] = orderable_key(ok ? s0 * (x[i * d] - x[0]) : 0.0);
     val[i] = static_cast<int>(i);
   }
 }
@@ -46,7 +48,7 @@ __global__ void k_gather_scaled(const double* __restrict__ x, const int* __restr
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = perm[r];
     const double sc[3] = {s0, s1, s2};
-    for (int k = 0; k < d; ++k) t[k * n + r] = sc[k] * x[i * d + k] + 0.0;
+    for (int k = 0; k < d; ++k) t[k * n + r] = sc[k] * (x[i * d + k] - x[k]) + 0.0;   // centred on point 0
   }
 }
 

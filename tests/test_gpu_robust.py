@@ -46,3 +46,21 @@ def test_d23_edges(gpm, d, kind, ell):
     out = plan.kmvm(to_dev(v)).cpu().numpy()
     check_rows(out, x, v, 3 if d == 2 else 5, "l1", ells, 1.0, what=f"d{d} {kind} ell={ell}")
     plan.close()
+
+
+@pytest.mark.parametrize("d,two_nu,form", [(1, 7, 0), (2, 9, 1), (3, 5, 0), (3, 3, 1)])
+def test_far_offset_short_lengthscale(gpm, d, two_nu, form):
+    """Coordinates 1e4 from the origin with lengthscales of 1e-5..1e-3 of the data's extent:
+    offset / l ~ 1e9, so scaling before centring would lose 1e-7 of every scaled distance
+    (found by tools/fuzz_parity.py with FUZZ_WIDE=1); the plan centres on the first point."""
+    rng = np.random.default_rng(100 + d)
+    n = 3000
+    x = -9.3e3 + rng.random((n, d))
+    ell = tuple(float(e) for e in 10 ** rng.uniform(-4.5, -2.5, d))
+    v = rng.standard_normal(n)
+    plan = gpm.Plan(to_dev(x), gpm.Kernel(two_nu, ell, 1.0, form=form))
+    out = plan.kmvm(to_dev(v)).cpu().numpy()
+    check_rows(out, x, v, two_nu, ["l1", "product"][form], ell, 1.0, what=f"offset d={d}")
+    g = plan.kmvm_dlengthscale(to_dev(v)).cpu().numpy()
+    check_rows(g, x, v, two_nu, ["l1", "product"][form], ell, 1.0, grad=True, what=f"offset grad d={d}")
+    plan.close()

@@ -34,7 +34,8 @@ for it in range(cases):
     grad = rng.random() < 0.3
     kzx = (not grad) and rng.random() < 0.2
     rank = (not kzx) and rng.random() < 0.3
-    ell = tuple(float(x) for x in 10 ** rng.uniform(-1.6, 0.2, d))
+    wide = os.environ.get("FUZZ_WIDE") == "1"   # extreme lengthscales, scaled and shifted coordinates
+    ell = tuple(float(x) for x in 10 ** (rng.uniform(-3.5, 1.5, d) if wide else rng.uniform(-1.6, 0.2, d)))
     os_ = float(rng.uniform(0.5, 2.0))
     x = rng.random((n, d))
     mode = rng.integers(0, 3)
@@ -43,6 +44,10 @@ for it in range(cases):
     elif mode == 2 and n > 10:   # duplicates
         idx = rng.integers(0, n, n // 10)
         x[rng.integers(0, n, n // 10)] = x[idx]
+    if wide:
+        sc = 10 ** rng.uniform(-2, 3)
+        x = x * sc + rng.uniform(-1e4, 1e4)
+        ell = tuple(e * sc for e in ell)
     V = rng.standard_normal((nrhs, n))
     fname = ["l1", "product"][form]
     if kzx:
